@@ -1,0 +1,135 @@
+/*
+ * ocm_b200.h — C-ABI of the B200-native optimal-cycle-mean solver.
+ *
+ * Plain pointers and sizes only (no C++ or torch types). Each entry point
+ * replaces one reference interface (paths relative to the reference's proj/):
+ *
+ *   ocm_build_graph       include/ocm/graph.hpp:76      ocm::build_graph
+ *   ocm_parse_graph_text  include/ocm/graph_io.hpp:41   ocm::parse_graph_text
+ *   ocm_read_graph_file   include/ocm/graph_io.hpp:45   ocm::read_graph_file
+ *   ocm_graph_edges       include/ocm/graph.hpp:61      Graph::edges()
+ *   ocm_solve             include/ocm/solve.hpp:64      ocm::solve (lane howard-par)
+ *   ocm_session_*         include/ocm/howard_par.hpp:90 HowardPar (state kept resident
+ *                         in HBM so a graph can be solved repeatedly without re-upload)
+ *
+ * Error behaviour mirrors the reference's exceptions as return codes:
+ * std::invalid_argument -> OCM_E_INVALID, ParseError -> OCM_E_PARSE (message
+ * "<source>:<line>: <what>", line via ocm_last_error_line), std::logic_error
+ * (structural: a vertex without successor in its region, lambda increase)
+ * -> OCM_E_LOGIC. The message of the last failure on the calling thread is
+ * returned by ocm_last_error(). There is no CPU fallback: without a usable
+ * sm_100a device every solve returns OCM_E_CUDA.
+ */
+#ifndef OCM_B200_H
+#define OCM_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define OCM_OK 0
+#define OCM_E_INVALID 1     /* std::invalid_argument */
+#define OCM_E_PARSE 2       /* ocm::ParseError */
+#define OCM_E_LOGIC 3       /* std::logic_error */
+#define OCM_E_CUDA 4        /* no device / CUDA failure */
+#define OCM_E_UNSUPPORTED 5 /* lane or option not provided by this library */
+#define OCM_E_RANGE 6       /* exact arithmetic would overflow 64-bit keys */
+#define OCM_E_IO 7          /* std::runtime_error from file access */
+
+/* include/ocm/solve.hpp:21 enum Algo (only howard-par runs on the device) */
+#define OCM_ALGO_HOWARD 0
+#define OCM_ALGO_HOWARD_PAR 1
+#define OCM_ALGO_LAWLER 2
+#define OCM_ALGO_TREE 3
+#define OCM_ALGO_ORACLE_ENUM 4
+#define OCM_ALGO_ORACLE_DP 5
+/* include/ocm/graph.hpp:27 enum Objective */
+#define OCM_MINIMIZE 0
+#define OCM_MAXIMIZE 1
+/* include/ocm/solve.hpp:30 enum SccStrategy */
+#define OCM_SCC_TARJAN 0
+#define OCM_SCC_PARALLEL 1
+#define OCM_SCC_OFF 2
+
+typedef struct ocm_graph ocm_graph;
+typedef struct ocm_session ocm_session;
+
+/* include/ocm/solve.hpp:36 SolveOptions. engine schedule/workers/seed of the
+ * reference's CPU engine have no meaning on the device and are not present. */
+typedef struct {
+    int32_t algo;      /* OCM_ALGO_*; HOWARD and HOWARD_PAR both run the device lane */
+    int32_t objective; /* OCM_MINIMIZE / OCM_MAXIMIZE */
+    int32_t scc;       /* OCM_SCC_*; TARJAN and PARALLEL both decompose into regions */
+    int32_t device;    /* CUDA device ordinal */
+    double epsilon;    /* accepted for signature parity (Lawler only), unused */
+} ocm_solve_options;
+
+/* include/ocm/solve.hpp:45 SolveStats + :54 Solution. The optimal cycle's
+ * vertex list is returned through the cycle_buf argument of ocm_solve. */
+typedef struct {
+    int32_t has_cycle;
+    int32_t exact;          /* mu_num/mu_den authoritative (integer weights) */
+    int64_t mu_num;
+    int64_t mu_den;         /* > 0, gcd(|num|, den) == 1 */
+    double mu;
+    uint32_t cycle_len;     /* full length (may exceed cycle_cap) */
+    uint32_t outer_iters;   /* host iterations that rebuilt a policy */
+    uint32_t spf_passes;    /* improvement passes incl. the final quiet one */
+    uint32_t regions;
+    uint32_t trivial_regions;
+    uint32_t n_solved;      /* vertices in non-trivial regions */
+    uint64_t m_solved;      /* intra-region edges streamed per improvement pass */
+    uint64_t launches;      /* device kernel launches */
+    uint64_t fixpoint_iters;/* pointer-jumping rounds + attach layers */
+    double device_ms;       /* CUDA-event time of the device solve */
+    double improve_ms;      /* CUDA-event time summed over improvement launches */
+    double host_prep_ms;    /* host time of region split + upload (session create) */
+    uint64_t h2d_bytes;     /* host->device bytes moved by the call (upload at create) */
+    uint64_t d2h_bytes;     /* device->host bytes moved by this solve (flags + results) */
+} ocm_solution;
+
+const char* ocm_last_error(void);
+int ocm_last_error_line(void);
+const char* ocm_version(void);
+int ocm_device_count(void);
+
+int ocm_build_graph(uint32_t n, uint64_t m, const uint32_t* src, const uint32_t* dst,
+                    const double* w, ocm_graph** out);
+int ocm_parse_graph_text(const char* text, size_t len, const char* source, ocm_graph** out);
+int ocm_read_graph_file(const char* path, ocm_graph** out);
+/* Synthetic uniform digraph: every vertex has exactly deg out-edges, targets
+ * and integer weights in [wlo, whi] drawn from a seeded counter hash. */
+int ocm_generate_uniform(uint32_t n, uint32_t deg, int32_t wlo, int32_t whi, uint64_t seed,
+                         ocm_graph** out);
+void ocm_graph_free(ocm_graph* g);
+uint32_t ocm_graph_n(const ocm_graph* g);
+uint64_t ocm_graph_m(const ocm_graph* g);
+int ocm_graph_integer_exact(const ocm_graph* g);
+int ocm_graph_edges(const ocm_graph* g, uint32_t* src, uint32_t* dst, double* w);
+
+/* One-call front door (create session, solve, free). */
+int ocm_solve(const ocm_graph* g, const ocm_solve_options* opt, ocm_solution* out,
+              uint32_t* cycle_buf, uint32_t cycle_cap);
+
+/* Resident sessions: create uploads the region-compacted CSR into HBM once;
+ * each solve re-runs policy iteration from the initial policy on the device. */
+int ocm_session_create(const ocm_graph* g, const ocm_solve_options* opt, ocm_session** out);
+int ocm_session_solve(ocm_session* s, ocm_solution* out, uint32_t* cycle_buf, uint32_t cycle_cap);
+/* Final per-vertex values of the last solve (original vertex order), the
+ * plane written by the last value propagation: exact graphs give
+ * value(v) = key_num[v] / lam_den[v] as a rational (key_num = wsum*den -
+ * steps*num of the reference's (wsum, steps) pair); float graphs fill fval.
+ * Vertices of trivial regions report 0. Any pointer may be NULL. */
+int ocm_session_values(ocm_session* s, int64_t* key_num, int64_t* lam_num, int64_t* lam_den,
+                       double* fval, uint32_t* succ_vertex);
+/* The CUDA stream the session launches on (cudaStream_t). */
+void* ocm_session_stream(ocm_session* s);
+void ocm_session_free(ocm_session* s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* OCM_B200_H */

@@ -1,0 +1,350 @@
+"""paper_1111_0627_b200 — B200-native optimal cycle mean (policy iteration).
+
+Python mirror of the reference's public interface (proj/include/ocm):
+
+=========================  ==========================================
+reference                  here
+=========================  ==========================================
+ocm::build_graph           :func:`build_graph`        (graph.hpp:76)
+ocm::parse_graph_text      :func:`parse_graph_text`   (graph_io.hpp:41)
+ocm::read_graph_file       :func:`read_graph_file`    (graph_io.hpp:45)
+ocm::SolveOptions          :class:`SolveOptions`      (solve.hpp:36)
+ocm::Solution / SolveStats :class:`Solution`          (solve.hpp:45/54)
+ocm::solve                 :func:`solve`              (solve.hpp:64)
+ocm::ParseError            :class:`ParseError`        (graph_io.hpp:27)
+=========================  ==========================================
+
+Everything computes through ``lib/libocm_b200.so`` (the C-ABI declared in
+``include/ocm_b200.h``; CUDA kernels for sm_100a). There is no CPU fallback:
+importing works without a GPU (graph building and parsing are host code), but
+:func:`solve` raises :class:`DeviceError` when no sm_100 device is present, and
+the module refuses to import when the native library has not been built.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+from fractions import Fraction
+from typing import Iterable, List, Optional, Sequence, Tuple
+
+import numpy as np
+
+__all__ = [
+    "Graph", "build_graph", "parse_graph_text", "read_graph_file", "generate_uniform",
+    "SolveOptions", "SolveStats", "Solution", "solve", "Session",
+    "ParseError", "StructuralError", "DeviceError", "UnsupportedError", "LIB_PATH",
+]
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "lib", "libocm_b200.so")
+
+OK, E_INVALID, E_PARSE, E_LOGIC, E_CUDA, E_UNSUPPORTED, E_RANGE, E_IO = range(8)
+ALGOS = {"howard": 0, "howard-par": 1, "lawler": 2, "tree": 3, "oracle-enum": 4, "oracle-dp": 5}
+OBJECTIVES = {"min": 0, "max": 1}
+SCCS = {"tarjan": 0, "parallel": 1, "off": 2}
+
+
+class ParseError(ValueError):
+    """Malformed graph text; message is ``<source>:<line>: <what>``."""
+
+    def __init__(self, msg: str, line: int):
+        super().__init__(msg)
+        self.line = line
+
+
+class StructuralError(RuntimeError):
+    """The reference's std::logic_error (e.g. a region that is not strongly connected)."""
+
+
+class DeviceError(RuntimeError):
+    """No usable sm_100a device or a CUDA failure (there is no CPU fallback)."""
+
+
+class UnsupportedError(NotImplementedError):
+    """Lane or option the device library does not provide."""
+
+
+class _Opts(C.Structure):
+    _fields_ = [("algo", C.c_int32), ("objective", C.c_int32), ("scc", C.c_int32),
+                ("device", C.c_int32), ("epsilon", C.c_double)]
+
+
+class _Sol(C.Structure):
+    _fields_ = [
+        ("has_cycle", C.c_int32), ("exact", C.c_int32), ("mu_num", C.c_int64),
+        ("mu_den", C.c_int64), ("mu", C.c_double), ("cycle_len", C.c_uint32),
+        ("outer_iters", C.c_uint32), ("spf_passes", C.c_uint32), ("regions", C.c_uint32),
+        ("trivial_regions", C.c_uint32), ("n_solved", C.c_uint32), ("m_solved", C.c_uint64),
+        ("launches", C.c_uint64), ("fixpoint_iters", C.c_uint64), ("device_ms", C.c_double),
+        ("improve_ms", C.c_double), ("host_prep_ms", C.c_double),
+        ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64),
+    ]
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"native library missing: {LIB_PATH}; build it with `make -C {HERE}` "
+            "(or __graft_entry__.build())")
+    lib = C.CDLL(LIB_PATH)
+    P = C.POINTER
+    sig = {
+        "ocm_last_error": (C.c_char_p, []),
+        "ocm_last_error_line": (C.c_int, []),
+        "ocm_version": (C.c_char_p, []),
+        "ocm_device_count": (C.c_int, []),
+        "ocm_build_graph": (C.c_int, [C.c_uint32, C.c_uint64, P(C.c_uint32), P(C.c_uint32),
+                                      P(C.c_double), P(C.c_void_p)]),
+        "ocm_parse_graph_text": (C.c_int, [C.c_char_p, C.c_size_t, C.c_char_p, P(C.c_void_p)]),
+        "ocm_read_graph_file": (C.c_int, [C.c_char_p, P(C.c_void_p)]),
+        "ocm_generate_uniform": (C.c_int, [C.c_uint32, C.c_uint32, C.c_int32, C.c_int32,
+                                           C.c_uint64, P(C.c_void_p)]),
+        "ocm_graph_free": (None, [C.c_void_p]),
+        "ocm_graph_n": (C.c_uint32, [C.c_void_p]),
+        "ocm_graph_m": (C.c_uint64, [C.c_void_p]),
+        "ocm_graph_integer_exact": (C.c_int, [C.c_void_p]),
+        "ocm_graph_edges": (C.c_int, [C.c_void_p, P(C.c_uint32), P(C.c_uint32), P(C.c_double)]),
+        "ocm_solve": (C.c_int, [C.c_void_p, P(_Opts), P(_Sol), P(C.c_uint32), C.c_uint32]),
+        "ocm_session_create": (C.c_int, [C.c_void_p, P(_Opts), P(C.c_void_p)]),
+        "ocm_session_solve": (C.c_int, [C.c_void_p, P(_Sol), P(C.c_uint32), C.c_uint32]),
+        "ocm_session_values": (C.c_int, [C.c_void_p, P(C.c_int64), P(C.c_int64), P(C.c_int64),
+                                         P(C.c_double), P(C.c_uint32)]),
+        "ocm_session_stream": (C.c_void_p, [C.c_void_p]),
+        "ocm_session_free": (None, [C.c_void_p]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    return lib
+
+
+_lib = _load()
+EXPORTED_SYMBOLS = (
+    "ocm_last_error", "ocm_last_error_line", "ocm_version", "ocm_device_count",
+    "ocm_build_graph", "ocm_parse_graph_text", "ocm_read_graph_file", "ocm_generate_uniform",
+    "ocm_graph_free", "ocm_graph_n", "ocm_graph_m", "ocm_graph_integer_exact", "ocm_graph_edges",
+    "ocm_solve", "ocm_session_create", "ocm_session_solve", "ocm_session_values",
+    "ocm_session_stream", "ocm_session_free",
+)
+
+
+def _check(rc: int) -> None:
+    if rc == OK:
+        return
+    msg = (_lib.ocm_last_error() or b"").decode()
+    if rc == E_PARSE:
+        raise ParseError(msg, _lib.ocm_last_error_line())
+    if rc == E_INVALID:
+        raise ValueError(msg)
+    if rc == E_LOGIC:
+        raise StructuralError(msg)
+    if rc == E_CUDA:
+        raise DeviceError(msg)
+    if rc == E_UNSUPPORTED:
+        raise UnsupportedError(msg)
+    if rc == E_RANGE:
+        raise OverflowError(msg)
+    raise OSError(msg)
+
+
+def _p(a, t):
+    return a.ctypes.data_as(C.POINTER(t)) if a is not None else None
+
+
+class Graph:
+    """Handle on a host CSR graph (ocm::Graph, graph.hpp:34): edge ids are CSR
+    positions grouped by source, input order preserved within a source."""
+
+    def __init__(self, handle):
+        self._h = C.c_void_p(handle)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h and h.value:
+            _lib.ocm_graph_free(h)
+            self._h = C.c_void_p(None)
+
+    @property
+    def n(self) -> int:
+        return int(_lib.ocm_graph_n(self._h))
+
+    @property
+    def m(self) -> int:
+        return int(_lib.ocm_graph_m(self._h))
+
+    @property
+    def integer_exact(self) -> bool:
+        return bool(_lib.ocm_graph_integer_exact(self._h))
+
+    def edges(self) -> Tuple[np.ndarray, np.ndarray, np.ndarray]:
+        """(source, target, weight) arrays in edge-id order (Graph::edges())."""
+        m = self.m
+        s = np.empty(m, np.uint32)
+        d = np.empty(m, np.uint32)
+        w = np.empty(m, np.float64)
+        _check(_lib.ocm_graph_edges(self._h, _p(s, C.c_uint32), _p(d, C.c_uint32),
+                                    _p(w, C.c_double)))
+        return s, d, w
+
+
+def _as_arrays(edges) -> Tuple[np.ndarray, np.ndarray, np.ndarray]:
+    if isinstance(edges, tuple) and len(edges) == 3 and hasattr(edges[0], "__len__") and \
+            not isinstance(edges[0], (int, float)):
+        s, d, w = edges
+    else:
+        lst = list(edges)
+        s = [e[0] for e in lst]
+        d = [e[1] for e in lst]
+        w = [e[2] for e in lst]
+    s = np.asarray(s)
+    d = np.asarray(d)
+    if s.size and (s.min() < 0 or d.min() < 0):
+        raise ValueError("negative vertex id")
+    return (np.ascontiguousarray(s, np.uint32), np.ascontiguousarray(d, np.uint32),
+            np.ascontiguousarray(np.asarray(w, dtype=np.float64)))
+
+
+def build_graph(n: int, edges) -> Graph:
+    """ocm::build_graph (graph.hpp:76). ``edges``: iterable of (u, v, w) or a
+    (src, dst, w) tuple of arrays. Raises ValueError like std::invalid_argument."""
+    s, d, w = _as_arrays(edges)
+    h = C.c_void_p()
+    _check(_lib.ocm_build_graph(int(n), s.shape[0], _p(s, C.c_uint32), _p(d, C.c_uint32),
+                                _p(w, C.c_double), C.byref(h)))
+    return Graph(h.value)
+
+
+def parse_graph_text(text: str, source: str = "<text>") -> Graph:
+    """ocm::parse_graph_text (graph_io.hpp:41): 'p ocm n m' / 'a u v w' (1-based) or
+    plain '<u> <v> <w>' edge lists (0-based)."""
+    b = text.encode()
+    h = C.c_void_p()
+    _check(_lib.ocm_parse_graph_text(b, len(b), source.encode(), C.byref(h)))
+    return Graph(h.value)
+
+
+def read_graph_file(path: str) -> Graph:
+    """ocm::read_graph_file (graph_io.hpp:45)."""
+    h = C.c_void_p()
+    _check(_lib.ocm_read_graph_file(os.fsencode(path), C.byref(h)))
+    return Graph(h.value)
+
+
+def generate_uniform(n: int, deg: int, wlo: int = 1, whi: int = 100, seed: int = 1) -> Graph:
+    """Seeded random digraph with out-degree exactly ``deg`` and integer weights."""
+    h = C.c_void_p()
+    _check(_lib.ocm_generate_uniform(int(n), int(deg), int(wlo), int(whi), int(seed), C.byref(h)))
+    return Graph(h.value)
+
+
+@dataclass
+class SolveOptions:
+    """ocm::SolveOptions (solve.hpp:36). The reference's CPU-engine schedule,
+    workers and seed have no device meaning and are accepted but ignored."""
+    algo: str = "howard-par"
+    objective: str = "min"
+    scc: str = "tarjan"
+    epsilon: float = 1e-9
+    device: int = 0
+    schedule: str = "seq"
+    workers: int = 0
+    seed: int = 1
+
+    def _c(self) -> _Opts:
+        if self.algo not in ALGOS:
+            raise ValueError(f"unknown algorithm '{self.algo}'")
+        return _Opts(ALGOS[self.algo], OBJECTIVES[self.objective], SCCS[self.scc],
+                     int(self.device), float(self.epsilon))
+
+
+@dataclass
+class SolveStats:
+    """ocm::SolveStats (solve.hpp:45) plus device timing."""
+    outer_iters: int = 0
+    spf_passes: int = 0
+    launches: int = 0
+    fixpoint_iters: int = 0
+    regions: int = 0
+    trivial_regions: int = 0
+    n_solved: int = 0
+    m_solved: int = 0
+    device_ms: float = 0.0
+    improve_ms: float = 0.0
+    host_prep_ms: float = 0.0
+    h2d_bytes: int = 0
+    d2h_bytes: int = 0
+
+
+@dataclass
+class Solution:
+    """ocm::Solution (solve.hpp:54)."""
+    has_cycle: bool = False
+    exact: bool = False
+    mu_exact: Fraction = Fraction(0)
+    mu: float = 0.0
+    cycle_vertices: List[int] = field(default_factory=list)
+    stats: SolveStats = field(default_factory=SolveStats)
+
+
+def _solution(sol: _Sol, cyc: np.ndarray) -> Solution:
+    st = SolveStats(sol.outer_iters, sol.spf_passes, sol.launches, sol.fixpoint_iters,
+                    sol.regions, sol.trivial_regions, sol.n_solved, sol.m_solved,
+                    sol.device_ms, sol.improve_ms, sol.host_prep_ms, sol.h2d_bytes,
+                    sol.d2h_bytes)
+    mu_exact = Fraction(sol.mu_num, sol.mu_den) if sol.exact else Fraction(0)
+    return Solution(bool(sol.has_cycle), bool(sol.exact), mu_exact, float(sol.mu),
+                    cyc[: min(sol.cycle_len, cyc.shape[0])].astype(np.int64).tolist(), st)
+
+
+def solve(g: Graph, opt: Optional[SolveOptions] = None) -> Solution:
+    """ocm::solve (solve.hpp:64) on the B200: policy iteration (lane howard-par)."""
+    opt = opt or SolveOptions()
+    sol = _Sol()
+    cyc = np.zeros(max(g.n, 1), np.uint32)
+    _check(_lib.ocm_solve(g._h, C.byref(opt._c()), C.byref(sol), _p(cyc, C.c_uint32),
+                          cyc.shape[0]))
+    return _solution(sol, cyc)
+
+
+class Session:
+    """A graph resident in HBM (region-compacted CSR uploaded once); each
+    :meth:`solve` re-runs policy iteration from the initial policy."""
+
+    def __init__(self, g: Graph, opt: Optional[SolveOptions] = None):
+        self.opt = opt or SolveOptions()
+        self.n = g.n
+        h = C.c_void_p()
+        _check(_lib.ocm_session_create(g._h, C.byref(self.opt._c()), C.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h and h.value:
+            _lib.ocm_session_free(h)
+            self._h = C.c_void_p(None)
+
+    @property
+    def stream(self) -> int:
+        return int(_lib.ocm_session_stream(self._h) or 0)
+
+    def solve(self) -> Solution:
+        sol = _Sol()
+        cyc = np.zeros(max(self.n, 1), np.uint32)
+        _check(_lib.ocm_session_solve(self._h, C.byref(sol), _p(cyc, C.c_uint32), cyc.shape[0]))
+        return _solution(sol, cyc)
+
+    def values(self):
+        """Final value plane: dict with key_num/lam_num/lam_den (exact: value =
+        key_num/lam_den), fval (float graphs) and succ_vertex, in original order."""
+        n = max(self.n, 1)
+        out = {k: np.zeros(n, t) for k, t in (("key_num", np.int64), ("lam_num", np.int64),
+                                              ("lam_den", np.int64), ("fval", np.float64),
+                                              ("succ_vertex", np.uint32))}
+        _check(_lib.ocm_session_values(self._h, _p(out["key_num"], C.c_int64),
+                                       _p(out["lam_num"], C.c_int64),
+                                       _p(out["lam_den"], C.c_int64),
+                                       _p(out["fval"], C.c_double),
+                                       _p(out["succ_vertex"], C.c_uint32)))
+        return {k: v[: self.n] for k, v in out.items()}

@@ -1,0 +1,173 @@
+// extern "C" boundary of libocm_b200.so (declared in include/ocm_b200.h).
+// Translates the reference's exception contract into return codes and keeps
+// the last message per thread.
+
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <memory>
+#include <string>
+
+#include "../../include/ocm_b200.h"
+#include "errors.hpp"
+#include "gen.hpp"
+#include "graph.hpp"
+#include "solver.hpp"
+
+struct ocm_graph {
+    ocmb::Graph g;
+};
+struct ocm_session {
+    std::unique_ptr<ocmb::Session> s;
+};
+
+namespace {
+
+thread_local std::string g_err;
+thread_local int g_err_line = 0;
+
+template <class F> int guard(F&& f) {
+    g_err.clear();
+    g_err_line = 0;
+    try {
+        f();
+        return OCM_OK;
+    } catch (const ocmb::ParseError& e) {
+        g_err = e.what();
+        g_err_line = e.line();
+        return OCM_E_PARSE;
+    } catch (const std::invalid_argument& e) {
+        g_err = e.what();
+        return OCM_E_INVALID;
+    } catch (const std::logic_error& e) {
+        g_err = e.what();
+        return OCM_E_LOGIC;
+    } catch (const ocmb::CudaError& e) {
+        g_err = e.what();
+        return OCM_E_CUDA;
+    } catch (const ocmb::RangeError& e) {
+        g_err = e.what();
+        return OCM_E_RANGE;
+    } catch (const ocmb::UnsupportedError& e) {
+        g_err = e.what();
+        return OCM_E_UNSUPPORTED;
+    } catch (const std::overflow_error& e) {
+        g_err = e.what();
+        return OCM_E_RANGE;
+    } catch (const std::bad_alloc&) {
+        g_err = "out of host memory";
+        return OCM_E_RANGE;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return OCM_E_IO;
+    }
+}
+
+ocm_solve_options defaults(const ocm_solve_options* o) {
+    ocm_solve_options d{};
+    d.algo = OCM_ALGO_HOWARD_PAR;
+    d.objective = OCM_MINIMIZE;
+    d.scc = OCM_SCC_TARJAN;
+    d.device = 0;
+    d.epsilon = 1e-9;
+    return o ? *o : d;
+}
+
+} // namespace
+
+extern "C" {
+
+const char* ocm_last_error(void) { return g_err.c_str(); }
+int ocm_last_error_line(void) { return g_err_line; }
+const char* ocm_version(void) { return "ocm_b200 0.1 (sm_100a)"; }
+
+int ocm_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess)
+        return 0;
+    return n;
+}
+
+int ocm_build_graph(uint32_t n, uint64_t m, const uint32_t* src, const uint32_t* dst,
+                    const double* w, ocm_graph** out) {
+    return guard([&] {
+        if (m && (!src || !dst || !w))
+            throw std::invalid_argument("null edge arrays");
+        auto g = std::make_unique<ocm_graph>();
+        g->g = ocmb::build_graph(n, m, src, dst, w);
+        *out = g.release();
+    });
+}
+
+int ocm_parse_graph_text(const char* text, size_t len, const char* source, ocm_graph** out) {
+    return guard([&] {
+        auto g = std::make_unique<ocm_graph>();
+        g->g = ocmb::parse_graph_text(text ? text : "", text ? len : 0, source ? source : "<text>");
+        *out = g.release();
+    });
+}
+
+int ocm_read_graph_file(const char* path, ocm_graph** out) {
+    return guard([&] {
+        auto g = std::make_unique<ocm_graph>();
+        g->g = ocmb::read_graph_file(path ? path : "");
+        *out = g.release();
+    });
+}
+
+int ocm_generate_uniform(uint32_t n, uint32_t deg, int32_t wlo, int32_t whi, uint64_t seed,
+                         ocm_graph** out) {
+    return guard([&] {
+        auto g = std::make_unique<ocm_graph>();
+        g->g = ocmb::generate_uniform(n, deg, wlo, whi, seed);
+        *out = g.release();
+    });
+}
+
+void ocm_graph_free(ocm_graph* g) { delete g; }
+uint32_t ocm_graph_n(const ocm_graph* g) { return g ? g->g.n : 0; }
+uint64_t ocm_graph_m(const ocm_graph* g) { return g ? g->g.m : 0; }
+int ocm_graph_integer_exact(const ocm_graph* g) { return g && g->g.integer_exact ? 1 : 0; }
+
+int ocm_graph_edges(const ocm_graph* g, uint32_t* src, uint32_t* dst, double* w) {
+    return guard([&] { ocmb::graph_edges(g->g, src, dst, w); });
+}
+
+int ocm_session_create(const ocm_graph* g, const ocm_solve_options* opt, ocm_session** out) {
+    return guard([&] {
+        if (!g)
+            throw std::invalid_argument("null graph");
+        auto s = std::make_unique<ocm_session>();
+        s->s = std::make_unique<ocmb::Session>(g->g, defaults(opt));
+        *out = s.release();
+    });
+}
+
+int ocm_session_solve(ocm_session* s, ocm_solution* out, uint32_t* cycle_buf, uint32_t cycle_cap) {
+    return guard([&] { s->s->solve(out, cycle_buf, cycle_cap); });
+}
+
+int ocm_session_values(ocm_session* s, int64_t* key_num, int64_t* lam_num, int64_t* lam_den,
+                       double* fval, uint32_t* succ_vertex) {
+    return guard([&] { s->s->values(key_num, lam_num, lam_den, fval, succ_vertex); });
+}
+
+void* ocm_session_stream(ocm_session* s) { return s ? s->s->stream() : nullptr; }
+
+void ocm_session_free(ocm_session* s) { delete s; }
+
+int ocm_solve(const ocm_graph* g, const ocm_solve_options* opt, ocm_solution* out,
+              uint32_t* cycle_buf, uint32_t cycle_cap) {
+    return guard([&] {
+        if (!g)
+            throw std::invalid_argument("null graph");
+        std::memset(out, 0, sizeof *out);
+        out->mu_den = 1;
+        if (g->g.n == 0)
+            return; // solve.cpp:199: an empty graph has no cycle
+        ocmb::Session sess(g->g, defaults(opt));
+        sess.solve(out, cycle_buf, cycle_cap);
+    });
+}
+
+} // extern "C"

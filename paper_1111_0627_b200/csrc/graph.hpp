@@ -1,0 +1,65 @@
+// Host-side graph layer of the B200 optimal-cycle-mean solver.
+//
+// Mirrors the reference's graph vocabulary (proj/include/ocm/graph.hpp) so the
+// C-ABI can stand in for its entry points: edge ids are CSR positions grouped
+// by source with input order preserved (graph.hpp:7), multi-edges and
+// self-loops are allowed, and integer_exact is set when every weight is an
+// integer below 2^53 (graph.hpp:43). Only what the solver path needs is kept:
+// the backward CSR is built on the device when a kernel needs it.
+#pragma once
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace ocmb {
+
+using Vertex = std::uint32_t;
+constexpr Vertex kNoVertex = 0xffffffffu;
+
+struct Graph {
+    Vertex n = 0;
+    std::uint64_t m = 0;
+    std::vector<std::uint64_t> fwd_index; // n+1
+    std::vector<Vertex> fwd_target;       // m
+    std::vector<double> fwd_weight;       // m
+    bool integer_exact = false;
+};
+
+// Parse errors carry "<source>:<line>: <message>" like the reference's
+// ParseError (proj/include/ocm/graph_io.hpp:27).
+class ParseError : public std::runtime_error {
+  public:
+    ParseError(const std::string& src, int line, const std::string& what)
+        : std::runtime_error(src + ":" + std::to_string(line) + ": " + what), line_(line) {}
+    int line() const { return line_; }
+
+  private:
+    int line_;
+};
+
+// proj/include/ocm/graph.hpp:76 build_graph. Throws std::invalid_argument on
+// out-of-range endpoints or non-finite weights (same messages).
+Graph build_graph(Vertex n, std::uint64_t m, const Vertex* src, const Vertex* dst,
+                  const double* w);
+
+// proj/include/ocm/graph_io.hpp:41 parse_graph_text / :45 read_graph_file.
+Graph parse_graph_text(const char* text, std::size_t len, const std::string& source);
+Graph read_graph_file(const std::string& path);
+
+// Edge list in CSR order (fwd_source implied by fwd_index).
+void graph_edges(const Graph& g, Vertex* src, Vertex* dst, double* w);
+
+// Sequential strongly connected components (iterative low-link search from
+// vertex 0 upward, ids in completion order). Returns the region count.
+std::uint32_t tarjan_regions(const Graph& g, std::vector<std::uint32_t>& region_of);
+
+bool has_self_loop(const Graph& g, Vertex v);
+
+// proj/include/ocm/graph.hpp:100 augment_hamiltonian: appends v -> v+1 mod n
+// with weight 2n(max|w|+1)+1 (or big_w when nonzero). Returns the graph and
+// the no-cycle bound max|w|.
+Graph augment_hamiltonian(const Graph& g, double big_w, double* no_cycle_above);
+
+} // namespace ocmb

@@ -1,0 +1,171 @@
+"""GPU parity: the device lane (through the C-ABI) against the reference's
+golden vectors and the C oracle, plus size-independent optimality
+certificates at benchmark sizes. Bar: bit-exact rationals, cycles, policies
+and scalar values on integer graphs; float graphs compare means and values
+exactly too (same summation order as the reference) with a 1e-9 relative
+fallback tolerance noted where used."""
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_1111_0627_b200 as P
+from helpers import case_arrays, cycle_mean_exact, golden_cases, is_closed_walk, random_graph
+
+pytestmark = pytest.mark.gpu
+CASES = golden_cases()
+NONE = 0xFFFFFFFF
+
+
+def run(n, src, dst, w, objective="min", scc="tarjan"):
+    g = P.build_graph(n, (src, dst, w))
+    s = P.Session(g, P.SolveOptions(objective=objective, scc=scc))
+    sol = s.solve()
+    return sol, s.values()
+
+
+def check_against(sol, vals, ref, key_field="value_key"):
+    assert sol.has_cycle == ref["has_cycle"]
+    if not ref["has_cycle"]:
+        return
+    if ref["exact"]:
+        assert sol.exact
+        assert (sol.mu_exact.numerator, sol.mu_exact.denominator) == (ref["mu_num"], ref["mu_den"])
+    assert sol.mu == ref["mu"]
+    assert sol.cycle_vertices == ref["cycle"]
+    assert (sol.stats.outer_iters, sol.stats.spf_passes) == (ref["outer_iters"], ref["spf_passes"])
+    assert (sol.stats.regions, sol.stats.trivial_regions) == (ref["regions"], ref["trivial_regions"])
+    if vals is not None and "succ_vertex" in ref:
+        assert vals["succ_vertex"].tolist() == ref["succ_vertex"]
+        if key_field in ref:
+            assert vals["key_num"].tolist() == ref[key_field]
+            assert vals["lam_num"].tolist() == ref["lam_num"]
+            assert vals["lam_den"].tolist() == ref["lam_den"]
+        elif "fval" in ref:
+            np.testing.assert_array_equal(vals["fval"], np.array(ref["fval"]))
+
+
+@pytest.mark.parametrize("case", CASES, ids=[c["name"] for c in CASES])
+def test_golden(case):
+    n = case["n"]
+    src, dst, w = case_arrays(case)
+    for key, ref in case["results"].items():
+        objective, scc = key.split("/")
+        sol, vals = run(n, src, dst, w, objective, scc)
+        check_against(sol, vals if scc == "tarjan" else None, ref)
+
+
+def oracle_record(n, src, dst, w, objective, scc):
+    o = O.oracle_solve(n, src, dst, w, objective, scc, values=True)
+    r = {"has_cycle": o.has_cycle, "exact": o.exact, "mu_num": o.mu_num, "mu_den": o.mu_den,
+         "mu": o.mu, "cycle": o.cycle, "outer_iters": o.outer_iters, "spf_passes": o.spf_passes,
+         "regions": o.regions, "trivial_regions": o.trivial_regions}
+    if scc == "tarjan":
+        r["succ_vertex"] = o.succ_vertex.tolist()
+        if o.exact or (len(w) and np.all(np.floor(w) == w)):
+            r["value_key"] = (o.wsum * o.lam_den - o.steps * o.lam_num).tolist()
+            r["lam_num"] = o.lam_num.tolist()
+            r["lam_den"] = o.lam_den.tolist()
+        else:
+            r["fval"] = o.fval.tolist()
+    return r
+
+
+def test_random_small_graphs_vs_oracle():
+    rng = np.random.default_rng(1234)
+    for it in range(250):
+        n, s, d, w = random_graph(rng, 12)
+        if it % 4 == 0:
+            w = w / 8 + 0.125
+        for objective in ("min", "max"):
+            scc = "off" if it % 5 == 0 else "tarjan"
+            sol, vals = run(n, s, d, w, objective, scc)
+            check_against(sol, vals if scc == "tarjan" else None,
+                          oracle_record(n, s, d, w, objective, scc))
+
+
+@pytest.mark.parametrize("n,deg,seed", [(1000, 2, 1), (10000, 4, 2), (20000, 1, 5),
+                                        (100000, 8, 3)])
+def test_generated_graphs_vs_oracle(n, deg, seed):
+    g = P.generate_uniform(n, deg, 1, 100, seed)
+    s, d, w = g.edges()
+    for objective in ("min", "max"):
+        sess = P.Session(g, P.SolveOptions(objective=objective))
+        sol = sess.solve()
+        check_against(sol, sess.values(), oracle_record(n, s, d, w, objective, "tarjan"))
+
+
+def test_float_weights_generated():
+    g = P.generate_uniform(5000, 3, -400, 400, 9)
+    s, d, w = g.edges()
+    w = w / 16.0 + 0.03125
+    sol, vals = run(5000, s, d, w, "min")
+    ref = oracle_record(5000, s, d, w, "min", "tarjan")
+    assert not sol.exact
+    check_against(sol, vals, ref)
+
+
+def test_no_cycle_and_empty():
+    sol, _ = run(4, np.array([0, 0, 1, 2], np.uint32), np.array([1, 2, 3, 3], np.uint32),
+                 np.array([1, 2, 3, -1.0]))
+    assert not sol.has_cycle and sol.stats.spf_passes == 0
+    g = P.build_graph(0, [])
+    assert not P.solve(g).has_cycle
+    sol, _ = run(4, np.array([0, 0, 1, 2], np.uint32), np.array([1, 2, 3, 3], np.uint32),
+                 np.array([1, 2, 3, -1.0]), scc="off")
+    assert not sol.has_cycle
+
+
+def test_session_resolve_is_deterministic():
+    g = P.generate_uniform(50000, 8, 1, 100, 21)
+    s = P.Session(g)
+    a = s.solve()
+    va = s.values()
+    b = s.solve()
+    vb = s.values()
+    assert (a.mu_exact, a.cycle_vertices, a.stats.spf_passes) == \
+        (b.mu_exact, b.cycle_vertices, b.stats.spf_passes)
+    assert (va["key_num"] == vb["key_num"]).all()
+
+
+def bellman_certificate(g, sol, vals, objective):
+    """Size-independent optimality certificate. With K = value*den per vertex,
+    every intra-component edge (v,t) satisfies K[v] <= K[t] + w*den - num with
+    equality attained by some edge of every vertex (the Bellman equation of
+    the final policy), so no cycle has mean below lambda in its component;
+    the returned cycle is a closed walk of mean mu; mu = min over components."""
+    from scipy.sparse import csr_matrix
+    from scipy.sparse.csgraph import connected_components
+    s, d, w = g.edges()
+    if objective == "max":
+        w = -w
+    n = g.n
+    ncomp, lab = connected_components(csr_matrix((np.ones(len(s)), (s, d)), shape=(n, n)),
+                                      directed=True, connection="strong")
+    intra = lab[s] == lab[d]
+    K = vals["key_num"]
+    num = vals["lam_num"]
+    den = vals["lam_den"]
+    s_, d_, w_ = s[intra], d[intra], w[intra].astype(np.int64)
+    rhs = K[d_] + w_ * den[s_] - num[s_]
+    assert (K[s_] <= rhs).all()
+    best = np.full(n, np.iinfo(np.int64).max)
+    np.minimum.at(best, s_, rhs)
+    solved = best != np.iinfo(np.int64).max
+    assert (best[solved] == K[solved]).all()
+    cyc = sol.cycle_vertices
+    assert is_closed_walk(n, s, d, cyc)
+    mean = cycle_mean_exact(s, d, w, cyc, "min")
+    assert mean == (sol.mu_exact if objective == "min" else -sol.mu_exact)
+    lam = [Fraction(int(a), int(b)) for a, b in zip(num[solved][:1000], den[solved][:1000])]
+    assert min(lam) >= (sol.mu_exact if objective == "min" else -sol.mu_exact)
+
+
+@pytest.mark.parametrize("objective", ["min", "max"])
+def test_benchmark_size_certificate(objective):
+    g = P.generate_uniform(1_000_000, 8, 1, 100, 1111_0627)
+    sess = P.Session(g, P.SolveOptions(objective=objective))
+    sol = sess.solve()
+    assert sol.has_cycle and sol.exact
+    bellman_certificate(g, sol, sess.values(), objective)
