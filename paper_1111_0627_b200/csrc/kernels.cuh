@@ -9,11 +9,12 @@
 //   k_cycle_stats    per-cycle (length, weight) segmented  howard_par.hpp:319
 //                    reduction, exact integers
 //   k_vote/k_adopt   per-region min (mean, anchor) vote    howard_par.hpp:56/339
+//   k_wincyc_*       values on the winning cycle (prefix   howard_par.hpp:494
+//                    sum by pointer jumping, cycle only)    valuePropagate
 //   k_keep           kept component = policy paths into    howard_par.hpp:370/393
-//                    the winning cycle
-//   k_attach         breadth-layered re-attachment         howard_par.hpp:433
-//   k_prop_*         value determination by pointer        howard_par.hpp:494
-//                    jumping along the policy tree
+//                    the winning cycle, + their values      (+ valuePropagate)
+//   k_attach         breadth-layered re-attachment, +      howard_par.hpp:433
+//                    values of re-attached vertices         (+ valuePropagate)
 //
 // Results are identical to the reference's (same lambda sequence, policy,
 // cycle and scalar values): every kernel computes the same function as the
@@ -55,12 +56,23 @@ struct __align__(16) PJV {
     std::uint32_t root;
 };
 
+// Pointer-doubling record for cycle detection: segment end, least vertex on
+// the segment, weight sum of the segment.
+struct __align__(16) PJC {
+    std::uint32_t nxt;
+    std::uint32_t mn;
+    long long w;
+};
+
 struct Flags {
     unsigned active_count;
     unsigned rem_count[2];
     int error;     // structural (no successor / not strongly connected)
     int overflow;  // exact keys would leave int64
     int lambda_up; // lambda increased inside a region
+    int verify_fail;    // cycle-detection round count too small
+    unsigned max_cycle; // longest winning cycle this iteration
+    unsigned wc_count;  // winning-cycle vertices listed
     unsigned notdone[kMaxRounds];
 };
 
@@ -85,9 +97,11 @@ struct KP {
     unsigned long long* slot;
     std::uint32_t* src;
     std::uint32_t* iters;
-    unsigned long long* pj[2];
+    PJC* pj[2];
     std::uint32_t* comp;
     std::uint32_t* mark;
+    std::uint32_t* mark2;
+    std::uint32_t* wlist;
     std::uint32_t* cyc_len;
     long long* cyc_wi;
     double* cyc_wf;
@@ -155,6 +169,7 @@ __global__ void k_init(KP p) {
         if (p.key_f)
             p.key_f[v] = 0.0;
         p.mark[v] = 0;
+        p.mark2[v] = 0;
     }
     for (std::size_t r = gtid(); r < p.R; r += gstride()) {
         p.lam_num[r] = 0;
@@ -354,45 +369,81 @@ __global__ void k_region_check(KP p) {
 
 // ------------------------------------------------------------ cycles
 //
-// Pointer doubling on the functional policy graph. pj[v] packs
-// (jump target << 32 | least vertex on the jumped segment). After K rounds
-// with 2^K >= region size, jump(v) lies on v's cycle and the least vertex of
-// jump(v)'s segment is the least vertex of that cycle: the anchor of v's
-// component (howard_par.hpp:310 cycle_anchor, minIndex). Every cycle vertex
-// is the image of some vertex under succ^(2^K), so scattering a stamp to
-// jump(v) marks exactly the cycle vertices (the survivors of the reference's
-// elimination fixpoint, howard_par.hpp:249). Regions are closed under succ,
-// so rounds run over all vertices without region checks.
+// Pointer doubling on the functional policy graph. pj[v] = (jump target,
+// least vertex on the jumped segment, weight sum of the segment). All
+// segments have the same length L = 2^k (synchronous doubling). Once
+// L >= tail + cycle length for every vertex, jump(v) lies on v's cycle and
+// the least vertex of jump(v)'s segment is the least vertex of that cycle:
+// the anchor of v's component (howard_par.hpp:310 cycle_anchor, minIndex),
+// and the image of succ^L is exactly the set of cycle vertices (the
+// survivors of the reference's elimination fixpoint, howard_par.hpp:249).
+// The round count is not fixed at log2(n): k_cycle_verify checks the two
+// conditions exactly and the host adds rounds until it holds.
+// Regions are closed under succ, so rounds run without region checks.
 
-__global__ void k_pj_init(KP p) {
-    for (std::size_t v = gtid(); v < p.N; v += gstride())
-        p.pj[0][v] = (static_cast<unsigned long long>(p.succ_v[v]) << 32) | v;
+template <bool EXACT> __global__ void k_pj_init(KP p) {
+    for (std::size_t v = gtid(); v < p.N; v += gstride()) {
+        PJC x;
+        x.nxt = p.succ_v[v];
+        x.mn = static_cast<std::uint32_t>(v);
+        x.w = EXACT ? static_cast<long long>(p.succ_wi[v]) : 0ll;
+        p.pj[0][v] = x;
+    }
 }
 
 __global__ void k_pj_round(KP p, int in) {
-    const unsigned long long* __restrict__ a = p.pj[in];
-    unsigned long long* __restrict__ o = p.pj[in ^ 1];
+    const PJC* __restrict__ a = p.pj[in];
+    PJC* __restrict__ o = p.pj[in ^ 1];
     for (std::size_t v = gtid(); v < p.N; v += gstride()) {
-        const unsigned long long x = a[v];
-        const unsigned long long y = a[x >> 32];
-        const unsigned long long lo = min(x & 0xffffffffull, y & 0xffffffffull);
-        o[v] = (y & 0xffffffff00000000ull) | lo;
+        const PJC x = a[v];
+        const PJC y = a[x.nxt];
+        PJC z;
+        z.nxt = y.nxt;
+        z.mn = min(x.mn, y.mn);
+        z.w = x.w + y.w;
+        o[v] = z;
     }
 }
 
 __global__ void k_cycle_mark(KP p, int in, std::uint32_t stamp) {
-    const unsigned long long* a = p.pj[in];
+    const PJC* a = p.pj[in];
     for (std::size_t v = gtid(); v < p.N; v += gstride()) {
         if (!working(p, v))
             continue;
-        const std::uint32_t j = static_cast<std::uint32_t>(a[v] >> 32);
-        p.comp[v] = static_cast<std::uint32_t>(a[j] & 0xffffffffull);
+        const std::uint32_t j = a[v].nxt;
+        p.comp[v] = a[j].mn;
         if (p.mark[j] != stamp) // many vertices share j: read before writing
             p.mark[j] = stamp;
         p.cyc_len[v] = 0;
         if (p.cyc_wi)
             p.cyc_wi[v] = 0;
     }
+}
+
+// Exact check of the round count. M = image of succ^L. Passes iff every
+// vertex of M has a predecessor in M (so M has no tail vertex, i.e. L >=
+// every tail) and comp is constant along succ inside M (so every window of
+// length L covers its whole cycle, i.e. L >= every cycle length).
+__global__ void k_cycle_verify1(KP p, std::uint32_t stamp) {
+    bool fail = false;
+    for (std::size_t v = gtid(); v < p.N; v += gstride()) {
+        if (p.mark[v] != stamp || !working(p, v))
+            continue;
+        const std::uint32_t s = p.succ_v[v];
+        fail |= p.comp[s] != p.comp[v];
+        if (p.mark2[s] != stamp)
+            p.mark2[s] = stamp;
+    }
+    if (__syncthreads_or(fail) && threadIdx.x == 0)
+        set_flag(&p.flags->verify_fail);
+}
+
+__global__ void k_cycle_verify2(KP p, std::uint32_t stamp) {
+    bool fail = false;
+    for (std::size_t v = gtid(); v < p.N; v += gstride())
+        fail |= p.mark[v] == stamp && p.mark2[v] != stamp && working(p, v);
+    if (__syncthreads_or(fail) && threadIdx.x == 0)
+        set_flag(&p.flags->verify_fail);
 }
 
 // Segmented reduction of (length, weight) per cycle, keyed by anchor.
@@ -510,6 +561,7 @@ template <bool EXACT> __global__ void k_adopt(KP p) {
             continue;
         }
         p.src[r] = static_cast<std::uint32_t>(a);
+        atomicMax(&p.flags->max_cycle, p.cyc_len[a]);
         if constexpr (EXACT) {
             long long num = p.cyc_wi[a], den = p.cyc_len[a];
             const long long g = gcd_ll(num, den);
@@ -533,31 +585,134 @@ template <bool EXACT> __global__ void k_adopt(KP p) {
     }
 }
 
+// ------------------------------------------------------------ values
+//
+// Value determination (howard_par.hpp:494 valuePropagate) without a separate
+// propagation fixpoint. With K = value * den, the reference computes
+// K(u) = K(succ u) + w*den - num along the rebuilt policy tree rooted at the
+// winning anchor. Three cases, all exact integer arithmetic:
+//  * winning-cycle vertices: a pointer-jumping prefix sum over the cycle
+//    vertices only, cut at the anchor (k_wincyc_*);
+//  * other kept vertices (their policy path enters the winning cycle): the
+//    doubling above already summed the weights of the length-L walk from v
+//    to jump(v) on the cycle; since the cycle's reduced weight is exactly 0,
+//    K(v) = W_L(v)*den - L*num + K(jump(v)) (k_keep);
+//  * re-attached vertices: K(x) = K(t) + w*den - num at attachment, t being
+//    connected in an earlier layer (k_attach).
+
+__global__ void k_wincyc_init(KP p, std::uint32_t stamp) {
+    for (std::size_t base = blockIdx.x * std::size_t(kBlock); base < p.N;
+         base += gridDim.x * std::size_t(kBlock)) {
+        const std::size_t v = base + threadIdx.x;
+        bool take = false;
+        std::uint32_t r = 0;
+        if (v < p.N && p.mark[v] == stamp && working(p, v)) {
+            r = p.reg[v];
+            take = p.comp[v] == p.src[r];
+        }
+        const unsigned slot = block_append(take, &p.flags->wc_count);
+        if (take) {
+            p.wlist[slot] = static_cast<std::uint32_t>(v);
+            PJV x;
+            const std::uint32_t root = p.src[r];
+            if (v == root) {
+                x.acc = 0;
+                x.nxt = root;
+            } else {
+                x.acc = static_cast<long long>(p.succ_wi[v]) * p.lam_den[r] - p.lam_num[r];
+                x.nxt = p.succ_v[v];
+            }
+            x.root = root;
+            p.pv[0][v] = x;
+        }
+    }
+}
+
+__global__ void k_wincyc_round(KP p, int round) {
+    if (round > 0 && *(volatile unsigned*)&p.flags->notdone[round - 1] == 0)
+        return;
+    const int in = round & 1;
+    const PJV* __restrict__ a = p.pv[in];
+    PJV* __restrict__ o = p.pv[in ^ 1];
+    const unsigned cnt = p.flags->wc_count;
+    bool nd = false;
+    for (std::size_t i = gtid(); i < cnt; i += gstride()) {
+        const std::uint32_t c = p.wlist[i];
+        const PJV x = a[c];
+        const PJV y = a[x.nxt];
+        PJV z;
+        z.acc = x.acc + y.acc;
+        z.nxt = y.nxt;
+        z.root = x.root;
+        o[c] = z;
+        nd |= y.nxt != x.root;
+    }
+    if (__syncthreads_or(nd) && threadIdx.x == 0)
+        set_flag(&p.flags->notdone[round]);
+}
+
+__global__ void k_wincyc_final(KP p, int rounds) {
+    int last = rounds - 1;
+    for (int j = 0; j < rounds; ++j)
+        if (p.flags->notdone[j] == 0) {
+            last = j;
+            break;
+        }
+    if (gtid() == 0 && p.flags->notdone[rounds - 1] != 0)
+        p.flags->error = 1;
+    const PJV* a = p.pv[(last & 1) ^ 1];
+    const unsigned cnt = p.flags->wc_count;
+    for (std::size_t i = gtid(); i < cnt; i += gstride()) {
+        const std::uint32_t c = p.wlist[i];
+        p.key_i[c] = a[c].acc;
+    }
+}
+
+__device__ __forceinline__ bool key_in_range(__int128 k) {
+    const __int128 lim = static_cast<__int128>(1) << 62;
+    return k < lim && k > -lim;
+}
+
 // Kept component: vertices whose policy path ends in the winning cycle keep
-// their edges (howard_par.hpp:393 markMinComponent); everyone else is queued
-// for re-attachment.
-__global__ void k_keep(KP p) {
+// their edges (howard_par.hpp:393 markMinComponent) and, in exact mode, get
+// their values from the doubling sums; everyone else is queued for
+// re-attachment.
+template <bool EXACT>
+__global__ void k_keep(KP p, int in, std::uint32_t stamp, unsigned long long L) {
+    const PJC* a = p.pj[in];
+    bool ovf = false;
     for (std::size_t base = blockIdx.x * std::size_t(kBlock); base < p.N;
          base += gridDim.x * std::size_t(kBlock)) {
         const std::size_t v = base + threadIdx.x;
         bool take = false;
         if (v < p.N && working(p, v)) {
-            const bool kept = p.comp[v] == p.src[p.reg[v]];
+            const std::uint32_t r = p.reg[v];
+            const bool kept = p.comp[v] == p.src[r];
             p.conn[v] = kept ? 0u : NONE;
             take = !kept;
+            if (EXACT && kept && p.mark[v] != stamp) {
+                const PJC x = a[v];
+                const __int128 k = static_cast<__int128>(x.w) * p.lam_den[r] -
+                                   static_cast<__int128>(L) * p.lam_num[r] + p.key_i[x.nxt];
+                ovf |= !key_in_range(k);
+                p.key_i[v] = static_cast<long long>(k);
+            }
         }
         const unsigned slot = block_append(take, &p.flags->rem_count[0]);
         if (take)
             p.rem[0][slot] = static_cast<std::uint32_t>(v);
     }
+    if (__syncthreads_or(ovf) && threadIdx.x == 0)
+        set_flag(&p.flags->overflow);
 }
 
 // One breadth layer of howard_par.hpp:433 connectGpi: a pending vertex
 // attaches through its smallest out-edge whose head was connected in an
 // earlier layer (conn < layer); connection stamps make the layer discipline
-// exact regardless of schedule.
+// exact regardless of schedule. Exact mode also sets the vertex's value.
 template <bool EXACT> __global__ void k_attach(KP p, int in, unsigned n_in, std::uint32_t layer) {
     const std::uint32_t* list = p.rem[in];
+    bool ovf = false;
     for (std::size_t base = blockIdx.x * std::size_t(kBlock); base < n_in;
          base += gridDim.x * std::size_t(kBlock)) {
         const std::size_t i = base + threadIdx.x;
@@ -576,10 +731,17 @@ template <bool EXACT> __global__ void k_attach(KP p, int in, unsigned n_in, std:
                 if (p.conn[t] < layer) {
                     p.succ_e[x] = e;
                     p.succ_v[x] = t;
-                    if constexpr (EXACT)
-                        p.succ_wi[x] = p.ew[e].y;
-                    else
+                    if constexpr (EXACT) {
+                        const int w = p.ew[e].y;
+                        p.succ_wi[x] = w;
+                        const std::uint32_t r = p.reg[x];
+                        const __int128 k = static_cast<__int128>(p.key_i[t]) +
+                                           static_cast<__int128>(w) * p.lam_den[r] - p.lam_num[r];
+                        ovf |= !key_in_range(k);
+                        p.key_i[x] = static_cast<long long>(k);
+                    } else {
                         p.succ_wf[x] = p.fe[e].w;
+                    }
                     p.conn[x] = layer;
                     pending = false;
                     break;
@@ -590,70 +752,8 @@ template <bool EXACT> __global__ void k_attach(KP p, int in, unsigned n_in, std:
         if (pending)
             p.rem[in ^ 1][slot] = x;
     }
-}
-
-// ------------------------------------------------------------ values
-//
-// Exact mode: value determination (howard_par.hpp:494 valuePropagate) as a
-// tree prefix sum by pointer jumping. The policy is now a tree into the
-// winning cycle; cutting it at the anchor (nxt = self, acc = 0) makes every
-// key the sum of w*den - num along the policy path to the anchor, which is
-// exactly value(u) = value(succ) + w - lambda scaled by den. Integer sums,
-// so the association order is irrelevant. Rounds are gated on device: round
-// j runs only if round j-1 still saw an unfinished vertex. Vertices of
-// finished regions are parked as their own roots.
-
-__global__ void k_prop_init(KP p) {
-    for (std::size_t v = gtid(); v < p.N; v += gstride()) {
-        const std::uint32_t r = p.reg[v];
-        PJV x;
-        if (!p.active[r] || v == p.src[r]) {
-            x.acc = 0;
-            x.nxt = static_cast<std::uint32_t>(v);
-            x.root = static_cast<std::uint32_t>(v);
-        } else {
-            x.acc = static_cast<long long>(p.succ_wi[v]) * p.lam_den[r] - p.lam_num[r];
-            x.nxt = p.succ_v[v];
-            x.root = p.src[r];
-        }
-        p.pv[0][v] = x;
-    }
-}
-
-__global__ void k_prop_round(KP p, int round) {
-    if (round > 0 && *(volatile unsigned*)&p.flags->notdone[round - 1] == 0)
-        return;
-    const int in = round & 1;
-    const PJV* __restrict__ a = p.pv[in];
-    PJV* __restrict__ o = p.pv[in ^ 1];
-    bool nd = false;
-    for (std::size_t v = gtid(); v < p.N; v += gstride()) {
-        const PJV x = a[v];
-        const PJV y = a[x.nxt];
-        PJV z;
-        z.acc = x.acc + y.acc;
-        z.nxt = y.nxt;
-        z.root = x.root;
-        o[v] = z;
-        nd |= y.nxt != x.root;
-    }
-    if (__syncthreads_or(nd) && threadIdx.x == 0)
-        set_flag(&p.flags->notdone[round]);
-}
-
-__global__ void k_prop_final(KP p, int rounds) {
-    int last = rounds - 1;
-    for (int j = 0; j < rounds; ++j)
-        if (p.flags->notdone[j] == 0) {
-            last = j;
-            break;
-        }
-    const PJV* a = p.pv[(last & 1) ^ 1];
-    if (gtid() == 0 && p.flags->notdone[rounds - 1] != 0)
-        p.flags->error = 1; // did not converge within the round budget
-    for (std::size_t v = gtid(); v < p.N; v += gstride())
-        if (working(p, v))
-            p.key_i[v] = a[v].acc;
+    if (__syncthreads_or(ovf) && threadIdx.x == 0)
+        set_flag(&p.flags->overflow);
 }
 
 // Float mode: level-synchronous propagation from the anchor, one policy

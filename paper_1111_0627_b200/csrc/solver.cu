@@ -66,14 +66,16 @@ struct DeviceState {
     int device = 0;
     int sms = 148;
     cudaStream_t stream = nullptr;
-    DBuf<std::uint32_t> row, reg, succ_e, succ_v, comp, mark, cyc_len, conn, rem0, rem1, src, iters;
+    DBuf<std::uint32_t> row, reg, succ_e, succ_v, comp, mark, mark2, wlist, cyc_len, conn, rem0, rem1,
+        src, iters;
     DBuf<PJV> pv0, pv1;
+    DBuf<PJC> pj0, pj1;
     DBuf<int2> ew;
     DBuf<FEdge> fe;
     DBuf<int> succ_wi, active, changed;
     DBuf<double> succ_wf, key_f, lam_f, cyc_wf;
     DBuf<long long> key_i, lam_num, lam_den, cyc_wi;
-    DBuf<unsigned long long> slot, pj0, pj1;
+    DBuf<unsigned long long> slot;
     DBuf<Flags> flags;
     Flags* h_flags = nullptr;
     std::vector<cudaEvent_t> ev;
@@ -279,7 +281,8 @@ Session::Session(const Graph& g, const ocm_solve_options& opt) : opt_(opt) {
     if (N)
         CK(cudaMemcpyAsync(d.reg.p, prep_.reg.data(), N * sizeof(std::uint32_t),
                            cudaMemcpyHostToDevice, d.stream));
-    for (auto* b : {&d.succ_e, &d.succ_v, &d.comp, &d.mark, &d.cyc_len, &d.conn, &d.rem0, &d.rem1})
+    for (auto* b : {&d.succ_e, &d.succ_v, &d.comp, &d.mark, &d.mark2, &d.wlist, &d.cyc_len, &d.conn,
+                    &d.rem0, &d.rem1})
         b->alloc(N1);
     d.pj0.alloc(N1);
     d.pj1.alloc(N1);
@@ -319,6 +322,8 @@ Session::Session(const Graph& g, const ocm_solve_options& opt) : opt_(opt) {
     p.pj[1] = d.pj1.p;
     p.comp = d.comp.p;
     p.mark = d.mark.p;
+    p.mark2 = d.mark2.p;
+    p.wlist = d.wlist.p;
     p.cyc_len = d.cyc_len.p;
     p.cyc_wi = d.cyc_wi.p;
     p.cyc_wf = d.cyc_wf.p;
@@ -402,11 +407,14 @@ template <class M> void Session::run(ocm_solution* out, std::uint32_t* cycle_buf
     CK(cudaEventRecord(d.ev_start, s));
     CK(cudaMemsetAsync(p.flags, 0, sizeof(Flags), s));
     if (p.N) {
-        k_init<<<gv, 256, 0, s>>>(p);
+        k_init<<<gv, kBlock, 0, s>>>(p);
         ++launches;
     }
-    const int K = std::max(1, ceil_log2(std::max<std::uint32_t>(prep_.max_region, 2)));
-    const int prop_rounds = std::min(kMaxRounds, K + 1);
+    // Upper bound on doubling rounds (2^K_max >= region size) and the
+    // session's running estimate of the rounds actually needed.
+    const int K_max = std::max(1, ceil_log2(std::max<std::uint32_t>(prep_.max_region, 2)));
+    int k_need = std::min(K_max, k_hint_);
+    std::uint32_t stamp = stamp_base_;
     while (p.N) {
         mark(0);
         CK(cudaMemsetAsync(&p.flags->active_count, 0, sizeof(unsigned), s));
@@ -414,44 +422,73 @@ template <class M> void Session::run(ocm_solution* out, std::uint32_t* cycle_buf
         launch_improve<EXACT>(p, d.sms, s, avg_deg);
         CK(cudaEventRecord(d.event(2 * passes + 1), s));
         ++passes;
-        k_region_check<<<gr, 256, 0, s>>>(p);
+        k_region_check<<<gr, kBlock, 0, s>>>(p);
         launches += 2;
         read_flags();
         if (hf.active_count == 0)
             break;
         ++outer;
-        const std::uint32_t stamp = outer;
 
-        // cycles of the policy graph
+        // cycles of the policy graph: double until the exact check passes
         mark(1);
-        k_pj_init<<<gv, 256, 0, s>>>(p);
+        k_pj_init<EXACT><<<gv, kBlock, 0, s>>>(p);
         ++launches;
-        int in = 0;
-        for (int k = 0; k < K; ++k, in ^= 1) {
-            k_pj_round<<<gv, 256, 0, s>>>(p, in);
-            ++launches;
+        int in = 0, k = 0;
+        for (;;) {
+            for (; k < k_need; ++k, in ^= 1) {
+                k_pj_round<<<gv, kBlock, 0, s>>>(p, in);
+                ++launches;
+                ++fix_iters;
+            }
+            ++stamp;
+            CK(cudaMemsetAsync(&p.flags->verify_fail, 0, sizeof(int), s));
+            k_cycle_mark<<<gv, kBlock, 0, s>>>(p, in, stamp);
+            k_cycle_verify1<<<gv, kBlock, 0, s>>>(p, stamp);
+            k_cycle_verify2<<<gv, kBlock, 0, s>>>(p, stamp);
+            launches += 3;
+            read_flags();
+            if (!hf.verify_fail)
+                break;
+            if (k >= K_max)
+                throw std::logic_error("cycle detection did not converge within log2(n) rounds");
+            k_need = k + 1;
         }
-        fix_iters += K;
+        k_hint_ = k;
+
         mark(2);
-        k_cycle_mark<<<gv, 256, 0, s>>>(p, in, stamp);
+        CK(cudaMemsetAsync(&p.flags->max_cycle, 0, 2 * sizeof(unsigned), s)); // + wc_count
         if constexpr (EXACT)
-            k_cycle_stats<<<gv, 256, 0, s>>>(p, stamp);
+            k_cycle_stats<<<gv, kBlock, 0, s>>>(p, stamp);
         else
-            k_cycle_walk_float<<<gv, 256, 0, s>>>(p);
-        k_vote<EXACT><<<gv, 256, 0, s>>>(p);
-        k_adopt<EXACT><<<gr, 256, 0, s>>>(p);
+            k_cycle_walk_float<<<gv, kBlock, 0, s>>>(p);
+        k_vote<EXACT><<<gv, kBlock, 0, s>>>(p);
+        k_adopt<EXACT><<<gr, kBlock, 0, s>>>(p);
+        launches += 3;
+        if constexpr (EXACT) {
+            // values of the winning cycle(s): prefix sums cut at the anchor
+            k_wincyc_init<<<gv, kBlock, 0, s>>>(p, stamp);
+            read_flags();
+            const int rounds = std::min(kMaxRounds, ceil_log2(std::max(hf.max_cycle, 2u)) + 1);
+            CK(cudaMemsetAsync(p.flags->notdone, 0, rounds * sizeof(unsigned), s));
+            const int gw = grid_for(hf.wc_count, d.sms);
+            for (int j = 0; j < rounds; ++j)
+                k_wincyc_round<<<gw, kBlock, 0, s>>>(p, j);
+            k_wincyc_final<<<gw, kBlock, 0, s>>>(p, rounds);
+            launches += 2 + rounds;
+            fix_iters += rounds;
+        }
         CK(cudaMemsetAsync(&p.flags->rem_count[0], 0, sizeof(unsigned), s));
-        k_keep<<<gv, 256, 0, s>>>(p);
-        launches += 5;
+        k_keep<EXACT><<<gv, kBlock, 0, s>>>(p, in, stamp, 1ull << k);
+        ++launches;
         read_flags();
 
-        // breadth-layered re-attachment
+        // breadth-layered re-attachment (+ values of re-attached vertices)
         mark(3);
         unsigned pending = hf.rem_count[0];
         int cur = 0;
         for (std::uint32_t layer = 1; pending > 0; ++layer) {
             CK(cudaMemsetAsync(&p.flags->rem_count[cur ^ 1], 0, sizeof(unsigned), s));
-            k_attach<EXACT><<<grid_for(pending, d.sms), 256, 0, s>>>(p, cur, pending, layer);
+            k_attach<EXACT><<<grid_for(pending, d.sms), kBlock, 0, s>>>(p, cur, pending, layer);
             ++launches;
             ++fix_iters;
             read_flags();
@@ -463,22 +500,14 @@ template <class M> void Session::run(ocm_solution* out, std::uint32_t* cycle_buf
             ++layers_total;
         }
 
-        // value determination
+        // float mode: level-synchronous value propagation (bit-exact order)
         mark(4);
-        if constexpr (EXACT) {
-            CK(cudaMemsetAsync(p.flags->notdone, 0, sizeof(hf.notdone), s));
-            k_prop_init<<<gv, 256, 0, s>>>(p);
-            for (int j = 0; j < prop_rounds; ++j)
-                k_prop_round<<<gv, 256, 0, s>>>(p, j);
-            k_prop_final<<<gv, 256, 0, s>>>(p, prop_rounds);
-            launches += 2 + prop_rounds;
-            fix_iters += prop_rounds;
-        } else {
-            k_fprop_init<<<gv, 256, 0, s>>>(p);
+        if constexpr (!EXACT) {
+            k_fprop_init<<<gv, kBlock, 0, s>>>(p);
             ++launches;
             for (std::uint32_t level = 1;; ++level) {
                 CK(cudaMemsetAsync(&p.flags->notdone[0], 0, sizeof(unsigned), s));
-                k_fprop_round<<<gv, 256, 0, s>>>(p, level, 0);
+                k_fprop_round<<<gv, kBlock, 0, s>>>(p, level, 0);
                 ++launches;
                 ++fix_iters;
                 read_flags();
@@ -489,6 +518,7 @@ template <class M> void Session::run(ocm_solution* out, std::uint32_t* cycle_buf
             }
         }
     }
+    stamp_base_ = stamp;
     mark(5);
     CK(cudaEventRecord(d.ev_end, s));
     CK(cudaStreamSynchronize(s));

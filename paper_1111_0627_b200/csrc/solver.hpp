@@ -58,6 +58,8 @@ class Session {
     std::uint64_t h2d_bytes_ = 0;
     std::unique_ptr<DeviceState> d_;
     bool solved_ = false;
+    int k_hint_ = 8;               // doubling rounds needed last iteration
+    std::uint32_t stamp_base_ = 0; // mark stamps stay unique across solves
 };
 
 } // namespace ocmb
