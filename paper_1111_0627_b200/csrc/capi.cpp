@@ -16,6 +16,39 @@
 
 struct ocm_graph {
     ocmb::Graph g;
+    // Host arrays are page-locked on first device use (one registration per
+    // graph, released with the graph) so every later upload is a pinned copy.
+    bool pinned = false;
+    void pin() {
+        if (pinned)
+            return;
+        auto reg = [](const void* p, std::size_t bytes) {
+            return bytes == 0 || cudaHostRegister(const_cast<void*>(p), bytes,
+                                                   cudaHostRegisterPortable) == cudaSuccess;
+        };
+        const bool ok = reg(g.fwd_index.data(), g.fwd_index.size() * sizeof(std::uint64_t)) &&
+                        reg(g.fwd_target.data(), g.fwd_target.size() * sizeof(std::uint32_t)) &&
+                        reg(g.fwd_weight.data(), g.fwd_weight.size() * sizeof(double));
+        if (!ok) {
+            unpin();
+            cudaGetLastError();
+            return;
+        }
+        pinned = true;
+    }
+    void unpin() {
+        for (const void* p : {static_cast<const void*>(g.fwd_index.data()),
+                              static_cast<const void*>(g.fwd_target.data()),
+                              static_cast<const void*>(g.fwd_weight.data())})
+            if (p)
+                cudaHostUnregister(const_cast<void*>(p));
+        cudaGetLastError();
+        pinned = false;
+    }
+    ~ocm_graph() {
+        if (pinned)
+            unpin();
+    }
 };
 struct ocm_session {
     std::unique_ptr<ocmb::Session> s;
@@ -137,6 +170,7 @@ int ocm_session_create(const ocm_graph* g, const ocm_solve_options* opt, ocm_ses
     return guard([&] {
         if (!g)
             throw std::invalid_argument("null graph");
+        const_cast<ocm_graph*>(g)->pin();
         auto s = std::make_unique<ocm_session>();
         s->s = std::make_unique<ocmb::Session>(g->g, defaults(opt));
         *out = s.release();
@@ -165,6 +199,7 @@ int ocm_solve(const ocm_graph* g, const ocm_solve_options* opt, ocm_solution* ou
         out->mu_den = 1;
         if (g->g.n == 0)
             return; // solve.cpp:199: an empty graph has no cycle
+        const_cast<ocm_graph*>(g)->pin();
         ocmb::Session sess(g->g, defaults(opt));
         sess.solve(out, cycle_buf, cycle_cap);
     });

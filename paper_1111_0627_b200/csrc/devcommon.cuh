@@ -1,0 +1,179 @@
+// Types and helpers shared by the device translation units (solver.cu,
+// prep.cu). Kernels themselves stay TU-local.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "errors.hpp"
+#include "prepinfo.hpp"
+
+#define CK(x)                                                                                  \
+    do {                                                                                       \
+        cudaError_t e_ = (x);                                                                  \
+        if (e_ != cudaSuccess)                                                                 \
+            throw ::ocmb::CudaError(std::string(#x) + ": " + cudaGetErrorString(e_));          \
+    } while (0)
+
+namespace ocmb {
+
+constexpr std::uint32_t NONE = 0xffffffffu;
+constexpr unsigned long long EMPTY = ~0ull;
+constexpr unsigned FULL = 0xffffffffu;
+constexpr int kMaxRounds = 64;
+constexpr int kBlock = 256;
+
+struct __align__(16) FEdge {
+    double w;
+    std::uint32_t t;
+    std::uint32_t pad;
+};
+
+// Pointer-jumping record for value determination: accumulated key along the
+// jumped segment, the segment end, and the root (anchor) of the vertex.
+struct __align__(16) PJV {
+    long long acc;
+    std::uint32_t nxt;
+    std::uint32_t root;
+};
+
+// Pointer-doubling record for cycle detection: segment end, least vertex on
+// the segment, weight sum of the segment.
+struct __align__(16) PJC {
+    std::uint32_t nxt;
+    std::uint32_t mn;
+    long long w;
+};
+
+struct Flags {
+    unsigned active_count;
+    unsigned rem_count[2];
+    int error;     // structural (no successor / not strongly connected)
+    int overflow;  // exact keys would leave int64
+    int lambda_up; // lambda increased inside a region
+    int verify_fail;    // cycle-detection round count too small
+    unsigned max_cycle; // longest winning cycle this iteration
+    unsigned wc_count;  // winning-cycle vertices listed
+    unsigned notdone[kMaxRounds];
+};
+
+// Everything a kernel may touch, passed by value.
+struct KP {
+    std::uint32_t N, R;
+    const std::uint32_t* row;
+    const int2* ew;  // exact: {target, weight}
+    const FEdge* fe; // float
+    const std::uint32_t* reg;
+    std::uint32_t* succ_e;
+    std::uint32_t* succ_v;
+    int* succ_wi;
+    double* succ_wf;
+    long long* key_i;
+    double* key_f;
+    long long* lam_num;
+    long long* lam_den;
+    double* lam_f;
+    int* active;
+    int* changed;
+    unsigned long long* slot;
+    std::uint32_t* src;
+    std::uint32_t* iters;
+    PJC* pj[2];
+    std::uint32_t* comp;
+    std::uint32_t* mark;
+    std::uint32_t* mark2;
+    std::uint32_t* wlist;
+    std::uint32_t* cyc_len;
+    long long* cyc_wi;
+    double* cyc_wf;
+    std::uint32_t* conn;
+    std::uint32_t* rem[2];
+    PJV* pv[2];
+    Flags* flags;
+    std::uint32_t max_region;
+    long long max_abs_w;
+};
+
+
+template <class T> struct DBuf {
+    T* p = nullptr;
+    std::size_t n = 0;
+    DBuf() = default;
+    DBuf(const DBuf&) = delete;
+    DBuf& operator=(const DBuf&) = delete;
+    void alloc(std::size_t k) {
+        release();
+        if (k)
+            CK(cudaMalloc(&p, k * sizeof(T)));
+        n = k;
+    }
+    void release() {
+        if (p)
+            cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    ~DBuf() { release(); }
+};
+
+inline int grid_for(std::size_t work, int sms, int per_sm = 8) {
+    const std::size_t blocks = (work + kBlock - 1) / kBlock;
+    const std::size_t cap = std::size_t(sms) * per_sm;
+    return static_cast<int>(blocks < 1 ? 1 : (blocks > cap ? cap : blocks));
+}
+
+inline int ceil_log2(std::uint64_t x) {
+    int k = 0;
+    while ((1ull << k) < x)
+        ++k;
+    return k;
+}
+
+// Device state of a session: the prepared graph plus solver scratch.
+struct DeviceState {
+    int device = 0;
+    int sms = 148;
+    cudaStream_t stream = nullptr;
+    DBuf<std::uint32_t> row, reg, succ_e, succ_v, comp, mark, mark2, wlist, cyc_len, conn, rem0,
+        rem1, src, iters;
+    DBuf<PJV> pv0, pv1;
+    DBuf<PJC> pj0, pj1;
+    DBuf<int2> ew;
+    DBuf<FEdge> fe;
+    DBuf<int> succ_wi, active, changed;
+    DBuf<double> succ_wf, key_f, lam_f, cyc_wf;
+    DBuf<long long> key_i, lam_num, lam_den, cyc_wi;
+    DBuf<unsigned long long> slot;
+    DBuf<Flags> flags;
+    Flags* h_flags = nullptr;
+    std::vector<cudaEvent_t> ev;
+    cudaEvent_t ev_start = nullptr, ev_end = nullptr;
+    KP kp{};
+
+    ~DeviceState() {
+        for (cudaEvent_t e : ev)
+            cudaEventDestroy(e);
+        if (ev_start)
+            cudaEventDestroy(ev_start);
+        if (ev_end)
+            cudaEventDestroy(ev_end);
+        if (h_flags)
+            cudaFreeHost(h_flags);
+        if (stream)
+            cudaStreamDestroy(stream);
+    }
+    cudaEvent_t event(std::size_t i) {
+        while (ev.size() <= i) {
+            cudaEvent_t e;
+            CK(cudaEventCreate(&e));
+            ev.push_back(e);
+        }
+        return ev[i];
+    }
+};
+
+} // namespace ocmb

@@ -51,15 +51,4 @@ Graph read_graph_file(const std::string& path);
 // Edge list in CSR order (fwd_source implied by fwd_index).
 void graph_edges(const Graph& g, Vertex* src, Vertex* dst, double* w);
 
-// Sequential strongly connected components (iterative low-link search from
-// vertex 0 upward, ids in completion order). Returns the region count.
-std::uint32_t tarjan_regions(const Graph& g, std::vector<std::uint32_t>& region_of);
-
-bool has_self_loop(const Graph& g, Vertex v);
-
-// proj/include/ocm/graph.hpp:100 augment_hamiltonian: appends v -> v+1 mod n
-// with weight 2n(max|w|+1)+1 (or big_w when nonzero). Returns the graph and
-// the no-cycle bound max|w|.
-Graph augment_hamiltonian(const Graph& g, double big_w, double* no_cycle_above);
-
 } // namespace ocmb

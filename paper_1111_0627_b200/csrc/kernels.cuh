@@ -33,85 +33,10 @@
 
 #include <cstdint>
 
+#include "devcommon.cuh"
+
 namespace ocmb {
 namespace {
-
-constexpr std::uint32_t NONE = 0xffffffffu;
-constexpr unsigned long long EMPTY = ~0ull;
-constexpr unsigned FULL = 0xffffffffu;
-constexpr int kMaxRounds = 64;
-constexpr int kBlock = 256;
-
-struct __align__(16) FEdge {
-    double w;
-    std::uint32_t t;
-    std::uint32_t pad;
-};
-
-// Pointer-jumping record for value determination: accumulated key along the
-// jumped segment, the segment end, and the root (anchor) of the vertex.
-struct __align__(16) PJV {
-    long long acc;
-    std::uint32_t nxt;
-    std::uint32_t root;
-};
-
-// Pointer-doubling record for cycle detection: segment end, least vertex on
-// the segment, weight sum of the segment.
-struct __align__(16) PJC {
-    std::uint32_t nxt;
-    std::uint32_t mn;
-    long long w;
-};
-
-struct Flags {
-    unsigned active_count;
-    unsigned rem_count[2];
-    int error;     // structural (no successor / not strongly connected)
-    int overflow;  // exact keys would leave int64
-    int lambda_up; // lambda increased inside a region
-    int verify_fail;    // cycle-detection round count too small
-    unsigned max_cycle; // longest winning cycle this iteration
-    unsigned wc_count;  // winning-cycle vertices listed
-    unsigned notdone[kMaxRounds];
-};
-
-// Everything a kernel may touch, passed by value.
-struct KP {
-    std::uint32_t N, R;
-    const std::uint32_t* row;
-    const int2* ew;  // exact: {target, weight}
-    const FEdge* fe; // float
-    const std::uint32_t* reg;
-    std::uint32_t* succ_e;
-    std::uint32_t* succ_v;
-    int* succ_wi;
-    double* succ_wf;
-    long long* key_i;
-    double* key_f;
-    long long* lam_num;
-    long long* lam_den;
-    double* lam_f;
-    int* active;
-    int* changed;
-    unsigned long long* slot;
-    std::uint32_t* src;
-    std::uint32_t* iters;
-    PJC* pj[2];
-    std::uint32_t* comp;
-    std::uint32_t* mark;
-    std::uint32_t* mark2;
-    std::uint32_t* wlist;
-    std::uint32_t* cyc_len;
-    long long* cyc_wi;
-    double* cyc_wf;
-    std::uint32_t* conn;
-    std::uint32_t* rem[2];
-    PJV* pv[2];
-    Flags* flags;
-    std::uint32_t max_region;
-    long long max_abs_w;
-};
 
 __device__ __forceinline__ bool working(const KP& p, std::uint32_t v) {
     return p.active[p.reg[v]] != 0;
@@ -171,11 +96,11 @@ __global__ void k_init(KP p) {
         p.mark[v] = 0;
         p.mark2[v] = 0;
     }
-    for (std::size_t r = gtid(); r < p.R; r += gstride()) {
+    for (std::size_t r = gtid(); r <= p.R; r += gstride()) { // slot R: trivial vertices
         p.lam_num[r] = 0;
         p.lam_den[r] = 1;
         p.lam_f[r] = 0.0;
-        p.active[r] = 1;
+        p.active[r] = r < p.R ? 1 : 0;
         p.changed[r] = 0;
         p.slot[r] = EMPTY;
         p.src[r] = NONE;
@@ -384,7 +309,8 @@ __global__ void k_region_check(KP p) {
 template <bool EXACT> __global__ void k_pj_init(KP p) {
     for (std::size_t v = gtid(); v < p.N; v += gstride()) {
         PJC x;
-        x.nxt = p.succ_v[v];
+        const std::uint32_t sv = p.succ_v[v];
+        x.nxt = sv == NONE ? static_cast<std::uint32_t>(v) : sv; // trivial vertices: self
         x.mn = static_cast<std::uint32_t>(v);
         x.w = EXACT ? static_cast<long long>(p.succ_wi[v]) : 0ll;
         p.pj[0][v] = x;

@@ -1,0 +1,668 @@
+// Device-side preparation: upload the host CSR once, split it into solver
+// regions (strongly connected components, proj/src/scc.cpp), drop trivial
+// regions and cross-region edges, and pack the intra-region CSR the solver
+// streams every policy iteration.
+//
+// SCC on the device (the reference's --scc parallel lane, scc.cpp:105, does
+// the same decomposition with trim + pivoted forward/backward reachability on
+// its CPU engine; any correct partition gives the same solver result):
+//   1. queue-based trimming of vertices with no in- or out-neighbour
+//      (self-loops ignored) -- each is its own singleton component;
+//   2. forward/backward BFS from the max-degree pivot: the intersection is
+//      the pivot's component (the giant one on the benchmark graphs);
+//   3. whatever remains is finished by max-label colouring: labels flow
+//      forward to a fixpoint, each colour's root collects its component by a
+//      backward closure inside the colour, repeat (re-trimming first).
+// Vertices keep their original ids; trivial vertices get region R (never
+// active) and empty intra-region edge lists.
+
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "../../include/ocm_b200.h"
+#include "devcommon.cuh"
+#include "graph.hpp"
+
+namespace ocmb {
+
+void device_prepare(const Graph& g, const ocm_solve_options& opt, DeviceState& d, PrepInfo& info);
+
+namespace {
+
+__device__ __forceinline__ std::size_t tid_() {
+    return blockIdx.x * std::size_t(blockDim.x) + threadIdx.x;
+}
+__device__ __forceinline__ std::size_t stride_() { return std::size_t(gridDim.x) * blockDim.x; }
+
+__device__ __forceinline__ unsigned append_block(bool take, unsigned* counter) {
+    __shared__ unsigned s_cnt[kBlock / 32];
+    __shared__ unsigned s_base;
+    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const unsigned bal = __ballot_sync(FULL, take);
+    if (lane == 0)
+        s_cnt[warp] = __popc(bal);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned tot = 0;
+        for (unsigned w = 0; w < blockDim.x / 32; ++w) {
+            const unsigned c = s_cnt[w];
+            s_cnt[w] = tot;
+            tot += c;
+        }
+        s_base = tot ? atomicAdd(counter, tot) : 0u;
+    }
+    __syncthreads();
+    const unsigned slot = s_base + s_cnt[warp] + __popc(bal & ((1u << lane) - 1u));
+    __syncthreads();
+    return slot;
+}
+
+struct PrepCounters {
+    unsigned q[2];       // frontier sizes
+    unsigned remaining;  // unassigned vertices
+    int changed;
+    int bad_weight;      // exact weight outside int32
+    unsigned long long max_abs_bits; // max |w| as double bits
+    unsigned long long pivot;        // (score << 32) | ~v
+    unsigned max_region;
+    unsigned regions_total;
+    unsigned R;
+};
+
+__global__ void kp_row32(const std::uint64_t* r64, std::uint32_t* r32, std::size_t n1) {
+    for (std::size_t i = tid_(); i < n1; i += stride_())
+        r32[i] = static_cast<std::uint32_t>(r64[i]);
+}
+
+// Out-degree / in-degree without self-loops, self-loop flags, max |w|.
+__global__ void kp_degrees(std::uint32_t n, const std::uint32_t* row, const std::uint32_t* tgt,
+                           const double* w, std::uint32_t* outd, std::uint32_t* ind,
+                           std::uint8_t* self, PrepCounters* pc) {
+    unsigned long long mx = 0;
+    for (std::size_t vv = tid_(); vv < n; vv += stride_()) {
+        const std::uint32_t v = static_cast<std::uint32_t>(vv);
+        std::uint32_t o = 0;
+        std::uint8_t s = 0;
+        for (std::uint32_t e = row[v]; e < row[v + 1]; ++e) {
+            const std::uint32_t t = tgt[e];
+            const double a = fabs(w[e]);
+            const unsigned long long bits = __double_as_longlong(a);
+            mx = bits > mx ? bits : mx;
+            if (t == v) {
+                s = 1;
+            } else {
+                ++o;
+                atomicAdd(&ind[t], 1u);
+            }
+        }
+        outd[v] = o;
+        self[v] = s;
+    }
+    if (mx)
+        atomicMax(&pc->max_abs_bits, mx);
+}
+
+// Backward CSR (no self-loops): bsrc grouped by target.
+__global__ void kp_bwd_fill(std::uint32_t n, const std::uint32_t* row, const std::uint32_t* tgt,
+                            std::uint32_t* cursor, std::uint32_t* bsrc) {
+    for (std::size_t vv = tid_(); vv < n; vv += stride_()) {
+        const std::uint32_t v = static_cast<std::uint32_t>(vv);
+        for (std::uint32_t e = row[v]; e < row[v + 1]; ++e) {
+            const std::uint32_t t = tgt[e];
+            if (t != v)
+                bsrc[atomicAdd(&cursor[t], 1u)] = v;
+        }
+    }
+}
+
+// Initial trim frontier among unassigned vertices: in- or out-degree 0.
+__global__ void kp_trim_seed(std::uint32_t n, const std::uint32_t* ind, const std::uint32_t* outd,
+                             std::uint32_t* lab, std::uint32_t* q, PrepCounters* pc) {
+    for (std::size_t base = blockIdx.x * std::size_t(kBlock); base < n;
+         base += gridDim.x * std::size_t(kBlock)) {
+        const std::size_t v = base + threadIdx.x;
+        bool take = false;
+        if (v < n && lab[v] == NONE && (ind[v] == 0 || outd[v] == 0)) {
+            lab[v] = static_cast<std::uint32_t>(v);
+            take = true;
+        }
+        const unsigned slot = append_block(take, &pc->q[0]);
+        if (take)
+            q[slot] = static_cast<std::uint32_t>(v);
+    }
+}
+
+// Process one trim frontier: each trimmed vertex removes its edges from the
+// neighbours' counters; a neighbour reaching zero is trimmed next.
+__global__ void kp_trim_step(const std::uint32_t* row, const std::uint32_t* tgt,
+                             const std::uint32_t* brow, const std::uint32_t* bsrc,
+                             std::uint32_t* ind, std::uint32_t* outd, std::uint32_t* lab,
+                             const std::uint32_t* qin, unsigned nin, std::uint32_t* qout,
+                             unsigned* qout_count) {
+    for (std::size_t i = tid_(); i < nin; i += stride_()) {
+        const std::uint32_t v = qin[i];
+        for (std::uint32_t e = row[v]; e < row[v + 1]; ++e) {
+            const std::uint32_t t = tgt[e];
+            if (t == v || lab[t] != NONE)
+                continue;
+            if (atomicSub(&ind[t], 1u) == 1u && atomicCAS(&lab[t], NONE, t) == NONE)
+                qout[atomicAdd(qout_count, 1u)] = t;
+        }
+        for (std::uint32_t s = brow[v]; s < brow[v + 1]; ++s) {
+            const std::uint32_t u = bsrc[s];
+            if (lab[u] != NONE)
+                continue;
+            if (atomicSub(&outd[u], 1u) == 1u && atomicCAS(&lab[u], NONE, u) == NONE)
+                qout[atomicAdd(qout_count, 1u)] = u;
+        }
+    }
+}
+
+// Recount degrees inside the unassigned subgraph (pull, no atomics).
+__global__ void kp_recount(std::uint32_t n, const std::uint32_t* row, const std::uint32_t* tgt,
+                           const std::uint32_t* brow, const std::uint32_t* bsrc,
+                           const std::uint32_t* lab, std::uint32_t* ind, std::uint32_t* outd,
+                           PrepCounters* pc) {
+    unsigned rem = 0;
+    for (std::size_t vv = tid_(); vv < n; vv += stride_()) {
+        const std::uint32_t v = static_cast<std::uint32_t>(vv);
+        if (lab[v] != NONE)
+            continue;
+        ++rem;
+        std::uint32_t o = 0, i = 0;
+        for (std::uint32_t e = row[v]; e < row[v + 1]; ++e) {
+            const std::uint32_t t = tgt[e];
+            o += (t != v && lab[t] == NONE);
+        }
+        for (std::uint32_t s = brow[v]; s < brow[v + 1]; ++s)
+            i += lab[bsrc[s]] == NONE;
+        outd[v] = o;
+        ind[v] = i;
+    }
+    rem = __reduce_add_sync(FULL, rem);
+    if ((threadIdx.x & 31) == 0 && rem)
+        atomicAdd(&pc->remaining, rem);
+}
+
+__global__ void kp_pick_pivot(std::uint32_t n, const std::uint32_t* lab, const std::uint32_t* ind,
+                              const std::uint32_t* outd, PrepCounters* pc) {
+    unsigned long long best = 0;
+    for (std::size_t vv = tid_(); vv < n; vv += stride_()) {
+        if (lab[vv] != NONE)
+            continue;
+        const unsigned long long score =
+            min(0xffffffffull, (1ull + ind[vv]) * (1ull + outd[vv]));
+        const unsigned long long key = (score << 32) | (0xffffffffull - vv);
+        best = key > best ? key : best;
+    }
+    if (best)
+        atomicMax(&pc->pivot, best);
+}
+
+// One BFS level restricted to unassigned vertices; vis[] holds the stamp.
+__global__ void kp_bfs_level(const std::uint32_t* row, const std::uint32_t* col,
+                             const std::uint32_t* lab, std::uint32_t* vis, std::uint32_t stamp,
+                             const std::uint32_t* qin, unsigned nin, std::uint32_t* qout,
+                             unsigned* qout_count) {
+    for (std::size_t i = tid_(); i < nin; i += stride_()) {
+        const std::uint32_t u = qin[i];
+        for (std::uint32_t e = row[u]; e < row[u + 1]; ++e) {
+            const std::uint32_t t = col[e];
+            if (lab[t] != NONE || vis[t] == stamp)
+                continue;
+            if (atomicExch(&vis[t], stamp) != stamp)
+                qout[atomicAdd(qout_count, 1u)] = t;
+        }
+    }
+}
+
+__global__ void kp_assign_both(std::uint32_t n, const std::uint32_t* visf, const std::uint32_t* visb,
+                               std::uint32_t sf, std::uint32_t sb, std::uint32_t pivot,
+                               std::uint32_t* lab) {
+    for (std::size_t v = tid_(); v < n; v += stride_())
+        if (lab[v] == NONE && visf[v] == sf && visb[v] == sb)
+            lab[v] = pivot;
+}
+
+// Colouring: colour = max id among vertices reaching v (in-place, pull).
+__global__ void kp_color_init(std::uint32_t n, const std::uint32_t* lab, std::uint32_t* color) {
+    for (std::size_t v = tid_(); v < n; v += stride_())
+        if (lab[v] == NONE)
+            color[v] = static_cast<std::uint32_t>(v);
+}
+
+__global__ void kp_color_prop(std::uint32_t n, const std::uint32_t* brow, const std::uint32_t* bsrc,
+                              const std::uint32_t* lab, std::uint32_t* color, PrepCounters* pc) {
+    bool ch = false;
+    for (std::size_t vv = tid_(); vv < n; vv += stride_()) {
+        if (lab[vv] != NONE)
+            continue;
+        std::uint32_t c = color[vv];
+        const std::uint32_t c0 = c;
+        for (std::uint32_t s = brow[vv]; s < brow[vv + 1]; ++s) {
+            const std::uint32_t u = bsrc[s];
+            if (lab[u] == NONE) {
+                const std::uint32_t cu = *(volatile std::uint32_t*)&color[u];
+                c = cu > c ? cu : c;
+            }
+        }
+        if (c != c0) {
+            color[vv] = c;
+            ch = true;
+        }
+    }
+    if (__syncthreads_or(ch) && threadIdx.x == 0)
+        pc->changed = 1;
+}
+
+// Backward closure inside each colour from its root (in-place, pull).
+__global__ void kp_color_roots(std::uint32_t n, const std::uint32_t* lab, const std::uint32_t* color,
+                               std::uint32_t* in_scc, std::uint32_t stamp) {
+    for (std::size_t v = tid_(); v < n; v += stride_())
+        if (lab[v] == NONE && color[v] == v)
+            in_scc[v] = stamp;
+}
+
+__global__ void kp_color_close(std::uint32_t n, const std::uint32_t* row, const std::uint32_t* tgt,
+                               const std::uint32_t* lab, const std::uint32_t* color,
+                               std::uint32_t* in_scc, std::uint32_t stamp, PrepCounters* pc) {
+    bool ch = false;
+    for (std::size_t vv = tid_(); vv < n; vv += stride_()) {
+        if (lab[vv] != NONE || in_scc[vv] == stamp)
+            continue;
+        const std::uint32_t c = color[vv];
+        for (std::uint32_t e = row[vv]; e < row[vv + 1]; ++e) {
+            const std::uint32_t t = tgt[e];
+            if (lab[t] == NONE && color[t] == c &&
+                *(volatile std::uint32_t*)&in_scc[t] == stamp) {
+                in_scc[vv] = stamp;
+                ch = true;
+                break;
+            }
+        }
+    }
+    if (__syncthreads_or(ch) && threadIdx.x == 0)
+        pc->changed = 1;
+}
+
+__global__ void kp_color_assign(std::uint32_t n, const std::uint32_t* color,
+                                const std::uint32_t* in_scc, std::uint32_t stamp,
+                                std::uint32_t* lab) {
+    for (std::size_t v = tid_(); v < n; v += stride_())
+        if (lab[v] == NONE && in_scc[v] == stamp)
+            lab[v] = color[v];
+}
+
+// Component sizes at the representatives (lab[r] == r).
+__global__ void kp_sizes(std::uint32_t n, const std::uint32_t* lab, std::uint32_t* size) {
+    for (std::size_t v = tid_(); v < n; v += stride_())
+        atomicAdd(&size[lab[v]], 1u);
+}
+
+__global__ void kp_nontrivial(std::uint32_t n, const std::uint32_t* lab, const std::uint32_t* size,
+                              const std::uint8_t* self, std::uint32_t* flag, PrepCounters* pc) {
+    unsigned mx = 0, reps = 0;
+    for (std::size_t v = tid_(); v < n; v += stride_()) {
+        std::uint32_t f = 0;
+        if (lab[v] == v) {
+            ++reps;
+            f = (size[v] > 1 || self[v]) ? 1u : 0u;
+            if (f)
+                mx = size[v] > mx ? size[v] : mx;
+        }
+        flag[v] = f;
+    }
+    reps = __reduce_add_sync(FULL, reps);
+    mx = __reduce_max_sync(FULL, mx);
+    if ((threadIdx.x & 31) == 0) {
+        if (reps)
+            atomicAdd(&pc->regions_total, reps);
+        if (mx)
+            atomicMax(&pc->max_region, mx);
+    }
+}
+
+__global__ void kp_region_ids(std::uint32_t n, const std::uint32_t* lab, const std::uint32_t* flag,
+                              const std::uint32_t* rid, std::uint32_t R, std::uint32_t* reg) {
+    for (std::size_t v = tid_(); v < n; v += stride_()) {
+        const std::uint32_t r = lab[v];
+        reg[v] = flag[r] ? rid[r] : R;
+    }
+}
+
+__global__ void kp_count_intra(std::uint32_t n, std::uint32_t R, const std::uint32_t* row,
+                               const std::uint32_t* tgt, const std::uint32_t* reg,
+                               std::uint32_t* cnt) {
+    for (std::size_t vv = tid_(); vv < n; vv += stride_()) {
+        const std::uint32_t v = static_cast<std::uint32_t>(vv);
+        const std::uint32_t r = reg[v];
+        std::uint32_t c = 0;
+        if (r != R)
+            for (std::uint32_t e = row[v]; e < row[v + 1]; ++e)
+                c += reg[tgt[e]] == r;
+        cnt[v] = c;
+    }
+}
+
+template <bool EXACT>
+__global__ void kp_pack(std::uint32_t n, std::uint32_t R, const std::uint32_t* row,
+                        const std::uint32_t* tgt, const double* w, const std::uint32_t* reg,
+                        const std::uint32_t* nrow, double sign, int2* ew, FEdge* fe,
+                        PrepCounters* pc) {
+    bool bad = false;
+    for (std::size_t vv = tid_(); vv < n; vv += stride_()) {
+        const std::uint32_t v = static_cast<std::uint32_t>(vv);
+        const std::uint32_t r = reg[v];
+        if (r == R)
+            continue;
+        std::uint32_t k = nrow[v];
+        for (std::uint32_t e = row[v]; e < row[v + 1]; ++e) {
+            const std::uint32_t t = tgt[e];
+            if (reg[t] != r)
+                continue;
+            const double x = sign * w[e];
+            if constexpr (EXACT) {
+                bad |= !(fabs(x) <= 2147483647.0);
+                ew[k] = make_int2(static_cast<int>(t), static_cast<int>(x));
+            } else {
+                fe[k] = FEdge{x, t, 0u};
+            }
+            ++k;
+        }
+    }
+    if (__syncthreads_or(bad) && threadIdx.x == 0)
+        pc->bad_weight = 1;
+}
+
+// Hamiltonian augmentation (graph.cpp:105) packed directly: vertex v keeps
+// its edges and gains v -> v+1 mod n with weight big_w (already in the
+// minimised orientation), appended last so edge order is preserved.
+template <bool EXACT>
+__global__ void kp_pack_hamiltonian(std::uint32_t n, const std::uint32_t* row,
+                                    const std::uint32_t* tgt, const double* w, double sign,
+                                    double big_w, int2* ew, FEdge* fe, std::uint32_t* nrow,
+                                    std::uint32_t* reg, PrepCounters* pc) {
+    bool bad = false;
+    for (std::size_t vv = tid_(); vv <= n; vv += stride_()) {
+        const std::uint32_t v = static_cast<std::uint32_t>(vv);
+        nrow[v] = row[v] + v;
+        if (v == n)
+            continue;
+        reg[v] = 0;
+        std::uint32_t k = row[v] + v;
+        for (std::uint32_t e = row[v]; e <= row[v + 1]; ++e) {
+            const bool extra = e == row[v + 1];
+            const std::uint32_t t = extra ? (v + 1) % n : tgt[e];
+            const double x = extra ? big_w : sign * w[e];
+            if constexpr (EXACT) {
+                bad |= !(fabs(x) <= 2147483647.0);
+                ew[k] = make_int2(static_cast<int>(t), static_cast<int>(x));
+            } else {
+                fe[k] = FEdge{x, t, 0u};
+            }
+            ++k;
+        }
+    }
+    if (__syncthreads_or(bad) && threadIdx.x == 0)
+        pc->bad_weight = 1;
+}
+
+template <class T> void exclusive_scan(const T* in, T* out, std::size_t n, cudaStream_t s) {
+    std::size_t bytes = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, n, s));
+    DBuf<unsigned char> tmp;
+    tmp.alloc(std::max<std::size_t>(bytes, 1));
+    CK(cub::DeviceScan::ExclusiveSum(tmp.p, bytes, in, out, n, s));
+    CK(cudaStreamSynchronize(s));
+}
+
+} // namespace
+
+void device_prepare(const Graph& g, const ocm_solve_options& opt, DeviceState& d, PrepInfo& info) {
+    cudaStream_t s = d.stream;
+    const std::uint32_t n = g.n;
+    const std::uint64_t m = g.m;
+    const int sms = d.sms;
+    info.n = n;
+    info.scc_off = opt.scc == OCM_SCC_OFF;
+    info.exact = g.integer_exact;
+    const double sign = opt.objective == OCM_MAXIMIZE ? -1.0 : 1.0;
+    const int gv = grid_for(n, sms);
+
+    // ---- upload (the host arrays are pinned once per graph by the C-ABI)
+    DBuf<std::uint64_t> row64;
+    DBuf<std::uint32_t> row, tgt;
+    DBuf<double> w;
+    row64.alloc(std::size_t(n) + 1);
+    row.alloc(std::size_t(n) + 1);
+    tgt.alloc(std::max<std::uint64_t>(m, 1));
+    w.alloc(std::max<std::uint64_t>(m, 1));
+    CK(cudaMemcpyAsync(row64.p, g.fwd_index.data(), (std::size_t(n) + 1) * 8, cudaMemcpyHostToDevice, s));
+    if (m) {
+        CK(cudaMemcpyAsync(tgt.p, g.fwd_target.data(), m * 4, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(w.p, g.fwd_weight.data(), m * 8, cudaMemcpyHostToDevice, s));
+    }
+    info.h2d_bytes = (std::size_t(n) + 1) * 8 + m * 12;
+    kp_row32<<<grid_for(n + 1, sms), kBlock, 0, s>>>(row64.p, row.p, std::size_t(n) + 1);
+    row64.release();
+
+    DBuf<PrepCounters> pcd;
+    pcd.alloc(1);
+    PrepCounters pc{};
+    CK(cudaMemsetAsync(pcd.p, 0, sizeof(PrepCounters), s));
+    DBuf<std::uint32_t> outd, ind;
+    DBuf<std::uint8_t> self;
+    outd.alloc(std::max<std::uint32_t>(n, 1));
+    ind.alloc(std::max<std::uint32_t>(n, 1));
+    self.alloc(std::max<std::uint32_t>(n, 1));
+    CK(cudaMemsetAsync(ind.p, 0, std::size_t(n) * 4, s));
+    kp_degrees<<<gv, kBlock, 0, s>>>(n, row.p, tgt.p, w.p, outd.p, ind.p, self.p, pcd.p);
+    auto read_pc = [&] {
+        CK(cudaMemcpyAsync(&pc, pcd.p, sizeof pc, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+    };
+    read_pc();
+    double max_abs;
+    {
+        unsigned long long bits = pc.max_abs_bits;
+        std::memcpy(&max_abs, &bits, sizeof max_abs);
+    }
+
+    d.reg.alloc(std::max<std::uint32_t>(n, 1));
+    d.row.alloc(std::size_t(n) + 1 + (info.scc_off ? 0 : 0));
+
+    if (info.scc_off) {
+        // ---- single region: the Hamiltonian-augmented graph (solve.cpp:53)
+        const double big_w = 2.0 * double(n) * (max_abs + 1.0) + 1.0;
+        if (!std::isfinite(big_w) || big_w >= 9007199254740992.0)
+            throw std::overflow_error("hamiltonian weight too large to stay exact");
+        info.no_cycle_above = max_abs;
+        info.R = 1;
+        info.regions_total = 1;
+        info.trivial = 0;
+        info.max_region = n;
+        info.M = m + n;
+        if (info.M >= 0xffffffffull)
+            throw UnsupportedError("more than 2^32-1 edges after augmentation");
+        if (info.exact)
+            d.ew.alloc(info.M);
+        else
+            d.fe.alloc(info.M);
+        if (info.exact)
+            kp_pack_hamiltonian<true><<<grid_for(n + 1, sms), kBlock, 0, s>>>(
+                n, row.p, tgt.p, w.p, sign, big_w, d.ew.p, nullptr, d.row.p, d.reg.p, pcd.p);
+        else
+            kp_pack_hamiltonian<false><<<grid_for(n + 1, sms), kBlock, 0, s>>>(
+                n, row.p, tgt.p, w.p, sign, big_w, nullptr, d.fe.p, d.row.p, d.reg.p, pcd.p);
+        info.max_abs_w = static_cast<long long>(std::max(max_abs, big_w));
+        read_pc();
+        if (info.exact && pc.bad_weight)
+            throw UnsupportedError("integer weights beyond 32 bits are not supported by the device lane");
+        return;
+    }
+
+    // ---- backward CSR (no self-loops)
+    const auto t_scc = std::chrono::steady_clock::now();
+    DBuf<std::uint32_t> brow, bsrc, cursor;
+    brow.alloc(std::size_t(n) + 1);
+    CK(cudaMemsetAsync(brow.p + n, 0, 4, s));
+    // brow[0..n] = exclusive scan of ind (ind[n] treated as 0 via n+1 scan)
+    {
+        DBuf<std::uint32_t> ind1;
+        ind1.alloc(std::size_t(n) + 1);
+        CK(cudaMemsetAsync(ind1.p + n, 0, 4, s));
+        CK(cudaMemcpyAsync(ind1.p, ind.p, std::size_t(n) * 4, cudaMemcpyDeviceToDevice, s));
+        exclusive_scan(ind1.p, brow.p, std::size_t(n) + 1, s);
+    }
+    std::uint32_t mb = 0;
+    CK(cudaMemcpy(&mb, brow.p + n, 4, cudaMemcpyDeviceToHost));
+    bsrc.alloc(std::max<std::uint32_t>(mb, 1));
+    cursor.alloc(std::max<std::uint32_t>(n, 1));
+    CK(cudaMemcpyAsync(cursor.p, brow.p, std::size_t(n) * 4, cudaMemcpyDeviceToDevice, s));
+    kp_bwd_fill<<<gv, kBlock, 0, s>>>(n, row.p, tgt.p, cursor.p, bsrc.p);
+    cursor.release();
+
+    // ---- SCC
+    DBuf<std::uint32_t> lab, q0, q1, visf, visb, aux;
+    lab.alloc(std::max<std::uint32_t>(n, 1));
+    q0.alloc(std::max<std::uint32_t>(n, 1));
+    q1.alloc(std::max<std::uint32_t>(n, 1));
+    visf.alloc(std::max<std::uint32_t>(n, 1));
+    visb.alloc(std::max<std::uint32_t>(n, 1));
+    CK(cudaMemsetAsync(lab.p, 0xff, std::size_t(n) * 4, s));
+    CK(cudaMemsetAsync(visf.p, 0, std::size_t(n) * 4, s));
+    CK(cudaMemsetAsync(visb.p, 0, std::size_t(n) * 4, s));
+    std::uint32_t stamp = 0;
+    DBuf<std::uint32_t>* qs[2] = {&q0, &q1};
+
+    auto trim = [&] {
+        CK(cudaMemsetAsync(&pcd.p->q[0], 0, 8, s));
+        kp_trim_seed<<<gv, kBlock, 0, s>>>(n, ind.p, outd.p, lab.p, q0.p, pcd.p);
+        read_pc();
+        unsigned cnt = pc.q[0];
+        int cur = 0;
+        while (cnt) {
+            CK(cudaMemsetAsync(&pcd.p->q[cur ^ 1], 0, 4, s));
+            kp_trim_step<<<grid_for(cnt, sms), kBlock, 0, s>>>(
+                row.p, tgt.p, brow.p, bsrc.p, ind.p, outd.p, lab.p, qs[cur]->p, cnt,
+                qs[cur ^ 1]->p, &pcd.p->q[cur ^ 1]);
+            read_pc();
+            cnt = pc.q[cur ^ 1];
+            cur ^= 1;
+        }
+    };
+    auto remaining = [&] {
+        CK(cudaMemsetAsync(&pcd.p->remaining, 0, 4, s));
+        kp_recount<<<gv, kBlock, 0, s>>>(n, row.p, tgt.p, brow.p, bsrc.p, lab.p, ind.p, outd.p, pcd.p);
+        read_pc();
+        return pc.remaining;
+    };
+    auto bfs = [&](const std::uint32_t* r, const std::uint32_t* c, std::uint32_t* vis,
+                   std::uint32_t st, std::uint32_t start) {
+        CK(cudaMemcpyAsync(q0.p, &start, 4, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(vis + start, &st, 4, cudaMemcpyHostToDevice, s));
+        unsigned cnt = 1;
+        int cur = 0;
+        while (cnt) {
+            CK(cudaMemsetAsync(&pcd.p->q[cur ^ 1], 0, 4, s));
+            kp_bfs_level<<<grid_for(cnt, sms), kBlock, 0, s>>>(r, c, lab.p, vis, st, qs[cur]->p,
+                                                               cnt, qs[cur ^ 1]->p,
+                                                               &pcd.p->q[cur ^ 1]);
+            read_pc();
+            cnt = pc.q[cur ^ 1];
+            cur ^= 1;
+        }
+    };
+
+    trim();
+    if (remaining()) {
+        // forward/backward reachability from the best-connected pivot
+        CK(cudaMemsetAsync(&pcd.p->pivot, 0, 8, s));
+        kp_pick_pivot<<<gv, kBlock, 0, s>>>(n, lab.p, ind.p, outd.p, pcd.p);
+        read_pc();
+        const std::uint32_t pivot = 0xffffffffu - static_cast<std::uint32_t>(pc.pivot & 0xffffffffull);
+        const std::uint32_t sf = ++stamp, sb = ++stamp;
+        bfs(row.p, tgt.p, visf.p, sf, pivot);
+        bfs(brow.p, bsrc.p, visb.p, sb, pivot);
+        kp_assign_both<<<gv, kBlock, 0, s>>>(n, visf.p, visb.p, sf, sb, pivot, lab.p);
+        // finish the rest by colouring, re-trimming between rounds
+        for (;;) {
+            if (!remaining())
+                break;
+            trim();
+            if (!remaining())
+                break;
+            aux.alloc(std::max<std::uint32_t>(n, 1)); // colours
+            kp_color_init<<<gv, kBlock, 0, s>>>(n, lab.p, aux.p);
+            do {
+                CK(cudaMemsetAsync(&pcd.p->changed, 0, 4, s));
+                kp_color_prop<<<gv, kBlock, 0, s>>>(n, brow.p, bsrc.p, lab.p, aux.p, pcd.p);
+                read_pc();
+            } while (pc.changed);
+            const std::uint32_t sc = ++stamp;
+            kp_color_roots<<<gv, kBlock, 0, s>>>(n, lab.p, aux.p, visf.p, sc);
+            do {
+                CK(cudaMemsetAsync(&pcd.p->changed, 0, 4, s));
+                kp_color_close<<<gv, kBlock, 0, s>>>(n, row.p, tgt.p, lab.p, aux.p, visf.p, sc, pcd.p);
+                read_pc();
+            } while (pc.changed);
+            kp_color_assign<<<gv, kBlock, 0, s>>>(n, aux.p, visf.p, sc, lab.p);
+        }
+    }
+    brow.release();
+    bsrc.release();
+    q0.release();
+    q1.release();
+    visb.release();
+
+    // ---- regions: sizes, non-trivial flags, dense ids
+    DBuf<std::uint32_t>& size = visf; // reuse
+    CK(cudaMemsetAsync(size.p, 0, std::size_t(n) * 4, s));
+    kp_sizes<<<gv, kBlock, 0, s>>>(n, lab.p, size.p);
+    DBuf<std::uint32_t> flag, rid;
+    flag.alloc(std::size_t(n) + 1);
+    rid.alloc(std::size_t(n) + 1);
+    CK(cudaMemsetAsync(flag.p + n, 0, 4, s));
+    kp_nontrivial<<<gv, kBlock, 0, s>>>(n, lab.p, size.p, self.p, flag.p, pcd.p);
+    exclusive_scan(flag.p, rid.p, std::size_t(n) + 1, s);
+    std::uint32_t R = 0;
+    CK(cudaMemcpy(&R, rid.p + n, 4, cudaMemcpyDeviceToHost));
+    read_pc();
+    info.R = R;
+    info.regions_total = pc.regions_total;
+    info.trivial = pc.regions_total - R;
+    info.max_region = pc.max_region;
+    kp_region_ids<<<gv, kBlock, 0, s>>>(n, lab.p, flag.p, rid.p, R, d.reg.p);
+    info.scc_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_scc).count();
+
+    // ---- intra-region CSR
+    DBuf<std::uint32_t>& cnt = rid; // reuse (n+1)
+    kp_count_intra<<<gv, kBlock, 0, s>>>(n, R, row.p, tgt.p, d.reg.p, cnt.p);
+    CK(cudaMemsetAsync(cnt.p + n, 0, 4, s));
+    exclusive_scan(cnt.p, d.row.p, std::size_t(n) + 1, s);
+    std::uint32_t M = 0;
+    CK(cudaMemcpy(&M, d.row.p + n, 4, cudaMemcpyDeviceToHost));
+    info.M = M;
+    if (info.exact)
+        d.ew.alloc(std::max<std::uint32_t>(M, 1));
+    else
+        d.fe.alloc(std::max<std::uint32_t>(M, 1));
+    CK(cudaMemsetAsync(&pcd.p->bad_weight, 0, 4, s));
+    if (info.exact)
+        kp_pack<true><<<gv, kBlock, 0, s>>>(n, R, row.p, tgt.p, w.p, d.reg.p, d.row.p, sign, d.ew.p,
+                                            nullptr, pcd.p);
+    else
+        kp_pack<false><<<gv, kBlock, 0, s>>>(n, R, row.p, tgt.p, w.p, d.reg.p, d.row.p, sign,
+                                             nullptr, d.fe.p, pcd.p);
+    read_pc();
+    if (info.exact && pc.bad_weight)
+        throw UnsupportedError("integer weights beyond 32 bits are not supported by the device lane");
+    info.max_abs_w = static_cast<long long>(max_abs);
+}
+
+} // namespace ocmb

@@ -19,207 +19,7 @@
 
 namespace ocmb {
 
-namespace {
-
-#define CK(x)                                                                                  \
-    do {                                                                                       \
-        cudaError_t e_ = (x);                                                                  \
-        if (e_ != cudaSuccess)                                                                 \
-            throw CudaError(std::string(#x) + ": " + cudaGetErrorString(e_));                  \
-    } while (0)
-
-template <class T> struct DBuf {
-    T* p = nullptr;
-    std::size_t n = 0;
-    void alloc(std::size_t k) {
-        release();
-        if (k)
-            CK(cudaMalloc(&p, k * sizeof(T)));
-        n = k;
-    }
-    void release() {
-        if (p)
-            cudaFree(p);
-        p = nullptr;
-        n = 0;
-    }
-    ~DBuf() { release(); }
-};
-
-int grid_for(std::size_t work, int sms, int per_sm = 8) {
-    const std::size_t blocks = (work + 255) / 256;
-    return static_cast<int>(std::max<std::size_t>(1, std::min<std::size_t>(blocks, std::size_t(sms) * per_sm)));
-}
-
-int ceil_log2(std::uint64_t x) {
-    int k = 0;
-    while ((1ull << k) < x)
-        ++k;
-    return k;
-}
-
-} // namespace
-
-// ================================================================ state
-
-struct DeviceState {
-    int device = 0;
-    int sms = 148;
-    cudaStream_t stream = nullptr;
-    DBuf<std::uint32_t> row, reg, succ_e, succ_v, comp, mark, mark2, wlist, cyc_len, conn, rem0, rem1,
-        src, iters;
-    DBuf<PJV> pv0, pv1;
-    DBuf<PJC> pj0, pj1;
-    DBuf<int2> ew;
-    DBuf<FEdge> fe;
-    DBuf<int> succ_wi, active, changed;
-    DBuf<double> succ_wf, key_f, lam_f, cyc_wf;
-    DBuf<long long> key_i, lam_num, lam_den, cyc_wi;
-    DBuf<unsigned long long> slot;
-    DBuf<Flags> flags;
-    Flags* h_flags = nullptr;
-    std::vector<cudaEvent_t> ev;
-    cudaEvent_t ev_start = nullptr, ev_end = nullptr;
-    KP kp{};
-
-    ~DeviceState() {
-        for (cudaEvent_t e : ev)
-            cudaEventDestroy(e);
-        if (ev_start)
-            cudaEventDestroy(ev_start);
-        if (ev_end)
-            cudaEventDestroy(ev_end);
-        if (h_flags)
-            cudaFreeHost(h_flags);
-        if (stream)
-            cudaStreamDestroy(stream);
-    }
-    cudaEvent_t event(std::size_t i) {
-        while (ev.size() <= i) {
-            cudaEvent_t e;
-            CK(cudaEventCreate(&e));
-            ev.push_back(e);
-        }
-        return ev[i];
-    }
-};
-
-// ================================================================ host prep
-
-Prepared prepare(const Graph& g0, const ocm_solve_options& opt) {
-    Prepared pr;
-    pr.n_orig = g0.n;
-    pr.scc_off = opt.scc == OCM_SCC_OFF;
-    const double sign = opt.objective == OCM_MAXIMIZE ? -1.0 : 1.0;
-    Graph aug;
-    const Graph* gp = &g0;
-    if (pr.scc_off && g0.n > 0) {
-        // Augment the (sign-adjusted) graph: the reference negates before
-        // augmenting (solve.cpp:200-214), so big_w derives from |w| alike.
-        if (sign < 0) {
-            Graph neg = g0;
-            for (double& w : neg.fwd_weight)
-                w = -w;
-            aug = augment_hamiltonian(neg, 0.0, &pr.no_cycle_above);
-            for (double& w : aug.fwd_weight)
-                w = -w; // undone below by sign
-        } else {
-            aug = augment_hamiltonian(g0, 0.0, &pr.no_cycle_above);
-        }
-        gp = &aug;
-    }
-    const Graph& g = *gp;
-    pr.exact = g.integer_exact;
-    const std::uint32_t n = g.n;
-    std::vector<std::uint32_t> region_of;
-    std::vector<char> nontrivial;
-    std::uint32_t count = 0;
-    if (pr.scc_off) {
-        region_of.assign(n, 0);
-        count = n ? 1 : 0;
-        nontrivial.assign(count, 1);
-    } else {
-        count = tarjan_regions(g, region_of);
-        std::vector<std::uint32_t> size(count, 0);
-        for (std::uint32_t v = 0; v < n; ++v)
-            ++size[region_of[v]];
-        nontrivial.assign(count, 0);
-        for (std::uint32_t v = 0; v < n; ++v) {
-            const std::uint32_t r = region_of[v];
-            if (size[r] > 1 || has_self_loop(g, v))
-                nontrivial[r] = 1;
-        }
-    }
-    pr.regions_total = count;
-    // dense ids for non-trivial regions, in region id order
-    std::vector<std::uint32_t> rid(count, NONE);
-    for (std::uint32_t r = 0; r < count; ++r) {
-        if (nontrivial[r])
-            rid[r] = pr.R++;
-        else
-            ++pr.trivial;
-    }
-    std::vector<std::uint64_t> roff(static_cast<std::size_t>(pr.R) + 1, 0);
-    for (std::uint32_t v = 0; v < n; ++v)
-        if (rid[region_of[v]] != NONE)
-            ++roff[rid[region_of[v]] + 1];
-    for (std::uint32_t r = 0; r < pr.R; ++r) {
-        pr.max_region = std::max<std::uint32_t>(pr.max_region, static_cast<std::uint32_t>(roff[r + 1]));
-        roff[r + 1] += roff[r];
-    }
-    pr.N = static_cast<std::uint32_t>(roff[pr.R]);
-    pr.orig.resize(pr.N);
-    pr.reg.resize(pr.N);
-    std::vector<std::uint32_t> local(n, NONE);
-    {
-        std::vector<std::uint64_t> fill(roff.begin(), roff.end() - 1);
-        for (std::uint32_t v = 0; v < n; ++v) {
-            const std::uint32_t r = rid[region_of[v]];
-            if (r == NONE)
-                continue;
-            const std::uint64_t i = fill[r]++;
-            pr.orig[i] = v;
-            pr.reg[i] = r;
-            local[v] = static_cast<std::uint32_t>(i);
-        }
-    }
-    pr.row.assign(static_cast<std::size_t>(pr.N) + 1, 0);
-    std::uint64_t M = 0;
-    for (std::uint32_t i = 0; i < pr.N; ++i) {
-        const std::uint32_t v = pr.orig[i];
-        for (std::uint64_t e = g.fwd_index[v]; e < g.fwd_index[v + 1]; ++e)
-            if (region_of[g.fwd_target[e]] == region_of[v])
-                ++M;
-        if (M >= 0xffffffffull)
-            throw UnsupportedError("more than 2^32-1 intra-region edges");
-        pr.row[i + 1] = static_cast<std::uint32_t>(M);
-    }
-    pr.M = M;
-    pr.tgt.resize(M);
-    pr.w.resize(M);
-    double max_abs = 0.0;
-    std::uint64_t k = 0;
-    for (std::uint32_t i = 0; i < pr.N; ++i) {
-        const std::uint32_t v = pr.orig[i];
-        for (std::uint64_t e = g.fwd_index[v]; e < g.fwd_index[v + 1]; ++e) {
-            const std::uint32_t t = g.fwd_target[e];
-            if (region_of[t] != region_of[v])
-                continue;
-            pr.tgt[k] = local[t];
-            const double w = sign * g.fwd_weight[e];
-            pr.w[k] = w;
-            max_abs = std::max(max_abs, std::fabs(w));
-            ++k;
-        }
-    }
-    if (pr.exact) {
-        if (max_abs >= 2147483647.0)
-            throw UnsupportedError("integer weights beyond 32 bits are not supported by the "
-                                   "device lane");
-        pr.max_abs_w = static_cast<std::int64_t>(max_abs);
-    }
-    return pr;
-}
+void device_prepare(const Graph& g, const ocm_solve_options& opt, DeviceState& d, PrepInfo& info);
 
 // ================================================================ session
 
@@ -228,7 +28,6 @@ Session::Session(const Graph& g, const ocm_solve_options& opt) : opt_(opt) {
         throw UnsupportedError("only the policy-iteration lanes (howard, howard-par) run on the "
                                "device");
     const auto t0 = std::chrono::steady_clock::now();
-    prep_ = prepare(g, opt);
     d_ = std::make_unique<DeviceState>();
     DeviceState& d = *d_;
     int ndev = 0;
@@ -246,41 +45,21 @@ Session::Session(const Graph& g, const ocm_solve_options& opt) : opt_(opt) {
     CK(cudaEventCreate(&d.ev_end));
     CK(cudaMallocHost(&d.h_flags, sizeof(Flags)));
 
-    const std::size_t N = prep_.N, R = prep_.R, M = prep_.M;
-    const std::size_t N1 = std::max<std::size_t>(N, 1), R1 = std::max<std::size_t>(R, 1);
-    d.row.alloc(N + 1);
-    d.reg.alloc(N1);
+    device_prepare(g, opt, d, prep_);
+
+    const std::size_t N = prep_.n, R1 = std::size_t(prep_.R) + 1;
+    const std::size_t N1 = std::max<std::size_t>(N, 1);
     if (prep_.exact) {
-        std::vector<int2> packed(M);
-        for (std::size_t e = 0; e < M; ++e)
-            packed[e] = make_int2(static_cast<int>(prep_.tgt[e]), static_cast<int>(prep_.w[e]));
-        d.ew.alloc(std::max<std::size_t>(M, 1));
-        CK(cudaMemcpyAsync(d.ew.p, packed.data(), M * sizeof(int2), cudaMemcpyHostToDevice, d.stream));
-        h2d_bytes_ += M * sizeof(int2);
-        CK(cudaStreamSynchronize(d.stream));
         d.succ_wi.alloc(N1);
         d.key_i.alloc(N1);
         d.cyc_wi.alloc(N1);
         d.pv0.alloc(N1);
         d.pv1.alloc(N1);
     } else {
-        std::vector<FEdge> packed(M);
-        for (std::size_t e = 0; e < M; ++e)
-            packed[e] = FEdge{prep_.w[e], prep_.tgt[e], 0u};
-        d.fe.alloc(std::max<std::size_t>(M, 1));
-        CK(cudaMemcpyAsync(d.fe.p, packed.data(), M * sizeof(FEdge), cudaMemcpyHostToDevice, d.stream));
-        h2d_bytes_ += M * sizeof(FEdge);
-        CK(cudaStreamSynchronize(d.stream));
         d.succ_wf.alloc(N1);
         d.key_f.alloc(N1);
         d.cyc_wf.alloc(N1);
     }
-    CK(cudaMemcpyAsync(d.row.p, prep_.row.data(), (N + 1) * sizeof(std::uint32_t),
-                       cudaMemcpyHostToDevice, d.stream));
-    h2d_bytes_ += (2 * N + 1) * sizeof(std::uint32_t);
-    if (N)
-        CK(cudaMemcpyAsync(d.reg.p, prep_.reg.data(), N * sizeof(std::uint32_t),
-                           cudaMemcpyHostToDevice, d.stream));
     for (auto* b : {&d.succ_e, &d.succ_v, &d.comp, &d.mark, &d.mark2, &d.wlist, &d.cyc_len, &d.conn,
                     &d.rem0, &d.rem1})
         b->alloc(N1);
@@ -298,7 +77,7 @@ Session::Session(const Graph& g, const ocm_solve_options& opt) : opt_(opt) {
     CK(cudaStreamSynchronize(d.stream));
 
     KP& p = d.kp;
-    p.N = prep_.N;
+    p.N = prep_.n;
     p.R = prep_.R;
     p.row = d.row.p;
     p.ew = d.ew.p;
@@ -335,6 +114,7 @@ Session::Session(const Graph& g, const ocm_solve_options& opt) : opt_(opt) {
     p.flags = d.flags.p;
     p.max_region = prep_.max_region;
     p.max_abs_w = prep_.max_abs_w;
+    h2d_bytes_ = prep_.h2d_bytes;
     prep_ms_ = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
 }
 
@@ -371,7 +151,7 @@ template <class M> void Session::run(ocm_solution* out, std::uint32_t* cycle_buf
     cudaStream_t s = d.stream;
     const int gv = grid_for(p.N, d.sms);
     const int gr = grid_for(std::max<std::uint32_t>(p.R, 1), d.sms);
-    const double avg_deg = p.N ? double(prep_.M) / p.N : 1.0;
+    const double avg_deg = prep_.R ? double(prep_.M) / std::max<double>(1.0, double(prep_.n - prep_.trivial)) : 1.0;
     std::uint64_t launches = 0, fix_iters = 0;
     std::uint32_t passes = 0, outer = 0;
     Flags& hf = *d.h_flags;
@@ -556,7 +336,7 @@ template <class M> void Session::run(ocm_solution* out, std::uint32_t* cycle_buf
     out->spf_passes = passes;
     out->regions = prep_.regions_total;
     out->trivial_regions = prep_.trivial;
-    out->n_solved = prep_.N;
+    out->n_solved = prep_.n;
     out->m_solved = prep_.M;
     out->launches = launches;
     out->fixpoint_iters = fix_iters;
@@ -590,7 +370,7 @@ template <class M> void Session::run(ocm_solution* out, std::uint32_t* cycle_buf
             if (lf[a] != lf[b])
                 return lf[a] < lf[b];
         }
-        return prep_.orig[src[a]] < prep_.orig[src[b]];
+        return src[a] < src[b];
     };
     for (std::size_t r = 0; r < R; ++r) {
         if (its[r] == 0 || src[r] == NONE)
@@ -618,16 +398,16 @@ template <class M> void Session::run(ocm_solution* out, std::uint32_t* cycle_buf
         out->mu_den = den;
     }
     out->mu = mu;
-    std::vector<std::uint32_t> succ(prep_.N);
-    CK(cudaMemcpy(succ.data(), p.succ_v, prep_.N * sizeof(std::uint32_t), cudaMemcpyDeviceToHost));
-    out->d2h_bytes += prep_.N * sizeof(std::uint32_t);
+    std::vector<std::uint32_t> succ(prep_.n);
+    CK(cudaMemcpy(succ.data(), p.succ_v, prep_.n * sizeof(std::uint32_t), cudaMemcpyDeviceToHost));
+    out->d2h_bytes += prep_.n * sizeof(std::uint32_t);
     std::uint32_t u = src[best], len = 0;
     do {
         if (cycle_buf && len < cap)
-            cycle_buf[len] = prep_.orig[u];
+            cycle_buf[len] = u;
         ++len;
         u = succ[u];
-    } while (u != src[best] && len <= prep_.N);
+    } while (u != src[best] && len <= prep_.n);
     out->cycle_len = len;
 }
 
@@ -652,35 +432,27 @@ void Session::values(std::int64_t* key_num, std::int64_t* lam_num, std::int64_t*
     if (!solved_)
         throw std::logic_error("session has not been solved yet");
     DeviceState& d = *d_;
-    const std::size_t N = prep_.N, R = prep_.R, n = prep_.n_orig;
-    std::vector<long long> key(N), ln(R), ld(R);
-    std::vector<double> kf(N);
-    std::vector<std::uint32_t> sv(N);
-    if (N) {
+    const std::size_t n = prep_.n, R1 = std::size_t(prep_.R) + 1;
+    std::vector<long long> key(n), ln(R1), ld(R1);
+    std::vector<double> kf(n);
+    std::vector<std::uint32_t> sv(n), reg(n);
+    if (n) {
         if (prep_.exact)
-            CK(cudaMemcpy(key.data(), d.kp.key_i, N * sizeof(long long), cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy(key.data(), d.kp.key_i, n * sizeof(long long), cudaMemcpyDeviceToHost));
         else
-            CK(cudaMemcpy(kf.data(), d.kp.key_f, N * sizeof(double), cudaMemcpyDeviceToHost));
-        CK(cudaMemcpy(sv.data(), d.kp.succ_v, N * sizeof(std::uint32_t), cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy(kf.data(), d.kp.key_f, n * sizeof(double), cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(sv.data(), d.kp.succ_v, n * sizeof(std::uint32_t), cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(reg.data(), d.kp.reg, n * sizeof(std::uint32_t), cudaMemcpyDeviceToHost));
     }
-    if (R) {
-        CK(cudaMemcpy(ln.data(), d.kp.lam_num, R * sizeof(long long), cudaMemcpyDeviceToHost));
-        CK(cudaMemcpy(ld.data(), d.kp.lam_den, R * sizeof(long long), cudaMemcpyDeviceToHost));
-    }
+    CK(cudaMemcpy(ln.data(), d.kp.lam_num, R1 * sizeof(long long), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(ld.data(), d.kp.lam_den, R1 * sizeof(long long), cudaMemcpyDeviceToHost));
     for (std::size_t v = 0; v < n; ++v) {
-        if (key_num) key_num[v] = 0;
-        if (lam_num) lam_num[v] = 0;
-        if (lam_den) lam_den[v] = 1;
-        if (fval) fval[v] = 0.0;
-        if (succ_vertex) succ_vertex[v] = NONE;
-    }
-    for (std::size_t i = 0; i < N; ++i) {
-        const std::uint32_t v = prep_.orig[i];
-        if (key_num) key_num[v] = prep_.exact ? key[i] : 0;
-        if (lam_num) lam_num[v] = ln[prep_.reg[i]];
-        if (lam_den) lam_den[v] = ld[prep_.reg[i]];
-        if (fval) fval[v] = prep_.exact ? 0.0 : kf[i];
-        if (succ_vertex) succ_vertex[v] = prep_.orig[sv[i]];
+        const bool solved = reg[v] != prep_.R;
+        if (key_num) key_num[v] = solved && prep_.exact ? key[v] : 0;
+        if (lam_num) lam_num[v] = solved ? ln[reg[v]] : 0;
+        if (lam_den) lam_den[v] = solved ? ld[reg[v]] : 1;
+        if (fval) fval[v] = solved && !prep_.exact ? kf[v] : 0.0;
+        if (succ_vertex) succ_vertex[v] = solved ? sv[v] : NONE;
     }
 }
 

@@ -9,37 +9,11 @@
 
 #include "../../include/ocm_b200.h"
 #include "graph.hpp"
+#include "prepinfo.hpp"
 
 namespace ocmb {
 
-// Host-side split of a graph into solver regions: strongly connected
-// components (Tarjan) minus trivial ones, renumbered so every region is a
-// contiguous vertex range (ascending original id inside a region, so "least
-// vertex of a cycle" is the same under both numberings), with the CSR
-// restricted to intra-region edges (relative edge order preserved, so
-// "smallest edge id" tie-breaks are unchanged).
-struct Prepared {
-    std::uint32_t n_orig = 0;
-    std::uint32_t N = 0;            // vertices in non-trivial regions
-    std::uint32_t R = 0;            // non-trivial regions
-    std::uint32_t regions_total = 0;
-    std::uint32_t trivial = 0;
-    std::uint64_t M = 0;            // intra-region edges
-    std::uint32_t max_region = 0;
-    bool exact = false;
-    bool scc_off = false;
-    double no_cycle_above = 0.0;
-    std::int64_t max_abs_w = 0;     // exact mode
-    std::vector<std::uint32_t> orig;   // N
-    std::vector<std::uint32_t> reg;    // N
-    std::vector<std::uint32_t> row;    // N+1
-    std::vector<std::uint32_t> tgt;    // M
-    std::vector<double> w;             // M (already sign-flipped for maximize)
-};
-
-Prepared prepare(const Graph& g, const ocm_solve_options& opt);
-
-struct DeviceState; // defined in solver.cu
+struct DeviceState; // devcommon.cuh
 
 class Session {
   public:
@@ -53,7 +27,7 @@ class Session {
   private:
     template <class M> void run(ocm_solution* out, std::uint32_t* cycle_buf, std::uint32_t cap);
     ocm_solve_options opt_;
-    Prepared prep_;
+    PrepInfo prep_;
     double prep_ms_ = 0.0;
     std::uint64_t h2d_bytes_ = 0;
     std::unique_ptr<DeviceState> d_;
