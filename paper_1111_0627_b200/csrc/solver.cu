@@ -195,7 +195,7 @@ template <class M> void Session::run(ocm_solution* out, std::uint32_t* cycle_buf
     const int K_max = std::max(1, ceil_log2(std::max<std::uint32_t>(prep_.max_region, 2)));
     int k_need = std::min(K_max, k_hint_);
     std::uint32_t stamp = stamp_base_;
-    while (p.N) {
+    while (prep_.R > 0) {
         mark(0);
         CK(cudaMemsetAsync(&p.flags->active_count, 0, sizeof(unsigned), s));
         CK(cudaEventRecord(d.event(2 * passes), s));
