@@ -105,15 +105,20 @@ template <class T> struct DBuf {
     DBuf() = default;
     DBuf(const DBuf&) = delete;
     DBuf& operator=(const DBuf&) = delete;
-    void alloc(std::size_t k) {
+    // Stream-ordered allocation from the device's default memory pool (kept
+    // cached by the session), so re-creating sessions does not pay
+    // cudaMalloc/cudaFree synchronisation.
+    cudaStream_t st = nullptr;
+    void alloc(std::size_t k, cudaStream_t s = nullptr) {
         release();
+        st = s;
         if (k)
-            CK(cudaMalloc(&p, k * sizeof(T)));
+            CK(cudaMallocAsync(reinterpret_cast<void**>(&p), k * sizeof(T), st));
         n = k;
     }
     void release() {
         if (p)
-            cudaFree(p);
+            cudaFreeAsync(p, st);
         p = nullptr;
         n = 0;
     }
@@ -155,6 +160,32 @@ struct DeviceState {
     KP kp{};
 
     ~DeviceState() {
+        if (stream)
+            cudaStreamSynchronize(stream);
+        for (auto* b : {&row, &reg, &succ_e, &succ_v, &comp, &mark, &mark2, &wlist, &cyc_len, &conn,
+                        &rem0, &rem1, &src, &iters})
+            b->release();
+        pv0.release();
+        pv1.release();
+        pj0.release();
+        pj1.release();
+        ew.release();
+        fe.release();
+        succ_wi.release();
+        active.release();
+        changed.release();
+        succ_wf.release();
+        key_f.release();
+        lam_f.release();
+        cyc_wf.release();
+        key_i.release();
+        lam_num.release();
+        lam_den.release();
+        cyc_wi.release();
+        slot.release();
+        flags.release();
+        if (stream)
+            cudaStreamSynchronize(stream);
         for (cudaEvent_t e : ev)
             cudaEventDestroy(e);
         if (ev_start)

@@ -416,7 +416,7 @@ template <class T> void exclusive_scan(const T* in, T* out, std::size_t n, cudaS
     std::size_t bytes = 0;
     CK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, n, s));
     DBuf<unsigned char> tmp;
-    tmp.alloc(std::max<std::size_t>(bytes, 1));
+    tmp.alloc(std::max<std::size_t>(bytes, 1), s);
     CK(cub::DeviceScan::ExclusiveSum(tmp.p, bytes, in, out, n, s));
     CK(cudaStreamSynchronize(s));
 }
@@ -438,10 +438,10 @@ void device_prepare(const Graph& g, const ocm_solve_options& opt, DeviceState& d
     DBuf<std::uint64_t> row64;
     DBuf<std::uint32_t> row, tgt;
     DBuf<double> w;
-    row64.alloc(std::size_t(n) + 1);
-    row.alloc(std::size_t(n) + 1);
-    tgt.alloc(std::max<std::uint64_t>(m, 1));
-    w.alloc(std::max<std::uint64_t>(m, 1));
+    row64.alloc(std::size_t(n) + 1, s);
+    row.alloc(std::size_t(n) + 1, s);
+    tgt.alloc(std::max<std::uint64_t>(m, 1), s);
+    w.alloc(std::max<std::uint64_t>(m, 1), s);
     CK(cudaMemcpyAsync(row64.p, g.fwd_index.data(), (std::size_t(n) + 1) * 8, cudaMemcpyHostToDevice, s));
     if (m) {
         CK(cudaMemcpyAsync(tgt.p, g.fwd_target.data(), m * 4, cudaMemcpyHostToDevice, s));
@@ -452,14 +452,14 @@ void device_prepare(const Graph& g, const ocm_solve_options& opt, DeviceState& d
     row64.release();
 
     DBuf<PrepCounters> pcd;
-    pcd.alloc(1);
+    pcd.alloc(1, s);
     PrepCounters pc{};
     CK(cudaMemsetAsync(pcd.p, 0, sizeof(PrepCounters), s));
     DBuf<std::uint32_t> outd, ind;
     DBuf<std::uint8_t> self;
-    outd.alloc(std::max<std::uint32_t>(n, 1));
-    ind.alloc(std::max<std::uint32_t>(n, 1));
-    self.alloc(std::max<std::uint32_t>(n, 1));
+    outd.alloc(std::max<std::uint32_t>(n, 1), s);
+    ind.alloc(std::max<std::uint32_t>(n, 1), s);
+    self.alloc(std::max<std::uint32_t>(n, 1), s);
     CK(cudaMemsetAsync(ind.p, 0, std::size_t(n) * 4, s));
     kp_degrees<<<gv, kBlock, 0, s>>>(n, row.p, tgt.p, w.p, outd.p, ind.p, self.p, pcd.p);
     auto read_pc = [&] {
@@ -473,8 +473,8 @@ void device_prepare(const Graph& g, const ocm_solve_options& opt, DeviceState& d
         std::memcpy(&max_abs, &bits, sizeof max_abs);
     }
 
-    d.reg.alloc(std::max<std::uint32_t>(n, 1));
-    d.row.alloc(std::size_t(n) + 1 + (info.scc_off ? 0 : 0));
+    d.reg.alloc(std::max<std::uint32_t>(n, 1), s);
+    d.row.alloc(std::size_t(n) + 1 + (info.scc_off ? 0 : 0), s);
 
     if (info.scc_off) {
         // ---- single region: the Hamiltonian-augmented graph (solve.cpp:53)
@@ -490,9 +490,9 @@ void device_prepare(const Graph& g, const ocm_solve_options& opt, DeviceState& d
         if (info.M >= 0xffffffffull)
             throw UnsupportedError("more than 2^32-1 edges after augmentation");
         if (info.exact)
-            d.ew.alloc(info.M);
+            d.ew.alloc(info.M, s);
         else
-            d.fe.alloc(info.M);
+            d.fe.alloc(info.M, s);
         if (info.exact)
             kp_pack_hamiltonian<true><<<grid_for(n + 1, sms), kBlock, 0, s>>>(
                 n, row.p, tgt.p, w.p, sign, big_w, d.ew.p, nullptr, d.row.p, d.reg.p, pcd.p);
@@ -509,31 +509,31 @@ void device_prepare(const Graph& g, const ocm_solve_options& opt, DeviceState& d
     // ---- backward CSR (no self-loops)
     const auto t_scc = std::chrono::steady_clock::now();
     DBuf<std::uint32_t> brow, bsrc, cursor;
-    brow.alloc(std::size_t(n) + 1);
+    brow.alloc(std::size_t(n) + 1, s);
     CK(cudaMemsetAsync(brow.p + n, 0, 4, s));
     // brow[0..n] = exclusive scan of ind (ind[n] treated as 0 via n+1 scan)
     {
         DBuf<std::uint32_t> ind1;
-        ind1.alloc(std::size_t(n) + 1);
+        ind1.alloc(std::size_t(n) + 1, s);
         CK(cudaMemsetAsync(ind1.p + n, 0, 4, s));
         CK(cudaMemcpyAsync(ind1.p, ind.p, std::size_t(n) * 4, cudaMemcpyDeviceToDevice, s));
         exclusive_scan(ind1.p, brow.p, std::size_t(n) + 1, s);
     }
     std::uint32_t mb = 0;
     CK(cudaMemcpy(&mb, brow.p + n, 4, cudaMemcpyDeviceToHost));
-    bsrc.alloc(std::max<std::uint32_t>(mb, 1));
-    cursor.alloc(std::max<std::uint32_t>(n, 1));
+    bsrc.alloc(std::max<std::uint32_t>(mb, 1), s);
+    cursor.alloc(std::max<std::uint32_t>(n, 1), s);
     CK(cudaMemcpyAsync(cursor.p, brow.p, std::size_t(n) * 4, cudaMemcpyDeviceToDevice, s));
     kp_bwd_fill<<<gv, kBlock, 0, s>>>(n, row.p, tgt.p, cursor.p, bsrc.p);
     cursor.release();
 
     // ---- SCC
     DBuf<std::uint32_t> lab, q0, q1, visf, visb, aux;
-    lab.alloc(std::max<std::uint32_t>(n, 1));
-    q0.alloc(std::max<std::uint32_t>(n, 1));
-    q1.alloc(std::max<std::uint32_t>(n, 1));
-    visf.alloc(std::max<std::uint32_t>(n, 1));
-    visb.alloc(std::max<std::uint32_t>(n, 1));
+    lab.alloc(std::max<std::uint32_t>(n, 1), s);
+    q0.alloc(std::max<std::uint32_t>(n, 1), s);
+    q1.alloc(std::max<std::uint32_t>(n, 1), s);
+    visf.alloc(std::max<std::uint32_t>(n, 1), s);
+    visb.alloc(std::max<std::uint32_t>(n, 1), s);
     CK(cudaMemsetAsync(lab.p, 0xff, std::size_t(n) * 4, s));
     CK(cudaMemsetAsync(visf.p, 0, std::size_t(n) * 4, s));
     CK(cudaMemsetAsync(visb.p, 0, std::size_t(n) * 4, s));
@@ -597,7 +597,7 @@ void device_prepare(const Graph& g, const ocm_solve_options& opt, DeviceState& d
             trim();
             if (!remaining())
                 break;
-            aux.alloc(std::max<std::uint32_t>(n, 1)); // colours
+            aux.alloc(std::max<std::uint32_t>(n, 1), s); // colours
             kp_color_init<<<gv, kBlock, 0, s>>>(n, lab.p, aux.p);
             do {
                 CK(cudaMemsetAsync(&pcd.p->changed, 0, 4, s));
@@ -625,8 +625,8 @@ void device_prepare(const Graph& g, const ocm_solve_options& opt, DeviceState& d
     CK(cudaMemsetAsync(size.p, 0, std::size_t(n) * 4, s));
     kp_sizes<<<gv, kBlock, 0, s>>>(n, lab.p, size.p);
     DBuf<std::uint32_t> flag, rid;
-    flag.alloc(std::size_t(n) + 1);
-    rid.alloc(std::size_t(n) + 1);
+    flag.alloc(std::size_t(n) + 1, s);
+    rid.alloc(std::size_t(n) + 1, s);
     CK(cudaMemsetAsync(flag.p + n, 0, 4, s));
     kp_nontrivial<<<gv, kBlock, 0, s>>>(n, lab.p, size.p, self.p, flag.p, pcd.p);
     exclusive_scan(flag.p, rid.p, std::size_t(n) + 1, s);
@@ -649,9 +649,9 @@ void device_prepare(const Graph& g, const ocm_solve_options& opt, DeviceState& d
     CK(cudaMemcpy(&M, d.row.p + n, 4, cudaMemcpyDeviceToHost));
     info.M = M;
     if (info.exact)
-        d.ew.alloc(std::max<std::uint32_t>(M, 1));
+        d.ew.alloc(std::max<std::uint32_t>(M, 1), s);
     else
-        d.fe.alloc(std::max<std::uint32_t>(M, 1));
+        d.fe.alloc(std::max<std::uint32_t>(M, 1), s);
     CK(cudaMemsetAsync(&pcd.p->bad_weight, 0, 4, s));
     if (info.exact)
         kp_pack<true><<<gv, kBlock, 0, s>>>(n, R, row.p, tgt.p, w.p, d.reg.p, d.row.p, sign, d.ew.p,

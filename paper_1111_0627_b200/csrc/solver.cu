@@ -41,6 +41,13 @@ Session::Session(const Graph& g, const ocm_solve_options& opt) : opt_(opt) {
         throw CudaError(std::string("device ") + prop.name + " is not sm_100-class");
     d.sms = prop.multiProcessorCount;
     CK(cudaStreamCreateWithFlags(&d.stream, cudaStreamNonBlocking));
+    {
+        // keep freed blocks cached in the default pool across sessions
+        cudaMemPool_t pool;
+        CK(cudaDeviceGetDefaultMemPool(&pool, d.device));
+        std::uint64_t keep = ~0ull;
+        CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+    }
     CK(cudaEventCreate(&d.ev_start));
     CK(cudaEventCreate(&d.ev_end));
     CK(cudaMallocHost(&d.h_flags, sizeof(Flags)));
@@ -50,30 +57,30 @@ Session::Session(const Graph& g, const ocm_solve_options& opt) : opt_(opt) {
     const std::size_t N = prep_.n, R1 = std::size_t(prep_.R) + 1;
     const std::size_t N1 = std::max<std::size_t>(N, 1);
     if (prep_.exact) {
-        d.succ_wi.alloc(N1);
-        d.key_i.alloc(N1);
-        d.cyc_wi.alloc(N1);
-        d.pv0.alloc(N1);
-        d.pv1.alloc(N1);
+        d.succ_wi.alloc(N1, d.stream);
+        d.key_i.alloc(N1, d.stream);
+        d.cyc_wi.alloc(N1, d.stream);
+        d.pv0.alloc(N1, d.stream);
+        d.pv1.alloc(N1, d.stream);
     } else {
-        d.succ_wf.alloc(N1);
-        d.key_f.alloc(N1);
-        d.cyc_wf.alloc(N1);
+        d.succ_wf.alloc(N1, d.stream);
+        d.key_f.alloc(N1, d.stream);
+        d.cyc_wf.alloc(N1, d.stream);
     }
     for (auto* b : {&d.succ_e, &d.succ_v, &d.comp, &d.mark, &d.mark2, &d.wlist, &d.cyc_len, &d.conn,
                     &d.rem0, &d.rem1})
-        b->alloc(N1);
-    d.pj0.alloc(N1);
-    d.pj1.alloc(N1);
-    d.src.alloc(R1);
-    d.iters.alloc(R1);
-    d.active.alloc(R1);
-    d.changed.alloc(R1);
-    d.lam_f.alloc(R1);
-    d.lam_num.alloc(R1);
-    d.lam_den.alloc(R1);
-    d.slot.alloc(R1);
-    d.flags.alloc(1);
+        b->alloc(N1, d.stream);
+    d.pj0.alloc(N1, d.stream);
+    d.pj1.alloc(N1, d.stream);
+    d.src.alloc(R1, d.stream);
+    d.iters.alloc(R1, d.stream);
+    d.active.alloc(R1, d.stream);
+    d.changed.alloc(R1, d.stream);
+    d.lam_f.alloc(R1, d.stream);
+    d.lam_num.alloc(R1, d.stream);
+    d.lam_den.alloc(R1, d.stream);
+    d.slot.alloc(R1, d.stream);
+    d.flags.alloc(1, d.stream);
     CK(cudaStreamSynchronize(d.stream));
 
     KP& p = d.kp;
