@@ -58,6 +58,7 @@ struct Flags {
     int verify_fail;    // cycle-detection round count too small
     unsigned max_cycle; // longest winning cycle this iteration
     unsigned wc_count;  // winning-cycle vertices listed
+    int wc_short;       // winning-cycle prefix sums needed more rounds
     unsigned notdone[kMaxRounds];
 };
 

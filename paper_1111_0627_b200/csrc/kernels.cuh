@@ -205,9 +205,9 @@ template <bool EXACT, int G, int U> __global__ void __launch_bounds__(kBlock) k_
             for (int u = 0; u < U; ++u) {
                 if (e0 + u * G < e_end) {
                     if constexpr (EXACT)
-                        kk[u] = p.key_i[tt[u]];
+                        kk[u] = __ldg(&p.key_i[tt[u]]);
                     else
-                        kk[u] = p.key_f[tt[u]];
+                        kk[u] = __ldg(&p.key_f[tt[u]]);
                 }
             }
 #pragma unroll
@@ -307,6 +307,8 @@ __global__ void k_region_check(KP p) {
 // Regions are closed under succ, so rounds run without region checks.
 
 template <bool EXACT> __global__ void k_pj_init(KP p) {
+    if (*(volatile unsigned*)&p.flags->active_count == 0)
+        return; // quiet pass: no region left
     for (std::size_t v = gtid(); v < p.N; v += gstride()) {
         PJC x;
         const std::uint32_t sv = p.succ_v[v];
@@ -318,6 +320,8 @@ template <bool EXACT> __global__ void k_pj_init(KP p) {
 }
 
 __global__ void k_pj_round(KP p, int in) {
+    if (*(volatile unsigned*)&p.flags->active_count == 0)
+        return; // quiet pass: no region left
     const PJC* __restrict__ a = p.pj[in];
     PJC* __restrict__ o = p.pj[in ^ 1];
     for (std::size_t v = gtid(); v < p.N; v += gstride()) {
@@ -332,6 +336,8 @@ __global__ void k_pj_round(KP p, int in) {
 }
 
 __global__ void k_cycle_mark(KP p, int in, std::uint32_t stamp) {
+    if (*(volatile unsigned*)&p.flags->active_count == 0)
+        return; // quiet pass: no region left
     const PJC* a = p.pj[in];
     for (std::size_t v = gtid(); v < p.N; v += gstride()) {
         if (!working(p, v))
@@ -351,6 +357,8 @@ __global__ void k_cycle_mark(KP p, int in, std::uint32_t stamp) {
 // every tail) and comp is constant along succ inside M (so every window of
 // length L covers its whole cycle, i.e. L >= every cycle length).
 __global__ void k_cycle_verify1(KP p, std::uint32_t stamp) {
+    if (*(volatile unsigned*)&p.flags->active_count == 0)
+        return; // quiet pass: no region left
     bool fail = false;
     for (std::size_t v = gtid(); v < p.N; v += gstride()) {
         if (p.mark[v] != stamp || !working(p, v))
@@ -365,6 +373,8 @@ __global__ void k_cycle_verify1(KP p, std::uint32_t stamp) {
 }
 
 __global__ void k_cycle_verify2(KP p, std::uint32_t stamp) {
+    if (*(volatile unsigned*)&p.flags->active_count == 0)
+        return; // quiet pass: no region left
     bool fail = false;
     for (std::size_t v = gtid(); v < p.N; v += gstride())
         fail |= p.mark[v] == stamp && p.mark2[v] != stamp && working(p, v);
@@ -584,8 +594,11 @@ __global__ void k_wincyc_final(KP p, int rounds) {
             last = j;
             break;
         }
-    if (gtid() == 0 && p.flags->notdone[rounds - 1] != 0)
-        p.flags->error = 1;
+    if (p.flags->notdone[rounds - 1] != 0) {
+        if (gtid() == 0)
+            p.flags->wc_short = 1; // host re-runs with the exact round count
+        return;
+    }
     const PJV* a = p.pv[(last & 1) ^ 1];
     const unsigned cnt = p.flags->wc_count;
     for (std::size_t i = gtid(); i < cnt; i += gstride()) {

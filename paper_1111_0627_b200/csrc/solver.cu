@@ -131,14 +131,9 @@ void* Session::stream() const { return d_ ? d_->stream : nullptr; }
 
 namespace {
 
-template <bool EXACT> void launch_improve(const KP& p, int sms, cudaStream_t s, double avg_deg) {
-    // G lanes per vertex with U = 4 edges in flight per lane: G*U ~ degree.
-    constexpr int U = 4;
-    int G = 1;
-    while (G < 32 && G * U < avg_deg)
-        G *= 2;
+template <bool EXACT, int U> void launch_improve_u(const KP& p, int grid_sms, cudaStream_t s, int G) {
     const std::size_t threads = std::size_t(p.N) * G;
-    const int grid = grid_for(threads, sms, 8);
+    const int grid = grid_for(threads, grid_sms, 8);
     switch (G) {
     case 1: k_improve<EXACT, 1, U><<<grid, kBlock, 0, s>>>(p); break;
     case 2: k_improve<EXACT, 2, U><<<grid, kBlock, 0, s>>>(p); break;
@@ -146,6 +141,25 @@ template <bool EXACT> void launch_improve(const KP& p, int sms, cudaStream_t s, 
     case 8: k_improve<EXACT, 8, U><<<grid, kBlock, 0, s>>>(p); break;
     case 16: k_improve<EXACT, 16, U><<<grid, kBlock, 0, s>>>(p); break;
     default: k_improve<EXACT, 32, U><<<grid, kBlock, 0, s>>>(p); break;
+    }
+}
+
+// G lanes per vertex with U edges in flight per lane, G*U ~ average degree.
+// OCM_IMPROVE_G / OCM_IMPROVE_U override the choice (tuning sweeps).
+template <bool EXACT> void launch_improve(const KP& p, int sms, cudaStream_t s, double avg_deg) {
+    static const int env_g = std::getenv("OCM_IMPROVE_G") ? std::atoi(std::getenv("OCM_IMPROVE_G")) : 0;
+    static const int env_u = std::getenv("OCM_IMPROVE_U") ? std::atoi(std::getenv("OCM_IMPROVE_U")) : 0;
+    const int U = env_u ? env_u : 4;
+    int G = 1;
+    while (G < 32 && G * U < avg_deg)
+        G *= 2;
+    if (env_g)
+        G = env_g;
+    switch (U) {
+    case 1: launch_improve_u<EXACT, 1>(p, sms, s, G); break;
+    case 2: launch_improve_u<EXACT, 2>(p, sms, s, G); break;
+    case 8: launch_improve_u<EXACT, 8>(p, sms, s, G); break;
+    default: launch_improve_u<EXACT, 4>(p, sms, s, G); break;
     }
 }
 
@@ -198,10 +212,14 @@ template <class M> void Session::run(ocm_solution* out, std::uint32_t* cycle_buf
         ++launches;
     }
     // Upper bound on doubling rounds (2^K_max >= region size) and the
-    // session's running estimate of the rounds actually needed.
+    // session's running estimates of the rounds actually needed.
     const int K_max = std::max(1, ceil_log2(std::max<std::uint32_t>(prep_.max_region, 2)));
     int k_need = std::min(K_max, k_hint_);
     std::uint32_t stamp = stamp_base_;
+    // Two host synchronisations per iteration: (1) after the improvement pass
+    // and the cycle-detection check (termination + round-count verdict), (2)
+    // after the kept-component pass (re-attachment workload). Kernels between
+    // them are gated on device flags, so the quiet final pass costs no work.
     while (prep_.R > 0) {
         mark(0);
         CK(cudaMemsetAsync(&p.flags->active_count, 0, sizeof(unsigned), s));
@@ -211,16 +229,13 @@ template <class M> void Session::run(ocm_solution* out, std::uint32_t* cycle_buf
         ++passes;
         k_region_check<<<gr, kBlock, 0, s>>>(p);
         launches += 2;
-        read_flags();
-        if (hf.active_count == 0)
-            break;
-        ++outer;
 
         // cycles of the policy graph: double until the exact check passes
         mark(1);
         k_pj_init<EXACT><<<gv, kBlock, 0, s>>>(p);
         ++launches;
         int in = 0, k = 0;
+        bool quiet = false;
         for (;;) {
             for (; k < k_need; ++k, in ^= 1) {
                 k_pj_round<<<gv, kBlock, 0, s>>>(p, in);
@@ -234,16 +249,23 @@ template <class M> void Session::run(ocm_solution* out, std::uint32_t* cycle_buf
             k_cycle_verify2<<<gv, kBlock, 0, s>>>(p, stamp);
             launches += 3;
             read_flags();
+            if (hf.active_count == 0) {
+                quiet = true;
+                break;
+            }
             if (!hf.verify_fail)
                 break;
             if (k >= K_max)
                 throw std::logic_error("cycle detection did not converge within log2(n) rounds");
             k_need = k + 1;
         }
+        if (quiet)
+            break;
+        ++outer;
         k_hint_ = k;
 
         mark(2);
-        CK(cudaMemsetAsync(&p.flags->max_cycle, 0, 2 * sizeof(unsigned), s)); // + wc_count
+        CK(cudaMemsetAsync(&p.flags->max_cycle, 0, 3 * sizeof(unsigned), s)); // + wc_count, wc_short
         if constexpr (EXACT)
             k_cycle_stats<<<gv, kBlock, 0, s>>>(p, stamp);
         else
@@ -251,23 +273,40 @@ template <class M> void Session::run(ocm_solution* out, std::uint32_t* cycle_buf
         k_vote<EXACT><<<gv, kBlock, 0, s>>>(p);
         k_adopt<EXACT><<<gr, kBlock, 0, s>>>(p);
         launches += 3;
-        if constexpr (EXACT) {
-            // values of the winning cycle(s): prefix sums cut at the anchor
-            k_wincyc_init<<<gv, kBlock, 0, s>>>(p, stamp);
-            read_flags();
-            const int rounds = std::min(kMaxRounds, ceil_log2(std::max(hf.max_cycle, 2u)) + 1);
+        // values of the winning cycle(s): prefix sums cut at the anchor, with
+        // the round count of the previous iteration (+1); re-run exactly if short
+        auto wincyc = [&](int rounds) {
             CK(cudaMemsetAsync(p.flags->notdone, 0, rounds * sizeof(unsigned), s));
-            const int gw = grid_for(hf.wc_count, d.sms);
+            const int gw = grid_for(std::max<std::uint32_t>(prep_.max_region, 1), d.sms);
             for (int j = 0; j < rounds; ++j)
                 k_wincyc_round<<<gw, kBlock, 0, s>>>(p, j);
             k_wincyc_final<<<gw, kBlock, 0, s>>>(p, rounds);
-            launches += 2 + rounds;
+            launches += 1 + rounds;
             fix_iters += rounds;
+        };
+        auto keep = [&] {
+            CK(cudaMemsetAsync(&p.flags->rem_count[0], 0, sizeof(unsigned), s));
+            k_keep<EXACT><<<gv, kBlock, 0, s>>>(p, in, stamp, 1ull << k);
+            ++launches;
+        };
+        if constexpr (EXACT) {
+            k_wincyc_init<<<gv, kBlock, 0, s>>>(p, stamp);
+            ++launches;
+            wincyc(std::min(kMaxRounds, wc_hint_));
         }
-        CK(cudaMemsetAsync(&p.flags->rem_count[0], 0, sizeof(unsigned), s));
-        k_keep<EXACT><<<gv, kBlock, 0, s>>>(p, in, stamp, 1ull << k);
-        ++launches;
+        keep();
         read_flags();
+        if (EXACT && hf.wc_short) {
+            const int rounds = std::min(kMaxRounds, ceil_log2(std::max(hf.max_cycle, 2u)) + 1);
+            CK(cudaMemsetAsync(&p.flags->wc_short, 0, sizeof(int), s));
+            wincyc(rounds);
+            keep();
+            read_flags();
+            if (hf.wc_short)
+                throw std::logic_error("winning-cycle prefix sums did not converge");
+        }
+        if (EXACT)
+            wc_hint_ = std::max(2, ceil_log2(std::max(hf.max_cycle, 2u)) + 1);
 
         // breadth-layered re-attachment (+ values of re-attached vertices)
         mark(3);

@@ -33,6 +33,7 @@ class Session {
     std::unique_ptr<DeviceState> d_;
     bool solved_ = false;
     int k_hint_ = 8;               // doubling rounds needed last iteration
+    int wc_hint_ = 4;              // winning-cycle prefix-sum rounds (log2 cycle + 1)
     std::uint32_t stamp_base_ = 0; // mark stamps stay unique across solves
 };
 
