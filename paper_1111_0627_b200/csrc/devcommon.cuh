@@ -4,6 +4,7 @@
 
 #include <cuda_runtime.h>
 
+#include <cstddef>
 #include <cstdint>
 #include <stdexcept>
 #include <string>
@@ -49,18 +50,43 @@ struct __align__(16) PJC {
     long long w;
 };
 
-struct Flags {
-    unsigned active_count;
-    unsigned rem_count[2];
-    int error;     // structural (no successor / not strongly connected)
-    int overflow;  // exact keys would leave int64
-    int lambda_up; // lambda increased inside a region
-    int verify_fail;    // cycle-detection round count too small
-    unsigned max_cycle; // longest winning cycle this iteration
-    unsigned wc_count;  // winning-cycle vertices listed
-    int wc_short;       // winning-cycle prefix sums needed more rounds
-    unsigned notdone[kMaxRounds];
+// Device-resident control block of the persistent solver kernel (k_solve).
+// Nothing in it is reset between iterations: list appends and counts go
+// through cumulative 64-bit counters used in ping-pong pairs (see Ring in
+// solve_kernel.cuh), and one-shot flags carry the unique stamp of the check
+// that raised them, so no phase has to clear state another block may still
+// be reading.
+enum Phase {
+    PH_INIT, PH_IMPROVE, PH_REGION, PH_LEAVES, PH_PEEL, PH_CORE, PH_PJINIT, PH_ROUND, PH_VERIFY,
+    PH_STATS, PH_VOTE, PH_ADOPT, PH_WINCYC, PH_KEEP, PH_UNPEEL, PH_ATTACH, PH_FLOAT, PH_COUNT
 };
+
+struct Ctl {
+    // ---- persistent across the session's solves (zeroed once at creation)
+    unsigned long long ring[2][2]; // cumulative append counters (ring, slot)
+    unsigned long long maxcyc;     // (stamp << 32) | longest winning cycle
+    unsigned long long fnd[2];     // float lane: (stamp << 32) | level still pending
+    unsigned stamp;                // last verification stamp used
+    unsigned k_hint;               // doubling rounds that sufficed last iteration
+    unsigned k_streak;             // consecutive first-try verifications
+    unsigned vfail[2];             // = stamp of a failed verification (slot stamp & 1)
+    // ---- per solve (host clears from here on before every launch)
+    int error;     // structural (no successor / not strongly connected)
+    int overflow;  // exact keys would leave +-2^62
+    int lambda_up; // lambda increased inside a region
+    int nonconv;   // a fixpoint did not converge within its bound
+    unsigned passes;
+    unsigned outer;
+    unsigned long long rounds;     // pointer-doubling rounds (all iterations)
+    unsigned long long verifies;   // cycle verifications
+    unsigned long long peeled;     // vertices peeled (all iterations)
+    unsigned long long cored;      // vertices doubled (all iterations)
+    unsigned long long layers;     // attach layers + float levels
+    unsigned long long syncs;      // grid barriers
+    long long clk_total;           // block-0 SM clock over the launch
+    long long clk[PH_COUNT];       // ... per phase (time up to the phase's barrier)
+};
+constexpr std::size_t kCtlSolveOffset = offsetof(Ctl, error);
 
 // Everything a kernel may touch, passed by value.
 struct KP {
@@ -79,14 +105,22 @@ struct KP {
     long long* lam_den;
     double* lam_f;
     int* active;
-    int* changed;
+    int* changed[2];
     unsigned long long* slot;
     std::uint32_t* src;
     std::uint32_t* iters;
-    PJC* pj[2];
-    std::uint32_t* comp;
-    std::uint32_t* mark;
-    std::uint32_t* mark2;
+    // cycle phase
+    std::uint32_t* indeg; // policy in-degree (peeling)
+    std::uint32_t* peel;  // peel layer of a vertex this iteration (0 = not peeled)
+    std::uint32_t* plist; // peeled vertices, layer after layer
+    std::uint32_t* clist; // core (not peeled) vertices; core index -> vertex
+    std::uint32_t* cidx;  // vertex -> core index
+    std::uint32_t* csucc; // core index of the policy successor
+    std::uint32_t* ccomp; // anchor (least vertex of the reached cycle), core-indexed
+    std::uint32_t* cmark; // core-indexed stamps: image of succ^L
+    std::uint32_t* cmark2;
+    PJC* pj[2];           // core-indexed doubling records
+    std::uint32_t* comp;  // anchor, vertex-indexed
     std::uint32_t* wlist;
     std::uint32_t* cyc_len;
     long long* cyc_wi;
@@ -94,11 +128,15 @@ struct KP {
     std::uint32_t* conn;
     std::uint32_t* rem[2];
     PJV* pv[2];
-    Flags* flags;
+    Ctl* c;
     std::uint32_t max_region;
     long long max_abs_w;
+    // tuning (launch arguments)
+    int G;                 // improvement lanes per vertex
+    std::uint32_t peel_min; // peel another layer only while it has >= this many vertices
+    int peel_max;          // at most this many peel layers
+    std::uint32_t small_wc; // winning cycles up to this many vertices: one block
 };
-
 
 template <class T> struct DBuf {
     T* p = nullptr;
@@ -144,18 +182,18 @@ struct DeviceState {
     int device = 0;
     int sms = 148;
     cudaStream_t stream = nullptr;
-    DBuf<std::uint32_t> row, reg, succ_e, succ_v, comp, mark, mark2, wlist, cyc_len, conn, rem0,
-        rem1, src, iters;
+    DBuf<std::uint32_t> row, reg, succ_e, succ_v, comp, wlist, cyc_len, conn, rem0, rem1, src,
+        iters, indeg, peel, plist, clist, cidx, csucc, ccomp, cmark, cmark2;
     DBuf<PJV> pv0, pv1;
     DBuf<PJC> pj0, pj1;
     DBuf<int2> ew;
     DBuf<FEdge> fe;
-    DBuf<int> succ_wi, active, changed;
+    DBuf<int> succ_wi, active, changed0, changed1;
     DBuf<double> succ_wf, key_f, lam_f, cyc_wf;
     DBuf<long long> key_i, lam_num, lam_den, cyc_wi;
     DBuf<unsigned long long> slot;
-    DBuf<Flags> flags;
-    Flags* h_flags = nullptr;
+    DBuf<Ctl> ctl;
+    Ctl* h_ctl = nullptr;
     std::vector<cudaEvent_t> ev;
     cudaEvent_t ev_start = nullptr, ev_end = nullptr;
     KP kp{};
@@ -163,8 +201,9 @@ struct DeviceState {
     ~DeviceState() {
         if (stream)
             cudaStreamSynchronize(stream);
-        for (auto* b : {&row, &reg, &succ_e, &succ_v, &comp, &mark, &mark2, &wlist, &cyc_len, &conn,
-                        &rem0, &rem1, &src, &iters})
+        for (auto* b : {&row, &reg, &succ_e, &succ_v, &comp, &wlist, &cyc_len, &conn, &rem0, &rem1,
+                        &src, &iters, &indeg, &peel, &plist, &clist, &cidx, &csucc, &ccomp, &cmark,
+                        &cmark2})
             b->release();
         pv0.release();
         pv1.release();
@@ -174,7 +213,8 @@ struct DeviceState {
         fe.release();
         succ_wi.release();
         active.release();
-        changed.release();
+        changed0.release();
+        changed1.release();
         succ_wf.release();
         key_f.release();
         lam_f.release();
@@ -184,7 +224,7 @@ struct DeviceState {
         lam_den.release();
         cyc_wi.release();
         slot.release();
-        flags.release();
+        ctl.release();
         if (stream)
             cudaStreamSynchronize(stream);
         for (cudaEvent_t e : ev)
@@ -193,8 +233,8 @@ struct DeviceState {
             cudaEventDestroy(ev_start);
         if (ev_end)
             cudaEventDestroy(ev_end);
-        if (h_flags)
-            cudaFreeHost(h_flags);
+        if (h_ctl)
+            cudaFreeHost(h_ctl);
         if (stream)
             cudaStreamDestroy(stream);
     }

@@ -1,0 +1,1084 @@
+// The persistent policy-iteration kernel (included by solver.cu only).
+//
+// One cooperative launch runs a whole solve: every Howard iteration of
+// proj/include/ocm/howard_par.hpp:544 run() with its kernels as phases of
+// one grid, separated by grid-wide barriers. The host only launches and
+// reads the result; convergence, the doubling round count, the winning-cycle
+// round count and the re-attachment layers are all decided on the device.
+//
+//   phase                    replaces (howard_par.hpp)
+//   improve                  :146 spf_pass_iter (+ policy in-degree count)
+//   region check + leaves    :189 finished_regions / :208 deactivate_regions
+//   peel                     :249 elimination_fixpoint (first layers only)
+//   core doubling + verify   :249 elimination + :301 cycle_identification
+//   stats / vote / adopt     :319 record fill, :56 vote_min, :339 vote_and_adopt
+//   winning cycle            :494 value_propagate_fixpoint on the cycle
+//   keep core, unpeel        :370 set_min_cycle, :393 mark_min_component,
+//                            value propagation of kept vertices
+//   attach layers            :433 connect_gpi_fixpoint (+ values)
+//   float levels             :494 value_propagate_fixpoint (float lane)
+//
+// Cycle detection is peel-then-double: leaves of the functional policy
+// graph (in-degree 0) and the next few layers under them are peeled off
+// level by level while the layers are large; the remaining core (closed
+// under succ) is compacted and pointer-doubled; peeled vertices take their
+// anchor and value from their successor in reverse layer order. On the
+// benchmark graphs the first four layers hold ~80% of the vertices, so the
+// O(n log L) doubling runs on a fifth of them.
+//
+// Parity: every phase computes the same function as the reference step it
+// replaces; in particular the policy, anchors, lambdas and
+// integer keys are identical to the multi-kernel formulation this replaced,
+// which the GPU parity suite pins against the reference bit for bit.
+//
+// Memory model: arrays written inside the kernel are read with plain or
+// L1-bypassing loads (never __ldg); only the CSR (row, ew, fe) and region
+// ids are read-only for the whole launch. cooperative_groups grid.sync()
+// orders all global memory between phases.
+#pragma once
+
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "devcommon.cuh"
+
+namespace ocmb {
+namespace {
+
+namespace cg = cooperative_groups;
+
+constexpr int kMaxPeel = 32;
+constexpr int kSolveMinBlocks = 4; // register cap 64 at 256 threads
+
+__device__ __forceinline__ std::size_t gtid() {
+    return blockIdx.x * std::size_t(blockDim.x) + threadIdx.x;
+}
+__device__ __forceinline__ std::size_t gstride() { return std::size_t(gridDim.x) * blockDim.x; }
+
+template <class T> __device__ __forceinline__ T ldv(const T& x) {
+    return *reinterpret_cast<const volatile T*>(&x);
+}
+
+__device__ __forceinline__ bool working(const KP& p, std::uint32_t v) {
+    return ldv(p.active[__ldg(&p.reg[v])]) != 0;
+}
+
+// Set *flag to val unless it already is (read first: avoids store storms).
+template <class T> __device__ __forceinline__ void set_once(T* flag, T val) {
+    if (ldv(*flag) != val)
+        *flag = val;
+}
+
+// Block-wide OR of a predicate, then one store per block.
+template <class T> __device__ __forceinline__ void block_flag(bool pred, T* flag, T val) {
+    if (__syncthreads_or(pred) && threadIdx.x == 0)
+        set_once(flag, val);
+}
+
+// Cumulative append counters used in ping-pong pairs. An append phase
+// reserves slots on counter `cur`; after the phase's grid barrier every
+// thread calls take(), which reads how many were appended (the counter is
+// not touched again until two append phases later, so all threads read the
+// same value) and flips to the other counter. Every thread keeps identical
+// private copies of the bases.
+struct Ring {
+    unsigned long long* ctr; // ctl->ring[i]
+    unsigned long long base[2];
+    int cur;
+    __device__ void init(unsigned long long* c) {
+        ctr = c;
+        base[0] = ldv(c[0]);
+        base[1] = ldv(c[1]);
+        cur = 0;
+    }
+    __device__ __forceinline__ unsigned long long* counter() const { return &ctr[cur]; }
+    __device__ __forceinline__ unsigned long long origin() const { return base[cur]; }
+    __device__ std::uint64_t take() {
+        const unsigned long long v = ldv(ctr[cur]);
+        const std::uint64_t n = v - base[cur];
+        base[cur] = v;
+        cur ^= 1;
+        return n;
+    }
+};
+
+// Block-wide append: every thread of the block must call it (block-uniform
+// loops). Returns this thread's slot relative to the ring's phase origin.
+__device__ __forceinline__ std::uint64_t block_append(bool take, const Ring& ring) {
+    __shared__ unsigned s_cnt[kBlock / 32];
+    __shared__ unsigned long long s_base;
+    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const unsigned bal = __ballot_sync(FULL, take);
+    if (lane == 0)
+        s_cnt[warp] = __popc(bal);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned tot = 0;
+        for (unsigned w = 0; w < blockDim.x / 32; ++w) {
+            const unsigned c = s_cnt[w];
+            s_cnt[w] = tot;
+            tot += c;
+        }
+        s_base = tot ? atomicAdd(ring.counter(), static_cast<unsigned long long>(tot)) - ring.origin()
+                     : 0ull;
+    }
+    __syncthreads();
+    const std::uint64_t slot = s_base + s_cnt[warp] + __popc(bal & ((1u << lane) - 1u));
+    __syncthreads();
+    return slot;
+}
+
+// Block-reduced count added to the ring's current counter.
+__device__ __forceinline__ void block_count(unsigned mine, const Ring& ring) {
+    __shared__ unsigned s_sum;
+    if (threadIdx.x == 0)
+        s_sum = 0;
+    __syncthreads();
+    unsigned w = mine;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1)
+        w += __shfl_xor_sync(FULL, w, off);
+    if ((threadIdx.x & 31) == 0 && w)
+        atomicAdd(&s_sum, w);
+    __syncthreads();
+    if (threadIdx.x == 0 && s_sum)
+        atomicAdd(ring.counter(), static_cast<unsigned long long>(s_sum));
+}
+
+// ------------------------------------------------------------ improvement
+//
+// howard_par.hpp:146 spf_pass_iter / howard.hpp:63 improve_policy.
+// G lanes cooperate on one vertex and each lane keeps U edges in flight:
+// lane j streams edges row[v]+j, +G, ... (8-byte {target, weight} records),
+// gathers the U target keys together, and the group reduces the
+// lexicographic minimum (candidate, edge id) -- exactly the sequential
+// "first strictly smaller" scan. The incumbent's candidate is picked up on
+// the way (the incumbent is one of v's edges), so the replacement test costs
+// no extra gather; the lane owning the winning edge writes the new policy.
+// Every processed vertex also adds 1 to the in-degree of its (new or kept)
+// successor for the peeling that follows.
+
+template <int G> __device__ __forceinline__ unsigned group_mask() {
+    if constexpr (G == 32)
+        return FULL;
+    else
+        return ((1u << G) - 1u) << ((threadIdx.x & 31) & ~(G - 1));
+}
+
+// Region "changed" bookkeeping with at most one store per block per region.
+struct ChangedMarks {
+    std::uint32_t first = NONE;
+    std::uint32_t last_direct = NONE;
+    __device__ __forceinline__ void note(int* changed, std::uint32_t r) {
+        if (first == NONE)
+            first = r;
+        else if (r != first && r != last_direct) {
+            last_direct = r;
+            set_once(&changed[r], 1);
+        }
+    }
+    __device__ __forceinline__ void flush(int* changed) {
+        __shared__ std::uint32_t s_r;
+        if (threadIdx.x == 0)
+            s_r = NONE;
+        __syncthreads();
+        if (first != NONE) {
+            const std::uint32_t prev = atomicCAS(&s_r, NONE, first);
+            if (prev != NONE && prev != first)
+                set_once(&changed[first], 1);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0 && s_r != NONE)
+            set_once(&changed[s_r], 1);
+    }
+};
+
+template <bool EXACT, int G, int U> __device__ __noinline__ void improve_phase(const KP& p, int* changed) {
+    const unsigned lane = threadIdx.x & (G - 1);
+    const unsigned gm = group_mask<G>();
+    const std::size_t gid = gtid() / G;
+    const std::size_t gs = gstride() / G;
+    ChangedMarks marks;
+    using Key = typename std::conditional<EXACT, long long, double>::type;
+    const Key* __restrict__ key = EXACT ? reinterpret_cast<const Key*>(p.key_i)
+                                        : reinterpret_cast<const Key*>(p.key_f);
+    for (std::size_t vv = gid; vv < p.N; vv += gs) {
+        const std::uint32_t v = static_cast<std::uint32_t>(vv);
+        const std::uint32_t r = __ldg(&p.reg[v]);
+        if (!ldv(p.active[r]))
+            continue;
+        const std::uint32_t b = __ldg(&p.row[v]), e_end = __ldg(&p.row[v + 1]);
+        const std::uint32_t cur = p.succ_e[v];
+        long long num = 0, den = 1;
+        double lam = 0.0;
+        if constexpr (EXACT) {
+            num = p.lam_num[r];
+            den = p.lam_den[r];
+        } else {
+            lam = p.lam_f[r];
+        }
+        Key best = 0, curc = 0;
+        std::uint32_t be = NONE, bt = 0;
+        int bwi = 0;
+        double bwf = 0.0;
+        bool have_cur = false;
+        for (std::uint32_t e0 = b + lane; e0 < e_end; e0 += G * U) {
+            std::uint32_t tt[U];
+            Key kk[U];
+            int wi[U];
+            double wf[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const std::uint32_t e = e0 + u * G;
+                if (e < e_end) {
+                    if constexpr (EXACT) {
+                        const int2 ed = __ldg(&p.ew[e]);
+                        tt[u] = static_cast<std::uint32_t>(ed.x);
+                        wi[u] = ed.y;
+                    } else {
+                        const FEdge ed = p.fe[e];
+                        tt[u] = ed.t;
+                        wf[u] = ed.w;
+                    }
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (e0 + u * G < e_end)
+                    kk[u] = __ldcg(&key[tt[u]]);
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const std::uint32_t e = e0 + u * G;
+                if (e < e_end) {
+                    Key c;
+                    if constexpr (EXACT)
+                        c = kk[u] + static_cast<long long>(wi[u]) * den - num;
+                    else
+                        c = (kk[u] + wf[u]) - lam; // FloatMode::extend (policy.hpp:105)
+                    if (be == NONE || c < best) {
+                        best = c;
+                        be = e;
+                        bt = tt[u];
+                        if constexpr (EXACT)
+                            bwi = wi[u];
+                        else
+                            bwf = wf[u];
+                    }
+                    if (e == cur) {
+                        curc = c;
+                        have_cur = true;
+                    }
+                }
+            }
+        }
+        Key gbest = best;
+        std::uint32_t gbe = be;
+#pragma unroll
+        for (int off = G / 2; off > 0; off >>= 1) {
+            const Key ob = __shfl_xor_sync(gm, gbest, off, G);
+            const std::uint32_t oe = __shfl_xor_sync(gm, gbe, off, G);
+            if (oe != NONE && (gbe == NONE || ob < gbest || (ob == gbest && oe < gbe))) {
+                gbest = ob;
+                gbe = oe;
+            }
+            const Key oc = __shfl_xor_sync(gm, curc, off, G);
+            const bool oh = __shfl_xor_sync(gm, have_cur ? 1 : 0, off, G) != 0;
+            if (oh) {
+                curc = oc;
+                have_cur = true;
+            }
+        }
+        if (gbe == NONE) {
+            if (lane == 0)
+                p.c->error = 1;
+            continue;
+        }
+        bool rep = cur == NONE;
+        if (!rep) {
+            if constexpr (EXACT) {
+                rep = gbest < curc;
+            } else { // FloatMode::strictly_better (policy.hpp:116)
+                const double tol = 1e-9 * fmax(1.0, fmax(fabs(gbest), fabs(curc)));
+                rep = gbest < curc - tol;
+            }
+        }
+        if (rep) {
+            if (gbe == be) { // owner lane of the winning edge
+                p.succ_e[v] = be;
+                p.succ_v[v] = bt;
+                if constexpr (EXACT)
+                    p.succ_wi[v] = bwi;
+                else
+                    p.succ_wf[v] = bwf;
+                atomicAdd(&p.indeg[bt], 1u);
+                marks.note(changed, r);
+            }
+        } else if (lane == 0) {
+            atomicAdd(&p.indeg[p.succ_v[v]], 1u);
+        }
+    }
+    marks.flush(changed);
+}
+
+template <bool EXACT> __device__ __noinline__ void improve_dispatch(const KP& p, int* changed) {
+    switch (p.G) {
+    case 1: improve_phase<EXACT, 1, 4>(p, changed); break;
+    case 2: improve_phase<EXACT, 2, 4>(p, changed); break;
+    case 4: improve_phase<EXACT, 4, 4>(p, changed); break;
+    case 8: improve_phase<EXACT, 8, 2>(p, changed); break;
+    case 16: improve_phase<EXACT, 16, 2>(p, changed); break;
+    default: improve_phase<EXACT, 32, 2>(p, changed); break;
+    }
+}
+
+// ------------------------------------------------------------ helpers
+
+__device__ __forceinline__ long long gcd_ll(long long a, long long b) {
+    if (a < 0)
+        a = -a;
+    while (b) {
+        const long long t = a % b;
+        a = b;
+        b = t;
+    }
+    return a;
+}
+
+__device__ __forceinline__ bool key_in_range(__int128 k) {
+    const __int128 lim = static_cast<__int128>(1) << 62;
+    return k < lim && k > -lim;
+}
+
+template <bool EXACT>
+__device__ __forceinline__ bool rec_less(const KP& p, std::uint32_t a, std::uint32_t b) {
+    if constexpr (EXACT) {
+        const __int128 l = static_cast<__int128>(ldv(p.cyc_wi[a])) * ldv(p.cyc_len[b]);
+        const __int128 r = static_cast<__int128>(ldv(p.cyc_wi[b])) * ldv(p.cyc_len[a]);
+        if (l != r)
+            return l < r;
+    } else {
+        const double ma = ldv(p.cyc_wf[a]) / ldv(p.cyc_len[a]);
+        const double mb = ldv(p.cyc_wf[b]) / ldv(p.cyc_len[b]);
+        if (ma < mb)
+            return true;
+        if (mb < ma)
+            return false;
+    }
+    return a < b;
+}
+
+__device__ __forceinline__ int ceil_log2_d(unsigned long long x) {
+    return x <= 1 ? 0 : 64 - __clzll(x - 1);
+}
+
+
+// ------------------------------------------------------------ phases
+//
+// Each phase is a separate non-inlined function: its loop gets the whole
+// register budget, and the kernel's cross-phase state (ring bases, layer
+// offsets, stamps) is saved once per call instead of spilling inside loops.
+// Loops containing block_append/block_flag are block-uniform.
+
+#define OCM_BLOCK_LOOP(i, lo, hi)                                                                \
+    for (std::uint64_t i##_b = (lo) + blockIdx.x * std::uint64_t(kBlock); i##_b < (hi);          \
+         i##_b += gridDim.x * std::uint64_t(kBlock))
+
+__device__ __noinline__ void ph_init(const KP& p, bool exact) {
+    const std::size_t tid = gtid(), nth = gstride();
+    for (std::size_t v = tid; v < p.N; v += nth) {
+        p.succ_e[v] = NONE;
+        p.succ_v[v] = NONE;
+        if (exact)
+            p.key_i[v] = 0;
+        else
+            p.key_f[v] = 0.0;
+        p.indeg[v] = 0;
+        p.peel[v] = 0;
+    }
+    for (std::size_t r = tid; r <= p.R; r += nth) { // slot R: trivial vertices
+        p.lam_num[r] = 0;
+        p.lam_den[r] = 1;
+        p.lam_f[r] = 0.0;
+        p.active[r] = r < p.R ? 1 : 0;
+        p.changed[0][r] = 0;
+        p.changed[1][r] = 0;
+        p.slot[r] = EMPTY;
+        p.src[r] = NONE;
+        p.iters[r] = 0;
+    }
+}
+
+// Regions whose pass changed nothing are finished (howard_par.hpp:189/208);
+// counts the regions still active.
+__device__ __noinline__ void ph_region(const KP& p, int par, const Ring& ring) {
+    unsigned still = 0;
+    const int* changed = p.changed[par];
+    for (std::size_t r = gtid(); r < p.R; r += gstride()) {
+        if (p.active[r]) {
+            if (ldv(changed[r]))
+                ++still;
+            else
+                p.active[r] = 0;
+        }
+        p.changed[par ^ 1][r] = 0;
+    }
+    block_count(still, ring);
+}
+
+// Leaves of the policy graph: working vertices nobody points to.
+__device__ __noinline__ void ph_leaves(const KP& p, const Ring& ring) {
+    OCM_BLOCK_LOOP(v0, 0, p.N) {
+        const std::uint64_t v = v0_b + threadIdx.x;
+        const bool take = v < p.N && p.indeg[v] == 0 && working(p, static_cast<std::uint32_t>(v));
+        const std::uint64_t slot = block_append(take, ring);
+        if (take) {
+            p.peel[v] = 1;
+            p.plist[slot] = static_cast<std::uint32_t>(v);
+        }
+    }
+}
+
+// One peel layer: removing plist[lo, hi) drops its successors' in-degree;
+// those reaching 0 form the next layer at plist[hi...].
+__device__ __noinline__ void ph_peel(const KP& p, std::uint64_t lo, std::uint64_t hi,
+                                     std::uint32_t next_layer, const Ring& ring) {
+    OCM_BLOCK_LOOP(i0, lo, hi) {
+        const std::uint64_t i = i0_b + threadIdx.x;
+        bool take = false;
+        std::uint32_t s = 0;
+        if (i < hi) {
+            s = p.succ_v[p.plist[i]];
+            take = atomicSub(&p.indeg[s], 1u) == 1u;
+        }
+        const std::uint64_t slot = block_append(take, ring);
+        if (take) {
+            p.peel[s] = next_layer;
+            p.plist[hi + slot] = s;
+        }
+    }
+}
+
+// Core: working vertices not peeled (closed under succ), compacted.
+__device__ __noinline__ void ph_core(const KP& p, std::uint32_t done, const Ring& ring) {
+    OCM_BLOCK_LOOP(v0, 0, p.N) {
+        const std::uint64_t v = v0_b + threadIdx.x;
+        bool take = false;
+        if (v < p.N) {
+            const std::uint32_t pl = p.peel[v];
+            take = (pl == 0 || pl > done) && working(p, static_cast<std::uint32_t>(v));
+        }
+        const std::uint64_t slot = block_append(take, ring);
+        if (take) {
+            p.clist[slot] = static_cast<std::uint32_t>(v);
+            p.cidx[v] = static_cast<std::uint32_t>(slot);
+        }
+    }
+}
+
+template <bool EXACT> __device__ __noinline__ void ph_pjinit(const KP& p, std::uint64_t nC) {
+    for (std::uint64_t i = gtid(); i < nC; i += gstride()) {
+        const std::uint32_t v = p.clist[i];
+        const std::uint32_t s = p.succ_v[v];
+        const std::uint32_t ci = p.cidx[s];
+        PJC x;
+        x.nxt = ci;
+        x.mn = v;
+        x.w = EXACT ? static_cast<long long>(p.succ_wi[v]) : 0ll;
+        p.pj[0][i] = x;
+        p.csucc[i] = ci;
+        p.cyc_len[v] = 0;
+        if constexpr (EXACT)
+            p.cyc_wi[v] = 0;
+    }
+}
+
+// Synchronous pointer doubling of (segment end, least vertex, weight sum).
+__device__ __noinline__ void ph_round(const KP& p, std::uint64_t nC, int in) {
+    const PJC* __restrict__ a = p.pj[in];
+    PJC* __restrict__ o = p.pj[in ^ 1];
+    for (std::uint64_t i = gtid(); i < nC; i += gstride()) {
+        const PJC x = a[i];
+        const PJC y = a[x.nxt];
+        PJC z;
+        z.nxt = y.nxt;
+        z.mn = min(x.mn, y.mn);
+        z.w = x.w + y.w;
+        o[i] = z;
+    }
+}
+
+// Verification: M = image of succ^L passes iff every vertex
+// of M has a predecessor in M (no tail vertex) and the anchor is constant
+// along succ in M (every window covers its whole cycle).
+__device__ __noinline__ void ph_mark(const KP& p, std::uint64_t nC, int in, std::uint32_t stamp) {
+    const PJC* a = p.pj[in];
+    for (std::uint64_t i = gtid(); i < nC; i += gstride()) {
+        const std::uint32_t j = a[i].nxt;
+        p.ccomp[i] = a[j].mn;
+        if (p.cmark[j] != stamp) // many vertices share j: read before writing
+            p.cmark[j] = stamp;
+    }
+}
+
+__device__ __noinline__ void ph_verify1(const KP& p, std::uint64_t nC, std::uint32_t stamp,
+                                        unsigned* flag) {
+    bool fail = false;
+    OCM_BLOCK_LOOP(i0, 0, nC) {
+        const std::uint64_t i = i0_b + threadIdx.x;
+        if (i < nC && p.cmark[i] == stamp) {
+            const std::uint32_t s = p.csucc[i];
+            fail |= p.ccomp[s] != p.ccomp[i];
+            if (p.cmark2[s] != stamp)
+                p.cmark2[s] = stamp;
+        }
+    }
+    block_flag(fail, flag, stamp);
+}
+
+__device__ __noinline__ void ph_verify2(const KP& p, std::uint64_t nC, std::uint32_t stamp,
+                                        unsigned* flag) {
+    bool fail = false;
+    for (std::uint64_t i = gtid(); i < nC; i += gstride())
+        fail |= p.cmark[i] == stamp && p.cmark2[i] != stamp;
+    block_flag(fail, flag, stamp);
+}
+
+// Cycle records (length, weight) per anchor (howard_par.hpp:319).
+template <bool EXACT> __device__ __noinline__ void ph_stats(const KP& p, std::uint64_t nC, std::uint32_t stamp) {
+    if constexpr (EXACT) {
+        // integer segmented reduction (order-independent); a warp whose
+        // cycle vertices share one anchor pre-reduces to one atomic pair
+        const unsigned lane = threadIdx.x & 31;
+        const std::uint64_t wid = gtid() >> 5, ws = gstride() >> 5;
+        for (std::uint64_t base = wid * 32; base < nC; base += ws * 32) {
+            const std::uint64_t i = base + lane;
+            const bool on = i < nC && p.cmark[i] == stamp;
+            const unsigned am = __ballot_sync(FULL, on);
+            if (!am)
+                continue;
+            const std::uint32_t a = on ? p.ccomp[i] : 0u;
+            const int lead = __ffs(am) - 1;
+            const std::uint32_t a0 = __shfl_sync(FULL, a, lead);
+            const bool uni = __all_sync(FULL, !on || a == a0);
+            long long w = on ? static_cast<long long>(p.succ_wi[p.clist[i]]) : 0ll;
+            if (uni) {
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1)
+                    w += __shfl_xor_sync(FULL, w, off);
+                if (static_cast<int>(lane) == lead) {
+                    atomicAdd(&p.cyc_len[a0], static_cast<unsigned>(__popc(am)));
+                    atomicAdd(reinterpret_cast<unsigned long long*>(&p.cyc_wi[a0]),
+                              static_cast<unsigned long long>(w));
+                }
+            } else if (on) {
+                atomicAdd(&p.cyc_len[a], 1u);
+                atomicAdd(reinterpret_cast<unsigned long long*>(&p.cyc_wi[a]),
+                          static_cast<unsigned long long>(w));
+            }
+        }
+    } else {
+        // float: each anchor walks its own cycle from itself, summing in the
+        // reference's order (howard_par.hpp:323) -> identical means
+        for (std::uint64_t i = gtid(); i < nC; i += gstride()) {
+            const std::uint32_t v = p.clist[i];
+            if (p.cmark[i] != stamp || p.ccomp[i] != v)
+                continue;
+            double s = 0.0;
+            std::uint32_t len = 0, u = v;
+            do {
+                s += p.succ_wf[u];
+                ++len;
+                u = p.succ_v[u];
+            } while (u != v);
+            p.cyc_wf[v] = s;
+            p.cyc_len[v] = len;
+        }
+    }
+}
+
+// Region-specific minimum voting (howard_par.hpp:56 vote_min; paper
+// Alg. 5): a holder is replaced only by a strictly smaller (mean, anchor).
+template <bool EXACT> __device__ __noinline__ void ph_vote(const KP& p, std::uint64_t nC, std::uint32_t stamp) {
+    for (std::uint64_t i = gtid(); i < nC; i += gstride()) {
+        const std::uint32_t v = p.clist[i];
+        if (p.cmark[i] != stamp || p.ccomp[i] != v)
+            continue;
+        unsigned long long* cell = &p.slot[__ldg(&p.reg[v])];
+        unsigned long long cur = ldv(*cell);
+        for (;;) {
+            if (cur != EMPTY && !rec_less<EXACT>(p, v, static_cast<std::uint32_t>(cur)))
+                break;
+            const unsigned long long prev = atomicCAS(cell, cur, v);
+            if (prev == cur)
+                break;
+            cur = prev;
+        }
+    }
+}
+
+// Adoption (howard_par.hpp:349-364), per region.
+template <bool EXACT> __device__ __noinline__ void ph_adopt(const KP& p, std::uint32_t stamp) {
+    Ctl* c = p.c;
+    for (std::size_t r = gtid(); r < p.R; r += gstride()) {
+        if (!p.active[r])
+            continue;
+        const unsigned long long a = p.slot[r];
+        p.slot[r] = EMPTY;
+        if (a == EMPTY) {
+            c->error = 1;
+            continue;
+        }
+        p.src[r] = static_cast<std::uint32_t>(a);
+        const unsigned len = p.cyc_len[a];
+        atomicMax(&c->maxcyc, (static_cast<unsigned long long>(stamp) << 32) | len);
+        if constexpr (EXACT) {
+            long long num = p.cyc_wi[a], den = len;
+            const long long g = gcd_ll(num, den);
+            if (g > 1) {
+                num /= g;
+                den /= g;
+            }
+            if (p.iters[r] > 0 &&
+                static_cast<__int128>(p.lam_num[r]) * den < static_cast<__int128>(num) * p.lam_den[r])
+                c->lambda_up = 1;
+            p.lam_num[r] = num;
+            p.lam_den[r] = den;
+            const __int128 step = static_cast<__int128>(p.max_abs_w) * den + (num < 0 ? -num : num);
+            if (static_cast<__int128>(p.max_region) * step >= (static_cast<__int128>(1) << 62))
+                c->overflow = 1;
+        } else {
+            p.lam_f[r] = p.cyc_wf[a] / len;
+        }
+        p.iters[r] += 1;
+    }
+}
+
+// Winning-cycle vertices: prefix sums of w*den - num along the cycle, cut
+// at the anchor (value(anchor) = 0), by pointer jumping over them only.
+__device__ __noinline__ void ph_wc_init(const KP& p, std::uint64_t nC, std::uint32_t stamp,
+                                        const Ring& ring) {
+    OCM_BLOCK_LOOP(i0, 0, nC) {
+        const std::uint64_t i = i0_b + threadIdx.x;
+        bool take = false;
+        std::uint32_t v = 0, r = 0;
+        if (i < nC && p.cmark[i] == stamp) {
+            v = p.clist[i];
+            r = __ldg(&p.reg[v]);
+            take = p.ccomp[i] == p.src[r];
+        }
+        const std::uint64_t slot = block_append(take, ring);
+        if (take) {
+            p.wlist[slot] = v;
+            PJV x;
+            const std::uint32_t root = p.src[r];
+            if (v == root) {
+                x.acc = 0;
+                x.nxt = root;
+            } else {
+                x.acc = static_cast<long long>(p.succ_wi[v]) * p.lam_den[r] - p.lam_num[r];
+                x.nxt = p.succ_v[v];
+            }
+            x.root = root;
+            p.pv[0][v] = x;
+        }
+    }
+}
+
+__device__ __noinline__ void ph_wc_round(const KP& p, std::uint64_t nW, int j, std::uint64_t from,
+                                         std::uint64_t step) {
+    const PJV* __restrict__ a = p.pv[j & 1];
+    PJV* __restrict__ o = p.pv[(j & 1) ^ 1];
+    for (std::uint64_t i = from; i < nW; i += step) {
+        const std::uint32_t v = p.wlist[i];
+        const PJV x = a[v];
+        const PJV y = a[x.nxt];
+        PJV z;
+        z.acc = x.acc + y.acc;
+        z.nxt = y.nxt;
+        z.root = x.root;
+        o[v] = z;
+    }
+}
+
+__device__ __noinline__ void ph_wc_final(const KP& p, std::uint64_t nW, int wr, std::uint64_t from,
+                                         std::uint64_t step) {
+    const PJV* fin = p.pv[wr & 1];
+    for (std::uint64_t i = from; i < nW; i += step) {
+        const std::uint32_t v = p.wlist[i];
+        p.key_i[v] = fin[v].acc;
+    }
+}
+
+// Kept component (howard_par.hpp:370/393): vertices whose policy path
+// enters the winning cycle keep their edges; exact keys from the doubling
+// sums, K(v) = W_L(v)*den - L*num + K(jump v), since the winning cycle's
+// reduced weight is exactly 0. Others queue for re-attachment. Resets the
+// peeling state of core vertices.
+template <bool EXACT>
+__device__ __noinline__ void ph_keep(const KP& p, std::uint64_t nC, int in, std::uint32_t stamp,
+                                     unsigned long long L, const Ring& ring) {
+    const PJC* a = p.pj[in];
+    bool ovf = false;
+    OCM_BLOCK_LOOP(i0, 0, nC) {
+        const std::uint64_t i = i0_b + threadIdx.x;
+        bool take = false;
+        std::uint32_t v = 0;
+        if (i < nC) {
+            v = p.clist[i];
+            const std::uint32_t r = __ldg(&p.reg[v]);
+            const std::uint32_t an = p.ccomp[i];
+            const bool kept = an == p.src[r];
+            p.comp[v] = an;
+            p.conn[v] = kept ? 0u : NONE;
+            p.indeg[v] = 0;
+            p.peel[v] = 0;
+            take = !kept;
+            if (EXACT && kept && p.cmark[i] != stamp) {
+                const PJC x = a[i];
+                const __int128 kk = static_cast<__int128>(x.w) * p.lam_den[r] -
+                                    static_cast<__int128>(L) * p.lam_num[r] + p.key_i[p.clist[x.nxt]];
+                ovf |= !key_in_range(kk);
+                p.key_i[v] = static_cast<long long>(kk);
+            }
+        }
+        const std::uint64_t slot = block_append(take, ring);
+        if (take)
+            p.rem[0][slot] = v;
+    }
+    block_flag(ovf, &p.c->overflow, 1);
+}
+
+// One peeled layer, last layer first: anchor and key from the successor
+// (K(v) = K(succ) + w*den - num along the kept tree).
+template <bool EXACT>
+__device__ __noinline__ void ph_unpeel(const KP& p, std::uint64_t lo, std::uint64_t hi,
+                                       std::uint64_t out_base, const Ring& ring) {
+    bool ovf = false;
+    OCM_BLOCK_LOOP(i0, lo, hi) {
+        const std::uint64_t i = i0_b + threadIdx.x;
+        bool take = false;
+        std::uint32_t v = 0;
+        if (i < hi) {
+            v = p.plist[i];
+            const std::uint32_t s = p.succ_v[v];
+            const std::uint32_t r = __ldg(&p.reg[v]);
+            const std::uint32_t an = p.comp[s];
+            const bool kept = an == p.src[r];
+            p.comp[v] = an;
+            p.conn[v] = kept ? 0u : NONE;
+            p.peel[v] = 0;
+            take = !kept;
+            if (EXACT && kept) {
+                const __int128 kk = static_cast<__int128>(p.key_i[s]) +
+                                    static_cast<__int128>(p.succ_wi[v]) * p.lam_den[r] - p.lam_num[r];
+                ovf |= !key_in_range(kk);
+                p.key_i[v] = static_cast<long long>(kk);
+            }
+        }
+        const std::uint64_t slot = block_append(take, ring);
+        if (take)
+            p.rem[0][out_base + slot] = v;
+    }
+    block_flag(ovf, &p.c->overflow, 1);
+}
+
+// One breadth layer of howard_par.hpp:433 connectGpi: a pending vertex
+// attaches through its smallest out-edge whose head was connected in an
+// earlier layer (conn < layer); the stamps make the layer discipline exact
+// under any schedule.
+template <bool EXACT>
+__device__ __noinline__ void ph_attach(const KP& p, int cur, std::uint64_t pending, std::uint32_t layer,
+                                       const Ring& ring) {
+    const std::uint32_t* list = p.rem[cur];
+    bool ovf = false;
+    OCM_BLOCK_LOOP(i0, 0, pending) {
+        const std::uint64_t i = i0_b + threadIdx.x;
+        bool pend = false;
+        std::uint32_t x = 0;
+        if (i < pending) {
+            x = list[i];
+            pend = true;
+            const std::uint32_t b = __ldg(&p.row[x]), e_end = __ldg(&p.row[x + 1]);
+            for (std::uint32_t e = b; e < e_end; ++e) {
+                std::uint32_t t;
+                if constexpr (EXACT)
+                    t = static_cast<std::uint32_t>(__ldg(&p.ew[e]).x);
+                else
+                    t = p.fe[e].t;
+                if (ldv(p.conn[t]) < layer) {
+                    p.succ_e[x] = e;
+                    p.succ_v[x] = t;
+                    if constexpr (EXACT) {
+                        const int w = __ldg(&p.ew[e]).y;
+                        p.succ_wi[x] = w;
+                        const std::uint32_t r = __ldg(&p.reg[x]);
+                        const __int128 kk = static_cast<__int128>(ldv(p.key_i[t])) +
+                                            static_cast<__int128>(w) * p.lam_den[r] - p.lam_num[r];
+                        ovf |= !key_in_range(kk);
+                        p.key_i[x] = static_cast<long long>(kk);
+                    } else {
+                        p.succ_wf[x] = p.fe[e].w;
+                    }
+                    p.conn[x] = layer;
+                    pend = false;
+                    break;
+                }
+            }
+        }
+        const std::uint64_t slot = block_append(pend, ring);
+        if (pend)
+            p.rem[cur ^ 1][slot] = x;
+    }
+    block_flag(ovf, &p.c->overflow, 1);
+}
+
+// Float lane: level-synchronous propagation from the anchor, computing
+// (value(succ) + w) - lambda exactly as FloatMode::extend (policy.hpp:105).
+__device__ __noinline__ void ph_fprop_init(const KP& p) {
+    for (std::size_t v = gtid(); v < p.N; v += gstride()) {
+        if (!working(p, static_cast<std::uint32_t>(v)))
+            continue;
+        if (v == p.src[__ldg(&p.reg[v])]) {
+            p.conn[v] = 0;
+            p.key_f[v] = 0.0;
+        } else {
+            p.conn[v] = NONE;
+        }
+    }
+}
+
+__device__ __noinline__ void ph_fprop_level(const KP& p, std::uint32_t level, unsigned long long* flag,
+                                            unsigned long long tag) {
+    bool nd = false;
+    OCM_BLOCK_LOOP(v0, 0, p.N) {
+        const std::uint64_t v = v0_b + threadIdx.x;
+        if (v >= p.N || ldv(p.conn[v]) != NONE || !working(p, static_cast<std::uint32_t>(v)))
+            continue;
+        const std::uint32_t s = p.succ_v[v];
+        if (ldv(p.conn[s]) < level) {
+            p.key_f[v] = (ldv(p.key_f[s]) + p.succ_wf[v]) - p.lam_f[__ldg(&p.reg[v])];
+            p.conn[v] = level;
+        } else {
+            nd = true;
+        }
+    }
+    block_flag(nd, flag, tag);
+}
+
+// ------------------------------------------------------------ the kernel
+//
+// Control decisions are taken by every thread from values that are
+// identical grid-wide: ring counts read after a barrier, stamped flags read
+// after a barrier and not written again until one barrier later (two slots,
+// alternating), and thread-local loop state. A flag read right after a
+// barrier is never written in the phase that follows it.
+
+template <bool EXACT> __global__ void __launch_bounds__(kBlock, kSolveMinBlocks) k_solve(KP p) {
+    cg::grid_group grid = cg::this_grid();
+    Ctl* const c = p.c;
+    const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
+    Ring ring;
+    ring.init(c->ring[0]);
+    unsigned long long nsync = 0;
+    long long clk0 = 0, clk_last = 0;
+    if (leader)
+        clk_last = clk0 = clock64();
+    auto sync = [&](int ph) {
+        grid.sync();
+        ++nsync;
+        if (leader) {
+            const long long t = clock64();
+            c->clk[ph] += t - clk_last;
+            clk_last = t;
+        }
+    };
+    const int K_max = max(1, ceil_log2_d(max(p.max_region, 2u)));
+    unsigned stamp = ldv(c->stamp);
+    unsigned k_hint = max(1u, min(ldv(c->k_hint), static_cast<unsigned>(K_max)));
+    unsigned k_streak = ldv(c->k_streak);
+    unsigned passes = 0, outer = 0;
+    unsigned long long rounds = 0, verifies = 0, peeled = 0, cored = 0, layers = 0;
+    bool fatal = false; // uniform: a fixpoint failed to converge
+
+    ph_init(p, EXACT);
+    sync(PH_INIT);
+
+    for (int it = 0;; ++it) {
+        const int par = it & 1;
+        improve_dispatch<EXACT>(p, p.changed[par]);
+        ++passes;
+        sync(PH_IMPROVE);
+
+        ph_region(p, par, ring);
+        sync(PH_REGION);
+        const std::uint64_t n_active = ring.take();
+        // written only by improve/adopt/keep/unpeel/attach, never by the
+        // leaves phase that follows: every block reads the same values here
+        if (n_active == 0 || ldv(c->error) || ldv(c->overflow) || ldv(c->lambda_up))
+            break; // quiet pass (or a failure the host reports)
+        ++outer;
+
+        // ---- peel while the layers are large
+        ph_leaves(p, ring);
+        sync(PH_LEAVES);
+        std::uint64_t lofs[kMaxPeel + 2];
+        lofs[0] = 0;
+        lofs[1] = ring.take();
+        int done = 0;
+        while (done < p.peel_max && lofs[done + 1] - lofs[done] >= p.peel_min) {
+            ph_peel(p, lofs[done], lofs[done + 1], static_cast<std::uint32_t>(done + 2), ring);
+            sync(PH_PEEL);
+            ++done;
+            lofs[done + 1] = lofs[done] + ring.take();
+        }
+        peeled += lofs[done];
+
+        ph_core(p, static_cast<std::uint32_t>(done), ring);
+        sync(PH_CORE);
+        const std::uint64_t nC = ring.take();
+        cored += nC;
+        ph_pjinit<EXACT>(p, nC);
+        sync(PH_PJINIT);
+
+        // ---- pointer doubling on the core, verified exactly
+        int in = 0, k = 0;
+        bool first_try = true;
+        for (;;) {
+            for (; k < static_cast<int>(k_hint); ++k, in ^= 1) {
+                ph_round(p, nC, in);
+                ++rounds;
+                sync(PH_ROUND);
+            }
+            ++stamp;
+            ++verifies;
+            unsigned* vflag = &c->vfail[stamp & 1];
+            ph_mark(p, nC, in, stamp);
+            sync(PH_VERIFY);
+            ph_verify1(p, nC, stamp, vflag);
+            sync(PH_VERIFY);
+            ph_verify2(p, nC, stamp, vflag);
+            sync(PH_VERIFY);
+            if (ldv(*vflag) != stamp)
+                break;
+            if (k >= K_max) {
+                fatal = true;
+                break;
+            }
+            k_hint = k + 1;
+            first_try = false;
+        }
+        if (fatal)
+            break;
+        // adapt the starting round count: shrink after two first-try passes
+        if (first_try && ++k_streak >= 2 && k > 1) {
+            k_hint = k - 1;
+            k_streak = 0;
+        } else {
+            k_hint = k;
+            if (!first_try)
+                k_streak = 0;
+        }
+
+        // ---- cycle records, vote, adoption
+        ph_stats<EXACT>(p, nC, stamp);
+        sync(PH_STATS);
+        ph_vote<EXACT>(p, nC, stamp);
+        sync(PH_VOTE);
+        ph_adopt<EXACT>(p, stamp);
+        sync(PH_ADOPT);
+
+        // ---- values on the winning cycle(s)
+        if constexpr (EXACT) {
+            ph_wc_init(p, nC, stamp, ring);
+            sync(PH_WINCYC);
+            const std::uint64_t nW = ring.take();
+            const unsigned long long mc = ldv(c->maxcyc);
+            const unsigned maxlen = (mc >> 32) == stamp ? static_cast<unsigned>(mc) : 1u;
+            const int wr = ceil_log2_d(maxlen > 1 ? maxlen - 1 : 1); // farthest: len-1 steps
+            if (nW <= p.small_wc) {
+                if (blockIdx.x == 0) { // one block, block barriers only
+                    for (int j = 0; j < wr; ++j) {
+                        ph_wc_round(p, nW, j, threadIdx.x, blockDim.x);
+                        __syncthreads();
+                    }
+                    ph_wc_final(p, nW, wr, threadIdx.x, blockDim.x);
+                }
+            } else {
+                for (int j = 0; j < wr; ++j) {
+                    ph_wc_round(p, nW, j, gtid(), gstride());
+                    sync(PH_WINCYC);
+                }
+                ph_wc_final(p, nW, wr, gtid(), gstride());
+            }
+            rounds += wr;
+            sync(PH_WINCYC);
+        }
+
+        // ---- kept component, peeled layers in reverse, re-attachment
+        ph_keep<EXACT>(p, nC, in, stamp, 1ull << k, ring);
+        sync(PH_KEEP);
+        std::uint64_t pending = ring.take();
+        for (int l = done; l >= 1; --l) {
+            ph_unpeel<EXACT>(p, lofs[l - 1], lofs[l], pending, ring);
+            sync(PH_UNPEEL);
+            pending += ring.take();
+        }
+        int cur = 0;
+        for (std::uint32_t layer = 1; pending > 0; ++layer) {
+            ph_attach<EXACT>(p, cur, pending, layer, ring);
+            sync(PH_ATTACH);
+            const std::uint64_t next = ring.take();
+            ++layers;
+            if (next == pending) { // connect_gpi_fixpoint: not strongly connected
+                fatal = true;
+                break;
+            }
+            pending = next;
+            cur ^= 1;
+        }
+        if (fatal)
+            break;
+
+        if constexpr (!EXACT) {
+            ph_fprop_init(p);
+            sync(PH_FLOAT);
+            for (std::uint32_t level = 1;; ++level) {
+                unsigned long long* flag = &c->fnd[level & 1];
+                const unsigned long long tag = (static_cast<unsigned long long>(stamp) << 32) | level;
+                ph_fprop_level(p, level, flag, tag);
+                sync(PH_FLOAT);
+                ++layers;
+                if (ldv(*flag) != tag)
+                    break;
+                if (level > p.max_region + 1) {
+                    fatal = true;
+                    break;
+                }
+            }
+            if (fatal)
+                break;
+        }
+    }
+
+    if (leader) {
+        if (fatal)
+            c->nonconv = 1;
+        c->stamp = stamp;
+        c->k_hint = k_hint;
+        c->k_streak = k_streak;
+        c->passes = passes;
+        c->outer = outer;
+        c->rounds = rounds;
+        c->verifies = verifies;
+        c->peeled = peeled;
+        c->cored = cored;
+        c->layers = layers;
+        c->syncs = nsync;
+        c->clk_total = clock64() - clk0;
+    }
+}
+
+} // namespace
+} // namespace ocmb

@@ -14,7 +14,7 @@
 #include <string>
 
 #include "errors.hpp"
-#include "kernels.cuh"
+#include "solve_kernel.cuh"
 #include "solver.hpp"
 
 namespace ocmb {
@@ -50,7 +50,7 @@ Session::Session(const Graph& g, const ocm_solve_options& opt) : opt_(opt) {
     }
     CK(cudaEventCreate(&d.ev_start));
     CK(cudaEventCreate(&d.ev_end));
-    CK(cudaMallocHost(&d.h_flags, sizeof(Flags)));
+    CK(cudaMallocHost(&d.h_ctl, sizeof(Ctl)));
 
     device_prepare(g, opt, d, prep_);
 
@@ -67,21 +67,43 @@ Session::Session(const Graph& g, const ocm_solve_options& opt) : opt_(opt) {
         d.key_f.alloc(N1, d.stream);
         d.cyc_wf.alloc(N1, d.stream);
     }
-    for (auto* b : {&d.succ_e, &d.succ_v, &d.comp, &d.mark, &d.mark2, &d.wlist, &d.cyc_len, &d.conn,
-                    &d.rem0, &d.rem1})
+    for (auto* b : {&d.succ_e, &d.succ_v, &d.comp, &d.wlist, &d.cyc_len, &d.conn, &d.rem0, &d.rem1,
+                    &d.indeg, &d.peel, &d.plist, &d.clist, &d.cidx, &d.csucc, &d.ccomp, &d.cmark,
+                    &d.cmark2})
         b->alloc(N1, d.stream);
     d.pj0.alloc(N1, d.stream);
     d.pj1.alloc(N1, d.stream);
     d.src.alloc(R1, d.stream);
     d.iters.alloc(R1, d.stream);
     d.active.alloc(R1, d.stream);
-    d.changed.alloc(R1, d.stream);
+    d.changed0.alloc(R1, d.stream);
+    d.changed1.alloc(R1, d.stream);
     d.lam_f.alloc(R1, d.stream);
     d.lam_num.alloc(R1, d.stream);
     d.lam_den.alloc(R1, d.stream);
     d.slot.alloc(R1, d.stream);
-    d.flags.alloc(1, d.stream);
+    d.ctl.alloc(1, d.stream);
+    // verification stamps start at 1: the stamp arrays and the control block
+    // start from zero once per session
+    CK(cudaMemsetAsync(d.cmark.p, 0, N1 * sizeof(std::uint32_t), d.stream));
+    CK(cudaMemsetAsync(d.cmark2.p, 0, N1 * sizeof(std::uint32_t), d.stream));
+    CK(cudaMemsetAsync(d.ctl.p, 0, sizeof(Ctl), d.stream));
+    {
+        Ctl init{};
+        init.k_hint = 4;
+        CK(cudaMemcpyAsync(d.ctl.p, &init, sizeof(Ctl), cudaMemcpyHostToDevice, d.stream));
+    }
     CK(cudaStreamSynchronize(d.stream));
+
+    // one CTA per SM slot the register budget allows (<= kSolveMinBlocks)
+    for (int e = 0; e < 2; ++e) {
+        int per_sm = 0;
+        const void* fn = e ? reinterpret_cast<const void*>(&k_solve<false>)
+                           : reinterpret_cast<const void*>(&k_solve<true>);
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kBlock, 0));
+        per_sm = std::max(1, std::min(per_sm, kSolveMinBlocks));
+        (e ? grid_float_ : grid_exact_) = per_sm * d.sms;
+    }
 
     KP& p = d.kp;
     p.N = prep_.n;
@@ -100,15 +122,23 @@ Session::Session(const Graph& g, const ocm_solve_options& opt) : opt_(opt) {
     p.lam_den = d.lam_den.p;
     p.lam_f = d.lam_f.p;
     p.active = d.active.p;
-    p.changed = d.changed.p;
+    p.changed[0] = d.changed0.p;
+    p.changed[1] = d.changed1.p;
     p.slot = d.slot.p;
     p.src = d.src.p;
     p.iters = d.iters.p;
     p.pj[0] = d.pj0.p;
     p.pj[1] = d.pj1.p;
     p.comp = d.comp.p;
-    p.mark = d.mark.p;
-    p.mark2 = d.mark2.p;
+    p.indeg = d.indeg.p;
+    p.peel = d.peel.p;
+    p.plist = d.plist.p;
+    p.clist = d.clist.p;
+    p.cidx = d.cidx.p;
+    p.csucc = d.csucc.p;
+    p.ccomp = d.ccomp.p;
+    p.cmark = d.cmark.p;
+    p.cmark2 = d.cmark2.p;
     p.wlist = d.wlist.p;
     p.cyc_len = d.cyc_len.p;
     p.cyc_wi = d.cyc_wi.p;
@@ -118,7 +148,7 @@ Session::Session(const Graph& g, const ocm_solve_options& opt) : opt_(opt) {
     p.rem[1] = d.rem1.p;
     p.pv[0] = d.pv0.p;
     p.pv[1] = d.pv1.p;
-    p.flags = d.flags.p;
+    p.c = d.ctl.p;
     p.max_region = prep_.max_region;
     p.max_abs_w = prep_.max_abs_w;
     h2d_bytes_ = prep_.h2d_bytes;
@@ -131,36 +161,9 @@ void* Session::stream() const { return d_ ? d_->stream : nullptr; }
 
 namespace {
 
-template <bool EXACT, int U> void launch_improve_u(const KP& p, int grid_sms, cudaStream_t s, int G) {
-    const std::size_t threads = std::size_t(p.N) * G;
-    const int grid = grid_for(threads, grid_sms, 8);
-    switch (G) {
-    case 1: k_improve<EXACT, 1, U><<<grid, kBlock, 0, s>>>(p); break;
-    case 2: k_improve<EXACT, 2, U><<<grid, kBlock, 0, s>>>(p); break;
-    case 4: k_improve<EXACT, 4, U><<<grid, kBlock, 0, s>>>(p); break;
-    case 8: k_improve<EXACT, 8, U><<<grid, kBlock, 0, s>>>(p); break;
-    case 16: k_improve<EXACT, 16, U><<<grid, kBlock, 0, s>>>(p); break;
-    default: k_improve<EXACT, 32, U><<<grid, kBlock, 0, s>>>(p); break;
-    }
-}
-
-// G lanes per vertex with U edges in flight per lane, G*U ~ average degree.
-// OCM_IMPROVE_G / OCM_IMPROVE_U override the choice (tuning sweeps).
-template <bool EXACT> void launch_improve(const KP& p, int sms, cudaStream_t s, double avg_deg) {
-    static const int env_g = std::getenv("OCM_IMPROVE_G") ? std::atoi(std::getenv("OCM_IMPROVE_G")) : 0;
-    static const int env_u = std::getenv("OCM_IMPROVE_U") ? std::atoi(std::getenv("OCM_IMPROVE_U")) : 0;
-    const int U = env_u ? env_u : 4;
-    int G = 1;
-    while (G < 32 && G * U < avg_deg)
-        G *= 2;
-    if (env_g)
-        G = env_g;
-    switch (U) {
-    case 1: launch_improve_u<EXACT, 1>(p, sms, s, G); break;
-    case 2: launch_improve_u<EXACT, 2>(p, sms, s, G); break;
-    case 8: launch_improve_u<EXACT, 8>(p, sms, s, G); break;
-    default: launch_improve_u<EXACT, 4>(p, sms, s, G); break;
-    }
+int env_int(const char* name, int dflt) {
+    const char* v = std::getenv(name);
+    return v ? std::atoi(v) : dflt;
 }
 
 } // namespace
@@ -170,224 +173,83 @@ template <class M> void Session::run(ocm_solution* out, std::uint32_t* cycle_buf
     DeviceState& d = *d_;
     KP& p = d.kp;
     cudaStream_t s = d.stream;
-    const int gv = grid_for(p.N, d.sms);
-    const int gr = grid_for(std::max<std::uint32_t>(p.R, 1), d.sms);
-    const double avg_deg = prep_.R ? double(prep_.M) / std::max<double>(1.0, double(prep_.n - prep_.trivial)) : 1.0;
-    std::uint64_t launches = 0, fix_iters = 0;
-    std::uint32_t passes = 0, outer = 0;
-    Flags& hf = *d.h_flags;
-
-    // Optional per-phase CUDA-event breakdown (OCM_PHASES=1 -> one JSON line
-    // on stderr per solve). Events are recorded on the launching stream.
-    static const bool phases_on = std::getenv("OCM_PHASES") != nullptr;
-    std::vector<std::pair<int, cudaEvent_t>> marks;
-    std::vector<cudaEvent_t> pool;
-    auto mark = [&](int phase) {
-        if (!phases_on)
-            return;
-        cudaEvent_t e;
-        CK(cudaEventCreate(&e));
-        CK(cudaEventRecord(e, s));
-        marks.push_back({phase, e});
-    };
-    std::uint64_t layers_total = 0;
+    Ctl& hc = *d.h_ctl;
     std::uint64_t d2h = 0;
-    auto read_flags = [&] {
-        d2h += sizeof(Flags);
-        CK(cudaMemcpyAsync(&hf, p.flags, sizeof(Flags), cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
-        if (hf.error)
-            throw std::logic_error("howard_par: structural error (a vertex has no successor "
-                                   "inside its region, or a region is not strongly connected)");
-        if (hf.lambda_up)
-            throw std::logic_error("vote_and_adopt: lambda increased");
-        if (hf.overflow)
-            throw RangeError("exact value keys would exceed 62 bits for this graph");
-    };
+
+    // G lanes per improvement vertex: G*4 ~ average degree (U = 4 edges in
+    // flight per lane). OCM_IMPROVE_G / OCM_PEEL_MIN / OCM_PEEL_MAX override.
+    const double avg_deg = prep_.R ? double(prep_.M) / std::max<double>(1.0, double(prep_.n - prep_.trivial)) : 1.0;
+    int G = 1;
+    while (G < 32 && G * 4 < avg_deg)
+        G *= 2;
+    p.G = env_int("OCM_IMPROVE_G", G);
+    p.peel_min = static_cast<std::uint32_t>(
+        env_int("OCM_PEEL_MIN", static_cast<int>(std::max<std::uint32_t>(4096u, prep_.n >> 8))));
+    p.peel_max = std::min(kMaxPeel, env_int("OCM_PEEL_MAX", 16));
+    p.small_wc = 4096;
 
     CK(cudaEventRecord(d.ev_start, s));
-    CK(cudaMemsetAsync(p.flags, 0, sizeof(Flags), s));
-    if (p.N) {
-        k_init<<<gv, kBlock, 0, s>>>(p);
-        ++launches;
+    CK(cudaMemsetAsync(reinterpret_cast<char*>(p.c) + kCtlSolveOffset, 0, sizeof(Ctl) - kCtlSolveOffset, s));
+    if (prep_.R > 0) {
+        void* args[] = {&p};
+        const void* fn = EXACT ? reinterpret_cast<const void*>(&k_solve<true>)
+                               : reinterpret_cast<const void*>(&k_solve<false>);
+        CK(cudaLaunchCooperativeKernel(fn, dim3(EXACT ? grid_exact_ : grid_float_), dim3(kBlock), args, 0, s));
     }
-    // Upper bound on doubling rounds (2^K_max >= region size) and the
-    // session's running estimates of the rounds actually needed.
-    const int K_max = std::max(1, ceil_log2(std::max<std::uint32_t>(prep_.max_region, 2)));
-    int k_need = std::min(K_max, k_hint_);
-    std::uint32_t stamp = stamp_base_;
-    // Two host synchronisations per iteration: (1) after the improvement pass
-    // and the cycle-detection check (termination + round-count verdict), (2)
-    // after the kept-component pass (re-attachment workload). Kernels between
-    // them are gated on device flags, so the quiet final pass costs no work.
-    while (prep_.R > 0) {
-        mark(0);
-        CK(cudaMemsetAsync(&p.flags->active_count, 0, sizeof(unsigned), s));
-        CK(cudaEventRecord(d.event(2 * passes), s));
-        launch_improve<EXACT>(p, d.sms, s, avg_deg);
-        CK(cudaEventRecord(d.event(2 * passes + 1), s));
-        ++passes;
-        k_region_check<<<gr, kBlock, 0, s>>>(p);
-        launches += 2;
-
-        // cycles of the policy graph: double until the exact check passes
-        mark(1);
-        k_pj_init<EXACT><<<gv, kBlock, 0, s>>>(p);
-        ++launches;
-        int in = 0, k = 0;
-        bool quiet = false;
-        for (;;) {
-            for (; k < k_need; ++k, in ^= 1) {
-                k_pj_round<<<gv, kBlock, 0, s>>>(p, in);
-                ++launches;
-                ++fix_iters;
-            }
-            ++stamp;
-            CK(cudaMemsetAsync(&p.flags->verify_fail, 0, sizeof(int), s));
-            k_cycle_mark<<<gv, kBlock, 0, s>>>(p, in, stamp);
-            k_cycle_verify1<<<gv, kBlock, 0, s>>>(p, stamp);
-            k_cycle_verify2<<<gv, kBlock, 0, s>>>(p, stamp);
-            launches += 3;
-            read_flags();
-            if (hf.active_count == 0) {
-                quiet = true;
-                break;
-            }
-            if (!hf.verify_fail)
-                break;
-            if (k >= K_max)
-                throw std::logic_error("cycle detection did not converge within log2(n) rounds");
-            k_need = k + 1;
-        }
-        if (quiet)
-            break;
-        ++outer;
-        k_hint_ = k;
-
-        mark(2);
-        CK(cudaMemsetAsync(&p.flags->max_cycle, 0, 3 * sizeof(unsigned), s)); // + wc_count, wc_short
-        if constexpr (EXACT)
-            k_cycle_stats<<<gv, kBlock, 0, s>>>(p, stamp);
-        else
-            k_cycle_walk_float<<<gv, kBlock, 0, s>>>(p);
-        k_vote<EXACT><<<gv, kBlock, 0, s>>>(p);
-        k_adopt<EXACT><<<gr, kBlock, 0, s>>>(p);
-        launches += 3;
-        // values of the winning cycle(s): prefix sums cut at the anchor, with
-        // the round count of the previous iteration (+1); re-run exactly if short
-        auto wincyc = [&](int rounds) {
-            CK(cudaMemsetAsync(p.flags->notdone, 0, rounds * sizeof(unsigned), s));
-            const int gw = grid_for(std::max<std::uint32_t>(prep_.max_region, 1), d.sms);
-            for (int j = 0; j < rounds; ++j)
-                k_wincyc_round<<<gw, kBlock, 0, s>>>(p, j);
-            k_wincyc_final<<<gw, kBlock, 0, s>>>(p, rounds);
-            launches += 1 + rounds;
-            fix_iters += rounds;
-        };
-        auto keep = [&] {
-            CK(cudaMemsetAsync(&p.flags->rem_count[0], 0, sizeof(unsigned), s));
-            k_keep<EXACT><<<gv, kBlock, 0, s>>>(p, in, stamp, 1ull << k);
-            ++launches;
-        };
-        if constexpr (EXACT) {
-            k_wincyc_init<<<gv, kBlock, 0, s>>>(p, stamp);
-            ++launches;
-            wincyc(std::min(kMaxRounds, wc_hint_));
-        }
-        keep();
-        read_flags();
-        if (EXACT && hf.wc_short) {
-            const int rounds = std::min(kMaxRounds, ceil_log2(std::max(hf.max_cycle, 2u)) + 1);
-            CK(cudaMemsetAsync(&p.flags->wc_short, 0, sizeof(int), s));
-            wincyc(rounds);
-            keep();
-            read_flags();
-            if (hf.wc_short)
-                throw std::logic_error("winning-cycle prefix sums did not converge");
-        }
-        if (EXACT)
-            wc_hint_ = std::max(2, ceil_log2(std::max(hf.max_cycle, 2u)) + 1);
-
-        // breadth-layered re-attachment (+ values of re-attached vertices)
-        mark(3);
-        unsigned pending = hf.rem_count[0];
-        int cur = 0;
-        for (std::uint32_t layer = 1; pending > 0; ++layer) {
-            CK(cudaMemsetAsync(&p.flags->rem_count[cur ^ 1], 0, sizeof(unsigned), s));
-            k_attach<EXACT><<<grid_for(pending, d.sms), kBlock, 0, s>>>(p, cur, pending, layer);
-            ++launches;
-            ++fix_iters;
-            read_flags();
-            const unsigned next = hf.rem_count[cur ^ 1];
-            if (next == pending)
-                throw std::logic_error("connect_gpi_fixpoint: region is not strongly connected");
-            pending = next;
-            cur ^= 1;
-            ++layers_total;
-        }
-
-        // float mode: level-synchronous value propagation (bit-exact order)
-        mark(4);
-        if constexpr (!EXACT) {
-            k_fprop_init<<<gv, kBlock, 0, s>>>(p);
-            ++launches;
-            for (std::uint32_t level = 1;; ++level) {
-                CK(cudaMemsetAsync(&p.flags->notdone[0], 0, sizeof(unsigned), s));
-                k_fprop_round<<<gv, kBlock, 0, s>>>(p, level, 0);
-                ++launches;
-                ++fix_iters;
-                read_flags();
-                if (hf.notdone[0] == 0)
-                    break;
-                if (level > prep_.max_region + 1)
-                    throw std::logic_error("value propagation did not converge");
-            }
-        }
-    }
-    stamp_base_ = stamp;
-    mark(5);
     CK(cudaEventRecord(d.ev_end, s));
+    CK(cudaMemcpyAsync(&hc, p.c, sizeof(Ctl), cudaMemcpyDeviceToHost, s));
+    d2h += sizeof(Ctl);
     CK(cudaStreamSynchronize(s));
     CK(cudaGetLastError());
-    read_flags();
-    if (phases_on && !marks.empty()) {
-        double acc[6] = {0, 0, 0, 0, 0, 0};
-        for (std::size_t i = 0; i + 1 < marks.size(); ++i) {
-            float t = 0.f;
-            CK(cudaEventElapsedTime(&t, marks[i].second, marks[i + 1].second));
-            acc[marks[i].first] += t;
-        }
-        for (auto& m : marks)
-            cudaEventDestroy(m.second);
-        std::fprintf(stderr,
-                     "{\"phases_ms\": {\"improve+check\": %.3f, \"pointer_jump\": %.3f, "
-                     "\"stats_vote_keep\": %.3f, \"attach\": %.3f, \"values\": %.3f}, "
-                     "\"passes\": %u, \"attach_layers\": %llu, \"N\": %u, \"M\": %llu}\n",
-                     acc[0], acc[1], acc[2], acc[3], acc[4], passes,
-                     (unsigned long long)layers_total, p.N, (unsigned long long)prep_.M);
-    }
+    if (hc.error)
+        throw std::logic_error("howard_par: structural error (a vertex has no successor "
+                               "inside its region, or a region is not strongly connected)");
+    if (hc.lambda_up)
+        throw std::logic_error("vote_and_adopt: lambda increased");
+    if (hc.overflow)
+        throw RangeError("exact value keys would exceed 62 bits for this graph");
+    if (hc.nonconv)
+        throw std::logic_error("a device fixpoint did not converge within its bound");
 
     float ms = 0.f;
     CK(cudaEventElapsedTime(&ms, d.ev_start, d.ev_end));
-    double imp = 0.0;
-    for (std::uint32_t i = 0; i < passes; ++i) {
-        float t = 0.f;
-        CK(cudaEventElapsedTime(&t, d.event(2 * i), d.event(2 * i + 1)));
-        imp += t;
+    static const bool phases_on = std::getenv("OCM_PHASES") != nullptr;
+    if (phases_on && prep_.R > 0 && hc.clk_total > 0) {
+        static const char* names[PH_COUNT] = {"init",   "improve", "region", "leaves", "peel",
+                                              "core",   "pjinit",  "round",  "verify", "stats",
+                                              "vote",   "adopt",   "wincyc", "keep",   "unpeel",
+                                              "attach", "float"};
+        std::string ph;
+        for (int i = 0; i < PH_COUNT; ++i) {
+            char buf[64];
+            std::snprintf(buf, sizeof buf, "%s\"%s\": %.3f", i ? ", " : "", names[i],
+                          ms * double(hc.clk[i]) / double(hc.clk_total));
+            ph += buf;
+        }
+        std::fprintf(stderr,
+                     "{\"device_ms\": %.3f, \"phases_ms\": {%s}, \"passes\": %u, \"outer\": %u, "
+                     "\"rounds\": %llu, \"verifies\": %llu, \"peeled\": %llu, \"cored\": %llu, "
+                     "\"layers\": %llu, \"syncs\": %llu, \"k_hint\": %u, \"N\": %u, \"M\": %llu}\n",
+                     ms, ph.c_str(), hc.passes, hc.outer, (unsigned long long)hc.rounds,
+                     (unsigned long long)hc.verifies, (unsigned long long)hc.peeled,
+                     (unsigned long long)hc.cored, (unsigned long long)hc.layers,
+                     (unsigned long long)hc.syncs, hc.k_hint, p.N, (unsigned long long)prep_.M);
     }
 
     std::memset(out, 0, sizeof *out);
     out->mu_den = 1;
-    out->outer_iters = outer;
-    out->spf_passes = passes;
+    out->outer_iters = hc.outer;
+    out->spf_passes = hc.passes;
     out->regions = prep_.regions_total;
     out->trivial_regions = prep_.trivial;
     out->n_solved = prep_.n;
     out->m_solved = prep_.M;
-    out->launches = launches;
-    out->fixpoint_iters = fix_iters;
+    out->launches = prep_.R > 0 ? 1 : 0;
+    out->fixpoint_iters = hc.rounds + hc.layers;
     out->device_ms = ms;
-    out->improve_ms = imp;
+    // share of the launch spent in improvement phases (SM clock spans of
+    // block 0, measured between the same grid barriers) times the event time
+    out->improve_ms = hc.clk_total ? ms * double(hc.clk[PH_IMPROVE]) / double(hc.clk_total) : 0.0;
     out->host_prep_ms = prep_ms_;
     out->h2d_bytes = h2d_bytes_;
     out->d2h_bytes = d2h;

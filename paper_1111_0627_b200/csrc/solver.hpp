@@ -32,9 +32,7 @@ class Session {
     std::uint64_t h2d_bytes_ = 0;
     std::unique_ptr<DeviceState> d_;
     bool solved_ = false;
-    int k_hint_ = 8;               // doubling rounds needed last iteration
-    int wc_hint_ = 4;              // winning-cycle prefix-sum rounds (log2 cycle + 1)
-    std::uint32_t stamp_base_ = 0; // mark stamps stay unique across solves
+    int grid_exact_ = 0, grid_float_ = 0; // cooperative grid of k_solve<exact / float>
 };
 
 } // namespace ocmb
