@@ -8,6 +8,7 @@
  *   ocm_parse_graph_text  include/ocm/graph_io.hpp:41   ocm::parse_graph_text
  *   ocm_read_graph_file   include/ocm/graph_io.hpp:45   ocm::read_graph_file
  *   ocm_graph_edges       include/ocm/graph.hpp:61      Graph::edges()
+ *   ocm_generate_model    include/ocm/model_gen.hpp:67  ocm::generate_model
  *   ocm_solve             include/ocm/solve.hpp:64      ocm::solve (lane howard-par)
  *   ocm_session_*         include/ocm/howard_par.hpp:90 HowardPar (state kept resident
  *                         in HBM so a graph can be solved repeatedly without re-upload)
@@ -104,6 +105,22 @@ int ocm_read_graph_file(const char* path, ocm_graph** out);
  * and integer weights in [wlo, whi] drawn from a seeded counter hash. */
 int ocm_generate_uniform(uint32_t n, uint32_t deg, int32_t wlo, int32_t whi, uint64_t seed,
                          ocm_graph** out);
+/* include/ocm/model_gen.hpp:31 Scenario::Transition */
+typedef struct {
+    uint32_t from;
+    uint32_t to;
+    int64_t cost;
+    int32_t acquires; /* enabled only while the server is free */
+    int32_t releases; /* enabled only for the current holder */
+} ocm_transition;
+/* include/ocm/model_gen.hpp:67 generate_model(scenario, clients): the
+ * reachable composite state space of `clients` interleaved copies of the
+ * scenario, vertices in breadth-first discovery order. max_states bounds the
+ * exploration (0 = the reference's kMaxModelStates, 5,000,000); exceeding it
+ * returns OCM_E_LOGIC ("state space exceeds N states", std::length_error). */
+int ocm_generate_model(uint32_t states, const ocm_transition* transitions, uint32_t n_transitions,
+                       int32_t uses_server, uint32_t clients, uint64_t max_states,
+                       ocm_graph** out);
 void ocm_graph_free(ocm_graph* g);
 uint32_t ocm_graph_n(const ocm_graph* g);
 uint64_t ocm_graph_m(const ocm_graph* g);

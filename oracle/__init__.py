@@ -247,3 +247,26 @@ def ref_values(n, src, dst, w, objective="min") -> CheckerResult:
     for k, v in a.items():
         setattr(out, k, v[: int(n)])
     return out
+
+
+def ref_generate_model(kind, clients, costs=()):
+    """The reference's ocm::generate_model (src/model_gen.cpp:90) through
+    oracle/_ref. kind: "worker" | "server" | "loop" (with costs)."""
+    lib = ref_lib()
+    fn = lib.ref_generate_model
+    fn.restype = C.c_int
+    fn.argtypes = [C.c_int, C.POINTER(C.c_int64), C.c_uint32, C.c_uint32, C.POINTER(C.c_uint32),
+                   C.POINTER(C.c_uint64), C.c_uint64, C.POINTER(C.c_uint32),
+                   C.POINTER(C.c_uint32), C.POINTER(C.c_double)]
+    k = {"worker": 0, "server": 1, "loop": 2}[kind]
+    cs = np.asarray(costs, dtype=np.int64)
+    n, m = C.c_uint32(), C.c_uint64()
+    if fn(k, _ptr(cs, C.c_int64), len(cs), clients, C.byref(n), C.byref(m), 0, None, None, None):
+        raise RuntimeError("reference: " + lib.ref_last_error().decode())
+    src = np.empty(m.value, np.uint32)
+    dst = np.empty(m.value, np.uint32)
+    w = np.empty(m.value, np.float64)
+    if fn(k, _ptr(cs, C.c_int64), len(cs), clients, C.byref(n), C.byref(m), m.value,
+          _ptr(src, C.c_uint32), _ptr(dst, C.c_uint32), _ptr(w, C.c_double)):
+        raise RuntimeError("reference: " + lib.ref_last_error().decode())
+    return n.value, src, dst, w

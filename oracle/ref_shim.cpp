@@ -9,6 +9,7 @@
 //   ocm::solve                 proj/include/ocm/solve.hpp:64  (src/solve.cpp:198)
 //   ocm::HowardPar<M>::run     proj/include/ocm/howard_par.hpp:544
 //   ocm::tarjan_scc            proj/include/ocm/scc.hpp:34
+//   ocm::generate_model        proj/include/ocm/model_gen.hpp:67
 //
 // Nothing here re-implements the algorithm; it only marshals arrays.
 
@@ -21,6 +22,7 @@
 
 #include "ocm/graph.hpp"
 #include "ocm/howard_par.hpp"
+#include "ocm/model_gen.hpp"
 #include "ocm/scc.hpp"
 #include "ocm/solve.hpp"
 
@@ -143,6 +145,34 @@ int ref_howard_values(uint32_t n, uint64_t m, const uint32_t* src, const uint32_
                 const ocm::EdgeId e = hp.pg.succ_edge[v];
                 succ_vertex[v] = e == ocm::kNoEdge ? ocm::kNoVertex : g.fwd_target[e];
             }
+        }
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 1;
+    }
+}
+
+// kind: 0 worker_scenario, 1 server_scenario, 2 loop_scenario(costs).
+// Writes the generated graph's edges in edge-id order when the capacity
+// suffices; always reports n and m. Returns 1 on a reference exception.
+int ref_generate_model(int kind, const int64_t* costs, uint32_t n_costs, uint32_t clients,
+                       uint32_t* n_out, uint64_t* m_out, uint64_t cap, uint32_t* src,
+                       uint32_t* dst, double* w) {
+    try {
+        ocm::Scenario sc = kind == 0 ? ocm::worker_scenario()
+                           : kind == 1 ? ocm::server_scenario()
+                                       : ocm::loop_scenario(std::vector<std::int64_t>(costs, costs + n_costs));
+        const ocm::GeneratedModel m = ocm::generate_model(sc, clients);
+        *n_out = m.graph.n;
+        *m_out = m.graph.m;
+        if (cap >= m.graph.m) {
+            for (uint32_t u = 0; u < m.graph.n; ++u)
+                for (uint64_t e = m.graph.fwd_index[u]; e < m.graph.fwd_index[u + 1]; ++e) {
+                    src[e] = u;
+                    dst[e] = m.graph.fwd_target[e];
+                    w[e] = m.graph.fwd_weight[e];
+                }
         }
         return 0;
     } catch (const std::exception& e) {

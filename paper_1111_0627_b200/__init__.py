@@ -32,12 +32,14 @@ import numpy as np
 
 __all__ = [
     "Graph", "build_graph", "parse_graph_text", "read_graph_file", "generate_uniform",
+    "Scenario", "Transition", "loop_scenario", "worker_scenario", "server_scenario",
+    "generate_model", "K_MAX_MODEL_STATES",
     "SolveOptions", "SolveStats", "Solution", "solve", "Session",
     "ParseError", "StructuralError", "DeviceError", "UnsupportedError", "LIB_PATH",
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libocm_b200.so")
+LIB_PATH = os.environ.get("OCM_LIB") or os.path.join(HERE, "lib", "libocm_b200.so")
 
 OK, E_INVALID, E_PARSE, E_LOGIC, E_CUDA, E_UNSUPPORTED, E_RANGE, E_IO = range(8)
 ALGOS = {"howard": 0, "howard-par": 1, "lawler": 2, "tree": 3, "oracle-enum": 4, "oracle-dp": 5}
@@ -63,6 +65,11 @@ class DeviceError(RuntimeError):
 
 class UnsupportedError(NotImplementedError):
     """Lane or option the device library does not provide."""
+
+
+class _Transition(C.Structure):
+    _fields_ = [("from_", C.c_uint32), ("to", C.c_uint32), ("cost", C.c_int64),
+                ("acquires", C.c_int32), ("releases", C.c_int32)]
 
 
 class _Opts(C.Structure):
@@ -100,6 +107,8 @@ def _load():
         "ocm_read_graph_file": (C.c_int, [C.c_char_p, P(C.c_void_p)]),
         "ocm_generate_uniform": (C.c_int, [C.c_uint32, C.c_uint32, C.c_int32, C.c_int32,
                                            C.c_uint64, P(C.c_void_p)]),
+        "ocm_generate_model": (C.c_int, [C.c_uint32, P(_Transition), C.c_uint32, C.c_int32,
+                                         C.c_uint32, C.c_uint64, P(C.c_void_p)]),
         "ocm_graph_free": (None, [C.c_void_p]),
         "ocm_graph_n": (C.c_uint32, [C.c_void_p]),
         "ocm_graph_m": (C.c_uint64, [C.c_void_p]),
@@ -124,6 +133,7 @@ _lib = _load()
 EXPORTED_SYMBOLS = (
     "ocm_last_error", "ocm_last_error_line", "ocm_version", "ocm_device_count",
     "ocm_build_graph", "ocm_parse_graph_text", "ocm_read_graph_file", "ocm_generate_uniform",
+    "ocm_generate_model",
     "ocm_graph_free", "ocm_graph_n", "ocm_graph_m", "ocm_graph_integer_exact", "ocm_graph_edges",
     "ocm_solve", "ocm_session_create", "ocm_session_solve", "ocm_session_values",
     "ocm_session_stream", "ocm_session_free",
@@ -236,6 +246,65 @@ def generate_uniform(n: int, deg: int, wlo: int = 1, whi: int = 100, seed: int =
     """Seeded random digraph with out-degree exactly ``deg`` and integer weights."""
     h = C.c_void_p()
     _check(_lib.ocm_generate_uniform(int(n), int(deg), int(wlo), int(whi), int(seed), C.byref(h)))
+    return Graph(h.value)
+
+
+K_MAX_MODEL_STATES = 5_000_000  # proj/include/ocm/model_gen.hpp:70 kMaxModelStates
+
+
+@dataclass
+class Transition:
+    """proj/include/ocm/model_gen.hpp:31 Scenario::Transition."""
+    from_: int
+    to: int
+    cost: int
+    acquires: bool = False
+    releases: bool = False
+
+
+@dataclass
+class Scenario:
+    """proj/include/ocm/model_gen.hpp:29 Scenario."""
+    name: str
+    states: int
+    transitions: List[Transition]
+    uses_server: bool = False
+
+
+def loop_scenario(costs) -> Scenario:
+    """model_gen.cpp:10 loop_scenario: 0 -> 1 -> ... -> 0 with the given costs."""
+    costs = [int(c) for c in costs]
+    if not costs:
+        raise ValueError("loop scenario needs at least one transition")
+    k = len(costs)
+    return Scenario(f"loop{k}", k, [Transition(i, (i + 1) % k, costs[i]) for i in range(k)])
+
+
+def worker_scenario() -> Scenario:
+    """model_gen.cpp:21 worker_scenario (template "server-free")."""
+    return Scenario("worker", 3, [Transition(0, 1, 1), Transition(1, 0, 0), Transition(1, 2, 2),
+                                  Transition(2, 0, 3)])
+
+
+def server_scenario() -> Scenario:
+    """model_gen.cpp:34 server_scenario (template "server")."""
+    return Scenario("server", 4, [Transition(0, 1, 1), Transition(1, 0, 0),
+                                  Transition(1, 2, 2, acquires=True), Transition(2, 3, 5),
+                                  Transition(3, 0, 1, releases=True)], uses_server=True)
+
+
+def generate_model(sc: Scenario, clients: int, max_states: int = K_MAX_MODEL_STATES) -> Graph:
+    """model_gen.hpp:67 generate_model: composite state space of `clients`
+    interleaved copies of `sc`, vertices in breadth-first discovery order.
+    Raises ValueError on malformed scenarios and StructuralError (the
+    reference's std::length_error) past max_states."""
+    arr = (_Transition * max(1, len(sc.transitions)))()
+    for i, t in enumerate(sc.transitions):
+        arr[i] = _Transition(int(t.from_), int(t.to), int(t.cost), int(bool(t.acquires)),
+                             int(bool(t.releases)))
+    h = C.c_void_p()
+    _check(_lib.ocm_generate_model(int(sc.states), arr, len(sc.transitions), int(sc.uses_server),
+                                   int(clients), int(max_states), C.byref(h)))
     return Graph(h.value)
 
 

@@ -157,6 +157,24 @@ int ocm_generate_uniform(uint32_t n, uint32_t deg, int32_t wlo, int32_t whi, uin
     });
 }
 
+int ocm_generate_model(uint32_t states, const ocm_transition* transitions, uint32_t n_transitions,
+                       int32_t uses_server, uint32_t clients, uint64_t max_states,
+                       ocm_graph** out) {
+    return guard([&] {
+        if (n_transitions && !transitions)
+            throw std::invalid_argument("null transition array");
+        ocmb::Scenario sc;
+        sc.states = states;
+        sc.uses_server = uses_server != 0;
+        for (uint32_t i = 0; i < n_transitions; ++i)
+            sc.transitions.push_back({transitions[i].from, transitions[i].to, transitions[i].cost,
+                                      transitions[i].acquires != 0, transitions[i].releases != 0});
+        auto g = std::make_unique<ocm_graph>();
+        g->g = ocmb::generate_model(sc, clients, max_states ? max_states : 5000000ull);
+        *out = g.release();
+    });
+}
+
 void ocm_graph_free(ocm_graph* g) { delete g; }
 uint32_t ocm_graph_n(const ocm_graph* g) { return g ? g->g.n : 0; }
 uint64_t ocm_graph_m(const ocm_graph* g) { return g ? g->g.m : 0; }

@@ -57,14 +57,17 @@ struct __align__(16) PJC {
 // that raised them, so no phase has to clear state another block may still
 // be reading.
 enum Phase {
-    PH_INIT, PH_IMPROVE, PH_REGION, PH_LEAVES, PH_PEEL, PH_CORE, PH_PJINIT, PH_ROUND, PH_VERIFY,
-    PH_STATS, PH_VOTE, PH_ADOPT, PH_WINCYC, PH_KEEP, PH_UNPEEL, PH_ATTACH, PH_FLOAT, PH_COUNT
+    PH_INIT, PH_IMPROVE, PH_CLASSIFY, PH_ROUND, PH_VERIFY, PH_STATS, PH_VOTE, PH_WINCYC, PH_KEEP,
+    PH_LEAVES, PH_ATTACH, PH_FLOAT, PH_COUNT
 };
 
 struct Ctl {
     // ---- persistent across the session's solves (zeroed once at creation)
-    unsigned long long ring[2][2]; // cumulative append counters (ring, slot)
-    unsigned long long maxcyc;     // (stamp << 32) | longest winning cycle
+    unsigned long long ring[3][2]; // cumulative append counters (ring, slot)
+    unsigned long long done;       // blocks through the vote phase (cumulative)
+    unsigned long long wc_n[2];    // (stamp << 32) | winning-cycle vertices listed
+    unsigned wc_len[2];            // longest winning cycle (slot stamp & 1)
+    unsigned wc_big[2];            // = stamp when the grid must do the winning cycles
     unsigned long long fnd[2];     // float lane: (stamp << 32) | level still pending
     unsigned stamp;                // last verification stamp used
     unsigned k_hint;               // doubling rounds that sufficed last iteration
@@ -77,12 +80,12 @@ struct Ctl {
     int nonconv;   // a fixpoint did not converge within its bound
     unsigned passes;
     unsigned outer;
-    unsigned long long rounds;     // pointer-doubling rounds (all iterations)
-    unsigned long long verifies;   // cycle verifications
-    unsigned long long peeled;     // vertices peeled (all iterations)
+    unsigned rounds;               // pointer-doubling rounds (all iterations)
+    unsigned verifies;             // cycle verifications
+    unsigned long long peeled;     // leaves split off (all iterations)
     unsigned long long cored;      // vertices doubled (all iterations)
-    unsigned long long layers;     // attach layers + float levels
-    unsigned long long syncs;      // grid barriers
+    unsigned layers;               // attach layers + float levels
+    unsigned syncs;                // grid barriers
     long long clk_total;           // block-0 SM clock over the launch
     long long clk[PH_COUNT];       // ... per phase (time up to the phase's barrier)
 };
@@ -110,18 +113,14 @@ struct KP {
     std::uint32_t* src;
     std::uint32_t* iters;
     // cycle phase
-    std::uint32_t* indeg; // policy in-degree (peeling)
-    std::uint32_t* peel;  // peel layer of a vertex this iteration (0 = not peeled)
-    std::uint32_t* plist; // peeled vertices, layer after layer
-    std::uint32_t* clist; // core (not peeled) vertices; core index -> vertex
-    std::uint32_t* cidx;  // vertex -> core index
-    std::uint32_t* csucc; // core index of the policy successor
-    std::uint32_t* ccomp; // anchor (least vertex of the reached cycle), core-indexed
-    std::uint32_t* cmark; // core-indexed stamps: image of succ^L
+    std::uint32_t* indeg; // policy in-degree (leaf split)
+    std::uint32_t* plist; // leaves of the policy graph this iteration
+    std::uint32_t* clist; // the other working vertices (the core)
+    std::uint32_t* cmark; // verification stamps: image of succ^L
     std::uint32_t* cmark2;
-    PJC* pj[2];           // core-indexed doubling records
-    std::uint32_t* comp;  // anchor, vertex-indexed
-    std::uint32_t* wlist;
+    PJC* pj[2];           // doubling records (vertex-indexed)
+    std::uint32_t* comp;  // anchor: least vertex of the reached cycle
+    std::uint32_t* wlist; // cycle vertices (image of succ^L) this iteration
     std::uint32_t* cyc_len;
     long long* cyc_wi;
     double* cyc_wf;
@@ -133,8 +132,6 @@ struct KP {
     long long max_abs_w;
     // tuning (launch arguments)
     int G;                 // improvement lanes per vertex
-    std::uint32_t peel_min; // peel another layer only while it has >= this many vertices
-    int peel_max;          // at most this many peel layers
     std::uint32_t small_wc; // winning cycles up to this many vertices: one block
 };
 
@@ -183,7 +180,7 @@ struct DeviceState {
     int sms = 148;
     cudaStream_t stream = nullptr;
     DBuf<std::uint32_t> row, reg, succ_e, succ_v, comp, wlist, cyc_len, conn, rem0, rem1, src,
-        iters, indeg, peel, plist, clist, cidx, csucc, ccomp, cmark, cmark2;
+        iters, indeg, plist, clist, cmark, cmark2;
     DBuf<PJV> pv0, pv1;
     DBuf<PJC> pj0, pj1;
     DBuf<int2> ew;
@@ -202,8 +199,7 @@ struct DeviceState {
         if (stream)
             cudaStreamSynchronize(stream);
         for (auto* b : {&row, &reg, &succ_e, &succ_v, &comp, &wlist, &cyc_len, &conn, &rem0, &rem1,
-                        &src, &iters, &indeg, &peel, &plist, &clist, &cidx, &csucc, &ccomp, &cmark,
-                        &cmark2})
+                        &src, &iters, &indeg, &plist, &clist, &cmark, &cmark2})
             b->release();
         pv0.release();
         pv1.release();

@@ -49,25 +49,50 @@ namespace {
 
 namespace cg = cooperative_groups;
 
-constexpr int kMaxPeel = 32;
-constexpr int kSolveMinBlocks = 4; // register cap 64 at 256 threads
+#ifndef OCM_KEYLD_CG
+#define OCM_KEYLD_CG 1 // improvement key gathers: 1 = L2 only (ld.cg), 0 = L1-cached
+#endif
+#ifndef OCM_MINB
+#define OCM_MINB 4
+#endif
+constexpr int kSolveMinBlocks = OCM_MINB; // 4: register cap 64 at 256 threads
 
 __device__ __forceinline__ std::size_t gtid() {
     return blockIdx.x * std::size_t(blockDim.x) + threadIdx.x;
 }
 __device__ __forceinline__ std::size_t gstride() { return std::size_t(gridDim.x) * blockDim.x; }
 
+// Control values (counters, flags) read after a grid barrier: relaxed
+// gpu-scope loads, coherent at L2 and never hoisted across the barrier.
+__device__ __forceinline__ unsigned long long ldr(const unsigned long long& x) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(&x) : "memory");
+    return v;
+}
+__device__ __forceinline__ unsigned ldr(const unsigned& x) {
+    unsigned v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(&x) : "memory");
+    return v;
+}
+__device__ __forceinline__ int ldr(const int& x) {
+    int v;
+    asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(&x) : "memory");
+    return v;
+}
+// Data another thread may write in the same phase.
 template <class T> __device__ __forceinline__ T ldv(const T& x) {
     return *reinterpret_cast<const volatile T*>(&x);
 }
 
+// Plain loads are used for everything written in an earlier phase: the
+// grid barrier's fences make those writes visible.
 __device__ __forceinline__ bool working(const KP& p, std::uint32_t v) {
-    return ldv(p.active[__ldg(&p.reg[v])]) != 0;
+    return p.active[__ldg(&p.reg[v])] != 0;
 }
 
 // Set *flag to val unless it already is (read first: avoids store storms).
 template <class T> __device__ __forceinline__ void set_once(T* flag, T val) {
-    if (ldv(*flag) != val)
+    if (ldr(*flag) != val)
         *flag = val;
 }
 
@@ -89,14 +114,14 @@ struct Ring {
     int cur;
     __device__ void init(unsigned long long* c) {
         ctr = c;
-        base[0] = ldv(c[0]);
-        base[1] = ldv(c[1]);
+        base[0] = ldr(c[0]);
+        base[1] = ldr(c[1]);
         cur = 0;
     }
     __device__ __forceinline__ unsigned long long* counter() const { return &ctr[cur]; }
     __device__ __forceinline__ unsigned long long origin() const { return base[cur]; }
     __device__ std::uint64_t take() {
-        const unsigned long long v = ldv(ctr[cur]);
+        const unsigned long long v = ldr(ctr[cur]);
         const std::uint64_t n = v - base[cur];
         base[cur] = v;
         cur ^= 1;
@@ -195,7 +220,7 @@ struct ChangedMarks {
     }
 };
 
-template <bool EXACT, int G, int U> __device__ __noinline__ void improve_phase(const KP& p, int* changed) {
+template <bool EXACT, int G, int U> __device__ __forceinline__ void improve_phase(const KP& p, int* changed) {
     const unsigned lane = threadIdx.x & (G - 1);
     const unsigned gm = group_mask<G>();
     const std::size_t gid = gtid() / G;
@@ -207,7 +232,7 @@ template <bool EXACT, int G, int U> __device__ __noinline__ void improve_phase(c
     for (std::size_t vv = gid; vv < p.N; vv += gs) {
         const std::uint32_t v = static_cast<std::uint32_t>(vv);
         const std::uint32_t r = __ldg(&p.reg[v]);
-        if (!ldv(p.active[r]))
+        if (!p.active[r])
             continue;
         const std::uint32_t b = __ldg(&p.row[v]), e_end = __ldg(&p.row[v + 1]);
         const std::uint32_t cur = p.succ_e[v];
@@ -220,7 +245,7 @@ template <bool EXACT, int G, int U> __device__ __noinline__ void improve_phase(c
             lam = p.lam_f[r];
         }
         Key best = 0, curc = 0;
-        std::uint32_t be = NONE, bt = 0;
+        std::uint32_t be = NONE, bt = 0, cur_t = 0;
         int bwi = 0;
         double bwf = 0.0;
         bool have_cur = false;
@@ -247,7 +272,7 @@ template <bool EXACT, int G, int U> __device__ __noinline__ void improve_phase(c
 #pragma unroll
             for (int u = 0; u < U; ++u)
                 if (e0 + u * G < e_end)
-                    kk[u] = __ldcg(&key[tt[u]]);
+                    kk[u] = OCM_KEYLD_CG ? __ldcg(&key[tt[u]]) : key[tt[u]];
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 const std::uint32_t e = e0 + u * G;
@@ -268,11 +293,13 @@ template <bool EXACT, int G, int U> __device__ __noinline__ void improve_phase(c
                     }
                     if (e == cur) {
                         curc = c;
+                        cur_t = tt[u];
                         have_cur = true;
                     }
                 }
             }
         }
+        const bool saw_cur = have_cur; // this lane scanned the incumbent edge
         Key gbest = best;
         std::uint32_t gbe = be;
 #pragma unroll
@@ -312,17 +339,21 @@ template <bool EXACT, int G, int U> __device__ __noinline__ void improve_phase(c
                     p.succ_wi[v] = bwi;
                 else
                     p.succ_wf[v] = bwf;
+#ifndef OCM_INDEG_PHASE
                 atomicAdd(&p.indeg[bt], 1u);
+#endif
                 marks.note(changed, r);
             }
-        } else if (lane == 0) {
-            atomicAdd(&p.indeg[p.succ_v[v]], 1u);
+        } else if (saw_cur) {
+#ifndef OCM_INDEG_PHASE
+            atomicAdd(&p.indeg[cur_t], 1u);
+#endif
         }
     }
     marks.flush(changed);
 }
 
-template <bool EXACT> __device__ __noinline__ void improve_dispatch(const KP& p, int* changed) {
+template <bool EXACT> __device__ __forceinline__ void improve_dispatch(const KP& p, int* changed) {
     switch (p.G) {
     case 1: improve_phase<EXACT, 1, 4>(p, changed); break;
     case 2: improve_phase<EXACT, 2, 4>(p, changed); break;
@@ -376,16 +407,13 @@ __device__ __forceinline__ int ceil_log2_d(unsigned long long x) {
 
 // ------------------------------------------------------------ phases
 //
-// Each phase is a separate non-inlined function: its loop gets the whole
-// register budget, and the kernel's cross-phase state (ring bases, layer
-// offsets, stamps) is saved once per call instead of spilling inside loops.
 // Loops containing block_append/block_flag are block-uniform.
 
 #define OCM_BLOCK_LOOP(i, lo, hi)                                                                \
     for (std::uint64_t i##_b = (lo) + blockIdx.x * std::uint64_t(kBlock); i##_b < (hi);          \
          i##_b += gridDim.x * std::uint64_t(kBlock))
 
-__device__ __noinline__ void ph_init(const KP& p, bool exact) {
+__device__ __forceinline__ void ph_init(const KP& p, bool exact) {
     const std::size_t tid = gtid(), nth = gstride();
     for (std::size_t v = tid; v < p.N; v += nth) {
         p.succ_e[v] = NONE;
@@ -395,7 +423,6 @@ __device__ __noinline__ void ph_init(const KP& p, bool exact) {
         else
             p.key_f[v] = 0.0;
         p.indeg[v] = 0;
-        p.peel[v] = 0;
     }
     for (std::size_t r = tid; r <= p.R; r += nth) { // slot R: trivial vertices
         p.lam_num[r] = 0;
@@ -410,200 +437,252 @@ __device__ __noinline__ void ph_init(const KP& p, bool exact) {
     }
 }
 
-// Regions whose pass changed nothing are finished (howard_par.hpp:189/208);
-// counts the regions still active.
-__device__ __noinline__ void ph_region(const KP& p, int par, const Ring& ring) {
-    unsigned still = 0;
+// Region check (howard_par.hpp:189/208: a region whose pass changed nothing
+// is finished) fused with the split of the still-working vertices into
+// leaves of the policy graph (in-degree 0: never on a cycle, never the
+// successor of anyone) and the core, whose doubling records are initialised
+// here. A vertex still works iff its region changed in this pass (changed
+// is only ever raised for active regions).
+template <bool EXACT>
+__device__ __forceinline__ void ph_classify(const KP& p, int par, const Ring& ra, const Ring& rl,
+                                            const Ring& rc) {
     const int* changed = p.changed[par];
+    unsigned still = 0;
     for (std::size_t r = gtid(); r < p.R; r += gstride()) {
         if (p.active[r]) {
-            if (ldv(changed[r]))
+            if (changed[r])
                 ++still;
             else
                 p.active[r] = 0;
         }
         p.changed[par ^ 1][r] = 0;
     }
-    block_count(still, ring);
-}
-
-// Leaves of the policy graph: working vertices nobody points to.
-__device__ __noinline__ void ph_leaves(const KP& p, const Ring& ring) {
+    block_count(still, ra);
     OCM_BLOCK_LOOP(v0, 0, p.N) {
         const std::uint64_t v = v0_b + threadIdx.x;
-        const bool take = v < p.N && p.indeg[v] == 0 && working(p, static_cast<std::uint32_t>(v));
-        const std::uint64_t slot = block_append(take, ring);
-        if (take) {
-            p.peel[v] = 1;
-            p.plist[slot] = static_cast<std::uint32_t>(v);
+        bool leaf = false, core = false;
+        if (v < p.N && changed[__ldg(&p.reg[v])]) {
+            leaf = p.indeg[v] == 0;
+            core = !leaf;
+        }
+        const std::uint64_t ls = block_append(leaf, rl);
+        const std::uint64_t cs = block_append(core, rc);
+        if (leaf)
+            p.plist[ls] = static_cast<std::uint32_t>(v);
+        if (core) {
+            p.clist[cs] = static_cast<std::uint32_t>(v);
+            PJC x;
+            x.nxt = p.succ_v[v];
+            x.mn = static_cast<std::uint32_t>(v);
+            x.w = EXACT ? static_cast<long long>(p.succ_wi[v]) : 0ll;
+            p.pj[0][v] = x;
         }
     }
 }
 
-// One peel layer: removing plist[lo, hi) drops its successors' in-degree;
-// those reaching 0 form the next layer at plist[hi...].
-__device__ __noinline__ void ph_peel(const KP& p, std::uint64_t lo, std::uint64_t hi,
-                                     std::uint32_t next_layer, const Ring& ring) {
-    OCM_BLOCK_LOOP(i0, lo, hi) {
-        const std::uint64_t i = i0_b + threadIdx.x;
-        bool take = false;
-        std::uint32_t s = 0;
-        if (i < hi) {
-            s = p.succ_v[p.plist[i]];
-            take = atomicSub(&p.indeg[s], 1u) == 1u;
-        }
-        const std::uint64_t slot = block_append(take, ring);
-        if (take) {
-            p.peel[s] = next_layer;
-            p.plist[hi + slot] = s;
-        }
-    }
-}
-
-// Core: working vertices not peeled (closed under succ), compacted.
-__device__ __noinline__ void ph_core(const KP& p, std::uint32_t done, const Ring& ring) {
-    OCM_BLOCK_LOOP(v0, 0, p.N) {
-        const std::uint64_t v = v0_b + threadIdx.x;
-        bool take = false;
-        if (v < p.N) {
-            const std::uint32_t pl = p.peel[v];
-            take = (pl == 0 || pl > done) && working(p, static_cast<std::uint32_t>(v));
-        }
-        const std::uint64_t slot = block_append(take, ring);
-        if (take) {
-            p.clist[slot] = static_cast<std::uint32_t>(v);
-            p.cidx[v] = static_cast<std::uint32_t>(slot);
-        }
-    }
-}
-
-template <bool EXACT> __device__ __noinline__ void ph_pjinit(const KP& p, std::uint64_t nC) {
-    for (std::uint64_t i = gtid(); i < nC; i += gstride()) {
-        const std::uint32_t v = p.clist[i];
-        const std::uint32_t s = p.succ_v[v];
-        const std::uint32_t ci = p.cidx[s];
-        PJC x;
-        x.nxt = ci;
-        x.mn = v;
-        x.w = EXACT ? static_cast<long long>(p.succ_wi[v]) : 0ll;
-        p.pj[0][i] = x;
-        p.csucc[i] = ci;
-        p.cyc_len[v] = 0;
-        if constexpr (EXACT)
-            p.cyc_wi[v] = 0;
-    }
-}
-
-// Synchronous pointer doubling of (segment end, least vertex, weight sum).
-__device__ __noinline__ void ph_round(const KP& p, std::uint64_t nC, int in) {
+// Synchronous pointer doubling of (segment end, least vertex, weight sum)
+// over the core (closed under succ: a leaf is nobody's successor).
+__device__ __forceinline__ void ph_round(const KP& p, std::uint64_t nC, int in) {
     const PJC* __restrict__ a = p.pj[in];
     PJC* __restrict__ o = p.pj[in ^ 1];
     for (std::uint64_t i = gtid(); i < nC; i += gstride()) {
-        const PJC x = a[i];
+        const std::uint32_t v = p.clist[i];
+        const PJC x = a[v];
         const PJC y = a[x.nxt];
         PJC z;
         z.nxt = y.nxt;
         z.mn = min(x.mn, y.mn);
         z.w = x.w + y.w;
-        o[i] = z;
+        o[v] = z;
     }
 }
 
-// Verification: M = image of succ^L passes iff every vertex
-// of M has a predecessor in M (no tail vertex) and the anchor is constant
-// along succ in M (every window covers its whole cycle).
-__device__ __noinline__ void ph_mark(const KP& p, std::uint64_t nC, int in, std::uint32_t stamp) {
+// Verification. M = image of succ^L. It passes iff (A)
+// every vertex of M has a predecessor in M -- succ maps M into M, so this
+// is |succ(M)| = |M| -- and (B) the anchor is constant along succ in M
+// (every window covers its whole cycle). The mark phase records the anchors
+// and counts |M|; the check phase counts |succ(M)|, tests (B), lists M (the
+// cycle vertices, if it passes) and, in exact mode, already accumulates the
+// per-anchor (length, weight) records (howard_par.hpp:319), cleared here.
+__device__ __forceinline__ void ph_mark(const KP& p, std::uint64_t nC, int in, std::uint32_t stamp,
+                                        bool exact, const Ring& rm) {
     const PJC* a = p.pj[in];
+    unsigned fresh = 0;
     for (std::uint64_t i = gtid(); i < nC; i += gstride()) {
-        const std::uint32_t j = a[i].nxt;
-        p.ccomp[i] = a[j].mn;
-        if (p.cmark[j] != stamp) // many vertices share j: read before writing
-            p.cmark[j] = stamp;
+        const std::uint32_t v = p.clist[i];
+        const std::uint32_t j = a[v].nxt;
+        p.comp[v] = a[j].mn;
+        p.cyc_len[v] = 0;
+        if (exact)
+            p.cyc_wi[v] = 0;
+        // many vertices share j: read before the exchange
+        if (p.cmark[j] != stamp && atomicExch(&p.cmark[j], stamp) != stamp)
+            ++fresh;
     }
+    block_count(fresh, rm);
 }
 
-__device__ __noinline__ void ph_verify1(const KP& p, std::uint64_t nC, std::uint32_t stamp,
-                                        unsigned* flag) {
+template <bool EXACT>
+__device__ __forceinline__ void ph_check(const KP& p, std::uint64_t nC, std::uint32_t stamp,
+                                         unsigned* flag, const Ring& rs, const Ring& rl) {
     bool fail = false;
+    unsigned fresh = 0;
+    const unsigned lane = threadIdx.x & 31;
     OCM_BLOCK_LOOP(i0, 0, nC) {
         const std::uint64_t i = i0_b + threadIdx.x;
-        if (i < nC && p.cmark[i] == stamp) {
-            const std::uint32_t s = p.csucc[i];
-            fail |= p.ccomp[s] != p.ccomp[i];
-            if (p.cmark2[s] != stamp)
-                p.cmark2[s] = stamp;
+        std::uint32_t v = 0, a = 0;
+        bool on = false;
+        if (i < nC) {
+            v = p.clist[i];
+            on = p.cmark[v] == stamp;
         }
-    }
-    block_flag(fail, flag, stamp);
-}
-
-__device__ __noinline__ void ph_verify2(const KP& p, std::uint64_t nC, std::uint32_t stamp,
-                                        unsigned* flag) {
-    bool fail = false;
-    for (std::uint64_t i = gtid(); i < nC; i += gstride())
-        fail |= p.cmark[i] == stamp && p.cmark2[i] != stamp;
-    block_flag(fail, flag, stamp);
-}
-
-// Cycle records (length, weight) per anchor (howard_par.hpp:319).
-template <bool EXACT> __device__ __noinline__ void ph_stats(const KP& p, std::uint64_t nC, std::uint32_t stamp) {
-    if constexpr (EXACT) {
-        // integer segmented reduction (order-independent); a warp whose
-        // cycle vertices share one anchor pre-reduces to one atomic pair
-        const unsigned lane = threadIdx.x & 31;
-        const std::uint64_t wid = gtid() >> 5, ws = gstride() >> 5;
-        for (std::uint64_t base = wid * 32; base < nC; base += ws * 32) {
-            const std::uint64_t i = base + lane;
-            const bool on = i < nC && p.cmark[i] == stamp;
+        if (on) {
+            const std::uint32_t s = p.succ_v[v];
+            a = p.comp[v];
+            fail |= p.comp[s] != a;
+            if (p.cmark2[s] != stamp && atomicExch(&p.cmark2[s], stamp) != stamp)
+                ++fresh;
+        }
+        if constexpr (EXACT) {
+            // integer segmented reduction; a warp whose cycle vertices share
+            // one anchor pre-reduces to one atomic pair
             const unsigned am = __ballot_sync(FULL, on);
-            if (!am)
-                continue;
-            const std::uint32_t a = on ? p.ccomp[i] : 0u;
-            const int lead = __ffs(am) - 1;
-            const std::uint32_t a0 = __shfl_sync(FULL, a, lead);
-            const bool uni = __all_sync(FULL, !on || a == a0);
-            long long w = on ? static_cast<long long>(p.succ_wi[p.clist[i]]) : 0ll;
-            if (uni) {
+            if (am) {
+                const int lead = __ffs(am) - 1;
+                const std::uint32_t a0 = __shfl_sync(FULL, a, lead);
+                const bool uni = __all_sync(FULL, !on || a == a0);
+                long long w = on ? static_cast<long long>(p.succ_wi[v]) : 0ll;
+                if (uni) {
 #pragma unroll
-                for (int off = 16; off > 0; off >>= 1)
-                    w += __shfl_xor_sync(FULL, w, off);
-                if (static_cast<int>(lane) == lead) {
-                    atomicAdd(&p.cyc_len[a0], static_cast<unsigned>(__popc(am)));
-                    atomicAdd(reinterpret_cast<unsigned long long*>(&p.cyc_wi[a0]),
+                    for (int off = 16; off > 0; off >>= 1)
+                        w += __shfl_xor_sync(FULL, w, off);
+                    if (static_cast<int>(lane) == lead) {
+                        atomicAdd(&p.cyc_len[a0], static_cast<unsigned>(__popc(am)));
+                        atomicAdd(reinterpret_cast<unsigned long long*>(&p.cyc_wi[a0]),
+                                  static_cast<unsigned long long>(w));
+                    }
+                } else if (on) {
+                    atomicAdd(&p.cyc_len[a], 1u);
+                    atomicAdd(reinterpret_cast<unsigned long long*>(&p.cyc_wi[a]),
                               static_cast<unsigned long long>(w));
                 }
-            } else if (on) {
-                atomicAdd(&p.cyc_len[a], 1u);
-                atomicAdd(reinterpret_cast<unsigned long long*>(&p.cyc_wi[a]),
-                          static_cast<unsigned long long>(w));
             }
         }
-    } else {
-        // float: each anchor walks its own cycle from itself, summing in the
-        // reference's order (howard_par.hpp:323) -> identical means
-        for (std::uint64_t i = gtid(); i < nC; i += gstride()) {
-            const std::uint32_t v = p.clist[i];
-            if (p.cmark[i] != stamp || p.ccomp[i] != v)
-                continue;
-            double s = 0.0;
-            std::uint32_t len = 0, u = v;
-            do {
-                s += p.succ_wf[u];
-                ++len;
-                u = p.succ_v[u];
-            } while (u != v);
-            p.cyc_wf[v] = s;
-            p.cyc_len[v] = len;
+        const std::uint64_t slot = block_append(on, rl);
+        if (on)
+            p.wlist[slot] = v;
+    }
+    block_flag(fail, flag, stamp);
+    block_count(fresh, rs);
+}
+
+// Float lane: each anchor walks its own cycle from itself, summing in the
+// reference's order (howard_par.hpp:323) -> identical means. Runs after
+// the verification passed (the walk needs a true cycle).
+__device__ __forceinline__ void ph_stats_float(const KP& p, std::uint64_t nM) {
+    for (std::uint64_t i = gtid(); i < nM; i += gstride()) {
+        const std::uint32_t v = p.wlist[i];
+        if (p.comp[v] != v)
+            continue;
+        double s = 0.0;
+        std::uint32_t len = 0, u = v;
+        do {
+            s += p.succ_wf[u];
+            ++len;
+            u = p.succ_v[u];
+        } while (u != v);
+        p.cyc_wf[v] = s;
+        p.cyc_len[v] = len;
+    }
+}
+
+// Adoption (howard_par.hpp:349-364) of region r's winning record.
+template <bool EXACT> __device__ __forceinline__ unsigned adopt_region(const KP& p, std::uint32_t r) {
+    Ctl* c = p.c;
+    const unsigned long long a = p.slot[r];
+    p.slot[r] = EMPTY;
+    if (a == EMPTY) {
+        c->error = 1;
+        return 0;
+    }
+    p.src[r] = static_cast<std::uint32_t>(a);
+    const unsigned len = p.cyc_len[a];
+    if constexpr (EXACT) {
+        long long num = p.cyc_wi[a], den = len;
+        const long long g = gcd_ll(num, den);
+        if (g > 1) {
+            num /= g;
+            den /= g;
         }
+        if (p.iters[r] > 0 &&
+            static_cast<__int128>(p.lam_num[r]) * den < static_cast<__int128>(num) * p.lam_den[r])
+            c->lambda_up = 1;
+        p.lam_num[r] = num;
+        p.lam_den[r] = den;
+        const __int128 step = static_cast<__int128>(p.max_abs_w) * den + (num < 0 ? -num : num);
+        if (static_cast<__int128>(p.max_region) * step >= (static_cast<__int128>(1) << 62))
+            c->overflow = 1;
+    } else {
+        p.lam_f[r] = p.cyc_wf[a] / len;
+    }
+    p.iters[r] += 1;
+    return len;
+}
+
+// Winning-cycle values: prefix sums of w*den - num along the cycle, cut at
+// the anchor (value(anchor) = 0), by pointer jumping over those vertices.
+__device__ __forceinline__ void wc_init_one(const KP& p, std::uint32_t v, std::uint32_t r) {
+    PJV x;
+    const std::uint32_t root = p.src[r];
+    if (v == root) {
+        x.acc = 0;
+        x.nxt = root;
+    } else {
+        x.acc = static_cast<long long>(p.succ_wi[v]) * p.lam_den[r] - p.lam_num[r];
+        x.nxt = p.succ_v[v];
+    }
+    x.root = root;
+    p.pv[0][v] = x;
+}
+
+__device__ __forceinline__ void wc_round(const KP& p, const std::uint32_t* list, std::uint64_t nW, int j,
+                                         std::uint64_t from, std::uint64_t step) {
+    const PJV* __restrict__ a = p.pv[j & 1];
+    PJV* __restrict__ o = p.pv[(j & 1) ^ 1];
+    for (std::uint64_t i = from; i < nW; i += step) {
+        const std::uint32_t v = list[i];
+        const PJV x = a[v];
+        const PJV y = a[x.nxt];
+        PJV z;
+        z.acc = x.acc + y.acc;
+        z.nxt = y.nxt;
+        z.root = x.root;
+        o[v] = z;
+    }
+}
+
+__device__ __forceinline__ void wc_final(const KP& p, const std::uint32_t* list, std::uint64_t nW, int wr,
+                                         std::uint64_t from, std::uint64_t step) {
+    const PJV* fin = p.pv[wr & 1];
+    for (std::uint64_t i = from; i < nW; i += step) {
+        const std::uint32_t v = list[i];
+        p.key_i[v] = fin[v].acc;
     }
 }
 
 // Region-specific minimum voting (howard_par.hpp:56 vote_min; paper
-// Alg. 5): a holder is replaced only by a strictly smaller (mean, anchor).
-template <bool EXACT> __device__ __noinline__ void ph_vote(const KP& p, std::uint64_t nC, std::uint32_t stamp) {
-    for (std::uint64_t i = gtid(); i < nC; i += gstride()) {
-        const std::uint32_t v = p.clist[i];
-        if (p.cmark[i] != stamp || p.ccomp[i] != v)
+// Alg. 5: a holder is replaced only by a strictly smaller (mean, anchor)),
+// over the anchors among the nM cycle vertices in wlist. The last block to
+// finish voting adopts every region's winner and, when the winning cycles
+// are small, computes their values itself (block barriers only); otherwise
+// it raises wc_big and the grid does it after the barrier.
+template <bool EXACT>
+__device__ __forceinline__ void ph_vote(const KP& p, std::uint64_t nM, std::uint32_t stamp,
+                                        unsigned long long done_base) {
+    Ctl* c = p.c;
+    for (std::uint64_t i = gtid(); i < nM; i += gstride()) {
+        const std::uint32_t v = p.wlist[i];
+        if (p.comp[v] != v)
             continue;
         unsigned long long* cell = &p.slot[__ldg(&p.reg[v])];
         unsigned long long cur = ldv(*cell);
@@ -616,109 +695,61 @@ template <bool EXACT> __device__ __noinline__ void ph_vote(const KP& p, std::uin
             cur = prev;
         }
     }
-}
-
-// Adoption (howard_par.hpp:349-364), per region.
-template <bool EXACT> __device__ __noinline__ void ph_adopt(const KP& p, std::uint32_t stamp) {
-    Ctl* c = p.c;
-    for (std::size_t r = gtid(); r < p.R; r += gstride()) {
-        if (!p.active[r])
-            continue;
-        const unsigned long long a = p.slot[r];
-        p.slot[r] = EMPTY;
-        if (a == EMPTY) {
-            c->error = 1;
-            continue;
-        }
-        p.src[r] = static_cast<std::uint32_t>(a);
-        const unsigned len = p.cyc_len[a];
-        atomicMax(&c->maxcyc, (static_cast<unsigned long long>(stamp) << 32) | len);
-        if constexpr (EXACT) {
-            long long num = p.cyc_wi[a], den = len;
-            const long long g = gcd_ll(num, den);
-            if (g > 1) {
-                num /= g;
-                den /= g;
-            }
-            if (p.iters[r] > 0 &&
-                static_cast<__int128>(p.lam_num[r]) * den < static_cast<__int128>(num) * p.lam_den[r])
-                c->lambda_up = 1;
-            p.lam_num[r] = num;
-            p.lam_den[r] = den;
-            const __int128 step = static_cast<__int128>(p.max_abs_w) * den + (num < 0 ? -num : num);
-            if (static_cast<__int128>(p.max_region) * step >= (static_cast<__int128>(1) << 62))
-                c->overflow = 1;
-        } else {
-            p.lam_f[r] = p.cyc_wf[a] / len;
-        }
-        p.iters[r] += 1;
+    __shared__ int s_last;
+    __shared__ unsigned s_maxlen, s_nw;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const unsigned long long prev = atomicAdd(&c->done, 1ull);
+        s_last = prev == done_base + gridDim.x - 1;
+        s_maxlen = 0;
+        s_nw = 0;
+        __threadfence();
     }
-}
-
-// Winning-cycle vertices: prefix sums of w*den - num along the cycle, cut
-// at the anchor (value(anchor) = 0), by pointer jumping over them only.
-__device__ __noinline__ void ph_wc_init(const KP& p, std::uint64_t nC, std::uint32_t stamp,
-                                        const Ring& ring) {
-    OCM_BLOCK_LOOP(i0, 0, nC) {
-        const std::uint64_t i = i0_b + threadIdx.x;
-        bool take = false;
-        std::uint32_t v = 0, r = 0;
-        if (i < nC && p.cmark[i] == stamp) {
-            v = p.clist[i];
-            r = __ldg(&p.reg[v]);
-            take = p.ccomp[i] == p.src[r];
+    __syncthreads();
+    if (!s_last)
+        return;
+    for (std::uint32_t r = threadIdx.x; r < p.R; r += blockDim.x)
+        if (p.active[r]) {
+            const unsigned len = adopt_region<EXACT>(p, r);
+            atomicMax(&s_maxlen, len);
         }
-        const std::uint64_t slot = block_append(take, ring);
-        if (take) {
-            p.wlist[slot] = v;
-            PJV x;
-            const std::uint32_t root = p.src[r];
-            if (v == root) {
-                x.acc = 0;
-                x.nxt = root;
-            } else {
-                x.acc = static_cast<long long>(p.succ_wi[v]) * p.lam_den[r] - p.lam_num[r];
-                x.nxt = p.succ_v[v];
-            }
-            x.root = root;
-            p.pv[0][v] = x;
-        }
-    }
-}
-
-__device__ __noinline__ void ph_wc_round(const KP& p, std::uint64_t nW, int j, std::uint64_t from,
-                                         std::uint64_t step) {
-    const PJV* __restrict__ a = p.pv[j & 1];
-    PJV* __restrict__ o = p.pv[(j & 1) ^ 1];
-    for (std::uint64_t i = from; i < nW; i += step) {
+    if constexpr (!EXACT)
+        return;
+    __syncthreads();
+    // winning-cycle vertices among the cycle vertices (compacted in rem[1])
+    for (std::uint64_t i = threadIdx.x; i < nM; i += blockDim.x) {
         const std::uint32_t v = p.wlist[i];
-        const PJV x = a[v];
-        const PJV y = a[x.nxt];
-        PJV z;
-        z.acc = x.acc + y.acc;
-        z.nxt = y.nxt;
-        z.root = x.root;
-        o[v] = z;
+        const std::uint32_t r = __ldg(&p.reg[v]);
+        if (p.comp[v] == p.src[r]) {
+            p.rem[1][atomicAdd(&s_nw, 1u)] = v;
+            wc_init_one(p, v, r);
+        }
     }
+    __syncthreads();
+    const unsigned nW = s_nw, maxlen = s_maxlen;
+    c->wc_n[stamp & 1] = (static_cast<unsigned long long>(stamp) << 32) | nW;
+    c->wc_len[stamp & 1] = maxlen;
+    if (nW > p.small_wc) {
+        if (threadIdx.x == 0)
+            c->wc_big[stamp & 1] = stamp;
+        return;
+    }
+    const int wr = ceil_log2_d(maxlen > 1 ? maxlen - 1 : 1); // farthest: len-1 steps
+    for (int j = 0; j < wr; ++j) {
+        wc_round(p, p.rem[1], nW, j, threadIdx.x, blockDim.x);
+        __syncthreads();
+    }
+    wc_final(p, p.rem[1], nW, wr, threadIdx.x, blockDim.x);
 }
 
-__device__ __noinline__ void ph_wc_final(const KP& p, std::uint64_t nW, int wr, std::uint64_t from,
-                                         std::uint64_t step) {
-    const PJV* fin = p.pv[wr & 1];
-    for (std::uint64_t i = from; i < nW; i += step) {
-        const std::uint32_t v = p.wlist[i];
-        p.key_i[v] = fin[v].acc;
-    }
-}
-
-// Kept component (howard_par.hpp:370/393): vertices whose policy path
-// enters the winning cycle keep their edges; exact keys from the doubling
-// sums, K(v) = W_L(v)*den - L*num + K(jump v), since the winning cycle's
-// reduced weight is exactly 0. Others queue for re-attachment. Resets the
-// peeling state of core vertices.
+// Kept component (howard_par.hpp:370/393) on the core: vertices whose
+// policy path enters the winning cycle keep their edges; exact keys from the
+// doubling sums, K(v) = W_L(v)*den - L*num + K(jump v), since the winning
+// cycle's reduced weight is exactly 0. Others queue for re-attachment.
 template <bool EXACT>
-__device__ __noinline__ void ph_keep(const KP& p, std::uint64_t nC, int in, std::uint32_t stamp,
-                                     unsigned long long L, const Ring& ring) {
+__device__ __forceinline__ void ph_keep(const KP& p, std::uint64_t nC, int in, std::uint32_t stamp,
+                                        unsigned long long L, const Ring& ring) {
     const PJC* a = p.pj[in];
     bool ovf = false;
     OCM_BLOCK_LOOP(i0, 0, nC) {
@@ -728,17 +759,14 @@ __device__ __noinline__ void ph_keep(const KP& p, std::uint64_t nC, int in, std:
         if (i < nC) {
             v = p.clist[i];
             const std::uint32_t r = __ldg(&p.reg[v]);
-            const std::uint32_t an = p.ccomp[i];
-            const bool kept = an == p.src[r];
-            p.comp[v] = an;
+            const bool kept = p.comp[v] == p.src[r];
             p.conn[v] = kept ? 0u : NONE;
             p.indeg[v] = 0;
-            p.peel[v] = 0;
             take = !kept;
-            if (EXACT && kept && p.cmark[i] != stamp) {
-                const PJC x = a[i];
+            if (EXACT && kept && p.cmark[v] != stamp) {
+                const PJC x = a[v];
                 const __int128 kk = static_cast<__int128>(x.w) * p.lam_den[r] -
-                                    static_cast<__int128>(L) * p.lam_num[r] + p.key_i[p.clist[x.nxt]];
+                                    static_cast<__int128>(L) * p.lam_num[r] + p.key_i[x.nxt];
                 ovf |= !key_in_range(kk);
                 p.key_i[v] = static_cast<long long>(kk);
             }
@@ -750,17 +778,17 @@ __device__ __noinline__ void ph_keep(const KP& p, std::uint64_t nC, int in, std:
     block_flag(ovf, &p.c->overflow, 1);
 }
 
-// One peeled layer, last layer first: anchor and key from the successor
+// Leaves take anchor and key from their successor, always a core vertex
 // (K(v) = K(succ) + w*den - num along the kept tree).
 template <bool EXACT>
-__device__ __noinline__ void ph_unpeel(const KP& p, std::uint64_t lo, std::uint64_t hi,
-                                       std::uint64_t out_base, const Ring& ring) {
+__device__ __forceinline__ void ph_leafvals(const KP& p, std::uint64_t nL, std::uint64_t out_base,
+                                            const Ring& ring) {
     bool ovf = false;
-    OCM_BLOCK_LOOP(i0, lo, hi) {
+    OCM_BLOCK_LOOP(i0, 0, nL) {
         const std::uint64_t i = i0_b + threadIdx.x;
         bool take = false;
         std::uint32_t v = 0;
-        if (i < hi) {
+        if (i < nL) {
             v = p.plist[i];
             const std::uint32_t s = p.succ_v[v];
             const std::uint32_t r = __ldg(&p.reg[v]);
@@ -768,7 +796,6 @@ __device__ __noinline__ void ph_unpeel(const KP& p, std::uint64_t lo, std::uint6
             const bool kept = an == p.src[r];
             p.comp[v] = an;
             p.conn[v] = kept ? 0u : NONE;
-            p.peel[v] = 0;
             take = !kept;
             if (EXACT && kept) {
                 const __int128 kk = static_cast<__int128>(p.key_i[s]) +
@@ -789,8 +816,8 @@ __device__ __noinline__ void ph_unpeel(const KP& p, std::uint64_t lo, std::uint6
 // earlier layer (conn < layer); the stamps make the layer discipline exact
 // under any schedule.
 template <bool EXACT>
-__device__ __noinline__ void ph_attach(const KP& p, int cur, std::uint64_t pending, std::uint32_t layer,
-                                       const Ring& ring) {
+__device__ __forceinline__ void ph_attach(const KP& p, int cur, std::uint64_t pending, std::uint32_t layer,
+                                          const Ring& ring) {
     const std::uint32_t* list = p.rem[cur];
     bool ovf = false;
     OCM_BLOCK_LOOP(i0, 0, pending) {
@@ -836,7 +863,7 @@ __device__ __noinline__ void ph_attach(const KP& p, int cur, std::uint64_t pendi
 
 // Float lane: level-synchronous propagation from the anchor, computing
 // (value(succ) + w) - lambda exactly as FloatMode::extend (policy.hpp:105).
-__device__ __noinline__ void ph_fprop_init(const KP& p) {
+__device__ __forceinline__ void ph_fprop_init(const KP& p) {
     for (std::size_t v = gtid(); v < p.N; v += gstride()) {
         if (!working(p, static_cast<std::uint32_t>(v)))
             continue;
@@ -849,8 +876,8 @@ __device__ __noinline__ void ph_fprop_init(const KP& p) {
     }
 }
 
-__device__ __noinline__ void ph_fprop_level(const KP& p, std::uint32_t level, unsigned long long* flag,
-                                            unsigned long long tag) {
+__device__ __forceinline__ void ph_fprop_level(const KP& p, std::uint32_t level, unsigned long long* flag,
+                                               unsigned long long tag) {
     bool nd = false;
     OCM_BLOCK_LOOP(v0, 0, p.N) {
         const std::uint64_t v = v0_b + threadIdx.x;
@@ -879,9 +906,11 @@ template <bool EXACT> __global__ void __launch_bounds__(kBlock, kSolveMinBlocks)
     cg::grid_group grid = cg::this_grid();
     Ctl* const c = p.c;
     const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
-    Ring ring;
-    ring.init(c->ring[0]);
-    unsigned long long nsync = 0;
+    Ring ra, rl, rc; // active-region counts, lists, core list
+    ra.init(c->ring[0]);
+    rl.init(c->ring[1]);
+    rc.init(c->ring[2]);
+    unsigned nsync = 0;
     long long clk0 = 0, clk_last = 0;
     if (leader)
         clk_last = clk0 = clock64();
@@ -895,11 +924,12 @@ template <bool EXACT> __global__ void __launch_bounds__(kBlock, kSolveMinBlocks)
         }
     };
     const int K_max = max(1, ceil_log2_d(max(p.max_region, 2u)));
-    unsigned stamp = ldv(c->stamp);
-    unsigned k_hint = max(1u, min(ldv(c->k_hint), static_cast<unsigned>(K_max)));
-    unsigned k_streak = ldv(c->k_streak);
-    unsigned passes = 0, outer = 0;
-    unsigned long long rounds = 0, verifies = 0, peeled = 0, cored = 0, layers = 0;
+    unsigned stamp = ldr(c->stamp);
+    unsigned k_hint = max(1u, min(ldr(c->k_hint), static_cast<unsigned>(K_max)));
+    unsigned k_streak = ldr(c->k_streak);
+    unsigned passes = 0, outer = 0, rounds = 0, verifies = 0, layers = 0;
+    unsigned long long peeled = 0, cored = 0;
+    unsigned long long done_base = ldr(c->done);
     bool fatal = false; // uniform: a fixpoint failed to converge
 
     ph_init(p, EXACT);
@@ -911,40 +941,31 @@ template <bool EXACT> __global__ void __launch_bounds__(kBlock, kSolveMinBlocks)
         ++passes;
         sync(PH_IMPROVE);
 
-        ph_region(p, par, ring);
-        sync(PH_REGION);
-        const std::uint64_t n_active = ring.take();
-        // written only by improve/adopt/keep/unpeel/attach, never by the
-        // leaves phase that follows: every block reads the same values here
-        if (n_active == 0 || ldv(c->error) || ldv(c->overflow) || ldv(c->lambda_up))
+#ifdef OCM_INDEG_PHASE
+        // experiment: in-degrees counted in their own pass instead of in
+        // the improvement pass
+        for (std::size_t v = gtid(); v < p.N; v += gstride())
+            if (p.changed[par][__ldg(&p.reg[v])])
+                atomicAdd(&p.indeg[p.succ_v[v]], 1u);
+        sync(PH_CLASSIFY);
+#endif
+        ph_classify<EXACT>(p, par, ra, rl, rc);
+        sync(PH_CLASSIFY);
+        const std::uint64_t n_active = ra.take();
+        const std::uint64_t nL = rl.take();
+        const std::uint64_t nC = rc.take();
+        // written only by improve/adopt/keep/leafvals/attach, never by the
+        // rounds that follow: every block reads the same values here
+        if (n_active == 0 || ldr(c->error) || ldr(c->overflow) || ldr(c->lambda_up))
             break; // quiet pass (or a failure the host reports)
         ++outer;
-
-        // ---- peel while the layers are large
-        ph_leaves(p, ring);
-        sync(PH_LEAVES);
-        std::uint64_t lofs[kMaxPeel + 2];
-        lofs[0] = 0;
-        lofs[1] = ring.take();
-        int done = 0;
-        while (done < p.peel_max && lofs[done + 1] - lofs[done] >= p.peel_min) {
-            ph_peel(p, lofs[done], lofs[done + 1], static_cast<std::uint32_t>(done + 2), ring);
-            sync(PH_PEEL);
-            ++done;
-            lofs[done + 1] = lofs[done] + ring.take();
-        }
-        peeled += lofs[done];
-
-        ph_core(p, static_cast<std::uint32_t>(done), ring);
-        sync(PH_CORE);
-        const std::uint64_t nC = ring.take();
+        peeled += nL;
         cored += nC;
-        ph_pjinit<EXACT>(p, nC);
-        sync(PH_PJINIT);
 
         // ---- pointer doubling on the core, verified exactly
         int in = 0, k = 0;
         bool first_try = true;
+        std::uint64_t nM = 0;
         for (;;) {
             for (; k < static_cast<int>(k_hint); ++k, in ^= 1) {
                 ph_round(p, nC, in);
@@ -954,13 +975,14 @@ template <bool EXACT> __global__ void __launch_bounds__(kBlock, kSolveMinBlocks)
             ++stamp;
             ++verifies;
             unsigned* vflag = &c->vfail[stamp & 1];
-            ph_mark(p, nC, in, stamp);
+            ph_mark(p, nC, in, stamp, EXACT, ra);
             sync(PH_VERIFY);
-            ph_verify1(p, nC, stamp, vflag);
+            const std::uint64_t m_size = ra.take();
+            ph_check<EXACT>(p, nC, stamp, vflag, rc, rl);
             sync(PH_VERIFY);
-            ph_verify2(p, nC, stamp, vflag);
-            sync(PH_VERIFY);
-            if (ldv(*vflag) != stamp)
+            const std::uint64_t s_size = rc.take();
+            nM = rl.take();
+            if (ldr(*vflag) != stamp && s_size == m_size)
                 break;
             if (k >= K_max) {
                 fatal = true;
@@ -981,55 +1003,38 @@ template <bool EXACT> __global__ void __launch_bounds__(kBlock, kSolveMinBlocks)
                 k_streak = 0;
         }
 
-        // ---- cycle records, vote, adoption
-        ph_stats<EXACT>(p, nC, stamp);
-        sync(PH_STATS);
-        ph_vote<EXACT>(p, nC, stamp);
+        // ---- vote, adoption and the winning cycles' values
+        if constexpr (!EXACT) {
+            ph_stats_float(p, nM);
+            sync(PH_STATS);
+        }
+        ph_vote<EXACT>(p, nM, stamp, done_base);
+        done_base += gridDim.x;
         sync(PH_VOTE);
-        ph_adopt<EXACT>(p, stamp);
-        sync(PH_ADOPT);
-
-        // ---- values on the winning cycle(s)
-        if constexpr (EXACT) {
-            ph_wc_init(p, nC, stamp, ring);
-            sync(PH_WINCYC);
-            const std::uint64_t nW = ring.take();
-            const unsigned long long mc = ldv(c->maxcyc);
-            const unsigned maxlen = (mc >> 32) == stamp ? static_cast<unsigned>(mc) : 1u;
-            const int wr = ceil_log2_d(maxlen > 1 ? maxlen - 1 : 1); // farthest: len-1 steps
-            if (nW <= p.small_wc) {
-                if (blockIdx.x == 0) { // one block, block barriers only
-                    for (int j = 0; j < wr; ++j) {
-                        ph_wc_round(p, nW, j, threadIdx.x, blockDim.x);
-                        __syncthreads();
-                    }
-                    ph_wc_final(p, nW, wr, threadIdx.x, blockDim.x);
-                }
-            } else {
-                for (int j = 0; j < wr; ++j) {
-                    ph_wc_round(p, nW, j, gtid(), gstride());
-                    sync(PH_WINCYC);
-                }
-                ph_wc_final(p, nW, wr, gtid(), gstride());
+        if (EXACT && ldr(c->wc_big[stamp & 1]) == stamp) {
+            const std::uint64_t nW = static_cast<std::uint32_t>(ldr(c->wc_n[stamp & 1]));
+            const unsigned maxlen = ldr(c->wc_len[stamp & 1]);
+            const int wr = ceil_log2_d(maxlen > 1 ? maxlen - 1 : 1);
+            for (int j = 0; j < wr; ++j) {
+                wc_round(p, p.rem[1], nW, j, gtid(), gstride());
+                sync(PH_WINCYC);
             }
-            rounds += wr;
+            wc_final(p, p.rem[1], nW, wr, gtid(), gstride());
             sync(PH_WINCYC);
         }
 
-        // ---- kept component, peeled layers in reverse, re-attachment
-        ph_keep<EXACT>(p, nC, in, stamp, 1ull << k, ring);
+        // ---- kept component (core, then leaves), re-attachment
+        ph_keep<EXACT>(p, nC, in, stamp, 1ull << k, rl);
         sync(PH_KEEP);
-        std::uint64_t pending = ring.take();
-        for (int l = done; l >= 1; --l) {
-            ph_unpeel<EXACT>(p, lofs[l - 1], lofs[l], pending, ring);
-            sync(PH_UNPEEL);
-            pending += ring.take();
-        }
+        std::uint64_t pending = rl.take();
+        ph_leafvals<EXACT>(p, nL, pending, rl);
+        sync(PH_LEAVES);
+        pending += rl.take();
         int cur = 0;
         for (std::uint32_t layer = 1; pending > 0; ++layer) {
-            ph_attach<EXACT>(p, cur, pending, layer, ring);
+            ph_attach<EXACT>(p, cur, pending, layer, rl);
             sync(PH_ATTACH);
-            const std::uint64_t next = ring.take();
+            const std::uint64_t next = rl.take();
             ++layers;
             if (next == pending) { // connect_gpi_fixpoint: not strongly connected
                 fatal = true;
@@ -1050,7 +1055,7 @@ template <bool EXACT> __global__ void __launch_bounds__(kBlock, kSolveMinBlocks)
                 ph_fprop_level(p, level, flag, tag);
                 sync(PH_FLOAT);
                 ++layers;
-                if (ldv(*flag) != tag)
+                if (ldr(*flag) != tag)
                     break;
                 if (level > p.max_region + 1) {
                     fatal = true;

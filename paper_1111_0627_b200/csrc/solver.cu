@@ -68,8 +68,7 @@ Session::Session(const Graph& g, const ocm_solve_options& opt) : opt_(opt) {
         d.cyc_wf.alloc(N1, d.stream);
     }
     for (auto* b : {&d.succ_e, &d.succ_v, &d.comp, &d.wlist, &d.cyc_len, &d.conn, &d.rem0, &d.rem1,
-                    &d.indeg, &d.peel, &d.plist, &d.clist, &d.cidx, &d.csucc, &d.ccomp, &d.cmark,
-                    &d.cmark2})
+                    &d.indeg, &d.plist, &d.clist, &d.cmark, &d.cmark2})
         b->alloc(N1, d.stream);
     d.pj0.alloc(N1, d.stream);
     d.pj1.alloc(N1, d.stream);
@@ -131,12 +130,8 @@ Session::Session(const Graph& g, const ocm_solve_options& opt) : opt_(opt) {
     p.pj[1] = d.pj1.p;
     p.comp = d.comp.p;
     p.indeg = d.indeg.p;
-    p.peel = d.peel.p;
     p.plist = d.plist.p;
     p.clist = d.clist.p;
-    p.cidx = d.cidx.p;
-    p.csucc = d.csucc.p;
-    p.ccomp = d.ccomp.p;
     p.cmark = d.cmark.p;
     p.cmark2 = d.cmark2.p;
     p.wlist = d.wlist.p;
@@ -176,16 +171,14 @@ template <class M> void Session::run(ocm_solution* out, std::uint32_t* cycle_buf
     Ctl& hc = *d.h_ctl;
     std::uint64_t d2h = 0;
 
-    // G lanes per improvement vertex: G*4 ~ average degree (U = 4 edges in
-    // flight per lane). OCM_IMPROVE_G / OCM_PEEL_MIN / OCM_PEEL_MAX override.
+    // G lanes per improvement vertex (U = 4 edges in flight per lane): one
+    // lane up to degree 8 (measured best at 8), then G*8 ~ average degree.
+    // OCM_IMPROVE_G overrides.
     const double avg_deg = prep_.R ? double(prep_.M) / std::max<double>(1.0, double(prep_.n - prep_.trivial)) : 1.0;
     int G = 1;
-    while (G < 32 && G * 4 < avg_deg)
+    while (G < 32 && G * 8 < avg_deg)
         G *= 2;
     p.G = env_int("OCM_IMPROVE_G", G);
-    p.peel_min = static_cast<std::uint32_t>(
-        env_int("OCM_PEEL_MIN", static_cast<int>(std::max<std::uint32_t>(4096u, prep_.n >> 8))));
-    p.peel_max = std::min(kMaxPeel, env_int("OCM_PEEL_MAX", 16));
     p.small_wc = 4096;
 
     CK(cudaEventRecord(d.ev_start, s));
@@ -215,10 +208,9 @@ template <class M> void Session::run(ocm_solution* out, std::uint32_t* cycle_buf
     CK(cudaEventElapsedTime(&ms, d.ev_start, d.ev_end));
     static const bool phases_on = std::getenv("OCM_PHASES") != nullptr;
     if (phases_on && prep_.R > 0 && hc.clk_total > 0) {
-        static const char* names[PH_COUNT] = {"init",   "improve", "region", "leaves", "peel",
-                                              "core",   "pjinit",  "round",  "verify", "stats",
-                                              "vote",   "adopt",   "wincyc", "keep",   "unpeel",
-                                              "attach", "float"};
+        static const char* names[PH_COUNT] = {"init",  "improve", "classify", "round",
+                                              "verify", "stats",  "vote",     "wincyc",
+                                              "keep",  "leaves",  "attach",   "float"};
         std::string ph;
         for (int i = 0; i < PH_COUNT; ++i) {
             char buf[64];
@@ -228,12 +220,12 @@ template <class M> void Session::run(ocm_solution* out, std::uint32_t* cycle_buf
         }
         std::fprintf(stderr,
                      "{\"device_ms\": %.3f, \"phases_ms\": {%s}, \"passes\": %u, \"outer\": %u, "
-                     "\"rounds\": %llu, \"verifies\": %llu, \"peeled\": %llu, \"cored\": %llu, "
-                     "\"layers\": %llu, \"syncs\": %llu, \"k_hint\": %u, \"N\": %u, \"M\": %llu}\n",
-                     ms, ph.c_str(), hc.passes, hc.outer, (unsigned long long)hc.rounds,
-                     (unsigned long long)hc.verifies, (unsigned long long)hc.peeled,
-                     (unsigned long long)hc.cored, (unsigned long long)hc.layers,
-                     (unsigned long long)hc.syncs, hc.k_hint, p.N, (unsigned long long)prep_.M);
+                     "\"rounds\": %u, \"verifies\": %u, \"peeled\": %llu, \"cored\": %llu, "
+                     "\"layers\": %u, \"syncs\": %u, \"k_hint\": %u, \"N\": %u, \"M\": %llu}\n",
+                     ms, ph.c_str(), hc.passes, hc.outer, hc.rounds,
+                     hc.verifies, (unsigned long long)hc.peeled,
+                     (unsigned long long)hc.cored, hc.layers,
+                     hc.syncs, hc.k_hint, p.N, (unsigned long long)prep_.M);
     }
 
     std::memset(out, 0, sizeof *out);
@@ -245,7 +237,7 @@ template <class M> void Session::run(ocm_solution* out, std::uint32_t* cycle_buf
     out->n_solved = prep_.n;
     out->m_solved = prep_.M;
     out->launches = prep_.R > 0 ? 1 : 0;
-    out->fixpoint_iters = hc.rounds + hc.layers;
+    out->fixpoint_iters = std::uint64_t(hc.rounds) + hc.layers;
     out->device_ms = ms;
     // share of the launch spent in improvement phases (SM clock spans of
     // block 0, measured between the same grid barriers) times the event time

@@ -1,0 +1,75 @@
+"""Model generator (proj/include/ocm/model_gen.hpp) against the reference.
+
+CPU: the library's generate_model reproduces the reference's composite state
+spaces bit for bit (golden digests of the unmodified reference,
+tests/golden/make_model_golden.py) and its error contract. GPU: the device
+lane solves the generated models to the reference's optimal cycle means.
+"""
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+
+import paper_1111_0627_b200 as P
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "model_golden.json")))
+
+
+def scenario(kind):
+    if kind == "worker":
+        return P.worker_scenario()
+    if kind == "server":
+        return P.server_scenario()
+    return P.loop_scenario(GOLD["loop_costs"])
+
+
+def digest(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+@pytest.mark.parametrize("case", GOLD["cases"], ids=[f"{c['kind']}-{c['clients']}" for c in GOLD["cases"]])
+def test_model_matches_reference(case):
+    g = P.generate_model(scenario(case["kind"]), case["clients"])
+    assert (g.n, g.m) == (case["n"], case["m"])
+    s, d, w = g.edges()
+    assert (digest(s), digest(d), digest(w)) == (case["src"], case["dst"], case["w"])
+    assert g.integer_exact
+
+
+def test_model_errors():
+    with pytest.raises(P.StructuralError, match=GOLD["too_large_message"]):
+        P.generate_model(P.server_scenario(), 19)
+    with pytest.raises(ValueError, match="at least one state and one client"):
+        P.generate_model(P.server_scenario(), 0)
+    bad = P.Scenario("bad", 2, [P.Transition(0, 5, 1)])
+    with pytest.raises(ValueError, match="missing state"):
+        P.generate_model(bad, 2)
+    srv = P.Scenario("srv", 2, [P.Transition(0, 1, 1, acquires=True)])
+    with pytest.raises(ValueError, match="server-free"):
+        P.generate_model(srv, 2)
+    with pytest.raises(ValueError, match="64 bits"):
+        P.generate_model(P.loop_scenario([1] * 5), 30)
+    with pytest.raises(ValueError, match="at least one transition"):
+        P.loop_scenario([])
+
+
+def test_model_beyond_reference_bound():
+    # the library's own bound is a parameter; growth is monotone in clients
+    a = P.generate_model(P.worker_scenario(), 6)
+    b = P.generate_model(P.worker_scenario(), 7, max_states=10_000)
+    assert b.n == 3 * a.n == 2187
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", [c for c in GOLD["cases"] if "min" in c],
+                         ids=[f"{c['kind']}-{c['clients']}" for c in GOLD["cases"] if "min" in c])
+def test_model_solve_matches_reference(case):
+    g = P.generate_model(scenario(case["kind"]), case["clients"])
+    for obj in ("min", "max"):
+        sol = P.solve(g, P.SolveOptions(objective=obj))
+        num, den, cyc, clen = case[obj]
+        assert sol.has_cycle
+        assert (sol.mu_exact.numerator, sol.mu_exact.denominator) == (num, den), obj
+        assert len(sol.cycle_vertices) == clen and sol.cycle_vertices[:64] == cyc, obj
