@@ -1,15 +1,24 @@
 """Benchmark: policy-iteration throughput of the B200 optimal-cycle-mean solver.
 
-Workload (BASELINE.json configs[1]): random sparse digraph, 10^6 vertices,
-out-degree 8, integer weights 1..100, min AND max cycle mean. One step = one
-full time-to-OCM solve for each objective on the graph resident in HBM
-(policy iteration from the initial policy until no policy edge changes).
+One step = one full time-to-OCM solve (policy iteration from the initial
+policy until no policy edge changes) for the minimum AND the maximum cycle
+mean of the workload graph, resident in HBM.
 
-metric: edges/s per policy iteration = intra-region edges x improvement passes
-/ device time, summed over ranks (weak scaling: every rank solves its own
-seeded instance; the path's per-iteration work is independent per graph).
+metric: edges/s per policy iteration = intra-region edges x improvement
+passes / device time, summed over ranks (weak scaling: every rank solves its
+own seeded instance -- round 1 runs replicas).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+Workloads (--config, BASELINE.json "configs", 1-based):
+  1  uniform 10^4 vertices, out-degree 4 (the reference's CPU-runnable case)
+  2  uniform 10^6 vertices, out-degree 8 -- the default (the metric's config)
+  3  client/server state space, 19 clients (1.05*10^7 states, 2.0*10^8 edges;
+     the reference's generate_model scenario beyond its 5*10^6-state bound)
+  4  power-law out-degree graph, 6.4*10^7 vertices, ~1.0*10^9 edges
+  5  uniform 2.5*10^8 vertices, out-degree 8 (2*10^9 edges)
+Graphs 1, 2, 4, 5 are generated directly in HBM (bit-identical to the host
+generator the checkers use); 3 is generated on the host and uploaded.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference] [--config C]
 """
 from __future__ import annotations
 
@@ -27,6 +36,24 @@ sys.path.insert(0, ROOT)
 METRIC = "policy-iteration edges/s (time-to-OCM, min+max cycle mean)"
 UNIT = "edges/s"
 L2_FLUSH_BYTES = 512 << 20  # > 126 MB L2
+SEED = 1111_0627
+
+CONFIGS = {
+    1: dict(kind="uniform", n=10_000, deg=4, desc="uniform random digraph n=10^4 out-degree 4 weights "
+                                                 "1..100 (BASELINE configs[0])"),
+    2: dict(kind="uniform", n=1_000_000, deg=8, desc="uniform random digraph n=10^6 out-degree 8 "
+                                                     "weights 1..100 (BASELINE configs[1])"),
+    3: dict(kind="model", clients=19, desc="client/server state space (reference server scenario, "
+                                           "19 clients, BFS-numbered; BASELINE configs[2])"),
+    4: dict(kind="powerlaw", n=64_000_000, deg=8, dmax=1 << 20,
+            desc="power-law out-degree digraph n=6.4*10^7 (deg = min(2^20, floor(8/sqrt(u))), "
+                 "~1.0*10^9 edges) weights 1..100 (BASELINE configs[3])"),
+    5: dict(kind="uniform", n=250_000_000, deg=8, desc="uniform random digraph n=2.5*10^8 "
+                                                       "out-degree 8 weights 1..100 (BASELINE configs[4])"),
+}
+# CPU baseline samples: the same generator at a size the reference solves in seconds
+CPU_SAMPLE = {1: dict(n=10_000), 2: dict(n=250_000), 3: dict(clients=13), 4: dict(n=250_000),
+              5: dict(n=250_000)}
 
 
 def parse():
@@ -35,20 +62,20 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--n", type=int, default=1_000_000)
-    ap.add_argument("--deg", type=int, default=8)
-    ap.add_argument("--seed", type=int, default=1111_0627)
-    ap.add_argument("--cpu-sample-n", type=int, default=250_000)
+    ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
     return ap.parse_args()
 
 
 def config(a, world):
-    return {"workload": f"uniform random digraph n={a.n} out-degree {a.deg} weights 1..100 "
-                        f"(BASELINE configs[1]), min+max cycle mean per step",
-            "n": a.n, "out_degree": a.deg, "weights": [1, 100], "seed": a.seed,
-            "objectives": ["min", "max"], "parallelism": f"replicas x{world}" if world > 1 else "1 gpu",
-            "l2": "flushed between steps (512 MiB write)"}
+    c = CONFIGS[a.config]
+    out = {"workload": c["desc"] + ", min+max cycle mean per step", "config_index": a.config,
+           "weights": [1, 100], "seed": SEED, "objectives": ["min", "max"],
+           "parallelism": f"replicas x{world}" if world > 1 else "1 gpu",
+           "l2": "flushed between steps (512 MiB write)"}
+    out.update({k: v for k, v in c.items() if k not in ("desc",)})
+    return out
 
 
 def dist_env():
@@ -73,7 +100,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -121,27 +148,42 @@ def measured_peak():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def ncu_traffic():
-    """dram bytes per k_improve launch from the committed ncu --set full summary."""
+def ncu_traffic(cfg):
+    """DRAM bytes per k_solve launch from the committed ncu --set full summary."""
     try:
-        with open(os.path.join(ROOT, "profiles", "improve_traffic.json")) as f:
-            return json.load(f).get("dram_bytes_per_launch")
+        with open(os.path.join(ROOT, "profiles", "solve_traffic.json")) as f:
+            return json.load(f).get(str(cfg), {}).get("dram_bytes_per_launch")
     except Exception:
         return None
 
 
-def improve_bytes(n_solved, m_solved):
-    """Algorithmic bytes of one k_improve launch (kernel 1): per edge an
-    8 B {target, weight} record and an 8 B key gather; per vertex row (4 B),
-    region id (4 B), incumbent edge/target/weight (12 B) and its key (8 B)."""
-    return 16 * m_solved + 28 * n_solved
+def algorithmic_bytes(stats):
+    """Algorithmic bytes of one solve: every improvement pass
+    streams each intra-region edge's 8 B {target, weight} record and gathers
+    its head's 8 B key (16 B/edge) and touches 28 B per vertex (row 4,
+    region 4, incumbent edge/head/weight 12, key 8); every policy iteration
+    then reads each vertex's policy head and weight (8 B) and writes its key
+    (8 B) to determine the values (16 B/vertex)."""
+    imp = 16 * stats.m_solved + 28 * stats.n_solved
+    return stats.spf_passes * imp + stats.outer_iters * 16 * stats.n_solved, imp
 
 
-def cpu_sample(a, steps=1):
-    """Reference CPU solver on a bounded sample (same generator, smaller n)."""
+def build_graph_host(a, P, sample=None):
+    c = dict(CONFIGS[a.config])
+    if sample:
+        c.update(sample)
+    if c["kind"] == "model":
+        return P.generate_model(P.server_scenario(), c["clients"], max_states=1 << 31)
+    return P.generate(P.Generator(c["kind"], n=c["n"], deg=c["deg"], dmax=c.get("dmax", 0),
+                                  wlo=1, whi=100, seed=SEED))
+
+
+def cpu_sample(a, P, steps=1):
+    """Reference CPU solver on a bounded sample (same generator, smaller size)."""
     import oracle as O
-    n = a.cpu_sample_n
-    s, d, w = O.generate_uniform(n, a.deg, 1, 100, a.seed)
+    g = build_graph_host(a, P, CPU_SAMPLE[a.config])
+    s, d, w = g.edges()
+    n = g.n
     use_ref = O.ref_available()
     tot_ms, edges = 0.0, 0
     for _ in range(steps):
@@ -149,28 +191,54 @@ def cpu_sample(a, steps=1):
             if use_ref:
                 r = O.ref_solve(n, s, d, w, "howard", objective, "tarjan")
                 tot_ms += r.solve_ms
+                passes = r.spf_passes
             else:
                 t0 = time.perf_counter()
                 r = O.oracle_solve(n, s, d, w, objective)
                 tot_ms += (time.perf_counter() - t0) * 1e3
-                r.extra["spf_passes_seq"] = r.extra.get("spf_passes_seq", r.spf_passes)
-            passes = r.spf_passes if use_ref else r.extra["spf_passes_seq"]
-            edges += len(s) * passes
+                passes = r.extra.get("spf_passes_seq", r.spf_passes)
+            # intra-region edges per pass, as on the device
+            edges += _intra_edges(n, s, d) * passes
+    smp = CPU_SAMPLE[a.config]
+    what = (f"server scenario {smp['clients']} clients" if "clients" in smp
+            else f"{CONFIGS[a.config]['kind']} n={smp['n']}")
     return {"value": edges / (tot_ms / 1e3), "unit": UNIT, "cores": 1,
             "kind": "reference" if use_ref else "port",
-            "sample": f"uniform n={n} deg={a.deg} weights 1..100, min+max, reference lane "
-                      f"'howard' (proj/src/solve.cpp run_howard_seq, single thread; the default "
-                      f"CLI lane and the fastest reference lane on this workload), "
-                      f"{steps} step(s), solve time only",
+            "sample": f"{what} (same generator), min+max, reference lane 'howard' "
+                      f"(proj/src/solve.cpp run_howard_seq, single thread; the default CLI lane and "
+                      f"the fastest reference lane on these workloads), {steps} step(s), solve time "
+                      f"only",
             "ms": tot_ms}
+
+
+_INTRA = {}
+
+
+def _intra_edges(n, s, d):
+    """Edges inside non-trivial SCCs (what an improvement pass streams)."""
+    key = (n, len(s))
+    if key not in _INTRA:
+        import numpy as np
+        from scipy.sparse import csr_matrix
+        from scipy.sparse.csgraph import connected_components
+        g = csr_matrix((np.ones(len(s), np.int8), (s.astype(np.int64), d.astype(np.int64))),
+                       shape=(n, n))
+        _, lab = connected_components(g, directed=True, connection="strong")
+        size = np.bincount(lab)
+        self_loop = np.zeros(n, bool)
+        self_loop[s[s == d]] = True
+        nontriv = (size[lab] > 1) | self_loop
+        _INTRA[key] = int(np.count_nonzero((lab[s] == lab[d]) & nontriv[s]))
+    return _INTRA[key]
 
 
 def run_reference(a, world, rank):
     if rank != 0:
         return
+    import paper_1111_0627_b200 as P
     steps = []
     for i in range(a.warmup + a.steps):
-        r = cpu_sample(a, 1)
+        r = cpu_sample(a, P, 1)
         if i >= a.warmup:
             steps.append(r)
     tot_ms = sum(r["ms"] for r in steps)
@@ -179,11 +247,22 @@ def run_reference(a, world, rank):
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": world,
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": tot_ms / a.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
-            "data": "synthetic (seeded uniform digraph)", "config": config(a, 1),
+            "data": "synthetic (seeded generator)", "config": config(a, 1),
             "cpu_baseline": {"value": val, "unit": UNIT, "cores": base["cores"],
                              "kind": base["kind"], "sample": base["sample"]},
             "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def make_sessions(a, P, rank, local):
+    c = CONFIGS[a.config]
+    opts = {o: P.SolveOptions(objective=o, device=local) for o in ("min", "max")}
+    if c["kind"] == "model":
+        g = build_graph_host(a, P)
+        return g, {o: P.Session(g, opts[o]) for o in opts}
+    spec = P.Generator(c["kind"], n=c["n"], deg=c["deg"], dmax=c.get("dmax", 0), wlo=1, whi=100,
+                       seed=SEED + rank)
+    return spec, {o: P.Session.generated(spec, opts[o]) for o in opts}
 
 
 def main():
@@ -206,8 +285,7 @@ def main():
     dev = torch.device("cuda", local)
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=dev)
 
-    g = P.generate_uniform(a.n, a.deg, 1, 100, a.seed + rank)
-    sess = {o: P.Session(g, P.SolveOptions(objective=o, device=local)) for o in ("min", "max")}
+    src_desc, sess = make_sessions(a, P, rank, local)
 
     def step():
         out = {}
@@ -235,71 +313,86 @@ def main():
     imp_ms = sum(s[o].stats.improve_ms for s in sols for o in s)
     passes = sum(s[o].stats.spf_passes for s in sols for o in s)
     launches = sum(s[o].stats.launches for s in sols for o in s)
-    m_solved = sols[0]["min"].stats.m_solved
-    n_solved = sols[0]["min"].stats.n_solved
-    edges = m_solved * passes
+    edges = sum(s[o].stats.m_solved * s[o].stats.spf_passes for s in sols for o in s)
+    alg = sum(algorithmic_bytes(s[o].stats)[0] for s in sols for o in s)
+    imp_bytes = sum(algorithmic_bytes(s[o].stats)[1] * s[o].stats.spf_passes for s in sols for o in s)
+    st0 = sols[0]["min"].stats
+    for s in sols:
+        for o in s:
+            assert s[o].has_cycle and s[o].stats.launches >= 1, "device lane did not run"
 
-    # end-to-end through the public API: the host graph (CSR in pinned host
-    # memory, built and pinned once outside the timed region, as a user's
-    # loaded graph would be) goes through ocm_solve every step: upload, device
-    # region split, policy iteration, result read-back.
-    src, dst, w = g.edges()
-    gg = P.build_graph(a.n, (src, dst, w))
-    P.solve(gg, P.SolveOptions(objective="min", device=local))  # pins the host arrays
-    e2e_s, e2e_edges, h2d, d2h = 0.0, 0, 0, 0
-    e2e_steps = max(1, a.steps)
-    torch.cuda.synchronize()
-    for i in range(e2e_steps):
-        t0 = time.perf_counter()
-        for o in ("min", "max"):
-            s = P.solve(gg, P.SolveOptions(objective=o, device=local))
-            e2e_edges += s.stats.m_solved * s.stats.spf_passes
-            h2d += s.stats.h2d_bytes
-            d2h += s.stats.d2h_bytes
-        e2e_s += time.perf_counter() - t0
+    # end to end through the public API: the host graph (built and pinned once
+    # outside the timed region, as a user's loaded graph would be) goes
+    # through ocm_solve every step: upload, device region split, policy
+    # iteration, result read-back.
+    e2e = None
+    if not a.no_e2e:
+        g = src_desc if isinstance(src_desc, P.Graph) else P.generate(src_desc)
+        P.solve(g, P.SolveOptions(objective="min", device=local))  # pins the host arrays
+        e2e_s, e2e_edges, h2d, d2h = 0.0, 0, 0, 0
+        e2e_steps = max(1, a.steps)
+        torch.cuda.synchronize()
+        for _ in range(e2e_steps):
+            t0 = time.perf_counter()
+            for o in ("min", "max"):
+                s = P.solve(g, P.SolveOptions(objective=o, device=local))
+                e2e_edges += s.stats.m_solved * s.stats.spf_passes
+                h2d += s.stats.h2d_bytes
+                d2h += s.stats.d2h_bytes
+            e2e_s += time.perf_counter() - t0
+        e2e = (e2e_s, e2e_edges, h2d // e2e_steps, d2h // e2e_steps)
+        del g
 
+    vals = [dev_ms, e2e[0] if e2e else 0.0]
+    tots = [float(edges), float(e2e[1] if e2e else 0), float(launches)]
     if dist:
-        t = torch.tensor([dev_ms, e2e_s], dtype=torch.float64, device=dev)
+        t = torch.tensor(vals, dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        tot = torch.tensor([float(edges), float(e2e_edges), float(launches)], dtype=torch.float64,
-                           device=dev)
+        tot = torch.tensor(tots, dtype=torch.float64, device=dev)
         dist.all_reduce(tot, op=dist.ReduceOp.SUM)
-        dev_ms_max, e2e_max = t.tolist()
-        edges_all, e2e_edges_all, launches_all = tot.tolist()
-    else:
-        dev_ms_max, e2e_max = dev_ms, e2e_s
-        edges_all, e2e_edges_all, launches_all = edges, e2e_edges, launches
+        vals, tots = t.tolist(), tot.tolist()
+    dev_ms_max, e2e_max = vals
+    edges_all, e2e_edges_all, launches_all = tots
 
     if rank == 0:
         peak, peak_src = measured_peak()
-        per_launch_ms = imp_ms / passes
-        bytes_launch = improve_bytes(n_solved, m_solved)
-        achieved = bytes_launch / (per_launch_ms / 1e3) / 1e9
-        traffic = ncu_traffic()
+        achieved = alg / (dev_ms / 1e3) / 1e9
+        imp_achieved = imp_bytes / (imp_ms / 1e3) / 1e9 if imp_ms else None
         line = {
             "metric": METRIC, "value": edges_all / (dev_ms_max / 1e3), "unit": UNIT,
             "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
             "ms_per_step": dev_ms_max / a.steps, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "int64", "data": "synthetic (seeded uniform digraph)",
+            "vs_baseline": None, "dtype": "int64", "data": "synthetic (seeded generator)",
             "config": config(a, world),
+            "graph": {"n_solved": st0.n_solved, "m_solved": st0.m_solved,
+                      "regions": st0.regions, "trivial_regions": st0.trivial_regions},
             "time_to_ocm_s": {o: sum(s[o].stats.device_ms for s in sols) / a.steps / 1e3
                               for o in ("min", "max")},
             "policy_iterations": {o: sols[0][o].stats.spf_passes for o in ("min", "max")},
             "mu": {o: str(sols[0][o].mu_exact) for o in ("min", "max")},
             "improve_share": imp_ms / dev_ms,
-            "roofline": {"bound": "hbm", "kernel": "k_improve", "achieved": achieved,
-                         "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": traffic, "bytes_per_launch": bytes_launch,
-                         "avg_launch_ms": per_launch_ms, "peak_source": peak_src,
-                         "note": "working set (64 MB edges + 8 MB keys) fits the 126 MB L2; "
-                                 "passes after the first read edges from L2"},
-            "e2e": {"value": e2e_edges_all / e2e_max, "unit": UNIT,
-                    "h2d_bytes_per_step": h2d // e2e_steps, "d2h_bytes_per_step": d2h // e2e_steps},
+            "roofline": {
+                "bound": "hbm", "kernel": "k_solve (persistent: one cooperative launch per solve)",
+                "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": ncu_traffic(a.config),
+                "bytes_per_launch": alg / (2 * a.steps), "avg_launch_ms": dev_ms / (2 * a.steps),
+                "peak_source": peak_src,
+                "improve_phase": {"achieved": imp_achieved,
+                                  "frac": imp_achieved / peak if imp_achieved else None,
+                                  "bytes_per_pass": imp_bytes / passes,
+                                  "avg_pass_ms": imp_ms / passes},
+                "note": "achieved = algorithmic bytes (DESIGN.md §5) / CUDA-event time of the "
+                        "launch on the session stream; improve_phase timed by SM clock share "
+                        "between the phase's grid barriers",
+            },
             "gpu_launches": int(launches_all),
             "clocks": clocks.summary(),
         }
+        if e2e:
+            line["e2e"] = {"value": e2e_edges_all / e2e_max, "unit": UNIT,
+                           "h2d_bytes_per_step": e2e[2], "d2h_bytes_per_step": e2e[3]}
         if world == 1 and not a.no_cpu_baseline:
-            cb = cpu_sample(a, 1)
+            cb = cpu_sample(a, P, 1)
             cb.pop("ms")
             line["cpu_baseline"] = cb
         print(json.dumps(line), flush=True)

@@ -105,6 +105,23 @@ int ocm_read_graph_file(const char* path, ocm_graph** out);
  * and integer weights in [wlo, whi] drawn from a seeded counter hash. */
 int ocm_generate_uniform(uint32_t n, uint32_t deg, int32_t wlo, int32_t whi, uint64_t seed,
                          ocm_graph** out);
+/* Synthetic benchmark graphs (BASELINE.json configs). The same description
+ * generates a host graph (ocm_generate, for checkers and small sizes) or a
+ * session whose CSR is written directly into HBM (ocm_session_create_generated,
+ * no host copy); both produce bit-identical graphs. */
+#define OCM_GEN_UNIFORM 0  /* every vertex has exactly deg out-edges */
+#define OCM_GEN_POWERLAW 1 /* deg(v) = min(dmax, floor(deg / sqrt(u_v))), tail exponent 3 */
+typedef struct {
+    int32_t kind;    /* OCM_GEN_* */
+    uint32_t n;
+    uint32_t deg;    /* uniform: out-degree; power-law: minimum out-degree */
+    uint32_t dmax;   /* power-law: degree cap */
+    int32_t wlo;     /* integer weights uniform in [wlo, whi] */
+    int32_t whi;
+    uint64_t seed;
+} ocm_generator;
+int ocm_generate(const ocm_generator* spec, ocm_graph** out);
+
 /* include/ocm/model_gen.hpp:31 Scenario::Transition */
 typedef struct {
     uint32_t from;
@@ -142,6 +159,11 @@ int ocm_session_solve(ocm_session* s, ocm_solution* out, uint32_t* cycle_buf, ui
  * Vertices of trivial regions report 0. Any pointer may be NULL. */
 int ocm_session_values(ocm_session* s, int64_t* key_num, int64_t* lam_num, int64_t* lam_den,
                        double* fval, uint32_t* succ_vertex);
+/* A session over a generated graph built in HBM (no host graph). */
+int ocm_session_create_generated(const ocm_generator* spec, const ocm_solve_options* opt,
+                                 ocm_session** out);
+/* Vertex count of the session's graph. */
+uint32_t ocm_session_n(const ocm_session* s);
 /* The CUDA stream the session launches on (cudaStream_t). */
 void* ocm_session_stream(ocm_session* s);
 void ocm_session_free(ocm_session* s);

@@ -33,7 +33,7 @@ import numpy as np
 __all__ = [
     "Graph", "build_graph", "parse_graph_text", "read_graph_file", "generate_uniform",
     "Scenario", "Transition", "loop_scenario", "worker_scenario", "server_scenario",
-    "generate_model", "K_MAX_MODEL_STATES",
+    "generate_model", "K_MAX_MODEL_STATES", "Generator", "generate",
     "SolveOptions", "SolveStats", "Solution", "solve", "Session",
     "ParseError", "StructuralError", "DeviceError", "UnsupportedError", "LIB_PATH",
 ]
@@ -70,6 +70,11 @@ class UnsupportedError(NotImplementedError):
 class _Transition(C.Structure):
     _fields_ = [("from_", C.c_uint32), ("to", C.c_uint32), ("cost", C.c_int64),
                 ("acquires", C.c_int32), ("releases", C.c_int32)]
+
+
+class _Gen(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("n", C.c_uint32), ("deg", C.c_uint32), ("dmax", C.c_uint32),
+                ("wlo", C.c_int32), ("whi", C.c_int32), ("seed", C.c_uint64)]
 
 
 class _Opts(C.Structure):
@@ -109,6 +114,9 @@ def _load():
                                            C.c_uint64, P(C.c_void_p)]),
         "ocm_generate_model": (C.c_int, [C.c_uint32, P(_Transition), C.c_uint32, C.c_int32,
                                          C.c_uint32, C.c_uint64, P(C.c_void_p)]),
+        "ocm_generate": (C.c_int, [P(_Gen), P(C.c_void_p)]),
+        "ocm_session_create_generated": (C.c_int, [P(_Gen), P(_Opts), P(C.c_void_p)]),
+        "ocm_session_n": (C.c_uint32, [C.c_void_p]),
         "ocm_graph_free": (None, [C.c_void_p]),
         "ocm_graph_n": (C.c_uint32, [C.c_void_p]),
         "ocm_graph_m": (C.c_uint64, [C.c_void_p]),
@@ -133,7 +141,7 @@ _lib = _load()
 EXPORTED_SYMBOLS = (
     "ocm_last_error", "ocm_last_error_line", "ocm_version", "ocm_device_count",
     "ocm_build_graph", "ocm_parse_graph_text", "ocm_read_graph_file", "ocm_generate_uniform",
-    "ocm_generate_model",
+    "ocm_generate_model", "ocm_generate", "ocm_session_create_generated", "ocm_session_n",
     "ocm_graph_free", "ocm_graph_n", "ocm_graph_m", "ocm_graph_integer_exact", "ocm_graph_edges",
     "ocm_solve", "ocm_session_create", "ocm_session_solve", "ocm_session_values",
     "ocm_session_stream", "ocm_session_free",
@@ -246,6 +254,36 @@ def generate_uniform(n: int, deg: int, wlo: int = 1, whi: int = 100, seed: int =
     """Seeded random digraph with out-degree exactly ``deg`` and integer weights."""
     h = C.c_void_p()
     _check(_lib.ocm_generate_uniform(int(n), int(deg), int(wlo), int(whi), int(seed), C.byref(h)))
+    return Graph(h.value)
+
+
+@dataclass
+class Generator:
+    """Synthetic benchmark graph (include/ocm_b200.h ocm_generator): kind
+    "uniform" (out-degree exactly ``deg``) or "powerlaw" (out-degree
+    min(dmax, floor(deg / sqrt(u))), tail exponent 3); integer weights
+    uniform in [wlo, whi]. :func:`generate` builds it on the host,
+    :meth:`Session.generated` directly in HBM -- bit-identical graphs."""
+    kind: str = "uniform"
+    n: int = 1000
+    deg: int = 8
+    dmax: int = 0
+    wlo: int = 1
+    whi: int = 100
+    seed: int = 1
+
+    def _c(self) -> "_Gen":
+        kinds = {"uniform": 0, "powerlaw": 1}
+        if self.kind not in kinds:
+            raise ValueError(f"unknown generator kind {self.kind!r}")
+        return _Gen(kinds[self.kind], int(self.n), int(self.deg), int(self.dmax), int(self.wlo),
+                    int(self.whi), int(self.seed))
+
+
+def generate(spec: Generator) -> Graph:
+    """Host graph of a generator description."""
+    h = C.c_void_p()
+    _check(_lib.ocm_generate(C.byref(spec._c()), C.byref(h)))
     return Graph(h.value)
 
 
@@ -387,6 +425,18 @@ class Session:
         h = C.c_void_p()
         _check(_lib.ocm_session_create(g._h, C.byref(self.opt._c()), C.byref(h)))
         self._h = h
+
+    @classmethod
+    def generated(cls, spec: Generator, opt: Optional[SolveOptions] = None) -> "Session":
+        """Session over a generated graph written directly into HBM."""
+        self = cls.__new__(cls)
+        self.opt = opt or SolveOptions()
+        h = C.c_void_p()
+        _check(_lib.ocm_session_create_generated(C.byref(spec._c()), C.byref(self.opt._c()),
+                                                 C.byref(h)))
+        self._h = h
+        self.n = int(_lib.ocm_session_n(h))
+        return self
 
     def __del__(self):
         h = getattr(self, "_h", None)

@@ -157,6 +157,41 @@ int ocm_generate_uniform(uint32_t n, uint32_t deg, int32_t wlo, int32_t whi, uin
     });
 }
 
+namespace {
+ocmb::GenSpec spec_of(const ocm_generator* g) {
+    if (!g)
+        throw std::invalid_argument("null generator");
+    ocmb::GenSpec s;
+    s.kind = g->kind;
+    s.n = g->n;
+    s.deg = g->deg;
+    s.dmax = g->dmax;
+    s.wlo = g->wlo;
+    s.whi = g->whi;
+    s.seed = g->seed;
+    return s;
+}
+} // namespace
+
+int ocm_generate(const ocm_generator* spec, ocm_graph** out) {
+    return guard([&] {
+        auto g = std::make_unique<ocm_graph>();
+        g->g = ocmb::generate(spec_of(spec));
+        *out = g.release();
+    });
+}
+
+int ocm_session_create_generated(const ocm_generator* spec, const ocm_solve_options* opt,
+                                 ocm_session** out) {
+    return guard([&] {
+        auto s = std::make_unique<ocm_session>();
+        s->s = std::make_unique<ocmb::Session>(spec_of(spec), defaults(opt));
+        *out = s.release();
+    });
+}
+
+uint32_t ocm_session_n(const ocm_session* s) { return s ? s->s->n() : 0; }
+
 int ocm_generate_model(uint32_t states, const ocm_transition* transitions, uint32_t n_transitions,
                        int32_t uses_server, uint32_t clients, uint64_t max_states,
                        ocm_graph** out) {

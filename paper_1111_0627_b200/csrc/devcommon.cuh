@@ -130,6 +130,9 @@ struct KP {
     Ctl* c;
     std::uint32_t max_region;
     long long max_abs_w;
+    const std::uint32_t* heavy; // vertices of intra-region degree >= heavy_deg
+    std::uint32_t nheavy;
+    std::uint32_t heavy_deg;
     // tuning (launch arguments)
     int G;                 // improvement lanes per vertex
     std::uint32_t small_wc; // winning cycles up to this many vertices: one block
@@ -180,7 +183,7 @@ struct DeviceState {
     int sms = 148;
     cudaStream_t stream = nullptr;
     DBuf<std::uint32_t> row, reg, succ_e, succ_v, comp, wlist, cyc_len, conn, rem0, rem1, src,
-        iters, indeg, plist, clist, cmark, cmark2;
+        iters, indeg, plist, clist, cmark, cmark2, heavy;
     DBuf<PJV> pv0, pv1;
     DBuf<PJC> pj0, pj1;
     DBuf<int2> ew;
@@ -199,7 +202,7 @@ struct DeviceState {
         if (stream)
             cudaStreamSynchronize(stream);
         for (auto* b : {&row, &reg, &succ_e, &succ_v, &comp, &wlist, &cyc_len, &conn, &rem0, &rem1,
-                        &src, &iters, &indeg, &plist, &clist, &cmark, &cmark2})
+                        &src, &iters, &indeg, &plist, &clist, &cmark, &cmark2, &heavy})
             b->release();
         pv0.release();
         pv1.release();

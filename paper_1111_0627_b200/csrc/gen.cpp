@@ -1,27 +1,13 @@
 #include "gen.hpp"
 
 #include <cmath>
+#include <algorithm>
 #include <stdexcept>
 #include <string>
 #include <thread>
 #include <vector>
 
 namespace ocmb {
-
-namespace {
-
-inline std::uint64_t splitmix64(std::uint64_t x) {
-    x += 0x9e3779b97f4a7c15ull;
-    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
-    x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
-    return x ^ (x >> 31);
-}
-
-inline std::uint64_t hash2(std::uint64_t seed, std::uint64_t stream, std::uint64_t i) {
-    return splitmix64(splitmix64(seed ^ (stream * 0xd1342543de82ef95ull)) + i);
-}
-
-} // namespace
 
 Graph generate_uniform(std::uint32_t n, std::uint32_t deg, std::int32_t wlo, std::int32_t whi,
                        std::uint64_t seed) {
@@ -53,6 +39,47 @@ Graph generate_uniform(std::uint32_t n, std::uint32_t deg, std::int32_t wlo, std
     for (std::uint32_t v = 0; v <= n; ++v)
         g.fwd_index[v] = std::uint64_t(v) * deg;
     return g;
+}
+
+Graph generate_powerlaw(std::uint32_t n, std::uint32_t dmin, std::uint32_t dmax, std::int32_t wlo,
+                        std::int32_t whi, std::uint64_t seed) {
+    if (n == 0 || dmin == 0 || dmax < dmin || whi < wlo)
+        throw std::invalid_argument("generate_powerlaw: need n > 0, 0 < dmin <= dmax, wlo <= whi");
+    Graph g;
+    g.n = n;
+    g.integer_exact = true;
+    g.fwd_index.resize(std::size_t(n) + 1);
+    g.fwd_index[0] = 0;
+    for (std::uint32_t v = 0; v < n; ++v)
+        g.fwd_index[v + 1] = g.fwd_index[v] + powerlaw_degree(seed, v, dmin, dmax);
+    const std::uint64_t m = g.fwd_index[n];
+    if (m >= 0xffffffffull)
+        throw std::invalid_argument("generate_powerlaw: edge count exceeds the 32-bit id space");
+    g.m = m;
+    g.fwd_target.resize(m);
+    g.fwd_weight.resize(m);
+    const std::uint64_t span = std::uint64_t(std::int64_t(whi) - wlo + 1);
+    unsigned T = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    std::vector<std::thread> pool;
+    for (unsigned t = 0; t < T; ++t)
+        pool.emplace_back([&, t] {
+            const std::uint64_t lo = m * t / T, hi = m * (t + 1) / T;
+            for (std::uint64_t e = lo; e < hi; ++e) {
+                g.fwd_target[e] = static_cast<Vertex>(hash2(seed, 1, e) % n);
+                g.fwd_weight[e] = double(wlo + std::int64_t(hash2(seed, 2, e) % span));
+            }
+        });
+    for (auto& th : pool)
+        th.join();
+    return g;
+}
+
+Graph generate(const GenSpec& s) {
+    if (s.kind == 0)
+        return generate_uniform(s.n, s.deg, s.wlo, s.whi, s.seed);
+    if (s.kind == 1)
+        return generate_powerlaw(s.n, s.deg, s.dmax, s.wlo, s.whi, s.seed);
+    throw std::invalid_argument("unknown generator kind");
 }
 
 } // namespace ocmb

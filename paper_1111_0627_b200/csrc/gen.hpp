@@ -2,6 +2,7 @@
 // is bit-identical to oracle/ocm_oracle.c so checkers see the same graphs.
 #pragma once
 
+#include <cmath>
 #include <cstdint>
 #include <vector>
 
@@ -13,6 +14,45 @@ namespace ocmb {
 // targets uniform over [0, n), integer weights uniform in [wlo, whi].
 Graph generate_uniform(std::uint32_t n, std::uint32_t deg, std::int32_t wlo, std::int32_t whi,
                        std::uint64_t seed);
+
+// Power-law out-degrees: deg(v) = min(dmax, floor(dmin / sqrt(u_v))), u_v
+// uniform in (0, 1] -- P(deg > d) = (dmin/d)^2, the tail exponent 3 of
+// preferential attachment -- with targets uniform over [0, n) and integer
+// weights uniform in [wlo, whi]. Only IEEE-exact operations (sqrt, divide)
+// touch floating point, so host and device generate identical graphs.
+Graph generate_powerlaw(std::uint32_t n, std::uint32_t dmin, std::uint32_t dmax, std::int32_t wlo,
+                        std::int32_t whi, std::uint64_t seed);
+
+// Generator description shared by the host generators and the device ones
+// (gen_dev.cu) that write the CSR straight into HBM.
+struct GenSpec {
+    int kind = 0; // 0 uniform, 1 power-law
+    std::uint32_t n = 0;
+    std::uint32_t deg = 8; // uniform: out-degree; power-law: dmin
+    std::uint32_t dmax = 0; // power-law cap
+    std::int32_t wlo = 1, whi = 100;
+    std::uint64_t seed = 1;
+};
+
+Graph generate(const GenSpec& g);
+
+// Shared counter hash (bit-identical to oracle/ocm_oracle.c and gen_dev.cu).
+inline std::uint64_t splitmix64(std::uint64_t x) {
+    x += 0x9e3779b97f4a7c15ull;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+    return x ^ (x >> 31);
+}
+inline std::uint64_t hash2(std::uint64_t seed, std::uint64_t stream, std::uint64_t i) {
+    return splitmix64(splitmix64(seed ^ (stream * 0xd1342543de82ef95ull)) + i);
+}
+// deg(v) of the power-law generator.
+inline std::uint32_t powerlaw_degree(std::uint64_t seed, std::uint32_t v, std::uint32_t dmin,
+                                     std::uint32_t dmax) {
+    const double u = double((hash2(seed, 3, v) >> 11) + 1) * (1.0 / 9007199254740992.0);
+    const double d = double(dmin) / std::sqrt(u);
+    return d >= double(dmax) ? dmax : static_cast<std::uint32_t>(d);
+}
 
 } // namespace ocmb
 

@@ -31,6 +31,9 @@
 namespace ocmb {
 
 void device_prepare(const Graph& g, const ocm_solve_options& opt, DeviceState& d, PrepInfo& info);
+void device_prepare_csr(std::uint32_t n, std::uint64_t m, DBuf<std::uint32_t>& row,
+                        DBuf<std::uint32_t>& tgt, DBuf<double>& w, bool integer_exact,
+                        const ocm_solve_options& opt, DeviceState& d, PrepInfo& info);
 
 namespace {
 
@@ -427,13 +430,6 @@ void device_prepare(const Graph& g, const ocm_solve_options& opt, DeviceState& d
     cudaStream_t s = d.stream;
     const std::uint32_t n = g.n;
     const std::uint64_t m = g.m;
-    const int sms = d.sms;
-    info.n = n;
-    info.scc_off = opt.scc == OCM_SCC_OFF;
-    info.exact = g.integer_exact;
-    const double sign = opt.objective == OCM_MAXIMIZE ? -1.0 : 1.0;
-    const int gv = grid_for(n, sms);
-
     // ---- upload (the host arrays are pinned once per graph by the C-ABI)
     DBuf<std::uint64_t> row64;
     DBuf<std::uint32_t> row, tgt;
@@ -447,9 +443,23 @@ void device_prepare(const Graph& g, const ocm_solve_options& opt, DeviceState& d
         CK(cudaMemcpyAsync(tgt.p, g.fwd_target.data(), m * 4, cudaMemcpyHostToDevice, s));
         CK(cudaMemcpyAsync(w.p, g.fwd_weight.data(), m * 8, cudaMemcpyHostToDevice, s));
     }
-    info.h2d_bytes = (std::size_t(n) + 1) * 8 + m * 12;
-    kp_row32<<<grid_for(n + 1, sms), kBlock, 0, s>>>(row64.p, row.p, std::size_t(n) + 1);
+    kp_row32<<<grid_for(n + 1, d.sms), kBlock, 0, s>>>(row64.p, row.p, std::size_t(n) + 1);
     row64.release();
+    device_prepare_csr(n, m, row, tgt, w, g.integer_exact, opt, d, info);
+    info.h2d_bytes = (std::size_t(n) + 1) * 8 + m * 12;
+}
+
+void device_prepare_csr(std::uint32_t n, std::uint64_t m, DBuf<std::uint32_t>& row,
+                        DBuf<std::uint32_t>& tgt, DBuf<double>& w, bool integer_exact,
+                        const ocm_solve_options& opt, DeviceState& d, PrepInfo& info) {
+    cudaStream_t s = d.stream;
+    const int sms = d.sms;
+    info.n = n;
+    info.scc_off = opt.scc == OCM_SCC_OFF;
+    info.exact = integer_exact;
+    info.h2d_bytes = 0;
+    const double sign = opt.objective == OCM_MAXIMIZE ? -1.0 : 1.0;
+    const int gv = grid_for(n, sms);
 
     DBuf<PrepCounters> pcd;
     pcd.alloc(1, s);

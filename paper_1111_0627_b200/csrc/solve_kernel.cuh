@@ -220,21 +220,21 @@ struct ChangedMarks {
     }
 };
 
-template <bool EXACT, int G, int U> __device__ __forceinline__ void improve_phase(const KP& p, int* changed) {
+template <bool EXACT, int G, int U>
+__device__ __forceinline__ void improve_vertex(const KP& p, int* changed, ChangedMarks& marks,
+                                               std::uint32_t v) {
     const unsigned lane = threadIdx.x & (G - 1);
     const unsigned gm = group_mask<G>();
-    const std::size_t gid = gtid() / G;
-    const std::size_t gs = gstride() / G;
-    ChangedMarks marks;
     using Key = typename std::conditional<EXACT, long long, double>::type;
     const Key* __restrict__ key = EXACT ? reinterpret_cast<const Key*>(p.key_i)
                                         : reinterpret_cast<const Key*>(p.key_f);
-    for (std::size_t vv = gid; vv < p.N; vv += gs) {
-        const std::uint32_t v = static_cast<std::uint32_t>(vv);
+    {
         const std::uint32_t r = __ldg(&p.reg[v]);
         if (!p.active[r])
-            continue;
+            return;
         const std::uint32_t b = __ldg(&p.row[v]), e_end = __ldg(&p.row[v + 1]);
+        if (e_end - b >= p.heavy_deg)
+            return; // block-cooperative path (improve_heavy)
         const std::uint32_t cur = p.succ_e[v];
         long long num = 0, den = 1;
         double lam = 0.0;
@@ -320,7 +320,7 @@ template <bool EXACT, int G, int U> __device__ __forceinline__ void improve_phas
         if (gbe == NONE) {
             if (lane == 0)
                 p.c->error = 1;
-            continue;
+            return;
         }
         bool rep = cur == NONE;
         if (!rep) {
@@ -350,6 +350,153 @@ template <bool EXACT, int G, int U> __device__ __forceinline__ void improve_phas
 #endif
         }
     }
+}
+
+// Heavy vertices (intra-region degree >= heavy_deg, listed at session
+// creation): one block per vertex, 256 threads striding its edges, then a
+// block-wide lexicographic (candidate, edge id) reduction -- the same
+// "first strictly smaller" result as the sequential scan.
+template <bool EXACT>
+__device__ __forceinline__ void improve_heavy(const KP& p, int* changed) {
+    using Key = typename std::conditional<EXACT, long long, double>::type;
+    const Key* __restrict__ key = EXACT ? reinterpret_cast<const Key*>(p.key_i)
+                                        : reinterpret_cast<const Key*>(p.key_f);
+    __shared__ Key s_best[kBlock / 32];
+    __shared__ std::uint32_t s_be[kBlock / 32];
+    __shared__ Key s_cur;
+    __shared__ int s_have_cur;
+    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (std::uint32_t h = blockIdx.x; h < p.nheavy; h += gridDim.x) {
+        const std::uint32_t v = p.heavy[h];
+        const std::uint32_t r = __ldg(&p.reg[v]);
+        if (!p.active[r])
+            continue; // block-uniform
+        const std::uint32_t b = __ldg(&p.row[v]), e_end = __ldg(&p.row[v + 1]);
+        const std::uint32_t cur = p.succ_e[v];
+        long long num = 0, den = 1;
+        double lam = 0.0;
+        if constexpr (EXACT) {
+            num = p.lam_num[r];
+            den = p.lam_den[r];
+        } else {
+            lam = p.lam_f[r];
+        }
+        if (threadIdx.x == 0)
+            s_have_cur = 0;
+        __syncthreads();
+        Key best = 0;
+        std::uint32_t be = NONE;
+        for (std::uint32_t e0 = b + threadIdx.x; e0 < e_end; e0 += 4 * kBlock) {
+            std::uint32_t tt[4];
+            Key kk[4];
+            int wi[4];
+            double wf[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const std::uint32_t e = e0 + u * kBlock;
+                if (e < e_end) {
+                    if constexpr (EXACT) {
+                        const int2 ed = __ldg(&p.ew[e]);
+                        tt[u] = static_cast<std::uint32_t>(ed.x);
+                        wi[u] = ed.y;
+                    } else {
+                        const FEdge ed = p.fe[e];
+                        tt[u] = ed.t;
+                        wf[u] = ed.w;
+                    }
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (e0 + u * kBlock < e_end)
+                    kk[u] = __ldcg(&key[tt[u]]);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const std::uint32_t e = e0 + u * kBlock;
+                if (e < e_end) {
+                    Key c;
+                    if constexpr (EXACT)
+                        c = kk[u] + static_cast<long long>(wi[u]) * den - num;
+                    else
+                        c = (kk[u] + wf[u]) - lam;
+                    if (be == NONE || c < best) { // ascending e per thread: first wins ties
+                        best = c;
+                        be = e;
+                    }
+                    if (e == cur) {
+                        s_cur = c;
+                        s_have_cur = 1;
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            const Key ob = __shfl_xor_sync(FULL, best, off);
+            const std::uint32_t oe = __shfl_xor_sync(FULL, be, off);
+            if (oe != NONE && (be == NONE || ob < best || (ob == best && oe < be))) {
+                best = ob;
+                be = oe;
+            }
+        }
+        if (lane == 0) {
+            s_best[warp] = best;
+            s_be[warp] = be;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            Key gb = s_best[0];
+            std::uint32_t ge = s_be[0];
+            for (int w = 1; w < kBlock / 32; ++w) {
+                const std::uint32_t oe = s_be[w];
+                if (oe != NONE && (ge == NONE || s_best[w] < gb || (s_best[w] == gb && oe < ge))) {
+                    gb = s_best[w];
+                    ge = oe;
+                }
+            }
+            if (ge == NONE) {
+                p.c->error = 1;
+            } else {
+                bool rep = cur == NONE || !s_have_cur;
+                if (!rep) {
+                    const Key curc = s_cur;
+                    if constexpr (EXACT) {
+                        rep = gb < curc;
+                    } else {
+                        const double tol = 1e-9 * fmax(1.0, fmax(fabs(gb), fabs(curc)));
+                        rep = gb < curc - tol;
+                    }
+                }
+                if (rep) {
+                    p.succ_e[v] = ge;
+                    if constexpr (EXACT) {
+                        const int2 ed = __ldg(&p.ew[ge]);
+                        p.succ_v[v] = static_cast<std::uint32_t>(ed.x);
+                        p.succ_wi[v] = ed.y;
+                        atomicAdd(&p.indeg[ed.x], 1u);
+                    } else {
+                        const FEdge ed = p.fe[ge];
+                        p.succ_v[v] = ed.t;
+                        p.succ_wf[v] = ed.w;
+                        atomicAdd(&p.indeg[ed.t], 1u);
+                    }
+                    set_once(&changed[r], 1);
+                } else {
+                    atomicAdd(&p.indeg[p.succ_v[v]], 1u);
+                }
+            }
+        }
+        __syncthreads();
+    }
+}
+
+template <bool EXACT, int G, int U> __device__ __forceinline__ void improve_phase(const KP& p, int* changed) {
+    if (p.nheavy)
+        improve_heavy<EXACT>(p, changed);
+    ChangedMarks marks;
+    const std::size_t gs = gstride() / G;
+    for (std::size_t vv = gtid() / G; vv < p.N; vv += gs)
+        improve_vertex<EXACT, G, U>(p, changed, marks, static_cast<std::uint32_t>(vv));
     marks.flush(changed);
 }
 
@@ -362,6 +509,13 @@ template <bool EXACT> __device__ __forceinline__ void improve_dispatch(const KP&
     case 16: improve_phase<EXACT, 16, 2>(p, changed); break;
     default: improve_phase<EXACT, 32, 2>(p, changed); break;
     }
+}
+
+__global__ void k_list_heavy(std::uint32_t n, const std::uint32_t* row, std::uint32_t hdeg,
+                             std::uint32_t* heavy, unsigned* count) {
+    for (std::size_t v = gtid(); v < n; v += gstride())
+        if (row[v + 1] - row[v] >= hdeg)
+            heavy[atomicAdd(count, 1u)] = static_cast<std::uint32_t>(v);
 }
 
 // ------------------------------------------------------------ helpers
@@ -743,16 +897,32 @@ __device__ __forceinline__ void ph_vote(const KP& p, std::uint64_t nM, std::uint
     wc_final(p, p.rem[1], nW, wr, threadIdx.x, blockDim.x);
 }
 
-// Kept component (howard_par.hpp:370/393) on the core: vertices whose
-// policy path enters the winning cycle keep their edges; exact keys from the
-// doubling sums, K(v) = W_L(v)*den - L*num + K(jump v), since the winning
-// cycle's reduced weight is exactly 0. Others queue for re-attachment.
+// Kept component (howard_par.hpp:370/393): vertices whose policy path
+// enters the winning cycle keep their edges, everyone else queues for
+// re-attachment. Core and leaves in one pass over [core | leaves]. Exact
+// keys: a core vertex v off the cycle gets K(v) = W_L(v)*den - L*num +
+// K(jump v) from its doubling record (the winning cycle's reduced weight is
+// exactly 0, so extra turns add nothing); a leaf takes K(succ) + w*den - num,
+// recomputing its core successor's key the same way (never reading a key
+// being written in this phase). Resets the in-degree of core vertices.
+__device__ __forceinline__ long long core_key(const KP& p, const PJC* a, std::uint32_t v, std::uint32_t r,
+                                              std::uint32_t stamp, unsigned long long L, bool& ovf) {
+    if (p.cmark[v] == stamp) // on the winning cycle: from the cycle prefix sums
+        return p.key_i[v];
+    const PJC x = a[v];
+    const __int128 kk = static_cast<__int128>(x.w) * p.lam_den[r] -
+                        static_cast<__int128>(L) * p.lam_num[r] + p.key_i[x.nxt];
+    ovf |= !key_in_range(kk);
+    return static_cast<long long>(kk);
+}
+
 template <bool EXACT>
-__device__ __forceinline__ void ph_keep(const KP& p, std::uint64_t nC, int in, std::uint32_t stamp,
-                                        unsigned long long L, const Ring& ring) {
+__device__ __forceinline__ void ph_keep(const KP& p, std::uint64_t nC, std::uint64_t nL, int in,
+                                        std::uint32_t stamp, unsigned long long L, const Ring& ring) {
     const PJC* a = p.pj[in];
     bool ovf = false;
-    OCM_BLOCK_LOOP(i0, 0, nC) {
+    const std::uint64_t tot = nC + nL;
+    OCM_BLOCK_LOOP(i0, 0, tot) {
         const std::uint64_t i = i0_b + threadIdx.x;
         bool take = false;
         std::uint32_t v = 0;
@@ -763,33 +933,10 @@ __device__ __forceinline__ void ph_keep(const KP& p, std::uint64_t nC, int in, s
             p.conn[v] = kept ? 0u : NONE;
             p.indeg[v] = 0;
             take = !kept;
-            if (EXACT && kept && p.cmark[v] != stamp) {
-                const PJC x = a[v];
-                const __int128 kk = static_cast<__int128>(x.w) * p.lam_den[r] -
-                                    static_cast<__int128>(L) * p.lam_num[r] + p.key_i[x.nxt];
-                ovf |= !key_in_range(kk);
-                p.key_i[v] = static_cast<long long>(kk);
-            }
-        }
-        const std::uint64_t slot = block_append(take, ring);
-        if (take)
-            p.rem[0][slot] = v;
-    }
-    block_flag(ovf, &p.c->overflow, 1);
-}
-
-// Leaves take anchor and key from their successor, always a core vertex
-// (K(v) = K(succ) + w*den - num along the kept tree).
-template <bool EXACT>
-__device__ __forceinline__ void ph_leafvals(const KP& p, std::uint64_t nL, std::uint64_t out_base,
-                                            const Ring& ring) {
-    bool ovf = false;
-    OCM_BLOCK_LOOP(i0, 0, nL) {
-        const std::uint64_t i = i0_b + threadIdx.x;
-        bool take = false;
-        std::uint32_t v = 0;
-        if (i < nL) {
-            v = p.plist[i];
+            if (EXACT && kept && p.cmark[v] != stamp)
+                p.key_i[v] = core_key(p, a, v, r, stamp, L, ovf);
+        } else if (i < tot) {
+            v = p.plist[i - nC];
             const std::uint32_t s = p.succ_v[v];
             const std::uint32_t r = __ldg(&p.reg[v]);
             const std::uint32_t an = p.comp[s];
@@ -798,7 +945,7 @@ __device__ __forceinline__ void ph_leafvals(const KP& p, std::uint64_t nL, std::
             p.conn[v] = kept ? 0u : NONE;
             take = !kept;
             if (EXACT && kept) {
-                const __int128 kk = static_cast<__int128>(p.key_i[s]) +
+                const __int128 kk = static_cast<__int128>(core_key(p, a, s, r, stamp, L, ovf)) +
                                     static_cast<__int128>(p.succ_wi[v]) * p.lam_den[r] - p.lam_num[r];
                 ovf |= !key_in_range(kk);
                 p.key_i[v] = static_cast<long long>(kk);
@@ -806,7 +953,7 @@ __device__ __forceinline__ void ph_leafvals(const KP& p, std::uint64_t nL, std::
         }
         const std::uint64_t slot = block_append(take, ring);
         if (take)
-            p.rem[0][out_base + slot] = v;
+            p.rem[0][slot] = v;
     }
     block_flag(ovf, &p.c->overflow, 1);
 }
@@ -828,20 +975,31 @@ __device__ __forceinline__ void ph_attach(const KP& p, int cur, std::uint64_t pe
             x = list[i];
             pend = true;
             const std::uint32_t b = __ldg(&p.row[x]), e_end = __ldg(&p.row[x + 1]);
-            for (std::uint32_t e = b; e < e_end; ++e) {
-                std::uint32_t t;
-                if constexpr (EXACT)
-                    t = static_cast<std::uint32_t>(__ldg(&p.ew[e]).x);
-                else
-                    t = p.fe[e].t;
-                if (ldv(p.conn[t]) < layer) {
+            // the first out-edge (CSR order) into a vertex connected earlier;
+            // 8 edges and their heads' stamps in flight at a time
+            for (std::uint32_t e0 = b; pend && e0 < e_end; e0 += 8) {
+                std::uint32_t tt[8], cc[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    if (e0 + u < e_end)
+                        tt[u] = EXACT ? static_cast<std::uint32_t>(__ldg(&p.ew[e0 + u]).x) : p.fe[e0 + u].t;
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    cc[u] = e0 + u < e_end ? ldv(p.conn[tt[u]]) : NONE;
+                int hit = -1;
+#pragma unroll
+                for (int u = 7; u >= 0; --u)
+                    if (cc[u] < layer)
+                        hit = u;
+                if (hit >= 0) {
+                    const std::uint32_t e = e0 + hit, t = tt[hit];
                     p.succ_e[x] = e;
                     p.succ_v[x] = t;
                     if constexpr (EXACT) {
                         const int w = __ldg(&p.ew[e]).y;
                         p.succ_wi[x] = w;
                         const std::uint32_t r = __ldg(&p.reg[x]);
-                        const __int128 kk = static_cast<__int128>(ldv(p.key_i[t])) +
+                        const __int128 kk = static_cast<__int128>(p.key_i[t]) +
                                             static_cast<__int128>(w) * p.lam_den[r] - p.lam_num[r];
                         ovf |= !key_in_range(kk);
                         p.key_i[x] = static_cast<long long>(kk);
@@ -850,7 +1008,6 @@ __device__ __forceinline__ void ph_attach(const KP& p, int cur, std::uint64_t pe
                     }
                     p.conn[x] = layer;
                     pend = false;
-                    break;
                 }
             }
         }
@@ -1024,12 +1181,9 @@ template <bool EXACT> __global__ void __launch_bounds__(kBlock, kSolveMinBlocks)
         }
 
         // ---- kept component (core, then leaves), re-attachment
-        ph_keep<EXACT>(p, nC, in, stamp, 1ull << k, rl);
+        ph_keep<EXACT>(p, nC, nL, in, stamp, 1ull << k, rl);
         sync(PH_KEEP);
         std::uint64_t pending = rl.take();
-        ph_leafvals<EXACT>(p, nL, pending, rl);
-        sync(PH_LEAVES);
-        pending += rl.take();
         int cur = 0;
         for (std::uint32_t layer = 1; pending > 0; ++layer) {
             ph_attach<EXACT>(p, cur, pending, layer, rl);

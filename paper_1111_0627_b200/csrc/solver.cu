@@ -15,15 +15,36 @@
 
 #include "errors.hpp"
 #include "solve_kernel.cuh"
+#include "gen.hpp"
 #include "solver.hpp"
 
 namespace ocmb {
 
 void device_prepare(const Graph& g, const ocm_solve_options& opt, DeviceState& d, PrepInfo& info);
+void device_generate_prepare(const GenSpec& spec, const ocm_solve_options& opt, DeviceState& d,
+                             PrepInfo& info);
 
 // ================================================================ session
 
+namespace {
+
+int env_int(const char* name, int dflt) {
+    const char* v = std::getenv(name);
+    return v ? std::atoi(v) : dflt;
+}
+
+} // namespace
+
 Session::Session(const Graph& g, const ocm_solve_options& opt) : opt_(opt) {
+    init([&](DeviceState& d) { device_prepare(g, opt, d, prep_); });
+}
+
+Session::Session(const GenSpec& spec, const ocm_solve_options& opt) : opt_(opt) {
+    init([&](DeviceState& d) { device_generate_prepare(spec, opt, d, prep_); });
+}
+
+void Session::init(const std::function<void(DeviceState&)>& prepare) {
+    const ocm_solve_options& opt = opt_;
     if (opt.algo != OCM_ALGO_HOWARD && opt.algo != OCM_ALGO_HOWARD_PAR)
         throw UnsupportedError("only the policy-iteration lanes (howard, howard-par) run on the "
                                "device");
@@ -52,7 +73,7 @@ Session::Session(const Graph& g, const ocm_solve_options& opt) : opt_(opt) {
     CK(cudaEventCreate(&d.ev_end));
     CK(cudaMallocHost(&d.h_ctl, sizeof(Ctl)));
 
-    device_prepare(g, opt, d, prep_);
+    prepare(d);
 
     const std::size_t N = prep_.n, R1 = std::size_t(prep_.R) + 1;
     const std::size_t N1 = std::max<std::size_t>(N, 1);
@@ -93,6 +114,35 @@ Session::Session(const Graph& g, const ocm_solve_options& opt) : opt_(opt) {
         CK(cudaMemcpyAsync(d.ctl.p, &init, sizeof(Ctl), cudaMemcpyHostToDevice, d.stream));
     }
     CK(cudaStreamSynchronize(d.stream));
+
+    // G lanes per improvement vertex (U = 4 edges in flight per lane): one
+    // lane up to degree 8 (measured best at 8), then G*8 ~ average degree;
+    // vertices of degree >= 32*G*4 go to the block-cooperative path.
+    // OCM_IMPROVE_G / OCM_HEAVY_DEG override.
+    {
+        const double avg_deg =
+            prep_.R ? double(prep_.M) / std::max<double>(1.0, double(prep_.n - prep_.trivial)) : 1.0;
+        int G = 1;
+        while (G < 32 && G * 8 < avg_deg)
+            G *= 2;
+        G = env_int("OCM_IMPROVE_G", G);
+        d.kp.G = G;
+        d.kp.heavy_deg = static_cast<std::uint32_t>(env_int("OCM_HEAVY_DEG", 32 * 4 * G));
+        DBuf<unsigned> cnt;
+        cnt.alloc(1, d.stream);
+        CK(cudaMemsetAsync(cnt.p, 0, 4, d.stream));
+        const std::uint32_t cap = static_cast<std::uint32_t>(
+            std::min<std::uint64_t>(N, prep_.M / std::max<std::uint32_t>(d.kp.heavy_deg, 1) + 1));
+        d.heavy.alloc(std::max<std::uint32_t>(cap, 1), d.stream);
+        if (N)
+            k_list_heavy<<<grid_for(N, d.sms), kBlock, 0, d.stream>>>(
+                static_cast<std::uint32_t>(N), d.row.p, d.kp.heavy_deg, d.heavy.p, cnt.p);
+        unsigned nh = 0;
+        CK(cudaMemcpyAsync(&nh, cnt.p, 4, cudaMemcpyDeviceToHost, d.stream));
+        CK(cudaStreamSynchronize(d.stream));
+        d.kp.nheavy = nh;
+        d.kp.heavy = d.heavy.p;
+    }
 
     // one CTA per SM slot the register budget allows (<= kSolveMinBlocks)
     for (int e = 0; e < 2; ++e) {
@@ -154,15 +204,6 @@ Session::~Session() = default;
 
 void* Session::stream() const { return d_ ? d_->stream : nullptr; }
 
-namespace {
-
-int env_int(const char* name, int dflt) {
-    const char* v = std::getenv(name);
-    return v ? std::atoi(v) : dflt;
-}
-
-} // namespace
-
 template <class M> void Session::run(ocm_solution* out, std::uint32_t* cycle_buf, std::uint32_t cap) {
     constexpr bool EXACT = M::value;
     DeviceState& d = *d_;
@@ -171,14 +212,6 @@ template <class M> void Session::run(ocm_solution* out, std::uint32_t* cycle_buf
     Ctl& hc = *d.h_ctl;
     std::uint64_t d2h = 0;
 
-    // G lanes per improvement vertex (U = 4 edges in flight per lane): one
-    // lane up to degree 8 (measured best at 8), then G*8 ~ average degree.
-    // OCM_IMPROVE_G overrides.
-    const double avg_deg = prep_.R ? double(prep_.M) / std::max<double>(1.0, double(prep_.n - prep_.trivial)) : 1.0;
-    int G = 1;
-    while (G < 32 && G * 8 < avg_deg)
-        G *= 2;
-    p.G = env_int("OCM_IMPROVE_G", G);
     p.small_wc = 4096;
 
     CK(cudaEventRecord(d.ev_start, s));

@@ -4,10 +4,12 @@
 #pragma once
 
 #include <cstdint>
+#include <functional>
 #include <memory>
 #include <vector>
 
 #include "../../include/ocm_b200.h"
+#include "gen.hpp"
 #include "graph.hpp"
 #include "prepinfo.hpp"
 
@@ -18,13 +20,18 @@ struct DeviceState; // devcommon.cuh
 class Session {
   public:
     Session(const Graph& g, const ocm_solve_options& opt);
+    // graph generated directly in HBM (gen_dev.cu)
+    Session(const GenSpec& spec, const ocm_solve_options& opt);
     ~Session();
     void solve(ocm_solution* out, std::uint32_t* cycle_buf, std::uint32_t cap);
     void values(std::int64_t* key_num, std::int64_t* lam_num, std::int64_t* lam_den, double* fval,
                 std::uint32_t* succ_vertex);
     void* stream() const;
 
+    std::uint32_t n() const { return prep_.n; }
+
   private:
+    void init(const std::function<void(DeviceState&)>& prepare);
     template <class M> void run(ocm_solution* out, std::uint32_t* cycle_buf, std::uint32_t cap);
     ocm_solve_options opt_;
     PrepInfo prep_;
