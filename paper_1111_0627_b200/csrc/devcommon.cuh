@@ -135,6 +135,7 @@ struct KP {
     std::uint32_t heavy_deg;
     // tuning (launch arguments)
     int G;                 // improvement lanes per vertex
+    int U;                 // edges in flight per lane (4, or 8 for G <= 2)
     std::uint32_t small_wc; // winning cycles up to this many vertices: one block
 };
 

@@ -501,12 +501,14 @@ template <bool EXACT, int G, int U> __device__ __forceinline__ void improve_phas
 }
 
 template <bool EXACT> __device__ __forceinline__ void improve_dispatch(const KP& p, int* changed) {
-    switch (p.G) {
-    case 1: improve_phase<EXACT, 1, 4>(p, changed); break;
-    case 2: improve_phase<EXACT, 2, 4>(p, changed); break;
-    case 4: improve_phase<EXACT, 4, 4>(p, changed); break;
-    case 8: improve_phase<EXACT, 8, 2>(p, changed); break;
-    case 16: improve_phase<EXACT, 16, 2>(p, changed); break;
+    switch (p.G | (p.U << 8)) {
+    case 1 | (8 << 8): improve_phase<EXACT, 1, 8>(p, changed); break;
+    case 2 | (8 << 8): improve_phase<EXACT, 2, 8>(p, changed); break;
+    case 1 | (4 << 8): improve_phase<EXACT, 1, 4>(p, changed); break;
+    case 2 | (4 << 8): improve_phase<EXACT, 2, 4>(p, changed); break;
+    case 4 | (4 << 8): improve_phase<EXACT, 4, 4>(p, changed); break;
+    case 8 | (4 << 8): improve_phase<EXACT, 8, 2>(p, changed); break;
+    case 16 | (4 << 8): improve_phase<EXACT, 16, 2>(p, changed); break;
     default: improve_phase<EXACT, 32, 2>(p, changed); break;
     }
 }

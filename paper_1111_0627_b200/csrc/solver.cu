@@ -127,6 +127,7 @@ void Session::init(const std::function<void(DeviceState&)>& prepare) {
             G *= 2;
         G = env_int("OCM_IMPROVE_G", G);
         d.kp.G = G;
+        d.kp.U = G <= 2 ? env_int("OCM_IMPROVE_U", 4) : 4;
         d.kp.heavy_deg = static_cast<std::uint32_t>(env_int("OCM_HEAVY_DEG", 32 * 4 * G));
         DBuf<unsigned> cnt;
         cnt.alloc(1, d.stream);
