@@ -65,6 +65,10 @@ def parse():
     ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--lane", default="replicas", choices=["replicas", "sharded"],
+                    help="replicas: every rank solves its own graph (weak scaling, the driver's "
+                         "run); sharded: all ranks solve one graph, vertices 1-D partitioned "
+                         "(strong scaling, DESIGN.md §7)")
     return ap.parse_args()
 
 
@@ -265,6 +269,78 @@ def make_sessions(a, P, rank, local):
     return spec, {o: P.Session.generated(spec, opts[o]) for o in opts}
 
 
+def run_sharded(a, world, rank, local):
+    """Strong scaling: one graph, every rank improves its vertex slice, the
+    policy slices are all-gathered over NCCL each iteration."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_1111_0627_b200 as P
+    from paper_1111_0627_b200.sharded import ShardSession, TorchComm, solve_sharded
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29511")
+        dist.init_process_group("nccl", rank=0, world_size=1)
+    comm = TorchComm()
+    c = CONFIGS[a.config]
+    if c["kind"] == "model":
+        src = build_graph_host(a, P)
+    else:
+        src = P.Generator(c["kind"], n=c["n"], deg=c["deg"], dmax=c.get("dmax", 0), wlo=1,
+                          whi=100, seed=SEED)  # the same graph on every rank
+    shards = {o: ShardSession(src, P.SolveOptions(objective=o, device=local), rank, world)
+              for o in ("min", "max")}
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=dev)
+    streams = {o: torch.cuda.ExternalStream(int(P._lib.ocm_session_stream(shards[o]._h)), device=dev)
+               for o in shards}
+
+    def step():
+        out, ms = {}, 0.0
+        for o in ("min", "max"):
+            flush.fill_(1)
+            torch.cuda.synchronize()
+            dist.barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(streams[o])
+            (out[o],) = solve_sharded([shards[o]], comm)
+            e1.record(streams[o])
+            e1.synchronize()
+            ms += e0.elapsed_time(e1)
+        return out, ms
+
+    for _ in range(a.warmup):
+        step()
+    sols, tot_ms = [], 0.0
+    with ClockSampler(local) as clocks:
+        for _ in range(a.steps):
+            out, ms = step()
+            sols.append(out)
+            tot_ms += ms
+    t = torch.tensor([tot_ms], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    edges = sum(s[o].stats.m_solved * s[o].stats.spf_passes for s in sols for o in s)
+    launches = sum(s[o].stats.launches for s in sols for o in s)
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": edges / (ms_max / 1e3), "unit": UNIT, "n_gpus": world,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms_max / a.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int64",
+            "data": "synthetic (seeded generator)",
+            "config": dict(config(a, world), parallelism=f"sharded x{world} (1-D vertex partition, "
+                                                        f"policy all-gather per iteration)"),
+            "time_to_ocm_s": {o: None for o in ("min", "max")},
+            "policy_iterations": {o: sols[0][o].stats.spf_passes for o in ("min", "max")},
+            "mu": {o: str(sols[0][o].mu_exact) for o in ("min", "max")},
+            "gpu_launches": int(launches), "clocks": clocks.summary(),
+            "note": "device time = CUDA events on the session stream around each sharded solve "
+                    "(launches + NCCL exchanges), max over ranks",
+        }
+        print(json.dumps(line), flush=True)
+
+
 def main():
     a = parse()
     world, rank, local = dist_env()
@@ -276,6 +352,12 @@ def main():
         run_reference(a, world, rank)
         if dist:
             dist.destroy_process_group()
+        return
+    if a.lane == "sharded":
+        run_sharded(a, world, rank, local)
+        import torch.distributed as tdist
+        if tdist.is_initialized():
+            tdist.destroy_process_group()
         return
 
     import torch

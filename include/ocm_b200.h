@@ -162,6 +162,35 @@ int ocm_session_values(ocm_session* s, int64_t* key_num, int64_t* lam_num, int64
 /* A session over a generated graph built in HBM (no host graph). */
 int ocm_session_create_generated(const ocm_generator* spec, const ocm_solve_options* opt,
                                  ocm_session** out);
+/* ---- sharded lane: vertices 1-D partitioned over `world`
+ * ranks (one process per GPU). Every rank holds the prepared graph; rank r
+ * improves the policy of vertices [r*chunk, (r+1)*chunk) only, and after
+ * each improvement pass the ranks exchange the policy slices (all-gather of
+ * succ_e, succ_v, succ_w in chunk-sized pieces) and max-reduce the per-region
+ * change flags (changed0/changed1, `regions` int32 each); cycle detection and
+ * value determination then run replicated. Pass exactly one of g / spec. */
+typedef struct {
+    uint32_t rank, world, chunk;
+    uint32_t own_lo, own_hi, n;
+    void* succ_e;          /* uint32[world*chunk] */
+    void* succ_v;          /* uint32[world*chunk] */
+    void* succ_w;          /* int32 (exact) or double (float) [world*chunk] */
+    uint32_t succ_w_bytes; /* 4 or 8 */
+    uint32_t regions;      /* entries of changed0/changed1 */
+    void* changed0;        /* int32[regions] */
+    void* changed1;
+    void* stream;          /* cudaStream_t the session launches on */
+} ocm_shard_buffers;
+int ocm_session_create_shard(const ocm_graph* g, const ocm_generator* spec,
+                             const ocm_solve_options* opt, uint32_t rank, uint32_t world,
+                             ocm_session** out);
+int ocm_session_shard_buffers(ocm_session* s, ocm_shard_buffers* out);
+/* One launch up to the next exchange point; *done = 1 when the solve finished
+ * (then read it with ocm_session_shard_finish). The first call of a solve
+ * starts it from the initial policy. */
+int ocm_session_shard_step(ocm_session* s, int32_t* done);
+int ocm_session_shard_finish(ocm_session* s, ocm_solution* out, uint32_t* cycle_buf,
+                             uint32_t cycle_cap);
 /* Vertex count of the session's graph. */
 uint32_t ocm_session_n(const ocm_session* s);
 /* The CUDA stream the session launches on (cudaStream_t). */

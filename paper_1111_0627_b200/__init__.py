@@ -77,6 +77,14 @@ class _Gen(C.Structure):
                 ("wlo", C.c_int32), ("whi", C.c_int32), ("seed", C.c_uint64)]
 
 
+class _ShardBuffers(C.Structure):
+    _fields_ = [("rank", C.c_uint32), ("world", C.c_uint32), ("chunk", C.c_uint32),
+                ("own_lo", C.c_uint32), ("own_hi", C.c_uint32), ("n", C.c_uint32),
+                ("succ_e", C.c_void_p), ("succ_v", C.c_void_p), ("succ_w", C.c_void_p),
+                ("succ_w_bytes", C.c_uint32), ("regions", C.c_uint32),
+                ("changed0", C.c_void_p), ("changed1", C.c_void_p), ("stream", C.c_void_p)]
+
+
 class _Opts(C.Structure):
     _fields_ = [("algo", C.c_int32), ("objective", C.c_int32), ("scc", C.c_int32),
                 ("device", C.c_int32), ("epsilon", C.c_double)]
@@ -117,6 +125,11 @@ def _load():
         "ocm_generate": (C.c_int, [P(_Gen), P(C.c_void_p)]),
         "ocm_session_create_generated": (C.c_int, [P(_Gen), P(_Opts), P(C.c_void_p)]),
         "ocm_session_n": (C.c_uint32, [C.c_void_p]),
+        "ocm_session_create_shard": (C.c_int, [C.c_void_p, P(_Gen), P(_Opts), C.c_uint32,
+                                               C.c_uint32, P(C.c_void_p)]),
+        "ocm_session_shard_buffers": (C.c_int, [C.c_void_p, P(_ShardBuffers)]),
+        "ocm_session_shard_step": (C.c_int, [C.c_void_p, P(C.c_int32)]),
+        "ocm_session_shard_finish": (C.c_int, [C.c_void_p, P(_Sol), P(C.c_uint32), C.c_uint32]),
         "ocm_graph_free": (None, [C.c_void_p]),
         "ocm_graph_n": (C.c_uint32, [C.c_void_p]),
         "ocm_graph_m": (C.c_uint64, [C.c_void_p]),
@@ -142,6 +155,8 @@ EXPORTED_SYMBOLS = (
     "ocm_last_error", "ocm_last_error_line", "ocm_version", "ocm_device_count",
     "ocm_build_graph", "ocm_parse_graph_text", "ocm_read_graph_file", "ocm_generate_uniform",
     "ocm_generate_model", "ocm_generate", "ocm_session_create_generated", "ocm_session_n",
+    "ocm_session_create_shard", "ocm_session_shard_buffers", "ocm_session_shard_step",
+    "ocm_session_shard_finish",
     "ocm_graph_free", "ocm_graph_n", "ocm_graph_m", "ocm_graph_integer_exact", "ocm_graph_edges",
     "ocm_solve", "ocm_session_create", "ocm_session_solve", "ocm_session_values",
     "ocm_session_stream", "ocm_session_free",
@@ -180,7 +195,7 @@ class Graph:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h and h.value:
+        if h and h.value and _lib is not None:
             _lib.ocm_graph_free(h)
             self._h = C.c_void_p(None)
 
@@ -440,7 +455,7 @@ class Session:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h and h.value:
+        if h and h.value and _lib is not None:
             _lib.ocm_session_free(h)
             self._h = C.c_void_p(None)
 

@@ -192,6 +192,36 @@ int ocm_session_create_generated(const ocm_generator* spec, const ocm_solve_opti
 
 uint32_t ocm_session_n(const ocm_session* s) { return s ? s->s->n() : 0; }
 
+int ocm_session_create_shard(const ocm_graph* g, const ocm_generator* spec,
+                             const ocm_solve_options* opt, uint32_t rank, uint32_t world,
+                             ocm_session** out) {
+    return guard([&] {
+        if ((g == nullptr) == (spec == nullptr))
+            throw std::invalid_argument("pass exactly one of a graph and a generator");
+        auto s = std::make_unique<ocm_session>();
+        if (g) {
+            const_cast<ocm_graph*>(g)->pin();
+            s->s = std::make_unique<ocmb::Session>(g->g, defaults(opt), rank, world);
+        } else {
+            s->s = std::make_unique<ocmb::Session>(spec_of(spec), defaults(opt), rank, world);
+        }
+        *out = s.release();
+    });
+}
+
+int ocm_session_shard_buffers(ocm_session* s, ocm_shard_buffers* out) {
+    return guard([&] { s->s->shard_buffers(out); });
+}
+
+int ocm_session_shard_step(ocm_session* s, int32_t* done) {
+    return guard([&] { *done = s->s->shard_step() ? 1 : 0; });
+}
+
+int ocm_session_shard_finish(ocm_session* s, ocm_solution* out, uint32_t* cycle_buf,
+                             uint32_t cycle_cap) {
+    return guard([&] { s->s->shard_finish(out, cycle_buf, cycle_cap); });
+}
+
 int ocm_generate_model(uint32_t states, const ocm_transition* transitions, uint32_t n_transitions,
                        int32_t uses_server, uint32_t clients, uint64_t max_states,
                        ocm_graph** out) {

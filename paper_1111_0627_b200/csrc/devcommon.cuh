@@ -78,6 +78,8 @@ struct Ctl {
     int overflow;  // exact keys would leave +-2^62
     int lambda_up; // lambda increased inside a region
     int nonconv;   // a fixpoint did not converge within its bound
+    unsigned it;         // iteration index (sharded launches resume it)
+    unsigned shard_done; // sharded lane: the last launch finished the solve
     unsigned passes;
     unsigned outer;
     unsigned rounds;               // pointer-doubling rounds (all iterations)
@@ -133,6 +135,8 @@ struct KP {
     const std::uint32_t* heavy; // vertices of intra-region degree >= heavy_deg
     std::uint32_t nheavy;
     std::uint32_t heavy_deg;
+    std::uint32_t own_lo, own_hi; // improvement range (all vertices unless sharded)
+    int indeg_in_improve;         // 1: the improvement pass counts policy in-degrees
     // tuning (launch arguments)
     int G;                 // improvement lanes per vertex
     int U;                 // edges in flight per lane (4, or 8 for G <= 2)

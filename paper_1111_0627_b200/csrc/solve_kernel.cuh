@@ -155,6 +155,39 @@ __device__ __forceinline__ std::uint64_t block_append(bool take, const Ring& rin
     return slot;
 }
 
+// Two appends (to two rings) with one set of block barriers.
+__device__ __forceinline__ void block_append2(bool ta, const Ring& ra, std::uint64_t& sa, bool tb,
+                                              const Ring& rb, std::uint64_t& sb) {
+    __shared__ unsigned s_a[kBlock / 32], s_b[kBlock / 32];
+    __shared__ unsigned long long s_base_a, s_base_b;
+    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const unsigned bal_a = __ballot_sync(FULL, ta), bal_b = __ballot_sync(FULL, tb);
+    if (lane == 0) {
+        s_a[warp] = __popc(bal_a);
+        s_b[warp] = __popc(bal_b);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned tot_a = 0, tot_b = 0;
+        for (unsigned w = 0; w < blockDim.x / 32; ++w) {
+            const unsigned ca = s_a[w], cb = s_b[w];
+            s_a[w] = tot_a;
+            s_b[w] = tot_b;
+            tot_a += ca;
+            tot_b += cb;
+        }
+        s_base_a = tot_a ? atomicAdd(ra.counter(), static_cast<unsigned long long>(tot_a)) - ra.origin()
+                         : 0ull;
+        s_base_b = tot_b ? atomicAdd(rb.counter(), static_cast<unsigned long long>(tot_b)) - rb.origin()
+                         : 0ull;
+    }
+    __syncthreads();
+    const unsigned below = (1u << lane) - 1u;
+    sa = s_base_a + s_a[warp] + __popc(bal_a & below);
+    sb = s_base_b + s_b[warp] + __popc(bal_b & below);
+    __syncthreads();
+}
+
 // Block-reduced count added to the ring's current counter.
 __device__ __forceinline__ void block_count(unsigned mine, const Ring& ring) {
     __shared__ unsigned s_sum;
@@ -339,15 +372,12 @@ __device__ __forceinline__ void improve_vertex(const KP& p, int* changed, Change
                     p.succ_wi[v] = bwi;
                 else
                     p.succ_wf[v] = bwf;
-#ifndef OCM_INDEG_PHASE
-                atomicAdd(&p.indeg[bt], 1u);
-#endif
+                if (p.indeg_in_improve)
+                    atomicAdd(&p.indeg[bt], 1u);
                 marks.note(changed, r);
             }
-        } else if (saw_cur) {
-#ifndef OCM_INDEG_PHASE
+        } else if (saw_cur && p.indeg_in_improve) {
             atomicAdd(&p.indeg[cur_t], 1u);
-#endif
         }
     }
 }
@@ -369,7 +399,7 @@ __device__ __forceinline__ void improve_heavy(const KP& p, int* changed) {
     for (std::uint32_t h = blockIdx.x; h < p.nheavy; h += gridDim.x) {
         const std::uint32_t v = p.heavy[h];
         const std::uint32_t r = __ldg(&p.reg[v]);
-        if (!p.active[r])
+        if (!p.active[r] || v < p.own_lo || v >= p.own_hi)
             continue; // block-uniform
         const std::uint32_t b = __ldg(&p.row[v]), e_end = __ldg(&p.row[v + 1]);
         const std::uint32_t cur = p.succ_e[v];
@@ -473,15 +503,17 @@ __device__ __forceinline__ void improve_heavy(const KP& p, int* changed) {
                         const int2 ed = __ldg(&p.ew[ge]);
                         p.succ_v[v] = static_cast<std::uint32_t>(ed.x);
                         p.succ_wi[v] = ed.y;
-                        atomicAdd(&p.indeg[ed.x], 1u);
+                        if (p.indeg_in_improve)
+                            atomicAdd(&p.indeg[ed.x], 1u);
                     } else {
                         const FEdge ed = p.fe[ge];
                         p.succ_v[v] = ed.t;
                         p.succ_wf[v] = ed.w;
-                        atomicAdd(&p.indeg[ed.t], 1u);
+                        if (p.indeg_in_improve)
+                            atomicAdd(&p.indeg[ed.t], 1u);
                     }
                     set_once(&changed[r], 1);
-                } else {
+                } else if (p.indeg_in_improve) {
                     atomicAdd(&p.indeg[p.succ_v[v]], 1u);
                 }
             }
@@ -495,7 +527,7 @@ template <bool EXACT, int G, int U> __device__ __forceinline__ void improve_phas
         improve_heavy<EXACT>(p, changed);
     ChangedMarks marks;
     const std::size_t gs = gstride() / G;
-    for (std::size_t vv = gtid() / G; vv < p.N; vv += gs)
+    for (std::size_t vv = p.own_lo + gtid() / G; vv < p.own_hi; vv += gs)
         improve_vertex<EXACT, G, U>(p, changed, marks, static_cast<std::uint32_t>(vv));
     marks.flush(changed);
 }
@@ -596,9 +628,9 @@ __device__ __forceinline__ void ph_init(const KP& p, bool exact) {
 // Region check (howard_par.hpp:189/208: a region whose pass changed nothing
 // is finished) fused with the split of the still-working vertices into
 // leaves of the policy graph (in-degree 0: never on a cycle, never the
-// successor of anyone) and the core, whose doubling records are initialised
-// here. A vertex still works iff its region changed in this pass (changed
-// is only ever raised for active regions).
+// successor of anyone) and the core, whose first doubling round is done
+// here. A vertex still works iff its region changed in this pass (changed is
+// only ever raised for active regions).
 template <bool EXACT>
 __device__ __forceinline__ void ph_classify(const KP& p, int par, const Ring& ra, const Ring& rl,
                                             const Ring& rc) {
@@ -621,17 +653,20 @@ __device__ __forceinline__ void ph_classify(const KP& p, int par, const Ring& ra
             leaf = p.indeg[v] == 0;
             core = !leaf;
         }
-        const std::uint64_t ls = block_append(leaf, rl);
-        const std::uint64_t cs = block_append(core, rc);
+        std::uint64_t ls, cs;
+        block_append2(leaf, rl, ls, core, rc, cs);
         if (leaf)
             p.plist[ls] = static_cast<std::uint32_t>(v);
         if (core) {
+            // the first doubling round, straight from the policy: the
+            // successor of a core vertex is a core vertex
             p.clist[cs] = static_cast<std::uint32_t>(v);
+            const std::uint32_t sv = p.succ_v[v];
             PJC x;
-            x.nxt = p.succ_v[v];
-            x.mn = static_cast<std::uint32_t>(v);
-            x.w = EXACT ? static_cast<long long>(p.succ_wi[v]) : 0ll;
-            p.pj[0][v] = x;
+            x.nxt = p.succ_v[sv];
+            x.mn = min(static_cast<std::uint32_t>(v), sv);
+            x.w = EXACT ? static_cast<long long>(p.succ_wi[v]) + p.succ_wi[sv] : 0ll;
+            p.pj[1][v] = x;
         }
     }
 }
@@ -1061,7 +1096,18 @@ __device__ __forceinline__ void ph_fprop_level(const KP& p, std::uint32_t level,
 // alternating), and thread-local loop state. A flag read right after a
 // barrier is never written in the phase that follows it.
 
-template <bool EXACT> __global__ void __launch_bounds__(kBlock, kSolveMinBlocks) k_solve(KP p) {
+// mode: kSolveFull runs a whole solve. The sharded lane splits every
+// iteration at its one exchange point: kShardBegin initialises and runs the
+// first improvement pass over the rank's own vertices; the host then
+// all-gathers the policy slices and max-reduces the region flags, and each
+// kShardResume recounts the policy in-degrees on the full (replicated)
+// policy, runs the rest of the iteration replicated, and the next owned
+// improvement pass -- or finishes (Ctl::shard_done). Loop state survives in
+// the control block between launches.
+constexpr int kSolveFull = 0, kShardBegin = 1, kShardResume = 2;
+
+template <bool EXACT>
+__global__ void __launch_bounds__(kBlock, kSolveMinBlocks) k_solve(KP p, int mode) {
     cg::grid_group grid = cg::this_grid();
     Ctl* const c = p.c;
     const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
@@ -1086,28 +1132,41 @@ template <bool EXACT> __global__ void __launch_bounds__(kBlock, kSolveMinBlocks)
     unsigned stamp = ldr(c->stamp);
     unsigned k_hint = max(1u, min(ldr(c->k_hint), static_cast<unsigned>(K_max)));
     unsigned k_streak = ldr(c->k_streak);
-    unsigned passes = 0, outer = 0, rounds = 0, verifies = 0, layers = 0;
-    unsigned long long peeled = 0, cored = 0;
+    // per-solve counters continue across the launches of a sharded solve
+    unsigned passes = ldr(c->passes), outer = ldr(c->outer), rounds = ldr(c->rounds);
+    unsigned verifies = ldr(c->verifies), layers = ldr(c->layers);
+    unsigned long long peeled = ldr(c->peeled), cored = ldr(c->cored);
     unsigned long long done_base = ldr(c->done);
-    bool fatal = false; // uniform: a fixpoint failed to converge
+    bool fatal = false;  // uniform: a fixpoint failed to converge
+    bool paused = false; // uniform: sharded launch ends at its exchange point
+    int it = static_cast<int>(ldr(c->it));
 
-    ph_init(p, EXACT);
-    sync(PH_INIT);
+    if (mode != kShardResume) {
+        ph_init(p, EXACT);
+        sync(PH_INIT);
+    }
+    bool skip_improve = mode == kShardResume;
 
-    for (int it = 0;; ++it) {
+    for (;; ++it) {
         const int par = it & 1;
-        improve_dispatch<EXACT>(p, p.changed[par]);
-        ++passes;
-        sync(PH_IMPROVE);
-
-#ifdef OCM_INDEG_PHASE
-        // experiment: in-degrees counted in their own pass instead of in
-        // the improvement pass
-        for (std::size_t v = gtid(); v < p.N; v += gstride())
-            if (p.changed[par][__ldg(&p.reg[v])])
-                atomicAdd(&p.indeg[p.succ_v[v]], 1u);
-        sync(PH_CLASSIFY);
-#endif
+        if (!skip_improve) {
+            improve_dispatch<EXACT>(p, p.changed[par]);
+            ++passes;
+            sync(PH_IMPROVE);
+            if (mode != kSolveFull) {
+                paused = true;
+                break;
+            }
+        }
+        skip_improve = false;
+        if (!p.indeg_in_improve) {
+            // the policy of the other ranks arrived by the exchange: count
+            // in-degrees over the full policy (replicated on every rank)
+            for (std::size_t v = gtid(); v < p.N; v += gstride())
+                if (p.changed[par][__ldg(&p.reg[v])])
+                    atomicAdd(&p.indeg[p.succ_v[v]], 1u);
+            sync(PH_CLASSIFY);
+        }
         ph_classify<EXACT>(p, par, ra, rl, rc);
         sync(PH_CLASSIFY);
         const std::uint64_t n_active = ra.take();
@@ -1121,8 +1180,10 @@ template <bool EXACT> __global__ void __launch_bounds__(kBlock, kSolveMinBlocks)
         peeled += nL;
         cored += nC;
 
-        // ---- pointer doubling on the core, verified exactly
-        int in = 0, k = 0;
+        // ---- pointer doubling on the core, verified exactly (round 1 was
+        // done by the classification)
+        int in = 1, k = 1;
+        ++rounds;
         bool first_try = true;
         std::uint64_t nM = 0;
         for (;;) {
@@ -1226,6 +1287,8 @@ template <bool EXACT> __global__ void __launch_bounds__(kBlock, kSolveMinBlocks)
     if (leader) {
         if (fatal)
             c->nonconv = 1;
+        c->it = static_cast<unsigned>(it);
+        c->shard_done = paused ? 0 : 1;
         c->stamp = stamp;
         c->k_hint = k_hint;
         c->k_streak = k_streak;
@@ -1237,7 +1300,7 @@ template <bool EXACT> __global__ void __launch_bounds__(kBlock, kSolveMinBlocks)
         c->cored = cored;
         c->layers = layers;
         c->syncs = nsync;
-        c->clk_total = clock64() - clk0;
+        c->clk_total += clock64() - clk0;
     }
 }
 

@@ -35,16 +35,21 @@ int env_int(const char* name, int dflt) {
 
 } // namespace
 
-Session::Session(const Graph& g, const ocm_solve_options& opt) : opt_(opt) {
+Session::Session(const Graph& g, const ocm_solve_options& opt, std::uint32_t rank, std::uint32_t world)
+    : opt_(opt), rank_(rank), world_(world) {
     init([&](DeviceState& d) { device_prepare(g, opt, d, prep_); });
 }
 
-Session::Session(const GenSpec& spec, const ocm_solve_options& opt) : opt_(opt) {
+Session::Session(const GenSpec& spec, const ocm_solve_options& opt, std::uint32_t rank,
+                 std::uint32_t world)
+    : opt_(opt), rank_(rank), world_(world) {
     init([&](DeviceState& d) { device_generate_prepare(spec, opt, d, prep_); });
 }
 
 void Session::init(const std::function<void(DeviceState&)>& prepare) {
     const ocm_solve_options& opt = opt_;
+    if (world_ == 0 || rank_ >= world_)
+        throw std::invalid_argument("shard rank must be below the world size");
     if (opt.algo != OCM_ALGO_HOWARD && opt.algo != OCM_ALGO_HOWARD_PAR)
         throw UnsupportedError("only the policy-iteration lanes (howard, howard-par) run on the "
                                "device");
@@ -77,18 +82,23 @@ void Session::init(const std::function<void(DeviceState&)>& prepare) {
 
     const std::size_t N = prep_.n, R1 = std::size_t(prep_.R) + 1;
     const std::size_t N1 = std::max<std::size_t>(N, 1);
+    // policy arrays are padded to world equal chunks for the all-gather
+    chunk_ = static_cast<std::uint32_t>((N + world_ - 1) / world_);
+    const std::size_t NP = std::max<std::size_t>(N1, std::size_t(chunk_) * world_);
     if (prep_.exact) {
-        d.succ_wi.alloc(N1, d.stream);
+        d.succ_wi.alloc(NP, d.stream);
         d.key_i.alloc(N1, d.stream);
         d.cyc_wi.alloc(N1, d.stream);
         d.pv0.alloc(N1, d.stream);
         d.pv1.alloc(N1, d.stream);
     } else {
-        d.succ_wf.alloc(N1, d.stream);
+        d.succ_wf.alloc(NP, d.stream);
         d.key_f.alloc(N1, d.stream);
         d.cyc_wf.alloc(N1, d.stream);
     }
-    for (auto* b : {&d.succ_e, &d.succ_v, &d.comp, &d.wlist, &d.cyc_len, &d.conn, &d.rem0, &d.rem1,
+    d.succ_e.alloc(NP, d.stream);
+    d.succ_v.alloc(NP, d.stream);
+    for (auto* b : {&d.comp, &d.wlist, &d.cyc_len, &d.conn, &d.rem0, &d.rem1,
                     &d.indeg, &d.plist, &d.clist, &d.cmark, &d.cmark2})
         b->alloc(N1, d.stream);
     d.pj0.alloc(N1, d.stream);
@@ -197,6 +207,9 @@ void Session::init(const std::function<void(DeviceState&)>& prepare) {
     p.c = d.ctl.p;
     p.max_region = prep_.max_region;
     p.max_abs_w = prep_.max_abs_w;
+    p.own_lo = static_cast<std::uint32_t>(std::min<std::size_t>(N, std::size_t(rank_) * chunk_));
+    p.own_hi = static_cast<std::uint32_t>(std::min<std::size_t>(N, std::size_t(rank_ + 1) * chunk_));
+    p.indeg_in_improve = world_ == 1 ? 1 : 0;
     h2d_bytes_ = prep_.h2d_bytes;
     prep_ms_ = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
 }
@@ -205,29 +218,36 @@ Session::~Session() = default;
 
 void* Session::stream() const { return d_ ? d_->stream : nullptr; }
 
-template <class M> void Session::run(ocm_solution* out, std::uint32_t* cycle_buf, std::uint32_t cap) {
+// One cooperative launch of k_solve in the given mode; returns its event time.
+template <class M> float Session::launch(int mode) {
     constexpr bool EXACT = M::value;
     DeviceState& d = *d_;
     KP& p = d.kp;
     cudaStream_t s = d.stream;
     Ctl& hc = *d.h_ctl;
-    std::uint64_t d2h = 0;
-
     p.small_wc = 4096;
-
+    if (mode != kShardResume) {
+        CK(cudaMemsetAsync(reinterpret_cast<char*>(p.c) + kCtlSolveOffset, 0,
+                           sizeof(Ctl) - kCtlSolveOffset, s));
+        d2h_ = 0;
+        solve_ms_ = 0.0;
+        launches_ = 0;
+    }
     CK(cudaEventRecord(d.ev_start, s));
-    CK(cudaMemsetAsync(reinterpret_cast<char*>(p.c) + kCtlSolveOffset, 0, sizeof(Ctl) - kCtlSolveOffset, s));
     if (prep_.R > 0) {
-        void* args[] = {&p};
+        void* args[] = {&p, &mode};
         const void* fn = EXACT ? reinterpret_cast<const void*>(&k_solve<true>)
                                : reinterpret_cast<const void*>(&k_solve<false>);
         CK(cudaLaunchCooperativeKernel(fn, dim3(EXACT ? grid_exact_ : grid_float_), dim3(kBlock), args, 0, s));
+        ++launches_;
     }
     CK(cudaEventRecord(d.ev_end, s));
     CK(cudaMemcpyAsync(&hc, p.c, sizeof(Ctl), cudaMemcpyDeviceToHost, s));
-    d2h += sizeof(Ctl);
+    d2h_ += sizeof(Ctl);
     CK(cudaStreamSynchronize(s));
     CK(cudaGetLastError());
+    if (prep_.R == 0)
+        hc.shard_done = 1;
     if (hc.error)
         throw std::logic_error("howard_par: structural error (a vertex has no successor "
                                "inside its region, or a region is not strongly connected)");
@@ -237,9 +257,21 @@ template <class M> void Session::run(ocm_solution* out, std::uint32_t* cycle_buf
         throw RangeError("exact value keys would exceed 62 bits for this graph");
     if (hc.nonconv)
         throw std::logic_error("a device fixpoint did not converge within its bound");
-
     float ms = 0.f;
     CK(cudaEventElapsedTime(&ms, d.ev_start, d.ev_end));
+    solve_ms_ += ms;
+    return ms;
+}
+
+// Result of the solve that just finished: counters, the optimal region's
+// lambda and its cycle (read back from the device).
+template <class M> void Session::collect(ocm_solution* out, std::uint32_t* cycle_buf, std::uint32_t cap) {
+    constexpr bool EXACT = M::value;
+    DeviceState& d = *d_;
+    KP& p = d.kp;
+    Ctl& hc = *d.h_ctl;
+    const double ms = solve_ms_;
+    std::uint64_t d2h = d2h_;
     static const bool phases_on = std::getenv("OCM_PHASES") != nullptr;
     if (phases_on && prep_.R > 0 && hc.clk_total > 0) {
         static const char* names[PH_COUNT] = {"init",  "improve", "classify", "round",
@@ -255,11 +287,11 @@ template <class M> void Session::run(ocm_solution* out, std::uint32_t* cycle_buf
         std::fprintf(stderr,
                      "{\"device_ms\": %.3f, \"phases_ms\": {%s}, \"passes\": %u, \"outer\": %u, "
                      "\"rounds\": %u, \"verifies\": %u, \"peeled\": %llu, \"cored\": %llu, "
-                     "\"layers\": %u, \"syncs\": %u, \"k_hint\": %u, \"N\": %u, \"M\": %llu}\n",
-                     ms, ph.c_str(), hc.passes, hc.outer, hc.rounds,
-                     hc.verifies, (unsigned long long)hc.peeled,
-                     (unsigned long long)hc.cored, hc.layers,
-                     hc.syncs, hc.k_hint, p.N, (unsigned long long)prep_.M);
+                     "\"layers\": %u, \"syncs\": %u, \"k_hint\": %u, \"launches\": %u, \"N\": %u, "
+                     "\"M\": %llu}\n",
+                     ms, ph.c_str(), hc.passes, hc.outer, hc.rounds, hc.verifies,
+                     (unsigned long long)hc.peeled, (unsigned long long)hc.cored, hc.layers, hc.syncs,
+                     hc.k_hint, launches_, p.N, (unsigned long long)prep_.M);
     }
 
     std::memset(out, 0, sizeof *out);
@@ -270,7 +302,7 @@ template <class M> void Session::run(ocm_solution* out, std::uint32_t* cycle_buf
     out->trivial_regions = prep_.trivial;
     out->n_solved = prep_.n;
     out->m_solved = prep_.M;
-    out->launches = prep_.R > 0 ? 1 : 0;
+    out->launches = launches_;
     out->fixpoint_iters = std::uint64_t(hc.rounds) + hc.layers;
     out->device_ms = ms;
     // share of the launch spent in improvement phases (SM clock spans of
@@ -354,11 +386,58 @@ struct FloatTag {
 
 void Session::solve(ocm_solution* out, std::uint32_t* cycle_buf, std::uint32_t cap) {
     CK(cudaSetDevice(d_->device));
-    if (prep_.exact)
-        run<ExactTag>(out, cycle_buf, cap);
-    else
-        run<FloatTag>(out, cycle_buf, cap);
+    if (world_ > 1)
+        throw std::invalid_argument("sharded session: drive it with shard_step / shard_finish");
+    if (prep_.exact) {
+        launch<ExactTag>(kSolveFull);
+        collect<ExactTag>(out, cycle_buf, cap);
+    } else {
+        launch<FloatTag>(kSolveFull);
+        collect<FloatTag>(out, cycle_buf, cap);
+    }
     solved_ = true;
+}
+
+bool Session::shard_step() {
+    CK(cudaSetDevice(d_->device));
+    const int mode = shard_started_ ? kShardResume : kShardBegin;
+    if (prep_.exact)
+        launch<ExactTag>(mode);
+    else
+        launch<FloatTag>(mode);
+    shard_started_ = true;
+    const bool done = d_->h_ctl->shard_done != 0;
+    if (done)
+        shard_started_ = false;
+    return done;
+}
+
+void Session::shard_finish(ocm_solution* out, std::uint32_t* cycle_buf, std::uint32_t cap) {
+    CK(cudaSetDevice(d_->device));
+    if (prep_.exact)
+        collect<ExactTag>(out, cycle_buf, cap);
+    else
+        collect<FloatTag>(out, cycle_buf, cap);
+    solved_ = true;
+}
+
+void Session::shard_buffers(ocm_shard_buffers* b) const {
+    const DeviceState& d = *d_;
+    std::memset(b, 0, sizeof *b);
+    b->rank = rank_;
+    b->world = world_;
+    b->chunk = chunk_;
+    b->own_lo = d.kp.own_lo;
+    b->own_hi = d.kp.own_hi;
+    b->n = prep_.n;
+    b->succ_e = d.succ_e.p;
+    b->succ_v = d.succ_v.p;
+    b->succ_w = prep_.exact ? static_cast<void*>(d.succ_wi.p) : static_cast<void*>(d.succ_wf.p);
+    b->succ_w_bytes = prep_.exact ? 4 : 8;
+    b->changed0 = d.changed0.p;
+    b->changed1 = d.changed1.p;
+    b->regions = prep_.R + 1;
+    b->stream = d.stream;
 }
 
 void Session::values(std::int64_t* key_num, std::int64_t* lam_num, std::int64_t* lam_den,

@@ -19,9 +19,13 @@ struct DeviceState; // devcommon.cuh
 
 class Session {
   public:
-    Session(const Graph& g, const ocm_solve_options& opt);
+    // rank/world > 1: a shard of the sharded lane; the rank
+    // improves the policy of vertices [rank*chunk, (rank+1)*chunk) only.
+    Session(const Graph& g, const ocm_solve_options& opt, std::uint32_t rank = 0,
+            std::uint32_t world = 1);
     // graph generated directly in HBM (gen_dev.cu)
-    Session(const GenSpec& spec, const ocm_solve_options& opt);
+    Session(const GenSpec& spec, const ocm_solve_options& opt, std::uint32_t rank = 0,
+            std::uint32_t world = 1);
     ~Session();
     void solve(ocm_solution* out, std::uint32_t* cycle_buf, std::uint32_t cap);
     void values(std::int64_t* key_num, std::int64_t* lam_num, std::int64_t* lam_den, double* fval,
@@ -30,9 +34,17 @@ class Session {
 
     std::uint32_t n() const { return prep_.n; }
 
+    // Sharded lane: one launch up to the next exchange point (true when the
+    // solve finished), the device buffers the host exchanges between
+    // launches, and the result of the finished solve.
+    bool shard_step();
+    void shard_buffers(ocm_shard_buffers* b) const;
+    void shard_finish(ocm_solution* out, std::uint32_t* cycle_buf, std::uint32_t cap);
+
   private:
     void init(const std::function<void(DeviceState&)>& prepare);
-    template <class M> void run(ocm_solution* out, std::uint32_t* cycle_buf, std::uint32_t cap);
+    template <class M> float launch(int mode);
+    template <class M> void collect(ocm_solution* out, std::uint32_t* cycle_buf, std::uint32_t cap);
     ocm_solve_options opt_;
     PrepInfo prep_;
     double prep_ms_ = 0.0;
@@ -40,6 +52,11 @@ class Session {
     std::unique_ptr<DeviceState> d_;
     bool solved_ = false;
     int grid_exact_ = 0, grid_float_ = 0; // cooperative grid of k_solve<exact / float>
+    std::uint32_t rank_ = 0, world_ = 1, chunk_ = 0;
+    bool shard_started_ = false;
+    double solve_ms_ = 0.0;   // event time of the current solve's launches
+    std::uint64_t d2h_ = 0;   // device->host bytes of the current solve
+    unsigned launches_ = 0;   // launches of the current solve
 };
 
 } // namespace ocmb
