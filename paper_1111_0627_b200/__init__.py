@@ -144,6 +144,8 @@ def _load():
         "ocm_session_free": (None, [C.c_void_p]),
     }
     for name, (res, args) in sig.items():
+        if os.environ.get("OCM_LIB") and not hasattr(lib, name):
+            continue  # experimental library override (scripts/build_variant.sh) may be older
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args

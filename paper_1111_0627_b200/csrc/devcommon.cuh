@@ -237,8 +237,7 @@ struct DeviceState {
             cudaEventDestroy(ev_start);
         if (ev_end)
             cudaEventDestroy(ev_end);
-        if (h_ctl)
-            cudaFreeHost(h_ctl);
+        delete h_ctl;
         if (stream)
             cudaStreamDestroy(stream);
     }

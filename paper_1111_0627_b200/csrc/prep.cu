@@ -21,6 +21,8 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -36,6 +38,18 @@ void device_prepare_csr(std::uint32_t n, std::uint64_t m, DBuf<std::uint32_t>& r
                         const ocm_solve_options& opt, DeviceState& d, PrepInfo& info);
 
 namespace {
+
+// One atomicMax per warp (warp-reduced, skipped when it cannot win): a
+// whole grid max-reducing into one word otherwise serialises at L2.
+__device__ __forceinline__ void warp_atomic_max(unsigned long long* dst, unsigned long long v) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        const unsigned long long o = __shfl_xor_sync(0xffffffffu, v, off);
+        v = o > v ? o : v;
+    }
+    if ((threadIdx.x & 31) == 0 && v && v > __ldcg(dst))
+        atomicMax(dst, v);
+}
 
 __device__ __forceinline__ std::size_t tid_() {
     return blockIdx.x * std::size_t(blockDim.x) + threadIdx.x;
@@ -106,8 +120,7 @@ __global__ void kp_degrees(std::uint32_t n, const std::uint32_t* row, const std:
         outd[v] = o;
         self[v] = s;
     }
-    if (mx)
-        atomicMax(&pc->max_abs_bits, mx);
+    warp_atomic_max(&pc->max_abs_bits, mx);
 }
 
 // Backward CSR (no self-loops): bsrc grouped by target.
@@ -203,8 +216,7 @@ __global__ void kp_pick_pivot(std::uint32_t n, const std::uint32_t* lab, const s
         const unsigned long long key = (score << 32) | (0xffffffffull - vv);
         best = key > best ? key : best;
     }
-    if (best)
-        atomicMax(&pc->pivot, best);
+    warp_atomic_max(&pc->pivot, best);
 }
 
 // One BFS level restricted to unassigned vertices; vis[] holds the stamp.
@@ -303,8 +315,16 @@ __global__ void kp_color_assign(std::uint32_t n, const std::uint32_t* color,
 
 // Component sizes at the representatives (lab[r] == r).
 __global__ void kp_sizes(std::uint32_t n, const std::uint32_t* lab, std::uint32_t* size) {
-    for (std::size_t v = tid_(); v < n; v += stride_())
-        atomicAdd(&size[lab[v]], 1u);
+    // warp-aggregated: lanes sharing a label add once (the giant component
+    // would otherwise serialise every vertex on one word)
+    for (std::size_t base = (tid_() & ~std::size_t(31)); base < n; base += stride_()) {
+        const std::size_t v = base + (threadIdx.x & 31);
+        const bool on = v < n;
+        const std::uint32_t l = on ? lab[v] : 0xffffffffu;
+        const unsigned peers = __match_any_sync(0xffffffffu, l);
+        if (on && (threadIdx.x & 31) == static_cast<unsigned>(__ffs(peers) - 1))
+            atomicAdd(&size[l], static_cast<unsigned>(__popc(peers)));
+    }
 }
 
 __global__ void kp_nontrivial(std::uint32_t n, const std::uint32_t* lab, const std::uint32_t* size,
@@ -445,6 +465,12 @@ void device_prepare(const Graph& g, const ocm_solve_options& opt, DeviceState& d
     }
     kp_row32<<<grid_for(n + 1, d.sms), kBlock, 0, s>>>(row64.p, row.p, std::size_t(n) + 1);
     row64.release();
+    if (std::getenv("OCM_PREP_TIMING")) {
+        const auto t0 = std::chrono::steady_clock::now();
+        CK(cudaStreamSynchronize(s));
+        std::fprintf(stderr, "{\"upload_wait_ms\": %.3f}\n",
+                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+    }
     device_prepare_csr(n, m, row, tgt, w, g.integer_exact, opt, d, info);
     info.h2d_bytes = (std::size_t(n) + 1) * 8 + m * 12;
 }
@@ -649,6 +675,7 @@ void device_prepare_csr(std::uint32_t n, std::uint64_t m, DBuf<std::uint32_t>& r
     info.max_region = pc.max_region;
     kp_region_ids<<<gv, kBlock, 0, s>>>(n, lab.p, flag.p, rid.p, R, d.reg.p);
     info.scc_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_scc).count();
+    const auto t_pack = std::chrono::steady_clock::now();
 
     // ---- intra-region CSR
     DBuf<std::uint32_t>& cnt = rid; // reuse (n+1)
@@ -673,6 +700,10 @@ void device_prepare_csr(std::uint32_t n, std::uint64_t m, DBuf<std::uint32_t>& r
     if (info.exact && pc.bad_weight)
         throw UnsupportedError("integer weights beyond 32 bits are not supported by the device lane");
     info.max_abs_w = static_cast<long long>(max_abs);
+    if (std::getenv("OCM_PREP_TIMING"))
+        std::fprintf(stderr, "{\"scc_ms\": %.3f, \"pack_ms\": %.3f, \"R\": %u}\n", info.scc_ms,
+                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_pack).count(),
+                     R);
 }
 
 } // namespace ocmb

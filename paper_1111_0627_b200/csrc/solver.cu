@@ -10,6 +10,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 
@@ -31,6 +33,44 @@ namespace {
 int env_int(const char* name, int dflt) {
     const char* v = std::getenv(name);
     return v ? std::atoi(v) : dflt;
+}
+
+// Per-device facts looked up once per process (device properties and the
+// cooperative occupancy of k_solve cost milliseconds per query).
+struct DeviceFacts {
+    int sms = 0, major = 0;
+    int per_sm[2] = {0, 0}; // k_solve<exact>, k_solve<float>
+    std::string name;
+};
+
+const DeviceFacts& device_facts(int dev) {
+    static std::mutex mu;
+    static std::map<int, DeviceFacts> cache;
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = cache.find(dev);
+    if (it != cache.end())
+        return it->second;
+    DeviceFacts f;
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, dev));
+    f.sms = prop.multiProcessorCount;
+    f.major = prop.major;
+    f.name = prop.name;
+    if (f.major >= 10) {
+        for (int e = 0; e < 2; ++e) {
+            int per_sm = 0;
+            const void* fn = e ? reinterpret_cast<const void*>(&k_solve<false>)
+                               : reinterpret_cast<const void*>(&k_solve<true>);
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kBlock, 0));
+            f.per_sm[e] = std::max(1, std::min(per_sm, kSolveMinBlocks));
+        }
+        // keep freed blocks cached in the default pool across sessions
+        cudaMemPool_t pool;
+        CK(cudaDeviceGetDefaultMemPool(&pool, dev));
+        std::uint64_t keep = ~0ull;
+        CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+    }
+    return cache.emplace(dev, f).first->second;
 }
 
 } // namespace
@@ -60,25 +100,20 @@ void Session::init(const std::function<void(DeviceState&)>& prepare) {
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
         throw CudaError("no CUDA device available (the solver has no CPU fallback)");
     d.device = opt.device;
+    if (d.device < 0 || d.device >= ndev)
+        throw std::invalid_argument("device ordinal out of range");
     CK(cudaSetDevice(d.device));
-    cudaDeviceProp prop;
-    CK(cudaGetDeviceProperties(&prop, d.device));
-    if (prop.major < 10)
-        throw CudaError(std::string("device ") + prop.name + " is not sm_100-class");
-    d.sms = prop.multiProcessorCount;
+    const DeviceFacts& facts = device_facts(d.device);
+    if (facts.major < 10)
+        throw CudaError("device " + facts.name + " is not sm_100-class");
+    d.sms = facts.sms;
     CK(cudaStreamCreateWithFlags(&d.stream, cudaStreamNonBlocking));
-    {
-        // keep freed blocks cached in the default pool across sessions
-        cudaMemPool_t pool;
-        CK(cudaDeviceGetDefaultMemPool(&pool, d.device));
-        std::uint64_t keep = ~0ull;
-        CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
-    }
     CK(cudaEventCreate(&d.ev_start));
     CK(cudaEventCreate(&d.ev_end));
-    CK(cudaMallocHost(&d.h_ctl, sizeof(Ctl)));
-
+    d.h_ctl = new Ctl{}; // 300 B read back per launch: pageable is fine
+    const auto t_prep = std::chrono::steady_clock::now();
     prepare(d);
+    const auto t_alloc = std::chrono::steady_clock::now();
 
     const std::size_t N = prep_.n, R1 = std::size_t(prep_.R) + 1;
     const std::size_t N1 = std::max<std::size_t>(N, 1);
@@ -156,14 +191,8 @@ void Session::init(const std::function<void(DeviceState&)>& prepare) {
     }
 
     // one CTA per SM slot the register budget allows (<= kSolveMinBlocks)
-    for (int e = 0; e < 2; ++e) {
-        int per_sm = 0;
-        const void* fn = e ? reinterpret_cast<const void*>(&k_solve<false>)
-                           : reinterpret_cast<const void*>(&k_solve<true>);
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kBlock, 0));
-        per_sm = std::max(1, std::min(per_sm, kSolveMinBlocks));
-        (e ? grid_float_ : grid_exact_) = per_sm * d.sms;
-    }
+    grid_exact_ = facts.per_sm[0] * d.sms;
+    grid_float_ = facts.per_sm[1] * d.sms;
 
     KP& p = d.kp;
     p.N = prep_.n;
@@ -211,7 +240,13 @@ void Session::init(const std::function<void(DeviceState&)>& prepare) {
     p.own_hi = static_cast<std::uint32_t>(std::min<std::size_t>(N, std::size_t(rank_ + 1) * chunk_));
     p.indeg_in_improve = world_ == 1 ? 1 : 0;
     h2d_bytes_ = prep_.h2d_bytes;
-    prep_ms_ = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    const auto t_end = std::chrono::steady_clock::now();
+    prep_ms_ = std::chrono::duration<double, std::milli>(t_end - t0).count();
+    if (std::getenv("OCM_PREP_TIMING")) {
+        auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+        std::fprintf(stderr, "{\"init_setup_ms\": %.3f, \"prepare_ms\": %.3f, \"session_alloc_ms\": %.3f}\n",
+                     ms(t0, t_prep), ms(t_prep, t_alloc), ms(t_alloc, t_end));
+    }
 }
 
 Session::~Session() = default;

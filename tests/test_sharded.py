@@ -153,5 +153,5 @@ print("ok", sol.mu_exact, sol.stats.launches)
 def test_torchcomm_nccl_world1():
     r = subprocess.run([sys.executable, "-c", NCCL_WORLD1, ROOT, str(_free_port())],
                        capture_output=True, text=True, timeout=300)
-    assert r.returncode == 0, r.stderr[-2000:]
+    assert r.returncode == 0, (r.stdout[-1000:], r.stderr[:3000])
     assert r.stdout.strip().splitlines()[-1].startswith("ok"), r.stdout
