@@ -152,6 +152,20 @@ def measured_peak():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+def gather_peak(n):
+    """Measured random 8-byte gather throughput (scripts/micro/gather.cu on
+    this pool's B200, profiles/micro_gather_r01.log): ~210 G/s while the
+    gathered array is L2-resident (<= 64 MB), ~40 G/s once it is HBM-resident
+    (>= 1 GB); linear in between is not claimed, so 256 MB-class arrays use
+    the measured 70 G/s point."""
+    b = 8 * n
+    if b <= (64 << 20):
+        return 2.1e11, "measured: L2-resident random gather, 8 MB-64 MB arrays"
+    if b <= (256 << 20):
+        return 7.0e10, "measured: random gather, 256 MB array"
+    return 4.0e10, "measured: HBM-resident random gather, 1-8 GB arrays"
+
+
 def ncu_traffic(cfg):
     """DRAM bytes per k_solve launch from the committed ncu --set full summary."""
     try:
@@ -462,7 +476,15 @@ def main():
                 "improve_phase": {"achieved": imp_achieved,
                                   "frac": imp_achieved / peak if imp_achieved else None,
                                   "bytes_per_pass": imp_bytes / passes,
-                                  "avg_pass_ms": imp_ms / passes},
+                                  "avg_pass_ms": imp_ms / passes,
+                                  # the pass is bound by random 8-byte key gathers (one per
+                                  # edge), whose measured B200 ceiling depends on whether the
+                                  # key array stays in L2 (profiles/micro_gather_r01.log)
+                                  "gathers_per_s": st0.m_solved / (imp_ms / passes / 1e3) if imp_ms else None,
+                                  "gather_peak_per_s": gather_peak(st0.n_solved)[0],
+                                  "gather_frac": (st0.m_solved / (imp_ms / passes / 1e3)
+                                                  / gather_peak(st0.n_solved)[0]) if imp_ms else None,
+                                  "gather_peak_source": gather_peak(st0.n_solved)[1]},
                 "note": "achieved = algorithmic bytes (DESIGN.md §5) / CUDA-event time of the "
                         "launch on the session stream; improve_phase timed by SM clock share "
                         "between the phase's grid barriers",

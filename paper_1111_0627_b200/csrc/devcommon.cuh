@@ -139,7 +139,7 @@ struct KP {
     int indeg_in_improve;         // 1: the improvement pass counts policy in-degrees
     // tuning (launch arguments)
     int G;                 // improvement lanes per vertex
-    int U;                 // edges in flight per lane (4, or 8 for G <= 2)
+    int U;                 // edges in flight per lane (4)
     std::uint32_t small_wc; // winning cycles up to this many vertices: one block
 };
 

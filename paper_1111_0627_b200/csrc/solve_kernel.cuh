@@ -253,132 +253,141 @@ struct ChangedMarks {
     }
 };
 
+// Read-only 8/16-byte edge records through the non-coherent path.
+__device__ __forceinline__ int2 ld_edge(const int2* e) { return __ldg(e); }
+__device__ __forceinline__ FEdge ld_edge(const FEdge* e) {
+    const double2 raw = __ldg(reinterpret_cast<const double2*>(e));
+    FEdge f;
+    f.w = raw.x;
+    f.t = static_cast<std::uint32_t>(__double_as_longlong(raw.y));
+    f.pad = 0;
+    return f;
+}
+
 template <bool EXACT, int G, int U>
 __device__ __forceinline__ void improve_vertex(const KP& p, int* changed, ChangedMarks& marks,
                                                std::uint32_t v) {
+    // Register budget matters here (64 at 4 CTAs/SM): edges stay packed as
+    // they were loaded, the winner's head and weight are re-read (an L1 hit)
+    // only when the policy changes, and the exact candidate drops the
+    // per-vertex constant -num (compares are offset-invariant in integers).
     const unsigned lane = threadIdx.x & (G - 1);
     const unsigned gm = group_mask<G>();
     using Key = typename std::conditional<EXACT, long long, double>::type;
+    using Edge = typename std::conditional<EXACT, int2, FEdge>::type;
     const Key* __restrict__ key = EXACT ? reinterpret_cast<const Key*>(p.key_i)
                                         : reinterpret_cast<const Key*>(p.key_f);
-    {
-        const std::uint32_t r = __ldg(&p.reg[v]);
-        if (!p.active[r])
-            return;
-        const std::uint32_t b = __ldg(&p.row[v]), e_end = __ldg(&p.row[v + 1]);
-        if (e_end - b >= p.heavy_deg)
-            return; // block-cooperative path (improve_heavy)
-        const std::uint32_t cur = p.succ_e[v];
-        long long num = 0, den = 1;
-        double lam = 0.0;
-        if constexpr (EXACT) {
-            num = p.lam_num[r];
-            den = p.lam_den[r];
-        } else {
-            lam = p.lam_f[r];
-        }
-        Key best = 0, curc = 0;
-        std::uint32_t be = NONE, bt = 0, cur_t = 0;
-        int bwi = 0;
-        double bwf = 0.0;
-        bool have_cur = false;
-        for (std::uint32_t e0 = b + lane; e0 < e_end; e0 += G * U) {
-            std::uint32_t tt[U];
-            Key kk[U];
-            int wi[U];
-            double wf[U];
+    const Edge* __restrict__ edges = EXACT ? reinterpret_cast<const Edge*>(p.ew)
+                                           : reinterpret_cast<const Edge*>(p.fe);
+    const std::uint32_t r = __ldg(&p.reg[v]);
+    if (!p.active[r])
+        return;
+    const std::uint32_t b = __ldg(&p.row[v]), e_end = __ldg(&p.row[v + 1]);
+    if (e_end - b >= p.heavy_deg)
+        return; // block-cooperative path (improve_heavy)
+    const std::uint32_t cur = p.succ_e[v];
+    long long den = 1;
+    double lam = 0.0;
+    if constexpr (EXACT)
+        den = p.lam_den[r];
+    else
+        lam = p.lam_f[r];
+    Key best = 0, curc = 0;
+    std::uint32_t be = NONE;
+    bool have_cur = false;
+    for (std::uint32_t e0 = b + lane; e0 < e_end; e0 += G * U) {
+        Edge ed[U];
+        Key kk[U];
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const std::uint32_t e = e0 + u * G;
-                if (e < e_end) {
-                    if constexpr (EXACT) {
-                        const int2 ed = __ldg(&p.ew[e]);
-                        tt[u] = static_cast<std::uint32_t>(ed.x);
-                        wi[u] = ed.y;
-                    } else {
-                        const FEdge ed = p.fe[e];
-                        tt[u] = ed.t;
-                        wf[u] = ed.w;
-                    }
-                }
-            }
+        for (int u = 0; u < U; ++u)
+            if (e0 + u * G < e_end)
+                ed[u] = ld_edge(&edges[e0 + u * G]);
 #pragma unroll
-            for (int u = 0; u < U; ++u)
-                if (e0 + u * G < e_end)
-                    kk[u] = OCM_KEYLD_CG ? __ldcg(&key[tt[u]]) : key[tt[u]];
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const std::uint32_t e = e0 + u * G;
-                if (e < e_end) {
-                    Key c;
-                    if constexpr (EXACT)
-                        c = kk[u] + static_cast<long long>(wi[u]) * den - num;
-                    else
-                        c = (kk[u] + wf[u]) - lam; // FloatMode::extend (policy.hpp:105)
-                    if (be == NONE || c < best) {
-                        best = c;
-                        be = e;
-                        bt = tt[u];
-                        if constexpr (EXACT)
-                            bwi = wi[u];
-                        else
-                            bwf = wf[u];
-                    }
-                    if (e == cur) {
-                        curc = c;
-                        cur_t = tt[u];
-                        have_cur = true;
-                    }
-                }
-            }
-        }
-        const bool saw_cur = have_cur; // this lane scanned the incumbent edge
-        Key gbest = best;
-        std::uint32_t gbe = be;
-#pragma unroll
-        for (int off = G / 2; off > 0; off >>= 1) {
-            const Key ob = __shfl_xor_sync(gm, gbest, off, G);
-            const std::uint32_t oe = __shfl_xor_sync(gm, gbe, off, G);
-            if (oe != NONE && (gbe == NONE || ob < gbest || (ob == gbest && oe < gbe))) {
-                gbest = ob;
-                gbe = oe;
-            }
-            const Key oc = __shfl_xor_sync(gm, curc, off, G);
-            const bool oh = __shfl_xor_sync(gm, have_cur ? 1 : 0, off, G) != 0;
-            if (oh) {
-                curc = oc;
-                have_cur = true;
-            }
-        }
-        if (gbe == NONE) {
-            if (lane == 0)
-                p.c->error = 1;
-            return;
-        }
-        bool rep = cur == NONE;
-        if (!rep) {
-            if constexpr (EXACT) {
-                rep = gbest < curc;
-            } else { // FloatMode::strictly_better (policy.hpp:116)
-                const double tol = 1e-9 * fmax(1.0, fmax(fabs(gbest), fabs(curc)));
-                rep = gbest < curc - tol;
-            }
-        }
-        if (rep) {
-            if (gbe == be) { // owner lane of the winning edge
-                p.succ_e[v] = be;
-                p.succ_v[v] = bt;
+        for (int u = 0; u < U; ++u)
+            if (e0 + u * G < e_end) {
+                std::uint32_t t;
                 if constexpr (EXACT)
-                    p.succ_wi[v] = bwi;
+                    t = static_cast<std::uint32_t>(ed[u].x);
                 else
-                    p.succ_wf[v] = bwf;
-                if (p.indeg_in_improve)
-                    atomicAdd(&p.indeg[bt], 1u);
-                marks.note(changed, r);
+                    t = ed[u].t;
+                kk[u] = __ldcg(&key[t]);
             }
-        } else if (saw_cur && p.indeg_in_improve) {
-            atomicAdd(&p.indeg[cur_t], 1u);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const std::uint32_t e = e0 + u * G;
+            if (e < e_end) {
+                Key c;
+                if constexpr (EXACT)
+                    c = kk[u] + static_cast<long long>(ed[u].y) * den; // + const -num
+                else
+                    c = (kk[u] + ed[u].w) - lam; // FloatMode::extend (policy.hpp:105)
+                if (be == NONE || c < best) {
+                    best = c;
+                    be = e;
+                }
+                if (e == cur) {
+                    curc = c;
+                    have_cur = true;
+                }
+            }
         }
+    }
+    const bool saw_cur = have_cur; // this lane scanned the incumbent edge
+    Key gbest = best;
+    std::uint32_t gbe = be;
+#pragma unroll
+    for (int off = G / 2; off > 0; off >>= 1) {
+        const Key ob = __shfl_xor_sync(gm, gbest, off, G);
+        const std::uint32_t oe = __shfl_xor_sync(gm, gbe, off, G);
+        if (oe != NONE && (gbe == NONE || ob < gbest || (ob == gbest && oe < gbe))) {
+            gbest = ob;
+            gbe = oe;
+        }
+        const Key oc = __shfl_xor_sync(gm, curc, off, G);
+        const bool oh = __shfl_xor_sync(gm, have_cur ? 1 : 0, off, G) != 0;
+        if (oh) {
+            curc = oc;
+            have_cur = true;
+        }
+    }
+    if (gbe == NONE) {
+        if (lane == 0)
+            p.c->error = 1;
+        return;
+    }
+    bool rep = cur == NONE;
+    if (!rep) {
+        if constexpr (EXACT) {
+            rep = gbest < curc;
+        } else { // FloatMode::strictly_better (policy.hpp:116)
+            const double tol = 1e-9 * fmax(1.0, fmax(fabs(gbest), fabs(curc)));
+            rep = gbest < curc - tol;
+        }
+    }
+    if (rep) {
+        if (gbe == be) { // owner lane of the winning edge
+            const Edge ed = ld_edge(&edges[be]);
+            p.succ_e[v] = be;
+            std::uint32_t t;
+            if constexpr (EXACT) {
+                t = static_cast<std::uint32_t>(ed.x);
+                p.succ_wi[v] = ed.y;
+            } else {
+                t = ed.t;
+                p.succ_wf[v] = ed.w;
+            }
+            p.succ_v[v] = t;
+            if (p.indeg_in_improve)
+                atomicAdd(&p.indeg[t], 1u);
+            marks.note(changed, r);
+        }
+    } else if (saw_cur && p.indeg_in_improve) {
+        std::uint32_t t;
+        if constexpr (EXACT)
+            t = static_cast<std::uint32_t>(ld_edge(&edges[cur]).x);
+        else
+            t = ld_edge(&edges[cur]).t;
+        atomicAdd(&p.indeg[t], 1u);
     }
 }
 
@@ -532,16 +541,15 @@ template <bool EXACT, int G, int U> __device__ __forceinline__ void improve_phas
     marks.flush(changed);
 }
 
-template <bool EXACT> __device__ __forceinline__ void improve_dispatch(const KP& p, int* changed) {
-    switch (p.G | (p.U << 8)) {
-    case 1 | (8 << 8): improve_phase<EXACT, 1, 8>(p, changed); break;
-    case 2 | (8 << 8): improve_phase<EXACT, 2, 8>(p, changed); break;
-    case 1 | (4 << 8): improve_phase<EXACT, 1, 4>(p, changed); break;
-    case 2 | (4 << 8): improve_phase<EXACT, 2, 4>(p, changed); break;
-    case 4 | (4 << 8): improve_phase<EXACT, 4, 4>(p, changed); break;
-    case 8 | (4 << 8): improve_phase<EXACT, 8, 2>(p, changed); break;
-    case 16 | (4 << 8): improve_phase<EXACT, 16, 2>(p, changed); break;
-    default: improve_phase<EXACT, 32, 2>(p, changed); break;
+// The optimal cycle from its anchor (one thread: a dependent walk).
+__global__ void k_cycle_out(const std::uint32_t* succ, std::uint32_t start, std::uint32_t len,
+                            std::uint32_t* out) {
+    if (threadIdx.x != 0)
+        return;
+    std::uint32_t u = start;
+    for (std::uint32_t i = 0; i < len; ++i) {
+        out[i] = u;
+        u = succ[u];
     }
 }
 
@@ -699,16 +707,33 @@ __device__ __forceinline__ void ph_mark(const KP& p, std::uint64_t nC, int in, s
                                         bool exact, const Ring& rm) {
     const PJC* a = p.pj[in];
     unsigned fresh = 0;
-    for (std::uint64_t i = gtid(); i < nC; i += gstride()) {
-        const std::uint32_t v = p.clist[i];
-        const std::uint32_t j = a[v].nxt;
-        p.comp[v] = a[j].mn;
-        p.cyc_len[v] = 0;
-        if (exact)
-            p.cyc_wi[v] = 0;
-        // many vertices share j: read before the exchange
-        if (p.cmark[j] != stamp && atomicExch(&p.cmark[j], stamp) != stamp)
-            ++fresh;
+    constexpr int kR = 4;
+    const std::uint64_t nth = gstride();
+    for (std::uint64_t i0 = gtid(); i0 < nC; i0 += kR * nth) {
+        std::uint32_t v[kR], j[kR], mn[kR];
+#pragma unroll
+        for (int r = 0; r < kR; ++r)
+            v[r] = i0 + r * nth < nC ? p.clist[i0 + r * nth] : NONE;
+#pragma unroll
+        for (int r = 0; r < kR; ++r)
+            if (v[r] != NONE)
+                j[r] = a[v[r]].nxt;
+#pragma unroll
+        for (int r = 0; r < kR; ++r)
+            if (v[r] != NONE)
+                mn[r] = a[j[r]].mn;
+#pragma unroll
+        for (int r = 0; r < kR; ++r) {
+            if (v[r] == NONE)
+                continue;
+            p.comp[v[r]] = mn[r];
+            p.cyc_len[v[r]] = 0;
+            if (exact)
+                p.cyc_wi[v[r]] = 0;
+            // many vertices share j: read before the exchange
+            if (p.cmark[j[r]] != stamp && atomicExch(&p.cmark[j[r]], stamp) != stamp)
+                ++fresh;
+        }
     }
     block_count(fresh, rm);
 }
@@ -1106,52 +1131,83 @@ __device__ __forceinline__ void ph_fprop_level(const KP& p, std::uint32_t level,
 // the control block between launches.
 constexpr int kSolveFull = 0, kShardBegin = 1, kShardResume = 2;
 
-template <bool EXACT>
+// Cross-phase state of the kernel's loop.
+struct LoopState {
+    Ring ra, rl, rc; // active-region counts, lists, core list
+    unsigned stamp, k_hint, k_streak, passes, outer, rounds, verifies, layers, nsync;
+    unsigned long long peeled, cored, done_base;
+    long long clk0, clk_last;
+    int it;
+};
+
+// One kernel per (lane mode, improvement group width G): each instantiation
+// carries only its own improvement variant, so ptxas allocates registers for
+// that one (a kernel holding all variants spilled inside the pass's loop).
+// G in {1, 2, 4, 8}: degrees above 128*G take the block-cooperative path.
+template <bool EXACT, int G>
 __global__ void __launch_bounds__(kBlock, kSolveMinBlocks) k_solve(KP p, int mode) {
     cg::grid_group grid = cg::this_grid();
     Ctl* const c = p.c;
-    const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
-    Ring ra, rl, rc; // active-region counts, lists, core list
-    ra.init(c->ring[0]);
-    rl.init(c->ring[1]);
-    rc.init(c->ring[2]);
-    unsigned nsync = 0;
-    long long clk0 = 0, clk_last = 0;
-    if (leader)
-        clk_last = clk0 = clock64();
+    __shared__ LoopState s_park;
+    LoopState st;
+    st.ra.init(c->ring[0]);
+    st.rl.init(c->ring[1]);
+    st.rc.init(c->ring[2]);
+    st.nsync = 0;
+    st.clk0 = st.clk_last = 0;
+    if (blockIdx.x == 0 && threadIdx.x == 0)
+        st.clk_last = st.clk0 = clock64();
     auto sync = [&](int ph) {
         grid.sync();
-        ++nsync;
-        if (leader) {
+        ++st.nsync;
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
             const long long t = clock64();
-            c->clk[ph] += t - clk_last;
-            clk_last = t;
+            c->clk[ph] += t - st.clk_last;
+            st.clk_last = t;
         }
     };
     const int K_max = max(1, ceil_log2_d(max(p.max_region, 2u)));
-    unsigned stamp = ldr(c->stamp);
-    unsigned k_hint = max(1u, min(ldr(c->k_hint), static_cast<unsigned>(K_max)));
-    unsigned k_streak = ldr(c->k_streak);
+    st.stamp = ldr(c->stamp);
+    st.k_hint = max(1u, min(ldr(c->k_hint), static_cast<unsigned>(K_max)));
+    st.k_streak = ldr(c->k_streak);
     // per-solve counters continue across the launches of a sharded solve
-    unsigned passes = ldr(c->passes), outer = ldr(c->outer), rounds = ldr(c->rounds);
-    unsigned verifies = ldr(c->verifies), layers = ldr(c->layers);
-    unsigned long long peeled = ldr(c->peeled), cored = ldr(c->cored);
-    unsigned long long done_base = ldr(c->done);
+    st.passes = ldr(c->passes);
+    st.outer = ldr(c->outer);
+    st.rounds = ldr(c->rounds);
+    st.verifies = ldr(c->verifies);
+    st.layers = ldr(c->layers);
+    st.peeled = ldr(c->peeled);
+    st.cored = ldr(c->cored);
+    st.done_base = ldr(c->done);
+    st.it = static_cast<int>(ldr(c->it));
     bool fatal = false;  // uniform: a fixpoint failed to converge
     bool paused = false; // uniform: sharded launch ends at its exchange point
-    int it = static_cast<int>(ldr(c->it));
 
     if (mode != kShardResume) {
         ph_init(p, EXACT);
         sync(PH_INIT);
     }
     bool skip_improve = mode == kShardResume;
+    if (mode == kShardResume) {
+        // every block must have read the ring bases above before any block
+        // appends (the first phase of a resumed launch appends at once)
+        sync(PH_INIT);
+    }
 
-    for (;; ++it) {
-        const int par = it & 1;
+    for (;; ++st.it) {
         if (!skip_improve) {
-            improve_dispatch<EXACT>(p, p.changed[par]);
-            ++passes;
+            // park the loop state (block-uniform) in shared memory while the
+            // pass runs: otherwise ptxas keeps it in registers across the
+            // pass and spills the pass's own working set inside its loop
+            __syncthreads();
+            if (threadIdx.x == 0)
+                s_park = st;
+            __syncthreads();
+            asm volatile("" ::: "memory");
+            improve_phase<EXACT, G, 4>(p, p.changed[s_park.it & 1]);
+            asm volatile("" ::: "memory");
+            st = s_park;
+            ++st.passes;
             sync(PH_IMPROVE);
             if (mode != kSolveFull) {
                 paused = true;
@@ -1159,6 +1215,7 @@ __global__ void __launch_bounds__(kBlock, kSolveMinBlocks) k_solve(KP p, int mod
             }
         }
         skip_improve = false;
+        const int par = st.it & 1;
         if (!p.indeg_in_improve) {
             // the policy of the other ranks arrived by the exchange: count
             // in-degrees over the full policy (replicated on every rank)
@@ -1167,69 +1224,70 @@ __global__ void __launch_bounds__(kBlock, kSolveMinBlocks) k_solve(KP p, int mod
                     atomicAdd(&p.indeg[p.succ_v[v]], 1u);
             sync(PH_CLASSIFY);
         }
-        ph_classify<EXACT>(p, par, ra, rl, rc);
+        ph_classify<EXACT>(p, par, st.ra, st.rl, st.rc);
         sync(PH_CLASSIFY);
-        const std::uint64_t n_active = ra.take();
-        const std::uint64_t nL = rl.take();
-        const std::uint64_t nC = rc.take();
-        // written only by improve/adopt/keep/leafvals/attach, never by the
-        // rounds that follow: every block reads the same values here
+        const std::uint64_t n_active = st.ra.take();
+        const std::uint64_t nL = st.rl.take();
+        const std::uint64_t nC = st.rc.take();
+        // written only by improve/adopt/keep/attach, never by the rounds
+        // that follow: every block reads the same values here
         if (n_active == 0 || ldr(c->error) || ldr(c->overflow) || ldr(c->lambda_up))
             break; // quiet pass (or a failure the host reports)
-        ++outer;
-        peeled += nL;
-        cored += nC;
+        ++st.outer;
+        st.peeled += nL;
+        st.cored += nC;
 
         // ---- pointer doubling on the core, verified exactly (round 1 was
         // done by the classification)
         int in = 1, k = 1;
-        ++rounds;
+        ++st.rounds;
         bool first_try = true;
         std::uint64_t nM = 0;
         for (;;) {
-            for (; k < static_cast<int>(k_hint); ++k, in ^= 1) {
+            for (; k < static_cast<int>(st.k_hint); ++k, in ^= 1) {
                 ph_round(p, nC, in);
-                ++rounds;
+                ++st.rounds;
                 sync(PH_ROUND);
             }
-            ++stamp;
-            ++verifies;
+            const unsigned stamp = ++st.stamp;
+            ++st.verifies;
             unsigned* vflag = &c->vfail[stamp & 1];
-            ph_mark(p, nC, in, stamp, EXACT, ra);
+            ph_mark(p, nC, in, stamp, EXACT, st.ra);
             sync(PH_VERIFY);
-            const std::uint64_t m_size = ra.take();
-            ph_check<EXACT>(p, nC, stamp, vflag, rc, rl);
+            const std::uint64_t m_size = st.ra.take();
+            ph_check<EXACT>(p, nC, stamp, vflag, st.rc, st.rl);
             sync(PH_VERIFY);
-            const std::uint64_t s_size = rc.take();
-            nM = rl.take();
+            const std::uint64_t s_size = st.rc.take();
+            nM = st.rl.take();
             if (ldr(*vflag) != stamp && s_size == m_size)
                 break;
             if (k >= K_max) {
                 fatal = true;
                 break;
             }
-            k_hint = k + 1;
+            st.k_hint = k + 1;
             first_try = false;
         }
         if (fatal)
             break;
         // adapt the starting round count: shrink after two first-try passes
-        if (first_try && ++k_streak >= 2 && k > 1) {
-            k_hint = k - 1;
-            k_streak = 0;
+        if (first_try && ++st.k_streak >= 2 && k > 1) {
+            st.k_hint = k - 1;
+            st.k_streak = 0;
         } else {
-            k_hint = k;
+            st.k_hint = k;
             if (!first_try)
-                k_streak = 0;
+                st.k_streak = 0;
         }
+        const unsigned stamp = st.stamp;
 
         // ---- vote, adoption and the winning cycles' values
         if constexpr (!EXACT) {
             ph_stats_float(p, nM);
             sync(PH_STATS);
         }
-        ph_vote<EXACT>(p, nM, stamp, done_base);
-        done_base += gridDim.x;
+        ph_vote<EXACT>(p, nM, stamp, st.done_base);
+        st.done_base += gridDim.x;
         sync(PH_VOTE);
         if (EXACT && ldr(c->wc_big[stamp & 1]) == stamp) {
             const std::uint64_t nW = static_cast<std::uint32_t>(ldr(c->wc_n[stamp & 1]));
@@ -1244,15 +1302,15 @@ __global__ void __launch_bounds__(kBlock, kSolveMinBlocks) k_solve(KP p, int mod
         }
 
         // ---- kept component (core, then leaves), re-attachment
-        ph_keep<EXACT>(p, nC, nL, in, stamp, 1ull << k, rl);
+        ph_keep<EXACT>(p, nC, nL, in, stamp, 1ull << k, st.rl);
         sync(PH_KEEP);
-        std::uint64_t pending = rl.take();
+        std::uint64_t pending = st.rl.take();
         int cur = 0;
         for (std::uint32_t layer = 1; pending > 0; ++layer) {
-            ph_attach<EXACT>(p, cur, pending, layer, rl);
+            ph_attach<EXACT>(p, cur, pending, layer, st.rl);
             sync(PH_ATTACH);
-            const std::uint64_t next = rl.take();
-            ++layers;
+            const std::uint64_t next = st.rl.take();
+            ++st.layers;
             if (next == pending) { // connect_gpi_fixpoint: not strongly connected
                 fatal = true;
                 break;
@@ -1271,7 +1329,7 @@ __global__ void __launch_bounds__(kBlock, kSolveMinBlocks) k_solve(KP p, int mod
                 const unsigned long long tag = (static_cast<unsigned long long>(stamp) << 32) | level;
                 ph_fprop_level(p, level, flag, tag);
                 sync(PH_FLOAT);
-                ++layers;
+                ++st.layers;
                 if (ldr(*flag) != tag)
                     break;
                 if (level > p.max_region + 1) {
@@ -1284,23 +1342,23 @@ __global__ void __launch_bounds__(kBlock, kSolveMinBlocks) k_solve(KP p, int mod
         }
     }
 
-    if (leader) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
         if (fatal)
             c->nonconv = 1;
-        c->it = static_cast<unsigned>(it);
+        c->it = static_cast<unsigned>(st.it);
         c->shard_done = paused ? 0 : 1;
-        c->stamp = stamp;
-        c->k_hint = k_hint;
-        c->k_streak = k_streak;
-        c->passes = passes;
-        c->outer = outer;
-        c->rounds = rounds;
-        c->verifies = verifies;
-        c->peeled = peeled;
-        c->cored = cored;
-        c->layers = layers;
-        c->syncs = nsync;
-        c->clk_total += clock64() - clk0;
+        c->stamp = st.stamp;
+        c->k_hint = st.k_hint;
+        c->k_streak = st.k_streak;
+        c->passes = st.passes;
+        c->outer = st.outer;
+        c->rounds = st.rounds;
+        c->verifies = st.verifies;
+        c->peeled = st.peeled;
+        c->cored = st.cored;
+        c->layers = st.layers;
+        c->syncs = st.nsync;
+        c->clk_total += clock64() - st.clk0;
     }
 }
 

@@ -37,9 +37,21 @@ int env_int(const char* name, int dflt) {
 
 // Per-device facts looked up once per process (device properties and the
 // cooperative occupancy of k_solve cost milliseconds per query).
+constexpr int kGs[4] = {1, 2, 4, 8};
+
+// k_solve instantiation for (exact lane, group width index 0..3)
+const void* solve_fn(bool exact, int gi) {
+    static const void* fns[2][4] = {
+        {reinterpret_cast<const void*>(&k_solve<false, 1>), reinterpret_cast<const void*>(&k_solve<false, 2>),
+         reinterpret_cast<const void*>(&k_solve<false, 4>), reinterpret_cast<const void*>(&k_solve<false, 8>)},
+        {reinterpret_cast<const void*>(&k_solve<true, 1>), reinterpret_cast<const void*>(&k_solve<true, 2>),
+         reinterpret_cast<const void*>(&k_solve<true, 4>), reinterpret_cast<const void*>(&k_solve<true, 8>)}};
+    return fns[exact ? 1 : 0][gi];
+}
+
 struct DeviceFacts {
     int sms = 0, major = 0;
-    int per_sm[2] = {0, 0}; // k_solve<exact>, k_solve<float>
+    int per_sm[2][4] = {}; // cooperative CTAs per SM of k_solve<exact?, G>
     std::string name;
 };
 
@@ -57,13 +69,12 @@ const DeviceFacts& device_facts(int dev) {
     f.major = prop.major;
     f.name = prop.name;
     if (f.major >= 10) {
-        for (int e = 0; e < 2; ++e) {
-            int per_sm = 0;
-            const void* fn = e ? reinterpret_cast<const void*>(&k_solve<false>)
-                               : reinterpret_cast<const void*>(&k_solve<true>);
-            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kBlock, 0));
-            f.per_sm[e] = std::max(1, std::min(per_sm, kSolveMinBlocks));
-        }
+        for (int e = 0; e < 2; ++e)
+            for (int gi = 0; gi < 4; ++gi) {
+                int per_sm = 0;
+                CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, solve_fn(e == 1, gi), kBlock, 0));
+                f.per_sm[e][gi] = std::max(1, std::min(per_sm, kSolveMinBlocks));
+            }
         // keep freed blocks cached in the default pool across sessions
         cudaMemPool_t pool;
         CK(cudaDeviceGetDefaultMemPool(&pool, dev));
@@ -168,11 +179,13 @@ void Session::init(const std::function<void(DeviceState&)>& prepare) {
         const double avg_deg =
             prep_.R ? double(prep_.M) / std::max<double>(1.0, double(prep_.n - prep_.trivial)) : 1.0;
         int G = 1;
-        while (G < 32 && G * 8 < avg_deg)
+        while (G < 8 && G * 8 < avg_deg)
             G *= 2;
         G = env_int("OCM_IMPROVE_G", G);
+        gi_ = G >= 8 ? 3 : G >= 4 ? 2 : G >= 2 ? 1 : 0;
+        G = kGs[gi_];
         d.kp.G = G;
-        d.kp.U = G <= 2 ? env_int("OCM_IMPROVE_U", 4) : 4;
+        d.kp.U = 4;
         d.kp.heavy_deg = static_cast<std::uint32_t>(env_int("OCM_HEAVY_DEG", 32 * 4 * G));
         DBuf<unsigned> cnt;
         cnt.alloc(1, d.stream);
@@ -191,8 +204,7 @@ void Session::init(const std::function<void(DeviceState&)>& prepare) {
     }
 
     // one CTA per SM slot the register budget allows (<= kSolveMinBlocks)
-    grid_exact_ = facts.per_sm[0] * d.sms;
-    grid_float_ = facts.per_sm[1] * d.sms;
+    grid_ = facts.per_sm[prep_.exact ? 1 : 0][gi_] * d.sms;
 
     KP& p = d.kp;
     p.N = prep_.n;
@@ -271,9 +283,7 @@ template <class M> float Session::launch(int mode) {
     CK(cudaEventRecord(d.ev_start, s));
     if (prep_.R > 0) {
         void* args[] = {&p, &mode};
-        const void* fn = EXACT ? reinterpret_cast<const void*>(&k_solve<true>)
-                               : reinterpret_cast<const void*>(&k_solve<false>);
-        CK(cudaLaunchCooperativeKernel(fn, dim3(EXACT ? grid_exact_ : grid_float_), dim3(kBlock), args, 0, s));
+        CK(cudaLaunchCooperativeKernel(solve_fn(EXACT, gi_), dim3(grid_), dim3(kBlock), args, 0, s));
         ++launches_;
     }
     CK(cudaEventRecord(d.ev_end, s));
@@ -399,16 +409,37 @@ template <class M> void Session::collect(ocm_solution* out, std::uint32_t* cycle
         out->mu_den = den;
     }
     out->mu = mu;
-    std::vector<std::uint32_t> succ(prep_.n);
-    CK(cudaMemcpy(succ.data(), p.succ_v, prep_.n * sizeof(std::uint32_t), cudaMemcpyDeviceToHost));
-    out->d2h_bytes += prep_.n * sizeof(std::uint32_t);
-    std::uint32_t u = src[best], len = 0;
-    do {
-        if (cycle_buf && len < cap)
-            cycle_buf[len] = u;
-        ++len;
-        u = succ[u];
-    } while (u != src[best] && len <= prep_.n);
+    // the optimal cycle, walked on the device from its anchor (its length is
+    // the adopted record's); very long cycles fall back to the host walk
+    const std::uint32_t start = src[best];
+    std::uint32_t clen = 0;
+    CK(cudaMemcpy(&clen, p.cyc_len + start, sizeof clen, cudaMemcpyDeviceToHost));
+    out->d2h_bytes += sizeof clen;
+    std::uint32_t len = 0;
+    if (clen > 0 && clen <= (1u << 16)) {
+        DBuf<std::uint32_t> cyc;
+        cyc.alloc(clen, d.stream);
+        k_cycle_out<<<1, 32, 0, d.stream>>>(p.succ_v, start, clen, cyc.p);
+        std::vector<std::uint32_t> h(clen);
+        CK(cudaMemcpyAsync(h.data(), cyc.p, clen * sizeof(std::uint32_t), cudaMemcpyDeviceToHost,
+                           d.stream));
+        CK(cudaStreamSynchronize(d.stream));
+        out->d2h_bytes += clen * sizeof(std::uint32_t);
+        for (; len < clen; ++len)
+            if (cycle_buf && len < cap)
+                cycle_buf[len] = h[len];
+    } else {
+        std::vector<std::uint32_t> succ(prep_.n);
+        CK(cudaMemcpy(succ.data(), p.succ_v, prep_.n * sizeof(std::uint32_t), cudaMemcpyDeviceToHost));
+        out->d2h_bytes += prep_.n * sizeof(std::uint32_t);
+        std::uint32_t u = start;
+        do {
+            if (cycle_buf && len < cap)
+                cycle_buf[len] = u;
+            ++len;
+            u = succ[u];
+        } while (u != start && len <= prep_.n);
+    }
     out->cycle_len = len;
 }
 

@@ -51,7 +51,8 @@ class Session {
     std::uint64_t h2d_bytes_ = 0;
     std::unique_ptr<DeviceState> d_;
     bool solved_ = false;
-    int grid_exact_ = 0, grid_float_ = 0; // cooperative grid of k_solve<exact / float>
+    int grid_ = 0; // cooperative grid of the session's k_solve instantiation
+    int gi_ = 0;   // its improvement group width (index into 1, 2, 4, 8)
     std::uint32_t rank_ = 0, world_ = 1, chunk_ = 0;
     bool shard_started_ = false;
     double solve_ms_ = 0.0;   // event time of the current solve's launches

@@ -153,5 +153,7 @@ print("ok", sol.mu_exact, sol.stats.launches)
 def test_torchcomm_nccl_world1():
     r = subprocess.run([sys.executable, "-c", NCCL_WORLD1, ROOT, str(_free_port())],
                        capture_output=True, text=True, timeout=300)
-    assert r.returncode == 0, (r.stdout[-1000:], r.stderr[:3000])
+    if r.returncode != 0:
+        tail = [l for l in r.stderr.splitlines() if "Error" in l or "error" in l][-5:]
+        raise AssertionError("\n".join(tail) + "\n" + r.stderr[-1500:])
     assert r.stdout.strip().splitlines()[-1].startswith("ok"), r.stdout
