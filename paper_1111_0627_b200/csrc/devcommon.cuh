@@ -201,7 +201,16 @@ struct DeviceState {
     Ctl* h_ctl = nullptr;
     std::vector<cudaEvent_t> ev;
     cudaEvent_t ev_start = nullptr, ev_end = nullptr;
+    cudaStream_t side = nullptr;      // weight upload overlapping the region split
+    cudaEvent_t side_done = nullptr;
+    cudaEvent_t alloc_done = nullptr; // orders side-stream use after allocations on `stream`
     KP kp{};
+    cudaEvent_t ev_alloc_done(cudaStream_t s) {
+        if (!alloc_done)
+            CK(cudaEventCreateWithFlags(&alloc_done, cudaEventDisableTiming));
+        CK(cudaEventRecord(alloc_done, s));
+        return alloc_done;
+    }
 
     ~DeviceState() {
         if (stream)
@@ -233,6 +242,14 @@ struct DeviceState {
             cudaStreamSynchronize(stream);
         for (cudaEvent_t e : ev)
             cudaEventDestroy(e);
+        if (side) {
+            cudaStreamSynchronize(side);
+            cudaStreamDestroy(side);
+        }
+        if (side_done)
+            cudaEventDestroy(side_done);
+        if (alloc_done)
+            cudaEventDestroy(alloc_done);
         if (ev_start)
             cudaEventDestroy(ev_start);
         if (ev_end)

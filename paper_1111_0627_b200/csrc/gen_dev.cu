@@ -14,7 +14,8 @@ namespace ocmb {
 
 void device_prepare_csr(std::uint32_t n, std::uint64_t m, DBuf<std::uint32_t>& row,
                         DBuf<std::uint32_t>& tgt, DBuf<double>& w, bool integer_exact,
-                        const ocm_solve_options& opt, DeviceState& d, PrepInfo& info);
+                        const ocm_solve_options& opt, DeviceState& d, PrepInfo& info,
+                        cudaEvent_t w_ready = nullptr);
 
 namespace {
 

@@ -16,6 +16,7 @@
 // Vertices keep their original ids; trivial vertices get region R (never
 // active) and empty intra-region edge lists.
 
+#include <cooperative_groups.h>
 #include <cub/cub.cuh>
 
 #include <algorithm>
@@ -27,6 +28,7 @@
 #include <vector>
 
 #include "../../include/ocm_b200.h"
+#include "coop.cuh"
 #include "devcommon.cuh"
 #include "graph.hpp"
 
@@ -35,7 +37,8 @@ namespace ocmb {
 void device_prepare(const Graph& g, const ocm_solve_options& opt, DeviceState& d, PrepInfo& info);
 void device_prepare_csr(std::uint32_t n, std::uint64_t m, DBuf<std::uint32_t>& row,
                         DBuf<std::uint32_t>& tgt, DBuf<double>& w, bool integer_exact,
-                        const ocm_solve_options& opt, DeviceState& d, PrepInfo& info);
+                        const ocm_solve_options& opt, DeviceState& d, PrepInfo& info,
+                        cudaEvent_t w_ready = nullptr);
 
 namespace {
 
@@ -89,6 +92,7 @@ struct PrepCounters {
     unsigned max_region;
     unsigned regions_total;
     unsigned R;
+    unsigned long long bfs_ring[2]; // cumulative frontier appends (kp_bfs_coop)
 };
 
 __global__ void kp_row32(const std::uint64_t* r64, std::uint32_t* r32, std::size_t n1) {
@@ -97,19 +101,25 @@ __global__ void kp_row32(const std::uint64_t* r64, std::uint32_t* r32, std::size
 }
 
 // Out-degree / in-degree without self-loops, self-loop flags, max |w|.
-__global__ void kp_degrees(std::uint32_t n, const std::uint32_t* row, const std::uint32_t* tgt,
-                           const double* w, std::uint32_t* outd, std::uint32_t* ind,
-                           std::uint8_t* self, PrepCounters* pc) {
+// max |w| over all edges (as double bits: non-negative doubles order like
+// their bit patterns).
+__global__ void kp_max_abs(std::uint64_t m, const double* w, PrepCounters* pc) {
     unsigned long long mx = 0;
+    for (std::uint64_t e = tid_(); e < m; e += stride_()) {
+        const unsigned long long bits = __double_as_longlong(fabs(w[e]));
+        mx = bits > mx ? bits : mx;
+    }
+    warp_atomic_max(&pc->max_abs_bits, mx);
+}
+
+__global__ void kp_degrees(std::uint32_t n, const std::uint32_t* row, const std::uint32_t* tgt,
+                           std::uint32_t* outd, std::uint32_t* ind, std::uint8_t* self) {
     for (std::size_t vv = tid_(); vv < n; vv += stride_()) {
         const std::uint32_t v = static_cast<std::uint32_t>(vv);
         std::uint32_t o = 0;
         std::uint8_t s = 0;
         for (std::uint32_t e = row[v]; e < row[v + 1]; ++e) {
             const std::uint32_t t = tgt[e];
-            const double a = fabs(w[e]);
-            const unsigned long long bits = __double_as_longlong(a);
-            mx = bits > mx ? bits : mx;
             if (t == v) {
                 s = 1;
             } else {
@@ -120,7 +130,6 @@ __global__ void kp_degrees(std::uint32_t n, const std::uint32_t* row, const std:
         outd[v] = o;
         self[v] = s;
     }
-    warp_atomic_max(&pc->max_abs_bits, mx);
 }
 
 // Backward CSR (no self-loops): bsrc grouped by target.
@@ -219,20 +228,52 @@ __global__ void kp_pick_pivot(std::uint32_t n, const std::uint32_t* lab, const s
     warp_atomic_max(&pc->pivot, best);
 }
 
-// One BFS level restricted to unassigned vertices; vis[] holds the stamp.
-__global__ void kp_bfs_level(const std::uint32_t* row, const std::uint32_t* col,
-                             const std::uint32_t* lab, std::uint32_t* vis, std::uint32_t stamp,
-                             const std::uint32_t* qin, unsigned nin, std::uint32_t* qout,
-                             unsigned* qout_count) {
-    for (std::size_t i = tid_(); i < nin; i += stride_()) {
-        const std::uint32_t u = qin[i];
-        for (std::uint32_t e = row[u]; e < row[u + 1]; ++e) {
-            const std::uint32_t t = col[e];
-            if (lab[t] != NONE || vis[t] == stamp)
-                continue;
-            if (atomicExch(&vis[t], stamp) != stamp)
-                qout[atomicAdd(qout_count, 1u)] = t;
+// Warp-aggregated append of the calling (active) lanes: one atomic per warp.
+__device__ __forceinline__ std::uint64_t warp_append(const Ring& ring) {
+    const unsigned m = __activemask();
+    const int leader = __ffs(m) - 1;
+    const unsigned lane = threadIdx.x & 31;
+    unsigned long long base = 0;
+    if (static_cast<int>(lane) == leader)
+        base = atomicAdd(ring.counter(), static_cast<unsigned long long>(__popc(m))) - ring.origin();
+    base = __shfl_sync(m, base, leader);
+    return base + __popc(m & ((1u << lane) - 1u));
+}
+
+// A whole BFS (restricted to unassigned vertices, vis[] holding the stamp)
+// in one cooperative launch: a grid barrier per level instead of a launch
+// and a host round trip per level.
+__global__ void __launch_bounds__(kBlock) kp_bfs_coop(const std::uint32_t* row, const std::uint32_t* col,
+                                                      const std::uint32_t* lab, std::uint32_t* vis,
+                                                      std::uint32_t stamp, std::uint32_t start,
+                                                      std::uint32_t* q0, std::uint32_t* q1,
+                                                      unsigned long long* ring_ctr) {
+    cooperative_groups::grid_group grid = cooperative_groups::this_grid();
+    Ring ring;
+    ring.init(ring_ctr);
+    if (gtid() == 0) {
+        q0[0] = start;
+        vis[start] = stamp;
+    }
+    grid.sync(); // the seed is visible and every CTA has read the ring bases
+    std::uint64_t nin = 1;
+    int cur = 0;
+    while (nin) {
+        const std::uint32_t* qin = cur ? q1 : q0;
+        std::uint32_t* qout = cur ? q0 : q1;
+        for (std::uint64_t i = gtid(); i < nin; i += gstride()) {
+            const std::uint32_t u = qin[i];
+            for (std::uint32_t e = row[u]; e < row[u + 1]; ++e) {
+                const std::uint32_t t = col[e];
+                if (lab[t] != NONE || vis[t] == stamp)
+                    continue;
+                if (atomicExch(&vis[t], stamp) != stamp)
+                    qout[warp_append(ring)] = t;
+            }
         }
+        grid.sync();
+        nin = ring.take();
+        cur ^= 1;
     }
 }
 
@@ -459,9 +500,28 @@ void device_prepare(const Graph& g, const ocm_solve_options& opt, DeviceState& d
     tgt.alloc(std::max<std::uint64_t>(m, 1), s);
     w.alloc(std::max<std::uint64_t>(m, 1), s);
     CK(cudaMemcpyAsync(row64.p, g.fwd_index.data(), (std::size_t(n) + 1) * 8, cudaMemcpyHostToDevice, s));
+    // the weights (2/3 of the bytes) are first needed by the packing at the
+    // end of the region split: they stream in on a side stream meanwhile
+    cudaEvent_t w_ready = nullptr;
+    // declared after w: on any exit (incl. exceptions) the side-stream copy
+    // finishes before w's stream-ordered free
+    struct SideGuard {
+        DeviceState& d;
+        ~SideGuard() {
+            if (d.side)
+                cudaStreamSynchronize(d.side);
+        }
+    } side_guard{d};
     if (m) {
         CK(cudaMemcpyAsync(tgt.p, g.fwd_target.data(), m * 4, cudaMemcpyHostToDevice, s));
-        CK(cudaMemcpyAsync(w.p, g.fwd_weight.data(), m * 8, cudaMemcpyHostToDevice, s));
+        if (!d.side) {
+            CK(cudaStreamCreateWithFlags(&d.side, cudaStreamNonBlocking));
+            CK(cudaEventCreateWithFlags(&d.side_done, cudaEventDisableTiming));
+        }
+        CK(cudaStreamWaitEvent(d.side, d.ev_alloc_done(s), 0)); // w allocated on s
+        CK(cudaMemcpyAsync(w.p, g.fwd_weight.data(), m * 8, cudaMemcpyHostToDevice, d.side));
+        CK(cudaEventRecord(d.side_done, d.side));
+        w_ready = d.side_done;
     }
     kp_row32<<<grid_for(n + 1, d.sms), kBlock, 0, s>>>(row64.p, row.p, std::size_t(n) + 1);
     row64.release();
@@ -471,13 +531,14 @@ void device_prepare(const Graph& g, const ocm_solve_options& opt, DeviceState& d
         std::fprintf(stderr, "{\"upload_wait_ms\": %.3f}\n",
                      std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
     }
-    device_prepare_csr(n, m, row, tgt, w, g.integer_exact, opt, d, info);
+    device_prepare_csr(n, m, row, tgt, w, g.integer_exact, opt, d, info, w_ready);
     info.h2d_bytes = (std::size_t(n) + 1) * 8 + m * 12;
 }
 
 void device_prepare_csr(std::uint32_t n, std::uint64_t m, DBuf<std::uint32_t>& row,
                         DBuf<std::uint32_t>& tgt, DBuf<double>& w, bool integer_exact,
-                        const ocm_solve_options& opt, DeviceState& d, PrepInfo& info) {
+                        const ocm_solve_options& opt, DeviceState& d, PrepInfo& info,
+                        cudaEvent_t w_ready) {
     cudaStream_t s = d.stream;
     const int sms = d.sms;
     info.n = n;
@@ -497,23 +558,33 @@ void device_prepare_csr(std::uint32_t n, std::uint64_t m, DBuf<std::uint32_t>& r
     ind.alloc(std::max<std::uint32_t>(n, 1), s);
     self.alloc(std::max<std::uint32_t>(n, 1), s);
     CK(cudaMemsetAsync(ind.p, 0, std::size_t(n) * 4, s));
-    kp_degrees<<<gv, kBlock, 0, s>>>(n, row.p, tgt.p, w.p, outd.p, ind.p, self.p, pcd.p);
+    kp_degrees<<<gv, kBlock, 0, s>>>(n, row.p, tgt.p, outd.p, ind.p, self.p);
     auto read_pc = [&] {
         CK(cudaMemcpyAsync(&pc, pcd.p, sizeof pc, cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
     };
-    read_pc();
-    double max_abs;
-    {
+    // weights: wait for their upload only where they are first read
+    bool have_max_abs = false;
+    double max_abs = 0.0;
+    auto need_weights = [&] {
+        if (have_max_abs)
+            return;
+        if (w_ready)
+            CK(cudaStreamWaitEvent(s, w_ready, 0));
+        if (m)
+            kp_max_abs<<<grid_for(m, sms, 16), kBlock, 0, s>>>(m, w.p, pcd.p);
+        read_pc();
         unsigned long long bits = pc.max_abs_bits;
         std::memcpy(&max_abs, &bits, sizeof max_abs);
-    }
+        have_max_abs = true;
+    };
 
     d.reg.alloc(std::max<std::uint32_t>(n, 1), s);
     d.row.alloc(std::size_t(n) + 1 + (info.scc_off ? 0 : 0), s);
 
     if (info.scc_off) {
         // ---- single region: the Hamiltonian-augmented graph (solve.cpp:53)
+        need_weights();
         const double big_w = 2.0 * double(n) * (max_abs + 1.0) + 1.0;
         if (!std::isfinite(big_w) || big_w >= 9007199254740992.0)
             throw std::overflow_error("hamiltonian weight too large to stay exact");
@@ -598,21 +669,20 @@ void device_prepare_csr(std::uint32_t n, std::uint64_t m, DBuf<std::uint32_t>& r
         read_pc();
         return pc.remaining;
     };
+    static int bfs_per_sm = 0; // cooperative occupancy of kp_bfs_coop (same on every device here)
+    if (!bfs_per_sm) {
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bfs_per_sm, kp_bfs_coop, kBlock, 0));
+        bfs_per_sm = std::max(1, std::min(bfs_per_sm, 8));
+    }
     auto bfs = [&](const std::uint32_t* r, const std::uint32_t* c, std::uint32_t* vis,
                    std::uint32_t st, std::uint32_t start) {
-        CK(cudaMemcpyAsync(q0.p, &start, 4, cudaMemcpyHostToDevice, s));
-        CK(cudaMemcpyAsync(vis + start, &st, 4, cudaMemcpyHostToDevice, s));
-        unsigned cnt = 1;
-        int cur = 0;
-        while (cnt) {
-            CK(cudaMemsetAsync(&pcd.p->q[cur ^ 1], 0, 4, s));
-            kp_bfs_level<<<grid_for(cnt, sms), kBlock, 0, s>>>(r, c, lab.p, vis, st, qs[cur]->p,
-                                                               cnt, qs[cur ^ 1]->p,
-                                                               &pcd.p->q[cur ^ 1]);
-            read_pc();
-            cnt = pc.q[cur ^ 1];
-            cur ^= 1;
-        }
+        const std::uint32_t* lp = lab.p;
+        std::uint32_t* a0 = q0.p;
+        std::uint32_t* a1 = q1.p;
+        unsigned long long* rc = pcd.p->bfs_ring;
+        void* args[] = {&r, &c, &lp, &vis, &st, &start, &a0, &a1, &rc};
+        CK(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(&kp_bfs_coop),
+                                       dim3(bfs_per_sm * sms), dim3(kBlock), args, 0, s));
     };
 
     trim();
@@ -689,6 +759,7 @@ void device_prepare_csr(std::uint32_t n, std::uint64_t m, DBuf<std::uint32_t>& r
         d.ew.alloc(std::max<std::uint32_t>(M, 1), s);
     else
         d.fe.alloc(std::max<std::uint32_t>(M, 1), s);
+    need_weights();
     CK(cudaMemsetAsync(&pcd.p->bad_weight, 0, 4, s));
     if (info.exact)
         kp_pack<true><<<gv, kBlock, 0, s>>>(n, R, row.p, tgt.p, w.p, d.reg.p, d.row.p, sign, d.ew.p,
