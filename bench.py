@@ -159,7 +159,7 @@ def gather_peak(n):
     (>= 1 GB); linear in between is not claimed, so 256 MB-class arrays use
     the measured 70 G/s point."""
     b = 8 * n
-    if b <= (64 << 20):
+    if b <= (126 << 20):  # fits the 126 MB L2 (measured at 8-64 MB)
         return 2.1e11, "measured: L2-resident random gather, 8 MB-64 MB arrays"
     if b <= (256 << 20):
         return 7.0e10, "measured: random gather, 256 MB array"
@@ -223,9 +223,10 @@ def cpu_sample(a, P, steps=1):
     return {"value": edges / (tot_ms / 1e3), "unit": UNIT, "cores": 1,
             "kind": "reference" if use_ref else "port",
             "sample": f"{what} (same generator), min+max, reference lane 'howard' "
-                      f"(proj/src/solve.cpp run_howard_seq, single thread; the default CLI lane and "
-                      f"the fastest reference lane on these workloads), {steps} step(s), solve time "
-                      f"only",
+                      f"(proj/src/solve.cpp run_howard_seq, single thread: the default CLI lane and "
+                      f"the fastest reference lane on these workloads -- its multi-threaded "
+                      f"howard-par lane measured 3.2x slower with 16 workers at n=10^5), "
+                      f"{steps} step(s), solve time only",
             "ms": tot_ms}
 
 

@@ -151,6 +151,18 @@ __device__ __forceinline__ void block_append2(bool ta, const Ring& ra, std::uint
     __syncthreads();
 }
 
+// Warp-aggregated append of the calling (active) lanes: one atomic per warp.
+__device__ __forceinline__ std::uint64_t warp_append(const Ring& ring) {
+    const unsigned m = __activemask();
+    const int leader = __ffs(m) - 1;
+    const unsigned lane = threadIdx.x & 31;
+    unsigned long long base = 0;
+    if (static_cast<int>(lane) == leader)
+        base = atomicAdd(ring.counter(), static_cast<unsigned long long>(__popc(m))) - ring.origin();
+    base = __shfl_sync(m, base, leader);
+    return base + __popc(m & ((1u << lane) - 1u));
+}
+
 // Block-reduced count added to the ring's current counter.
 __device__ __forceinline__ void block_count(unsigned mine, const Ring& ring) {
     __shared__ unsigned s_sum;

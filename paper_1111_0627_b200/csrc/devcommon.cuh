@@ -25,7 +25,6 @@ namespace ocmb {
 constexpr std::uint32_t NONE = 0xffffffffu;
 constexpr unsigned long long EMPTY = ~0ull;
 constexpr unsigned FULL = 0xffffffffu;
-constexpr int kMaxRounds = 64;
 constexpr int kBlock = 256;
 
 struct __align__(16) FEdge {

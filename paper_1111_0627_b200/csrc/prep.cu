@@ -228,18 +228,6 @@ __global__ void kp_pick_pivot(std::uint32_t n, const std::uint32_t* lab, const s
     warp_atomic_max(&pc->pivot, best);
 }
 
-// Warp-aggregated append of the calling (active) lanes: one atomic per warp.
-__device__ __forceinline__ std::uint64_t warp_append(const Ring& ring) {
-    const unsigned m = __activemask();
-    const int leader = __ffs(m) - 1;
-    const unsigned lane = threadIdx.x & 31;
-    unsigned long long base = 0;
-    if (static_cast<int>(lane) == leader)
-        base = atomicAdd(ring.counter(), static_cast<unsigned long long>(__popc(m))) - ring.origin();
-    base = __shfl_sync(m, base, leader);
-    return base + __popc(m & ((1u << lane) - 1u));
-}
-
 // A whole BFS (restricted to unassigned vertices, vis[] holding the stamp)
 // in one cooperative launch: a grid barrier per level instead of a launch
 // and a host round trip per level.

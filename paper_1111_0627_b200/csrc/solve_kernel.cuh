@@ -50,9 +50,6 @@ namespace {
 
 namespace cg = cooperative_groups;
 
-#ifndef OCM_KEYLD_CG
-#define OCM_KEYLD_CG 1 // improvement key gathers: 1 = L2 only (ld.cg), 0 = L1-cached
-#endif
 #ifndef OCM_MINB
 #define OCM_MINB 4
 #endif
@@ -561,9 +558,8 @@ __device__ __forceinline__ void ph_round(const KP& p, std::uint64_t nC, int in) 
 // cycle vertices, if it passes) and, in exact mode, already accumulates the
 // per-anchor (length, weight) records (howard_par.hpp:319), cleared here.
 __device__ __forceinline__ void ph_mark(const KP& p, std::uint64_t nC, int in, std::uint32_t stamp,
-                                        bool exact, const Ring& rm) {
+                                        bool exact, const Ring& rl) {
     const PJC* a = p.pj[in];
-    unsigned fresh = 0;
     constexpr int kR = 4;
     const std::uint64_t nth = gstride();
     for (std::uint64_t i0 = gtid(); i0 < nC; i0 += kR * nth) {
@@ -587,29 +583,29 @@ __device__ __forceinline__ void ph_mark(const KP& p, std::uint64_t nC, int in, s
             p.cyc_len[v[r]] = 0;
             if (exact)
                 p.cyc_wi[v[r]] = 0;
-            // many vertices share j: read before the exchange
+            // many vertices share j: read before the exchange; the first
+            // marker lists j, so M is enumerated without another full pass
             if (p.cmark[j[r]] != stamp && atomicExch(&p.cmark[j[r]], stamp) != stamp)
-                ++fresh;
+                p.wlist[warp_append(rl)] = j[r];
         }
     }
-    block_count(fresh, rm);
 }
 
+// Over the listed M only: (B) and |succ(M)|, and -- speculatively, exact
+// lane -- the per-anchor (length, weight) records (howard_par.hpp:319).
 template <bool EXACT>
-__device__ __forceinline__ void ph_check(const KP& p, std::uint64_t nC, std::uint32_t stamp,
-                                         unsigned* flag, const Ring& rs, const Ring& rl) {
+__device__ __forceinline__ void ph_check(const KP& p, std::uint64_t nM, std::uint32_t stamp,
+                                         unsigned* flag, const Ring& rs) {
     bool fail = false;
     unsigned fresh = 0;
     const unsigned lane = threadIdx.x & 31;
-    OCM_BLOCK_LOOP(i0, 0, nC) {
-        const std::uint64_t i = i0_b + threadIdx.x;
+    const std::uint64_t wid = gtid() >> 5, ws = gstride() >> 5;
+    for (std::uint64_t base = wid * 32; base < nM; base += ws * 32) {
+        const std::uint64_t i = base + lane;
+        const bool on = i < nM;
         std::uint32_t v = 0, a = 0;
-        bool on = false;
-        if (i < nC) {
-            v = p.clist[i];
-            on = p.cmark[v] == stamp;
-        }
         if (on) {
+            v = p.wlist[i];
             const std::uint32_t s = p.succ_v[v];
             a = p.comp[v];
             fail |= p.comp[s] != a;
@@ -620,30 +616,25 @@ __device__ __forceinline__ void ph_check(const KP& p, std::uint64_t nC, std::uin
             // integer segmented reduction; a warp whose cycle vertices share
             // one anchor pre-reduces to one atomic pair
             const unsigned am = __ballot_sync(FULL, on);
-            if (am) {
-                const int lead = __ffs(am) - 1;
-                const std::uint32_t a0 = __shfl_sync(FULL, a, lead);
-                const bool uni = __all_sync(FULL, !on || a == a0);
-                long long w = on ? static_cast<long long>(p.succ_wi[v]) : 0ll;
-                if (uni) {
+            const int lead = __ffs(am) - 1;
+            const std::uint32_t a0 = __shfl_sync(FULL, a, lead);
+            const bool uni = __all_sync(FULL, !on || a == a0);
+            long long w = on ? static_cast<long long>(p.succ_wi[v]) : 0ll;
+            if (uni) {
 #pragma unroll
-                    for (int off = 16; off > 0; off >>= 1)
-                        w += __shfl_xor_sync(FULL, w, off);
-                    if (static_cast<int>(lane) == lead) {
-                        atomicAdd(&p.cyc_len[a0], static_cast<unsigned>(__popc(am)));
-                        atomicAdd(reinterpret_cast<unsigned long long*>(&p.cyc_wi[a0]),
-                                  static_cast<unsigned long long>(w));
-                    }
-                } else if (on) {
-                    atomicAdd(&p.cyc_len[a], 1u);
-                    atomicAdd(reinterpret_cast<unsigned long long*>(&p.cyc_wi[a]),
+                for (int off = 16; off > 0; off >>= 1)
+                    w += __shfl_xor_sync(FULL, w, off);
+                if (static_cast<int>(lane) == lead) {
+                    atomicAdd(&p.cyc_len[a0], static_cast<unsigned>(__popc(am)));
+                    atomicAdd(reinterpret_cast<unsigned long long*>(&p.cyc_wi[a0]),
                               static_cast<unsigned long long>(w));
                 }
+            } else if (on) {
+                atomicAdd(&p.cyc_len[a], 1u);
+                atomicAdd(reinterpret_cast<unsigned long long*>(&p.cyc_wi[a]),
+                          static_cast<unsigned long long>(w));
             }
         }
-        const std::uint64_t slot = block_append(on, rl);
-        if (on)
-            p.wlist[slot] = v;
     }
     block_flag(fail, flag, stamp);
     block_count(fresh, rs);
@@ -1109,14 +1100,13 @@ __global__ void __launch_bounds__(kBlock, kSolveMinBlocks) k_solve(KP p, int mod
             const unsigned stamp = ++st.stamp;
             ++st.verifies;
             unsigned* vflag = &c->vfail[stamp & 1];
-            ph_mark(p, nC, in, stamp, EXACT, st.ra);
+            ph_mark(p, nC, in, stamp, EXACT, st.rl);
             sync(PH_VERIFY);
-            const std::uint64_t m_size = st.ra.take();
-            ph_check<EXACT>(p, nC, stamp, vflag, st.rc, st.rl);
+            nM = st.rl.take(); // |M|, listed in wlist
+            ph_check<EXACT>(p, nM, stamp, vflag, st.rc);
             sync(PH_VERIFY);
             const std::uint64_t s_size = st.rc.take();
-            nM = st.rl.take();
-            if (ldr(*vflag) != stamp && s_size == m_size)
+            if (ldr(*vflag) != stamp && s_size == nM)
                 break;
             if (k >= K_max) {
                 fatal = true;
