@@ -150,20 +150,21 @@ __device__ __forceinline__ void improve_vertex(const KP& p, int* changed, Change
     for (std::uint32_t e0 = b + lane; e0 < e_end; e0 += G * U) {
         Edge ed[U];
         Key kk[U];
+        // unconditional loads at a clamped edge id (always a valid edge of
+        // v; the tail is masked below): predicated array writes would send
+        // ed[]/kk[] to local memory
 #pragma unroll
         for (int u = 0; u < U; ++u)
-            if (e0 + u * G < e_end)
-                ed[u] = ld_edge(&edges[e0 + u * G]);
+            ed[u] = ld_edge(&edges[min(e0 + u * G, e_end - 1)]);
 #pragma unroll
-        for (int u = 0; u < U; ++u)
-            if (e0 + u * G < e_end) {
-                std::uint32_t t;
-                if constexpr (EXACT)
-                    t = static_cast<std::uint32_t>(ed[u].x);
-                else
-                    t = ed[u].t;
-                kk[u] = __ldcg(&key[t]);
-            }
+        for (int u = 0; u < U; ++u) {
+            std::uint32_t t;
+            if constexpr (EXACT)
+                t = static_cast<std::uint32_t>(ed[u].x);
+            else
+                t = ed[u].t;
+            kk[u] = __ldcg(&key[t]);
+        }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const std::uint32_t e = e0 + u * G;
@@ -284,23 +285,20 @@ __device__ __forceinline__ void improve_heavy(const KP& p, int* changed) {
             double wf[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-                const std::uint32_t e = e0 + u * kBlock;
-                if (e < e_end) {
-                    if constexpr (EXACT) {
-                        const int2 ed = __ldg(&p.ew[e]);
-                        tt[u] = static_cast<std::uint32_t>(ed.x);
-                        wi[u] = ed.y;
-                    } else {
-                        const FEdge ed = p.fe[e];
-                        tt[u] = ed.t;
-                        wf[u] = ed.w;
-                    }
+                const std::uint32_t e = min(e0 + u * kBlock, e_end - 1); // tail masked below
+                if constexpr (EXACT) {
+                    const int2 ed = __ldg(&p.ew[e]);
+                    tt[u] = static_cast<std::uint32_t>(ed.x);
+                    wi[u] = ed.y;
+                } else {
+                    const FEdge ed = ld_edge(&p.fe[e]);
+                    tt[u] = ed.t;
+                    wf[u] = ed.w;
                 }
             }
 #pragma unroll
             for (int u = 0; u < 4; ++u)
-                if (e0 + u * kBlock < e_end)
-                    kk[u] = __ldcg(&key[tt[u]]);
+                kk[u] = __ldcg(&key[tt[u]]);
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 const std::uint32_t e = e0 + u * kBlock;
@@ -734,6 +732,57 @@ __device__ __forceinline__ void wc_final(const KP& p, const std::uint32_t* list,
     }
 }
 
+// Winning cycles of up to kSmemCycle vertices (listed in rem[1]) by one CTA
+// entirely in shared memory: vertices get local slots through a small
+// open-addressing table, then the prefix sums cut at each anchor run as
+// ceil(log2(len-1)) pointer-jumping rounds over shared arrays.
+constexpr unsigned kSmemCycle = 512;
+
+__device__ __forceinline__ void wincyc_shared(const KP& p, unsigned nW, int wr) {
+    __shared__ std::uint32_t s_key[2 * kSmemCycle], s_val[2 * kSmemCycle];
+    __shared__ std::uint32_t s_nxt[2][kSmemCycle];
+    __shared__ long long s_acc[2][kSmemCycle];
+    constexpr unsigned kMask = 2 * kSmemCycle - 1;
+    for (unsigned i = threadIdx.x; i < 2 * kSmemCycle; i += blockDim.x)
+        s_key[i] = NONE;
+    __syncthreads();
+    for (unsigned i = threadIdx.x; i < nW; i += blockDim.x) {
+        const std::uint32_t v = p.rem[1][i];
+        unsigned h = (v * 2654435761u) & kMask;
+        while (atomicCAS(&s_key[h], NONE, v) != NONE)
+            h = (h + 1) & kMask;
+        s_val[h] = i;
+    }
+    __syncthreads();
+    for (unsigned i = threadIdx.x; i < nW; i += blockDim.x) {
+        const std::uint32_t v = p.rem[1][i];
+        const std::uint32_t r = p.R == 1 ? 0u : __ldg(&p.reg[v]);
+        if (v == p.src[r]) {
+            s_acc[0][i] = 0;
+            s_nxt[0][i] = i;
+        } else {
+            s_acc[0][i] = static_cast<long long>(p.succ_wi[v]) * p.lam_den[r] - p.lam_num[r];
+            const std::uint32_t sv = p.succ_v[v];
+            unsigned h = (sv * 2654435761u) & kMask;
+            while (s_key[h] != sv)
+                h = (h + 1) & kMask;
+            s_nxt[0][i] = s_val[h];
+        }
+    }
+    __syncthreads();
+    for (int j = 0; j < wr; ++j) {
+        const int a = j & 1, o = a ^ 1;
+        for (unsigned i = threadIdx.x; i < nW; i += blockDim.x) {
+            const std::uint32_t x = s_nxt[a][i];
+            s_acc[o][i] = s_acc[a][i] + s_acc[a][x];
+            s_nxt[o][i] = s_nxt[a][x];
+        }
+        __syncthreads();
+    }
+    for (unsigned i = threadIdx.x; i < nW; i += blockDim.x)
+        p.key_i[p.rem[1][i]] = s_acc[wr & 1][i];
+}
+
 // Region-specific minimum voting (howard_par.hpp:56 vote_min; paper
 // Alg. 5: a holder is replaced only by a strictly smaller (mean, anchor)),
 // over the anchors among the nM cycle vertices in wlist. The last block to
@@ -784,14 +833,21 @@ __device__ __forceinline__ void ph_vote(const KP& p, std::uint64_t nM, std::uint
     // winning-cycle vertices among the cycle vertices (compacted in rem[1])
     for (std::uint64_t i = threadIdx.x; i < nM; i += blockDim.x) {
         const std::uint32_t v = p.wlist[i];
-        const std::uint32_t r = __ldg(&p.reg[v]);
-        if (p.comp[v] == p.src[r]) {
+        const std::uint32_t r = p.R == 1 ? 0u : __ldg(&p.reg[v]);
+        if (p.comp[v] == p.src[r])
             p.rem[1][atomicAdd(&s_nw, 1u)] = v;
-            wc_init_one(p, v, r);
-        }
     }
     __syncthreads();
     const unsigned nW = s_nw, maxlen = s_maxlen;
+    const int wr = ceil_log2_d(maxlen > 1 ? maxlen - 1 : 1); // farthest: len-1 steps
+    if (nW <= kSmemCycle) {
+        wincyc_shared(p, nW, wr);
+        return;
+    }
+    for (std::uint64_t i = threadIdx.x; i < nW; i += blockDim.x) {
+        const std::uint32_t v = p.rem[1][i];
+        wc_init_one(p, v, p.R == 1 ? 0u : __ldg(&p.reg[v]));
+    }
     c->wc_n[stamp & 1] = (static_cast<unsigned long long>(stamp) << 32) | nW;
     c->wc_len[stamp & 1] = maxlen;
     if (nW > p.small_wc) {
@@ -799,7 +855,7 @@ __device__ __forceinline__ void ph_vote(const KP& p, std::uint64_t nM, std::uint
             c->wc_big[stamp & 1] = stamp;
         return;
     }
-    const int wr = ceil_log2_d(maxlen > 1 ? maxlen - 1 : 1); // farthest: len-1 steps
+    __syncthreads();
     for (int j = 0; j < wr; ++j) {
         wc_round(p, p.rem[1], nW, j, threadIdx.x, blockDim.x);
         __syncthreads();
@@ -838,7 +894,7 @@ __device__ __forceinline__ void ph_keep(const KP& p, std::uint64_t nC, std::uint
         std::uint32_t v = 0;
         if (i < nC) {
             v = p.clist[i];
-            const std::uint32_t r = __ldg(&p.reg[v]);
+            const std::uint32_t r = p.R == 1 ? 0u : __ldg(&p.reg[v]);
             const bool kept = p.comp[v] == p.src[r];
             p.conn[v] = kept ? 0u : NONE;
             p.indeg[v] = 0;
@@ -848,7 +904,7 @@ __device__ __forceinline__ void ph_keep(const KP& p, std::uint64_t nC, std::uint
         } else if (i < tot) {
             v = p.plist[i - nC];
             const std::uint32_t s = p.succ_v[v];
-            const std::uint32_t r = __ldg(&p.reg[v]);
+            const std::uint32_t r = p.R == 1 ? 0u : __ldg(&p.reg[v]);
             const std::uint32_t an = p.comp[s];
             const bool kept = an == p.src[r];
             p.comp[v] = an;
@@ -890,9 +946,10 @@ __device__ __forceinline__ void ph_attach(const KP& p, int cur, std::uint64_t pe
             for (std::uint32_t e0 = b; pend && e0 < e_end; e0 += 8) {
                 std::uint32_t tt[8], cc[8];
 #pragma unroll
-                for (int u = 0; u < 8; ++u)
-                    if (e0 + u < e_end)
-                        tt[u] = EXACT ? static_cast<std::uint32_t>(__ldg(&p.ew[e0 + u]).x) : p.fe[e0 + u].t;
+                for (int u = 0; u < 8; ++u) {
+                    const std::uint32_t e = min(e0 + u, e_end - 1); // tail masked below
+                    tt[u] = EXACT ? static_cast<std::uint32_t>(__ldg(&p.ew[e]).x) : p.fe[e].t;
+                }
 #pragma unroll
                 for (int u = 0; u < 8; ++u)
                     cc[u] = e0 + u < e_end ? ldv(p.conn[tt[u]]) : NONE;
