@@ -90,14 +90,37 @@ def dist_env():
 
 
 class ClockSampler:
-    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+    """SM clocks and throttle reasons sampled DURING the timed region
+    (B200_PROFILING.md clocks line): NVML polled every 2 ms from a thread
+    (the timed region of config 2 is ~100 ms, shorter than nvidia-smi's
+    start-up), falling back to `nvidia-smi -lms 50` where NVML is missing."""
+
+    HW = 0x8        # nvmlClocksEventReasonHwSlowdown
+    HW_THERMAL = 0x40
+    SW_THERMAL = 0x20
+    SW_POWER = 0x4
 
     def __init__(self, index):
         self.index = index
         self.proc = None
         self.lines = []
+        self.samples = []  # (sm_mhz, reasons bitmask)
+        self.max_mhz = None
+        self.nvml = None
+        self.stop = threading.Event()
 
     def __enter__(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.nvml = (pynvml, h)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            self.t = threading.Thread(target=self._poll, daemon=True)
+            self.t.start()
+            return self
+        except Exception:
+            self.nvml = None
         q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
              "clocks_event_reasons.sw_power_cap")
@@ -108,40 +131,70 @@ class ClockSampler:
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            time.sleep(0.3)  # let nvidia-smi start before the timed region
         except OSError:
             self.proc = None
         return self
+
+    def _poll(self):
+        pynvml, h = self.nvml
+        while not self.stop.is_set():
+            try:
+                mhz = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                try:
+                    rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                except AttributeError:
+                    rs = pynvml.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+                self.samples.append((mhz, rs))
+            except Exception:
+                pass
+            time.sleep(0.002)
 
     def _read(self):
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
     def __exit__(self, *exc):
+        self.stop.set()
         if self.proc:
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
             except subprocess.TimeoutExpired:
                 self.proc.kill()
+        elif self.nvml:
+            self.t.join(timeout=1)
 
     def summary(self):
         sm, mx, reasons = [], 0, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 6:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                mx = max(mx, float(parts[1]))
-            except ValueError:
-                continue
-            for nm, val in zip(names, parts[2:]):
-                if val.lower() == "active":
-                    reasons.add(nm)
+        if self.nvml:
+            for mhz, rs in self.samples:
+                sm.append(float(mhz))
+                for bit, nm in ((self.HW, "hw_slowdown"), (self.HW_THERMAL, "hw_thermal_slowdown"),
+                                (self.SW_THERMAL, "sw_thermal_slowdown"),
+                                (self.SW_POWER, "sw_power_cap")):
+                    if rs & bit:
+                        reasons.add(nm)
+            mx = float(self.max_mhz or 0)
+            src = "nvml (2 ms polling)"
+        else:
+            names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+            for ln in self.lines:
+                parts = [p.strip() for p in ln.split(",")]
+                if len(parts) < 6:
+                    continue
+                try:
+                    sm.append(float(parts[0]))
+                    mx = max(mx, float(parts[1]))
+                except ValueError:
+                    continue
+                for nm, val in zip(names, parts[2:]):
+                    if val.lower() == "active":
+                        reasons.add(nm)
+            src = "nvidia-smi -lms 50"
         sm.sort()
         return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx or None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm), "source": src}
 
 
 def measured_peak():

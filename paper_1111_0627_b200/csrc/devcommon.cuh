@@ -25,7 +25,10 @@ namespace ocmb {
 constexpr std::uint32_t NONE = 0xffffffffu;
 constexpr unsigned long long EMPTY = ~0ull;
 constexpr unsigned FULL = 0xffffffffu;
-constexpr int kBlock = 256;
+#ifndef OCM_BLOCK
+#define OCM_BLOCK 256
+#endif
+constexpr int kBlock = OCM_BLOCK;
 
 struct __align__(16) FEdge {
     double w;
