@@ -8,28 +8,27 @@
 //
 //   phase                    replaces (howard_par.hpp)
 //   improve                  :146 spf_pass_iter (+ policy in-degree count)
-//   region check + leaves    :189 finished_regions / :208 deactivate_regions
-//   peel                     :249 elimination_fixpoint (first layers only)
-//   core doubling + verify   :249 elimination + :301 cycle_identification
-//   stats / vote / adopt     :319 record fill, :56 vote_min, :339 vote_and_adopt
-//   winning cycle            :494 value_propagate_fixpoint on the cycle
-//   keep core, unpeel        :370 set_min_cycle, :393 mark_min_component,
+//   classify                 :189 finished_regions / :208 deactivate_regions,
+//                            leaf/core split + first doubling round
+//   round x k, mark, check   :249 elimination_fixpoint + :301 cycle_identification
+//                            (exact round-count verification), :319 records
+//   vote (+ last-CTA adopt,  :56 vote_min, :339 vote_and_adopt,
+//     winning-cycle values)  :494 value_propagate_fixpoint on the cycle
+//   keep                     :370 set_min_cycle, :393 mark_min_component,
 //                            value propagation of kept vertices
 //   attach layers            :433 connect_gpi_fixpoint (+ values)
 //   float levels             :494 value_propagate_fixpoint (float lane)
 //
-// Cycle detection is peel-then-double: leaves of the functional policy
-// graph (in-degree 0) and the next few layers under them are peeled off
-// level by level while the layers are large; the remaining core (closed
-// under succ) is compacted and pointer-doubled; peeled vertices take their
-// anchor and value from their successor in reverse layer order. On the
-// benchmark graphs the first four layers hold ~80% of the vertices, so the
-// O(n log L) doubling runs on a fifth of them.
+// Cycle detection is leaves-then-double: the leaves of the functional policy
+// graph (in-degree 0: never on a cycle, never anyone's successor; ~46% of the
+// vertices on the benchmark graphs) are split off, the remaining core (closed
+// under succ) is pointer-doubled, and leaves take anchor and value from their
+// (core) successor in the keep pass.
 //
 // Parity: every phase computes the same function as the reference step it
-// replaces; in particular the policy, anchors, lambdas and
-// integer keys are identical to the multi-kernel formulation this replaced,
-// which the GPU parity suite pins against the reference bit for bit.
+// replaces; the policy, anchors, lambdas, integer keys and
+// iteration counts are pinned against the reference bit for bit by the GPU
+// parity suite.
 //
 // Memory model: arrays written inside the kernel are read with plain or
 // L1-bypassing loads (never __ldg); only the CSR (row, ew, fe) and region
