@@ -70,7 +70,6 @@ struct Ctl {
     unsigned long long wc_n[2];    // (stamp << 32) | winning-cycle vertices listed
     unsigned wc_len[2];            // longest winning cycle (slot stamp & 1)
     unsigned wc_big[2];            // = stamp when the grid must do the winning cycles
-    unsigned long long fnd[2];     // float lane: (stamp << 32) | level still pending
     unsigned stamp;                // last verification stamp used
     unsigned k_hint;               // doubling rounds that sufficed last iteration
     unsigned k_streak;             // consecutive first-try verifications

@@ -986,35 +986,55 @@ __device__ __forceinline__ void ph_attach(const KP& p, int cur, std::uint64_t pe
 
 // Float lane: level-synchronous propagation from the anchor, computing
 // (value(succ) + w) - lambda exactly as FloatMode::extend (policy.hpp:105).
-__device__ __forceinline__ void ph_fprop_init(const KP& p) {
-    for (std::size_t v = gtid(); v < p.N; v += gstride()) {
-        if (!working(p, static_cast<std::uint32_t>(v)))
-            continue;
-        if (v == p.src[__ldg(&p.reg[v])]) {
-            p.conn[v] = 0;
-            p.key_f[v] = 0.0;
-        } else {
-            p.conn[v] = NONE;
+// Working vertices are the classified core and leaves; anchors start the
+// propagation, the rest are listed as pending.
+__device__ __forceinline__ void ph_fprop_init(const KP& p, std::uint64_t nC, std::uint64_t nL,
+                                              const Ring& ring) {
+    const std::uint64_t tot = nC + nL;
+    OCM_BLOCK_LOOP(i0, 0, tot) {
+        const std::uint64_t i = i0_b + threadIdx.x;
+        bool pend = false;
+        std::uint32_t v = 0;
+        if (i < tot) {
+            v = i < nC ? p.clist[i] : p.plist[i - nC];
+            if (v == p.src[p.R == 1 ? 0u : __ldg(&p.reg[v])]) {
+                p.conn[v] = 0;
+                p.key_f[v] = 0.0;
+            } else {
+                p.conn[v] = NONE;
+                pend = true;
+            }
         }
+        const std::uint64_t slot = block_append(pend, ring);
+        if (pend)
+            p.rem[0][slot] = v;
     }
 }
 
-__device__ __forceinline__ void ph_fprop_level(const KP& p, std::uint32_t level, unsigned long long* flag,
-                                               unsigned long long tag) {
-    bool nd = false;
-    OCM_BLOCK_LOOP(v0, 0, p.N) {
-        const std::uint64_t v = v0_b + threadIdx.x;
-        if (v >= p.N || ldv(p.conn[v]) != NONE || !working(p, static_cast<std::uint32_t>(v)))
-            continue;
-        const std::uint32_t s = p.succ_v[v];
-        if (ldv(p.conn[s]) < level) {
-            p.key_f[v] = (ldv(p.key_f[s]) + p.succ_wf[v]) - p.lam_f[__ldg(&p.reg[v])];
-            p.conn[v] = level;
-        } else {
-            nd = true;
+// One level over the still-pending vertices only: a vertex whose successor
+// was valued at an earlier level takes (value(succ) + w) - lambda; the rest
+// move to the next pending list.
+__device__ __forceinline__ void ph_fprop_level(const KP& p, int cur, std::uint64_t pending,
+                                               std::uint32_t level, const Ring& ring) {
+    const std::uint32_t* list = p.rem[cur];
+    OCM_BLOCK_LOOP(i0, 0, pending) {
+        const std::uint64_t i = i0_b + threadIdx.x;
+        bool pend = false;
+        std::uint32_t v = 0;
+        if (i < pending) {
+            v = list[i];
+            const std::uint32_t s = p.succ_v[v];
+            if (ldv(p.conn[s]) < level) {
+                p.key_f[v] = (ldv(p.key_f[s]) + p.succ_wf[v]) - p.lam_f[p.R == 1 ? 0u : __ldg(&p.reg[v])];
+                p.conn[v] = level;
+            } else {
+                pend = true;
+            }
         }
+        const std::uint64_t slot = block_append(pend, ring);
+        if (pend)
+            p.rem[cur ^ 1][slot] = v;
     }
-    block_flag(nd, flag, tag);
 }
 
 // ------------------------------------------------------------ the kernel
@@ -1225,20 +1245,21 @@ __global__ void __launch_bounds__(kBlock, kSolveMinBlocks) k_solve(KP p, int mod
             break;
 
         if constexpr (!EXACT) {
-            ph_fprop_init(p);
+            ph_fprop_init(p, nC, nL, st.rl);
             sync(PH_FLOAT);
-            for (std::uint32_t level = 1;; ++level) {
-                unsigned long long* flag = &c->fnd[level & 1];
-                const unsigned long long tag = (static_cast<unsigned long long>(stamp) << 32) | level;
-                ph_fprop_level(p, level, flag, tag);
+            std::uint64_t fpend = st.rl.take();
+            int fcur = 0;
+            for (std::uint32_t level = 1; fpend > 0; ++level) {
+                ph_fprop_level(p, fcur, fpend, level, st.rl);
                 sync(PH_FLOAT);
                 ++st.layers;
-                if (ldr(*flag) != tag)
-                    break;
-                if (level > p.max_region + 1) {
+                const std::uint64_t next = st.rl.take();
+                if (next == fpend) { // no progress: not a tree into the anchor
                     fatal = true;
                     break;
                 }
+                fpend = next;
+                fcur ^= 1;
             }
             if (fatal)
                 break;
