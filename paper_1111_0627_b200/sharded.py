@@ -116,21 +116,32 @@ class TorchComm:
 
     def exchange_arrays(self, policy: Sequence, flags: Sequence, chunk: int) -> None:
         """All-gather the rank's chunk of every policy array (in place) and
-        max-reduce the flag arrays."""
+        max-reduce the flag arrays. Non-NCCL backends (gloo: CPU tests, or
+        several ranks sharing one GPU) exchange through host copies."""
         for t in policy:
             mine = t.narrow(0, self.rank * chunk, chunk)
-            # NCCL allows the send buffer to be the receiver's own slice
-            self.dist.all_gather_into_tensor(t, mine if self.inplace else mine.clone(),
-                                             group=self.group)
+            if self.inplace:
+                # NCCL allows the send buffer to be the receiver's own slice
+                self.dist.all_gather_into_tensor(t, mine, group=self.group)
+            else:
+                host = t.cpu()
+                self.dist.all_gather_into_tensor(
+                    host, host.narrow(0, self.rank * chunk, chunk).clone(), group=self.group)
+                t.copy_(host)
         for f in flags:
-            self.dist.all_reduce(f, op=self.dist.ReduceOp.MAX, group=self.group)
+            if self.inplace:
+                self.dist.all_reduce(f, op=self.dist.ReduceOp.MAX, group=self.group)
+            else:
+                host = f.cpu()
+                self.dist.all_reduce(host, op=self.dist.ReduceOp.MAX, group=self.group)
+                f.copy_(host)
 
     def exchange(self, shards: Sequence[ShardSession]) -> None:
         import torch
         (sh,) = shards
         policy, flags = sh.tensors()
         self.exchange_arrays(policy, flags, sh.chunk)
-        torch.cuda.current_stream().synchronize()  # the next shard step reads them
+        torch.cuda.synchronize()  # the next shard step (session stream) reads them
 
 
 class LocalComm:
