@@ -1037,6 +1037,58 @@ __device__ __forceinline__ void ph_fprop_level(const KP& p, int cur, std::uint64
     }
 }
 
+// The float propagation without grid barriers: each thread owns up to 32
+// pending vertices (i = tid + j * threads) and keeps polling all of them,
+// valuing a vertex as soon as its successor is valued (acquire on conn, then
+// release). Chains resolve from the anchor; since no thread ever blocks on
+// one vertex, no vertex waits on work queued behind it. A bounded number of
+// empty polls turns a broken tree into the nonconv error instead of a hang.
+__device__ __forceinline__ unsigned ld_acquire(const std::uint32_t* a) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release(std::uint32_t* a, unsigned v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a), "r"(v) : "memory");
+}
+
+constexpr int kAsyncPerThread = 32;
+
+__device__ __forceinline__ void ph_fprop_async(const KP& p, int cur, std::uint64_t pending,
+                                               std::uint32_t level) {
+    const std::uint64_t tid = gtid(), nth = gstride();
+    const std::uint32_t* list = p.rem[cur];
+    unsigned todo = 0;
+    for (int j = 0; j < kAsyncPerThread; ++j)
+        if (tid + j * nth < pending)
+            todo |= 1u << j;
+    long long idle = 0;
+    while (todo) {
+        bool progress = false;
+        for (unsigned m = todo; m; m &= m - 1) {
+            const int j = __ffs(m) - 1;
+            const std::uint32_t v = list[tid + j * nth];
+            const std::uint32_t s = p.succ_v[v];
+            if (ld_acquire(&p.conn[s]) == NONE)
+                continue;
+            const double ks = __ldcg(&p.key_f[s]);
+            p.key_f[v] = (ks + p.succ_wf[v]) - p.lam_f[p.R == 1 ? 0u : __ldg(&p.reg[v])];
+            st_release(&p.conn[v], level);
+            todo &= ~(1u << j);
+            progress = true;
+        }
+        if (!progress) {
+            __nanosleep(100);
+            if (++idle > (1ll << 25)) { // seconds without progress: not a tree
+                p.c->nonconv = 1;
+                return;
+            }
+        } else {
+            idle = 0;
+        }
+    }
+}
+
 // ------------------------------------------------------------ the kernel
 //
 // Control decisions are taken by every thread from values that are
@@ -1249,7 +1301,10 @@ __global__ void __launch_bounds__(kBlock, kSolveMinBlocks) k_solve(KP p, int mod
             sync(PH_FLOAT);
             std::uint64_t fpend = st.rl.take();
             int fcur = 0;
-            for (std::uint32_t level = 1; fpend > 0; ++level) {
+            std::uint32_t level = 1;
+            // level-synchronous while the pending list is long, then
+            // barrier-free (up to kAsyncPerThread pending vertices per thread)
+            for (; fpend > kAsyncPerThread * gstride(); ++level) {
                 ph_fprop_level(p, fcur, fpend, level, st.rl);
                 sync(PH_FLOAT);
                 ++st.layers;
@@ -1260,6 +1315,15 @@ __global__ void __launch_bounds__(kBlock, kSolveMinBlocks) k_solve(KP p, int mod
                 }
                 fpend = next;
                 fcur ^= 1;
+            }
+            if (fatal)
+                break;
+            if (fpend > 0) {
+                ph_fprop_async(p, fcur, fpend, level);
+                sync(PH_FLOAT);
+                ++st.layers;
+                if (ldr(c->nonconv))
+                    fatal = true;
             }
             if (fatal)
                 break;
