@@ -426,7 +426,7 @@ def solve(g: Graph, opt: Optional[SolveOptions] = None) -> Solution:
     """ocm::solve (solve.hpp:64) on the B200: policy iteration (lane howard-par)."""
     opt = opt or SolveOptions()
     sol = _Sol()
-    cyc = np.zeros(max(g.n, 1), np.uint32)
+    cyc = np.empty(max(g.n, 1), np.uint32)  # only the first cycle_len entries are read
     _check(_lib.ocm_solve(g._h, C.byref(opt._c()), C.byref(sol), _p(cyc, C.c_uint32),
                           cyc.shape[0]))
     return _solution(sol, cyc)
@@ -467,7 +467,7 @@ class Session:
 
     def solve(self) -> Solution:
         sol = _Sol()
-        cyc = np.zeros(max(self.n, 1), np.uint32)
+        cyc = np.empty(max(self.n, 1), np.uint32)
         _check(_lib.ocm_session_solve(self._h, C.byref(sol), _p(cyc, C.c_uint32), cyc.shape[0]))
         return _solution(sol, cyc)
 

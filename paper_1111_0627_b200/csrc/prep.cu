@@ -229,13 +229,19 @@ __global__ void kp_pick_pivot(std::uint32_t n, const std::uint32_t* lab, const s
 }
 
 // A whole BFS (restricted to unassigned vertices, vis[] holding the stamp)
-// in one cooperative launch: a grid barrier per level instead of a launch
-// and a host round trip per level.
+// in one cooperative launch, a grid barrier per level instead of a launch and
+// a host round trip. Direction-optimising: while the frontier is a sizeable
+// share of the graph a level runs bottom-up -- every unvisited vertex scans
+// its in-edges (rrow/rcol) and stops at the first visited one -- instead of
+// pushing every frontier edge through an atomic exchange. Reachability only
+// (vis is monotone), so racing readers of vis[] stay correct; a bottom-up
+// level that adds nothing means the closure is complete.
 __global__ void __launch_bounds__(kBlock) kp_bfs_coop(const std::uint32_t* row, const std::uint32_t* col,
-                                                      const std::uint32_t* lab, std::uint32_t* vis,
-                                                      std::uint32_t stamp, std::uint32_t start,
-                                                      std::uint32_t* q0, std::uint32_t* q1,
-                                                      unsigned long long* ring_ctr) {
+                                                      const std::uint32_t* rrow, const std::uint32_t* rcol,
+                                                      std::uint32_t n, const std::uint32_t* lab,
+                                                      std::uint32_t* vis, std::uint32_t stamp,
+                                                      std::uint32_t start, std::uint32_t* q0,
+                                                      std::uint32_t* q1, unsigned long long* ring_ctr) {
     cooperative_groups::grid_group grid = cooperative_groups::this_grid();
     Ring ring;
     ring.init(ring_ctr);
@@ -249,14 +255,27 @@ __global__ void __launch_bounds__(kBlock) kp_bfs_coop(const std::uint32_t* row, 
     while (nin) {
         const std::uint32_t* qin = cur ? q1 : q0;
         std::uint32_t* qout = cur ? q0 : q1;
-        for (std::uint64_t i = gtid(); i < nin; i += gstride()) {
-            const std::uint32_t u = qin[i];
-            for (std::uint32_t e = row[u]; e < row[u + 1]; ++e) {
-                const std::uint32_t t = col[e];
-                if (lab[t] != NONE || vis[t] == stamp)
+        if (nin > (n >> 6)) { // bottom-up
+            for (std::uint64_t v = gtid(); v < n; v += gstride()) {
+                if (lab[v] != NONE || vis[v] == stamp)
                     continue;
-                if (atomicExch(&vis[t], stamp) != stamp)
-                    qout[warp_append(ring)] = t;
+                for (std::uint32_t e = rrow[v]; e < rrow[v + 1]; ++e)
+                    if (ldv(vis[rcol[e]]) == stamp) {
+                        vis[v] = stamp;
+                        qout[warp_append(ring)] = static_cast<std::uint32_t>(v);
+                        break;
+                    }
+            }
+        } else { // top-down
+            for (std::uint64_t i = gtid(); i < nin; i += gstride()) {
+                const std::uint32_t u = qin[i];
+                for (std::uint32_t e = row[u]; e < row[u + 1]; ++e) {
+                    const std::uint32_t t = col[e];
+                    if (lab[t] != NONE || vis[t] == stamp)
+                        continue;
+                    if (atomicExch(&vis[t], stamp) != stamp)
+                        qout[warp_append(ring)] = t;
+                }
             }
         }
         grid.sync();
@@ -662,13 +681,14 @@ void device_prepare_csr(std::uint32_t n, std::uint64_t m, DBuf<std::uint32_t>& r
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bfs_per_sm, kp_bfs_coop, kBlock, 0));
         bfs_per_sm = std::max(1, std::min(bfs_per_sm, 8));
     }
-    auto bfs = [&](const std::uint32_t* r, const std::uint32_t* c, std::uint32_t* vis,
-                   std::uint32_t st, std::uint32_t start) {
+    auto bfs = [&](const std::uint32_t* r, const std::uint32_t* c, const std::uint32_t* rr,
+                   const std::uint32_t* rc_, std::uint32_t* vis, std::uint32_t st, std::uint32_t start) {
         const std::uint32_t* lp = lab.p;
         std::uint32_t* a0 = q0.p;
         std::uint32_t* a1 = q1.p;
         unsigned long long* rc = pcd.p->bfs_ring;
-        void* args[] = {&r, &c, &lp, &vis, &st, &start, &a0, &a1, &rc};
+        std::uint32_t nn = n;
+        void* args[] = {&r, &c, &rr, &rc_, &nn, &lp, &vis, &st, &start, &a0, &a1, &rc};
         CK(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(&kp_bfs_coop),
                                        dim3(bfs_per_sm * sms), dim3(kBlock), args, 0, s));
     };
@@ -681,8 +701,8 @@ void device_prepare_csr(std::uint32_t n, std::uint64_t m, DBuf<std::uint32_t>& r
         read_pc();
         const std::uint32_t pivot = 0xffffffffu - static_cast<std::uint32_t>(pc.pivot & 0xffffffffull);
         const std::uint32_t sf = ++stamp, sb = ++stamp;
-        bfs(row.p, tgt.p, visf.p, sf, pivot);
-        bfs(brow.p, bsrc.p, visb.p, sb, pivot);
+        bfs(row.p, tgt.p, brow.p, bsrc.p, visf.p, sf, pivot);
+        bfs(brow.p, bsrc.p, row.p, tgt.p, visb.p, sb, pivot);
         kp_assign_both<<<gv, kBlock, 0, s>>>(n, visf.p, visb.p, sf, sb, pivot, lab.p);
         // finish the rest by colouring, re-trimming between rounds
         for (;;) {

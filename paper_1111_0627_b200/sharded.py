@@ -93,7 +93,7 @@ class ShardSession:
 
     def finish(self) -> Solution:
         sol = _Sol()
-        cyc = np.zeros(max(self.n, 1), np.uint32)
+        cyc = np.empty(max(self.n, 1), np.uint32)
         _check(_lib.ocm_session_shard_finish(self._h, C.byref(sol), cyc.ctypes.data_as(
             C.POINTER(C.c_uint32)), cyc.shape[0]))
         return _solution(sol, cyc)
