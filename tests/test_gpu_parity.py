@@ -169,3 +169,45 @@ def test_benchmark_size_certificate(objective):
     sol = sess.solve()
     assert sol.has_cycle and sol.exact
     bellman_certificate(g, sol, sess.values(), objective)
+
+
+def test_scc_parallel_matches_tarjan():
+    # --scc parallel (the reference's trim + pivoted reachability, scc.cpp:105)
+    # decomposes into the same regions: identical solver output
+    g = P.generate(P.Generator("powerlaw", n=30_000, deg=2, dmax=3000, seed=31))
+    for objective in ("min", "max"):
+        a = P.Session(g, P.SolveOptions(objective=objective, scc="tarjan"))
+        b = P.Session(g, P.SolveOptions(objective=objective, scc="parallel"))
+        sa, sb = a.solve(), b.solve()
+        assert (sa.mu_exact, sa.cycle_vertices, sa.stats.spf_passes, sa.stats.regions) == \
+            (sb.mu_exact, sb.cycle_vertices, sb.stats.spf_passes, sb.stats.regions)
+        assert np.array_equal(a.values()["key_num"], b.values()["key_num"])
+
+
+def test_limits_fail_loudly():
+    # integer weights beyond 32 bits: the exact device lane refuses (documented
+    # limit) instead of silently changing arithmetic
+    src = np.array([0, 1], np.uint32)
+    dst = np.array([1, 0], np.uint32)
+    g = P.build_graph(2, (src, dst, np.array([2.0 ** 40, 1.0])))
+    with pytest.raises(P.UnsupportedError, match="32 bits"):
+        P.solve(g)
+    # a device ordinal that does not exist
+    with pytest.raises(ValueError, match="device"):
+        P.solve(P.build_graph(2, (src, dst, np.array([1.0, 2.0]))), P.SolveOptions(device=99))
+
+
+def test_float_session_resolve_and_sessions_interleave():
+    g = P.generate_uniform(20_000, 4, -50, 50, 41)
+    s, d, w = g.edges()
+    gf = P.build_graph(g.n, (s, d, w / 8.0 + 0.0625))
+    fs = P.Session(gf)
+    es = P.Session(g, P.SolveOptions(objective="max"))
+    a = fs.solve()
+    e1 = es.solve()
+    b = fs.solve()
+    e2 = es.solve()
+    assert (a.mu, a.cycle_vertices, a.stats.spf_passes) == (b.mu, b.cycle_vertices, b.stats.spf_passes)
+    assert (e1.mu_exact, e1.cycle_vertices) == (e2.mu_exact, e2.cycle_vertices)
+    ref = oracle_record(g.n, s, d, w / 8.0 + 0.0625, "min", "tarjan")
+    check_against(a, fs.values(), ref)
