@@ -203,8 +203,15 @@ void Session::init(const std::function<void(DeviceState&)>& prepare) {
         d.kp.heavy = d.heavy.p;
     }
 
-    // one CTA per SM slot the register budget allows (<= kSolveMinBlocks)
+    // one CTA per SM slot the register budget allows (<= kSolveMinBlocks);
+    // small graphs take one CTA per kBlock vertices: fewer arrivals make every
+    // grid barrier cheaper and there is no work for more threads anyway
     grid_ = facts.per_sm[prep_.exact ? 1 : 0][gi_] * d.sms;
+    if (const int env_grid = env_int("OCM_GRID", 0))
+        grid_ = std::max(1, std::min(grid_, env_grid));
+    else
+        grid_ = static_cast<int>(std::max<std::size_t>(
+            1, std::min<std::size_t>(grid_, (N + kBlock - 1) / kBlock)));
 
     KP& p = d.kp;
     p.N = prep_.n;
