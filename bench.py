@@ -65,10 +65,12 @@ def parse():
     ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--lane", default="replicas", choices=["replicas", "sharded"],
+    ap.add_argument("--lane", default="replicas", choices=["replicas", "sharded", "fused"],
                     help="replicas: every rank solves its own graph (weak scaling, the driver's "
-                         "run); sharded: all ranks solve one graph, vertices 1-D partitioned "
-                         "(strong scaling, DESIGN.md §7)")
+                         "run); sharded: all ranks solve one graph, vertices 1-D partitioned, "
+                         "policy all-gathered by NCCL between launches; fused: the same inside one "
+                         "launch per rank, policy pushed into peer memory (strong scaling, "
+                         "DESIGN.md §7)")
     return ap.parse_args()
 
 
@@ -344,7 +346,8 @@ def run_sharded(a, world, rank, local):
     import torch.distributed as dist
 
     import paper_1111_0627_b200 as P
-    from paper_1111_0627_b200.sharded import ShardSession, TorchComm, solve_sharded
+    from paper_1111_0627_b200.sharded import (ShardSession, TorchComm, connect_torch, solve_fused,
+                                              solve_sharded)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if not dist.is_initialized():
@@ -360,6 +363,10 @@ def run_sharded(a, world, rank, local):
                           whi=100, seed=SEED)  # the same graph on every rank
     shards = {o: ShardSession(src, P.SolveOptions(objective=o, device=local), rank, world)
               for o in ("min", "max")}
+    fused = a.lane == "fused"
+    if fused:
+        for o in shards:
+            connect_torch(shards[o])
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=dev)
     streams = {o: torch.cuda.ExternalStream(int(P._lib.ocm_session_stream(shards[o]._h)), device=dev)
                for o in shards}
@@ -372,7 +379,10 @@ def run_sharded(a, world, rank, local):
             dist.barrier()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(streams[o])
-            (out[o],) = solve_sharded([shards[o]], comm)
+            if fused:
+                (out[o],) = solve_fused([shards[o]])
+            else:
+                (out[o],) = solve_sharded([shards[o]], comm)
             e1.record(streams[o])
             e1.synchronize()
             ms += e0.elapsed_time(e1)
@@ -397,8 +407,10 @@ def run_sharded(a, world, rank, local):
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms_max / a.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int64",
             "data": "synthetic (seeded generator)",
-            "config": dict(config(a, world), parallelism=f"sharded x{world} (1-D vertex partition, "
-                                                        f"policy all-gather per iteration)"),
+            "config": dict(config(a, world), parallelism=(
+                f"fused x{world} (1-D vertex partition, policy pushed into peer memory inside one "
+                f"launch per rank)" if fused else
+                f"sharded x{world} (1-D vertex partition, policy all-gather per iteration)")),
             "time_to_ocm_s": {o: None for o in ("min", "max")},
             "policy_iterations": {o: sols[0][o].stats.spf_passes for o in ("min", "max")},
             "mu": {o: str(sols[0][o].mu_exact) for o in ("min", "max")},
@@ -421,7 +433,7 @@ def main():
         if dist:
             dist.destroy_process_group()
         return
-    if a.lane == "sharded":
+    if a.lane in ("sharded", "fused"):
         run_sharded(a, world, rank, local)
         import torch.distributed as tdist
         if tdist.is_initialized():

@@ -191,6 +191,28 @@ int ocm_session_shard_buffers(ocm_session* s, ocm_shard_buffers* out);
 int ocm_session_shard_step(ocm_session* s, int32_t* done);
 int ocm_session_shard_finish(ocm_session* s, ocm_solution* out, uint32_t* cycle_buf,
                              uint32_t cycle_cap);
+/* ---- fused sharded lane: one persistent launch per solve per rank. During
+ * the improvement pass every changed policy entry is stored straight into
+ * the peers' replicas (NVLink stores into peer memory) and two cross-rank
+ * barriers per iteration (system-scope atomics on the peers' barrier words)
+ * replace the host exchange. Each rank publishes its buffer descriptor, all
+ * ranks connect with the full rank-ordered list (use_ipc = 1 across
+ * processes: the handles are opened with cudaIpcOpenMemHandle; 0 within one
+ * process: raw device pointers, peer access enabled when the devices
+ * differ), then every rank launches and finishes. All ranks must launch:
+ * a missing peer ends the solve with an error after a bounded wait. */
+typedef struct {
+    uint64_t ptr[6];           /* succ_e, succ_v, succ_w, changed0, changed1, barrier word */
+    unsigned char ipc[6][64];  /* cudaIpcMemHandle_t of each */
+    int32_t device;
+    uint32_t rank;
+} ocm_shard_peer;
+int ocm_session_shard_peer_info(ocm_session* s, ocm_shard_peer* out);
+int ocm_session_shard_connect(ocm_session* s, const ocm_shard_peer* peers, uint32_t world,
+                              int32_t use_ipc);
+int ocm_session_shard_fused_launch(ocm_session* s);
+int ocm_session_shard_fused_finish(ocm_session* s, ocm_solution* out, uint32_t* cycle_buf,
+                                   uint32_t cycle_cap);
 /* Vertex count of the session's graph. */
 uint32_t ocm_session_n(const ocm_session* s);
 /* The CUDA stream the session launches on (cudaStream_t). */

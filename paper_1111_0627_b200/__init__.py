@@ -85,6 +85,11 @@ class _ShardBuffers(C.Structure):
                 ("changed0", C.c_void_p), ("changed1", C.c_void_p), ("stream", C.c_void_p)]
 
 
+class _ShardPeer(C.Structure):
+    _fields_ = [("ptr", C.c_uint64 * 6), ("ipc", (C.c_ubyte * 64) * 6), ("device", C.c_int32),
+                ("rank", C.c_uint32)]
+
+
 class _Opts(C.Structure):
     _fields_ = [("algo", C.c_int32), ("objective", C.c_int32), ("scc", C.c_int32),
                 ("device", C.c_int32), ("epsilon", C.c_double)]
@@ -130,6 +135,11 @@ def _load():
         "ocm_session_shard_buffers": (C.c_int, [C.c_void_p, P(_ShardBuffers)]),
         "ocm_session_shard_step": (C.c_int, [C.c_void_p, P(C.c_int32)]),
         "ocm_session_shard_finish": (C.c_int, [C.c_void_p, P(_Sol), P(C.c_uint32), C.c_uint32]),
+        "ocm_session_shard_peer_info": (C.c_int, [C.c_void_p, P(_ShardPeer)]),
+        "ocm_session_shard_connect": (C.c_int, [C.c_void_p, P(_ShardPeer), C.c_uint32, C.c_int32]),
+        "ocm_session_shard_fused_launch": (C.c_int, [C.c_void_p]),
+        "ocm_session_shard_fused_finish": (C.c_int, [C.c_void_p, P(_Sol), P(C.c_uint32),
+                                                     C.c_uint32]),
         "ocm_graph_free": (None, [C.c_void_p]),
         "ocm_graph_n": (C.c_uint32, [C.c_void_p]),
         "ocm_graph_m": (C.c_uint64, [C.c_void_p]),
@@ -158,7 +168,8 @@ EXPORTED_SYMBOLS = (
     "ocm_build_graph", "ocm_parse_graph_text", "ocm_read_graph_file", "ocm_generate_uniform",
     "ocm_generate_model", "ocm_generate", "ocm_session_create_generated", "ocm_session_n",
     "ocm_session_create_shard", "ocm_session_shard_buffers", "ocm_session_shard_step",
-    "ocm_session_shard_finish",
+    "ocm_session_shard_finish", "ocm_session_shard_peer_info", "ocm_session_shard_connect",
+    "ocm_session_shard_fused_launch", "ocm_session_shard_fused_finish",
     "ocm_graph_free", "ocm_graph_n", "ocm_graph_m", "ocm_graph_integer_exact", "ocm_graph_edges",
     "ocm_solve", "ocm_session_create", "ocm_session_solve", "ocm_session_values",
     "ocm_session_stream", "ocm_session_free",

@@ -222,6 +222,28 @@ int ocm_session_shard_finish(ocm_session* s, ocm_solution* out, uint32_t* cycle_
     return guard([&] { s->s->shard_finish(out, cycle_buf, cycle_cap); });
 }
 
+int ocm_session_shard_peer_info(ocm_session* s, ocm_shard_peer* out) {
+    return guard([&] { s->s->shard_peer_info(out); });
+}
+
+int ocm_session_shard_connect(ocm_session* s, const ocm_shard_peer* peers, uint32_t world,
+                              int32_t use_ipc) {
+    return guard([&] {
+        if (!peers)
+            throw std::invalid_argument("null peer list");
+        s->s->shard_connect(peers, world, use_ipc != 0);
+    });
+}
+
+int ocm_session_shard_fused_launch(ocm_session* s) {
+    return guard([&] { s->s->fused_launch(); });
+}
+
+int ocm_session_shard_fused_finish(ocm_session* s, ocm_solution* out, uint32_t* cycle_buf,
+                                   uint32_t cycle_cap) {
+    return guard([&] { s->s->fused_finish(out, cycle_buf, cycle_cap); });
+}
+
 int ocm_generate_model(uint32_t states, const ocm_transition* transitions, uint32_t n_transitions,
                        int32_t uses_server, uint32_t clients, uint64_t max_states,
                        ocm_graph** out) {

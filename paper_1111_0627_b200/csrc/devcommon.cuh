@@ -29,6 +29,7 @@ constexpr unsigned FULL = 0xffffffffu;
 #define OCM_BLOCK 256
 #endif
 constexpr int kBlock = OCM_BLOCK;
+constexpr int kMaxShards = 8; // ranks of the fused sharded lane (one per GPU of a box)
 
 struct __align__(16) FEdge {
     double w;
@@ -73,12 +74,14 @@ struct Ctl {
     unsigned stamp;                // last verification stamp used
     unsigned k_hint;               // doubling rounds that sufficed last iteration
     unsigned k_streak;             // consecutive first-try verifications
+    unsigned xepoch;               // cross-rank barriers passed (fused sharded lane)
     unsigned vfail[2];             // = stamp of a failed verification (slot stamp & 1)
     // ---- per solve (host clears from here on before every launch)
     int error;     // structural (no successor / not strongly connected)
     int overflow;  // exact keys would leave +-2^62
     int lambda_up; // lambda increased inside a region
     int nonconv;   // a fixpoint did not converge within its bound
+    int xfail;     // fused sharded lane: a peer never reached the barrier
     unsigned it;         // iteration index (sharded launches resume it)
     unsigned shard_done; // sharded lane: the last launch finished the solve
     unsigned passes;
@@ -137,6 +140,16 @@ struct KP {
     std::uint32_t nheavy;
     std::uint32_t heavy_deg;
     std::uint32_t own_lo, own_hi; // improvement range (all vertices unless sharded)
+    // fused sharded lane (kShardFused): the rank's peers' policy replicas and
+    // flags (peer memory: NVLink-mapped IPC pointers between GPUs, plain
+    // pointers between shards sharing a GPU) and the cross-rank barrier words
+    int rank, world, fused;
+    std::uint32_t* peer_succ_e[kMaxShards];
+    std::uint32_t* peer_succ_v[kMaxShards];
+    void* peer_succ_w[kMaxShards];
+    int* peer_changed[2][kMaxShards];
+    unsigned* peer_xbar[kMaxShards];
+    unsigned* xbar;
     int indeg_in_improve;         // 1: the improvement pass counts policy in-degrees
     // tuning (launch arguments)
     int G;                 // improvement lanes per vertex
@@ -154,6 +167,7 @@ template <class T> struct DBuf {
     // cached by the session), so re-creating sessions does not pay
     // cudaMalloc/cudaFree synchronisation.
     cudaStream_t st = nullptr;
+    bool plain = false; // cudaMalloc'ed (IPC-exportable), not pool memory
     void alloc(std::size_t k, cudaStream_t s = nullptr) {
         release();
         st = s;
@@ -161,11 +175,26 @@ template <class T> struct DBuf {
             CK(cudaMallocAsync(reinterpret_cast<void**>(&p), k * sizeof(T), st));
         n = k;
     }
+    // Memory other processes can map (cudaIpcGetMemHandle does not accept
+    // stream-ordered pool allocations): the fused sharded lane's exchange
+    // buffers.
+    void alloc_shared(std::size_t k) {
+        release();
+        if (k)
+            CK(cudaMalloc(reinterpret_cast<void**>(&p), k * sizeof(T)));
+        plain = true;
+        n = k;
+    }
     void release() {
-        if (p)
-            cudaFreeAsync(p, st);
+        if (p) {
+            if (plain)
+                cudaFree(p);
+            else
+                cudaFreeAsync(p, st);
+        }
         p = nullptr;
         n = 0;
+        plain = false;
     }
     ~DBuf() { release(); }
 };
@@ -189,7 +218,7 @@ struct DeviceState {
     int sms = 148;
     cudaStream_t stream = nullptr;
     DBuf<std::uint32_t> row, reg, succ_e, succ_v, comp, wlist, cyc_len, conn, rem0, rem1, src,
-        iters, indeg, plist, clist, cmark, cmark2, heavy;
+        iters, indeg, plist, clist, cmark, cmark2, heavy, xbar;
     DBuf<PJV> pv0, pv1;
     DBuf<PJC> pj0, pj1;
     DBuf<int2> ew;
@@ -205,6 +234,7 @@ struct DeviceState {
     cudaStream_t side = nullptr;      // weight upload overlapping the region split
     cudaEvent_t side_done = nullptr;
     cudaEvent_t alloc_done = nullptr; // orders side-stream use after allocations on `stream`
+    std::vector<void*> ipc_opened;    // peer buffers mapped with cudaIpcOpenMemHandle
     KP kp{};
     cudaEvent_t ev_alloc_done(cudaStream_t s) {
         if (!alloc_done)
@@ -217,7 +247,7 @@ struct DeviceState {
         if (stream)
             cudaStreamSynchronize(stream);
         for (auto* b : {&row, &reg, &succ_e, &succ_v, &comp, &wlist, &cyc_len, &conn, &rem0, &rem1,
-                        &src, &iters, &indeg, &plist, &clist, &cmark, &cmark2, &heavy})
+                        &src, &iters, &indeg, &plist, &clist, &cmark, &cmark2, &heavy, &xbar})
             b->release();
         pv0.release();
         pv1.release();
@@ -243,6 +273,8 @@ struct DeviceState {
             cudaStreamSynchronize(stream);
         for (cudaEvent_t e : ev)
             cudaEventDestroy(e);
+        for (void* q : ipc_opened)
+            cudaIpcCloseMemHandle(q);
         if (side) {
             cudaStreamSynchronize(side);
             cudaStreamDestroy(side);

@@ -113,6 +113,25 @@ __device__ __forceinline__ FEdge ld_edge(const FEdge* e) {
     return f;
 }
 
+// Fused sharded lane: a vertex whose policy changed is stored straight into
+// every peer's replica (NVLink stores into peer memory; ordered before the
+// cross-rank barrier by a system-scope fence). Unchanged vertices are
+// already identical everywhere, so only changes travel.
+template <bool EXACT, class Edge>
+__device__ __forceinline__ void push_policy(const KP& p, std::uint32_t v, std::uint32_t e,
+                                            std::uint32_t t, const Edge& ed) {
+    for (int q = 0; q < p.world; ++q) {
+        if (q == p.rank)
+            continue;
+        p.peer_succ_e[q][v] = e;
+        p.peer_succ_v[q][v] = t;
+        if constexpr (EXACT)
+            static_cast<int*>(p.peer_succ_w[q])[v] = reinterpret_cast<const int2&>(ed).y;
+        else
+            static_cast<double*>(p.peer_succ_w[q])[v] = reinterpret_cast<const FEdge&>(ed).w;
+    }
+}
+
 template <bool EXACT, int G, int U>
 __device__ __forceinline__ void improve_vertex(const KP& p, int* changed, ChangedMarks& marks,
                                                std::uint32_t v) {
@@ -229,6 +248,8 @@ __device__ __forceinline__ void improve_vertex(const KP& p, int* changed, Change
                 p.succ_wf[v] = ed.w;
             }
             p.succ_v[v] = t;
+            if (p.fused)
+                push_policy<EXACT>(p, v, be, t, ed);
             if (p.indeg_in_improve)
                 atomicAdd(&p.indeg[t], 1u);
             marks.note(changed, r);
@@ -361,12 +382,16 @@ __device__ __forceinline__ void improve_heavy(const KP& p, int* changed) {
                         const int2 ed = __ldg(&p.ew[ge]);
                         p.succ_v[v] = static_cast<std::uint32_t>(ed.x);
                         p.succ_wi[v] = ed.y;
+                        if (p.fused)
+                            push_policy<EXACT>(p, v, ge, static_cast<std::uint32_t>(ed.x), ed);
                         if (p.indeg_in_improve)
                             atomicAdd(&p.indeg[ed.x], 1u);
                     } else {
-                        const FEdge ed = p.fe[ge];
+                        const FEdge ed = ld_edge(&p.fe[ge]);
                         p.succ_v[v] = ed.t;
                         p.succ_wf[v] = ed.w;
+                        if (p.fused)
+                            push_policy<EXACT>(p, v, ge, ed.t, ed);
                         if (p.indeg_in_improve)
                             atomicAdd(&p.indeg[ed.t], 1u);
                     }
@@ -1106,11 +1131,22 @@ __device__ __forceinline__ void ph_fprop_async(const KP& p, int cur, std::uint64
 // improvement pass -- or finishes (Ctl::shard_done). Loop state survives in
 // the control block between launches.
 constexpr int kSolveFull = 0, kShardBegin = 1, kShardResume = 2;
+// kShardFused: the whole sharded solve in one launch per rank -- changed
+// policy entries are stored into the peers' replicas during the improvement
+// pass and two cross-rank barriers per iteration (system-scope atomics on
+// the peers' barrier words) replace the host exchange.
+constexpr int kShardFused = 3;
+
+__device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* a) {
+    unsigned v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(a) : "memory");
+    return v;
+}
 
 // Cross-phase state of the kernel's loop.
 struct LoopState {
     Ring ra, rl, rc; // active-region counts, lists, core list
-    unsigned stamp, k_hint, k_streak, passes, outer, rounds, verifies, layers, nsync;
+    unsigned stamp, k_hint, k_streak, xepoch, passes, outer, rounds, verifies, layers, nsync;
     unsigned long long peeled, cored, done_base;
     long long clk0, clk_last;
     int it;
@@ -1142,10 +1178,37 @@ __global__ void __launch_bounds__(kBlock, kSolveMinBlocks) k_solve(KP p, int mod
             st.clk_last = t;
         }
     };
+    // cross-rank barrier of the fused sharded lane: local grid barrier, then
+    // the leader publishes (system fence) and bumps every rank's barrier word
+    // and waits for all ranks' bumps; a bounded wait turns a missing peer into
+    // an error instead of a hang. Returns false (uniformly) on timeout.
+    auto xbarrier = [&](int ph) -> bool {
+        sync(ph);
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            __threadfence_system();
+            const unsigned target = (++st.xepoch) * static_cast<unsigned>(p.world);
+            for (int q = 0; q < p.world; ++q)
+                atomicAdd_system(p.peer_xbar[q], 1u);
+            long long idle = 0;
+            while (ld_acquire_sys(p.xbar) < target) {
+                __nanosleep(64);
+                if (++idle > (1ll << 26)) {
+                    c->xfail = 1;
+                    break;
+                }
+            }
+            __threadfence_system();
+        } else {
+            ++st.xepoch; // every thread's copy stays in step
+        }
+        sync(ph);
+        return ldr(c->xfail) == 0;
+    };
     const int K_max = max(1, ceil_log2_d(max(p.max_region, 2u)));
     st.stamp = ldr(c->stamp);
     st.k_hint = max(1u, min(ldr(c->k_hint), static_cast<unsigned>(K_max)));
     st.k_streak = ldr(c->k_streak);
+    st.xepoch = ldr(c->xepoch);
     // per-solve counters continue across the launches of a sharded solve
     st.passes = ldr(c->passes);
     st.outer = ldr(c->outer);
@@ -1172,6 +1235,12 @@ __global__ void __launch_bounds__(kBlock, kSolveMinBlocks) k_solve(KP p, int mod
 
     for (;; ++st.it) {
         if (!skip_improve) {
+            // fused lane: every rank finished the previous iteration (whose
+            // replicated phases write the policy) before anyone pushes
+            if (mode == kShardFused && !xbarrier(PH_IMPROVE)) {
+                fatal = true;
+                break;
+            }
             // park the loop state (block-uniform) in shared memory while the
             // pass runs: otherwise ptxas keeps it in registers across the
             // pass and spills the pass's own working set inside its loop
@@ -1185,9 +1254,23 @@ __global__ void __launch_bounds__(kBlock, kSolveMinBlocks) k_solve(KP p, int mod
             st = s_park;
             ++st.passes;
             sync(PH_IMPROVE);
-            if (mode != kSolveFull) {
+            if (mode == kShardBegin || mode == kShardResume) {
                 paused = true;
                 break;
+            }
+            if (mode == kShardFused) {
+                // region flags raised here go to the peers too; then wait
+                // until every rank's policy pushes are visible
+                const int par = st.it & 1;
+                for (std::size_t r = gtid(); r < p.R; r += gstride())
+                    if (p.changed[par][r])
+                        for (int q = 0; q < p.world; ++q)
+                            if (q != p.rank)
+                                p.peer_changed[par][q][r] = 1;
+                if (!xbarrier(PH_IMPROVE)) {
+                    fatal = true;
+                    break;
+                }
             }
         }
         skip_improve = false;
@@ -1338,6 +1421,7 @@ __global__ void __launch_bounds__(kBlock, kSolveMinBlocks) k_solve(KP p, int mod
         c->stamp = st.stamp;
         c->k_hint = st.k_hint;
         c->k_streak = st.k_streak;
+        c->xepoch = st.xepoch;
         c->passes = st.passes;
         c->outer = st.outer;
         c->rounds = st.rounds;

@@ -131,19 +131,28 @@ void Session::init(const std::function<void(DeviceState&)>& prepare) {
     // policy arrays are padded to world equal chunks for the all-gather
     chunk_ = static_cast<std::uint32_t>((N + world_ - 1) / world_);
     const std::size_t NP = std::max<std::size_t>(N1, std::size_t(chunk_) * world_);
+    // exchange buffers of a sharded session can be mapped by peer processes
+    const bool shared = world_ > 1;
+    auto xalloc = [&](auto& buf, std::size_t k) {
+        if (shared)
+            buf.alloc_shared(k);
+        else
+            buf.alloc(k, d.stream);
+    };
     if (prep_.exact) {
-        d.succ_wi.alloc(NP, d.stream);
+        xalloc(d.succ_wi, NP);
         d.key_i.alloc(N1, d.stream);
         d.cyc_wi.alloc(N1, d.stream);
         d.pv0.alloc(N1, d.stream);
         d.pv1.alloc(N1, d.stream);
     } else {
-        d.succ_wf.alloc(NP, d.stream);
+        xalloc(d.succ_wf, NP);
         d.key_f.alloc(N1, d.stream);
         d.cyc_wf.alloc(N1, d.stream);
     }
-    d.succ_e.alloc(NP, d.stream);
-    d.succ_v.alloc(NP, d.stream);
+    xalloc(d.succ_e, NP);
+    xalloc(d.succ_v, NP);
+    xalloc(d.xbar, 1);
     for (auto* b : {&d.comp, &d.wlist, &d.cyc_len, &d.conn, &d.rem0, &d.rem1,
                     &d.indeg, &d.plist, &d.clist, &d.cmark, &d.cmark2})
         b->alloc(N1, d.stream);
@@ -152,8 +161,8 @@ void Session::init(const std::function<void(DeviceState&)>& prepare) {
     d.src.alloc(R1, d.stream);
     d.iters.alloc(R1, d.stream);
     d.active.alloc(R1, d.stream);
-    d.changed0.alloc(R1, d.stream);
-    d.changed1.alloc(R1, d.stream);
+    xalloc(d.changed0, R1);
+    xalloc(d.changed1, R1);
     d.lam_f.alloc(R1, d.stream);
     d.lam_num.alloc(R1, d.stream);
     d.lam_den.alloc(R1, d.stream);
@@ -164,6 +173,7 @@ void Session::init(const std::function<void(DeviceState&)>& prepare) {
     CK(cudaMemsetAsync(d.cmark.p, 0, N1 * sizeof(std::uint32_t), d.stream));
     CK(cudaMemsetAsync(d.cmark2.p, 0, N1 * sizeof(std::uint32_t), d.stream));
     CK(cudaMemsetAsync(d.ctl.p, 0, sizeof(Ctl), d.stream));
+    CK(cudaMemsetAsync(d.xbar.p, 0, sizeof(unsigned), d.stream));
     {
         Ctl init{};
         init.k_hint = 4;
@@ -258,6 +268,13 @@ void Session::init(const std::function<void(DeviceState&)>& prepare) {
     p.own_lo = static_cast<std::uint32_t>(std::min<std::size_t>(N, std::size_t(rank_) * chunk_));
     p.own_hi = static_cast<std::uint32_t>(std::min<std::size_t>(N, std::size_t(rank_ + 1) * chunk_));
     p.indeg_in_improve = world_ == 1 ? 1 : 0;
+    p.rank = static_cast<int>(rank_);
+    p.world = static_cast<int>(world_);
+    p.fused = 0;
+    p.xbar = d.xbar.p;
+    for (int q = 0; q < kMaxShards; ++q)
+        p.peer_xbar[q] = nullptr;
+    p.peer_xbar[rank_ < static_cast<std::uint32_t>(kMaxShards) ? rank_ : 0] = d.xbar.p;
     h2d_bytes_ = prep_.h2d_bytes;
     const auto t_end = std::chrono::steady_clock::now();
     prep_ms_ = std::chrono::duration<double, std::milli>(t_end - t0).count();
@@ -273,13 +290,15 @@ Session::~Session() = default;
 void* Session::stream() const { return d_ ? d_->stream : nullptr; }
 
 // One cooperative launch of k_solve in the given mode; returns its event time.
-template <class M> float Session::launch(int mode) {
+// One cooperative launch of k_solve in the given mode: enqueue, then (unless
+// the caller overlaps it with peers' launches) wait and check the outcome.
+template <class M> void Session::launch_async(int mode) {
     constexpr bool EXACT = M::value;
     DeviceState& d = *d_;
     KP& p = d.kp;
     cudaStream_t s = d.stream;
-    Ctl& hc = *d.h_ctl;
     p.small_wc = 4096;
+    p.fused = mode == kShardFused ? 1 : 0;
     if (mode != kShardResume) {
         CK(cudaMemsetAsync(reinterpret_cast<char*>(p.c) + kCtlSolveOffset, 0,
                            sizeof(Ctl) - kCtlSolveOffset, s));
@@ -294,12 +313,22 @@ template <class M> float Session::launch(int mode) {
         ++launches_;
     }
     CK(cudaEventRecord(d.ev_end, s));
-    CK(cudaMemcpyAsync(&hc, p.c, sizeof(Ctl), cudaMemcpyDeviceToHost, s));
+}
+
+float Session::launch_wait() {
+    DeviceState& d = *d_;
+    Ctl& hc = *d.h_ctl;
+    // (a copy into pageable memory blocks the host until the kernel is done:
+    // issued here, not in launch_async, so peers' launches are not held up)
+    CK(cudaMemcpyAsync(d.h_ctl, d.kp.c, sizeof(Ctl), cudaMemcpyDeviceToHost, d.stream));
     d2h_ += sizeof(Ctl);
-    CK(cudaStreamSynchronize(s));
+    CK(cudaStreamSynchronize(d.stream));
     CK(cudaGetLastError());
     if (prep_.R == 0)
         hc.shard_done = 1;
+    if (hc.xfail)
+        throw std::runtime_error("fused sharded lane: a peer rank never reached the cross-rank "
+                                 "barrier (are all ranks launched and connected?)");
     if (hc.error)
         throw std::logic_error("howard_par: structural error (a vertex has no successor "
                                "inside its region, or a region is not strongly connected)");
@@ -313,6 +342,11 @@ template <class M> float Session::launch(int mode) {
     CK(cudaEventElapsedTime(&ms, d.ev_start, d.ev_end));
     solve_ms_ += ms;
     return ms;
+}
+
+template <class M> float Session::launch(int mode) {
+    launch_async<M>(mode);
+    return launch_wait();
 }
 
 // Result of the solve that just finished: counters, the optimal region's
@@ -487,6 +521,86 @@ bool Session::shard_step() {
 
 void Session::shard_finish(ocm_solution* out, std::uint32_t* cycle_buf, std::uint32_t cap) {
     CK(cudaSetDevice(d_->device));
+    if (prep_.exact)
+        collect<ExactTag>(out, cycle_buf, cap);
+    else
+        collect<FloatTag>(out, cycle_buf, cap);
+    solved_ = true;
+}
+
+void Session::shard_peer_info(ocm_shard_peer* out) const {
+    const DeviceState& d = *d_;
+    std::memset(out, 0, sizeof *out);
+    out->device = d.device;
+    out->rank = rank_;
+    const void* bufs[6] = {d.succ_e.p, d.succ_v.p,
+                           prep_.exact ? static_cast<const void*>(d.succ_wi.p)
+                                       : static_cast<const void*>(d.succ_wf.p),
+                           d.changed0.p, d.changed1.p, d.xbar.p};
+    for (int i = 0; i < 6; ++i) {
+        out->ptr[i] = reinterpret_cast<std::uint64_t>(bufs[i]);
+        if (world_ > 1) {
+            cudaIpcMemHandle_t h;
+            CK(cudaIpcGetMemHandle(&h, const_cast<void*>(bufs[i])));
+            static_assert(sizeof h == sizeof out->ipc[0], "IPC handle size");
+            std::memcpy(out->ipc[i], &h, sizeof h);
+        }
+    }
+}
+
+void Session::shard_connect(const ocm_shard_peer* peers, std::uint32_t world, bool ipc) {
+    DeviceState& d = *d_;
+    if (world != world_)
+        throw std::invalid_argument("peer list does not match the session's world size");
+    if (world_ > static_cast<std::uint32_t>(kMaxShards))
+        throw std::invalid_argument("the fused sharded lane supports at most 8 ranks");
+    CK(cudaSetDevice(d.device));
+    KP& p = d.kp;
+    for (std::uint32_t q = 0; q < world; ++q) {
+        if (peers[q].rank != q)
+            throw std::invalid_argument("peer list must be ordered by rank");
+        void* b[6];
+        for (int i = 0; i < 6; ++i) {
+            if (q == rank_) {
+                b[i] = reinterpret_cast<void*>(peers[q].ptr[i]);
+            } else if (ipc) {
+                cudaIpcMemHandle_t h;
+                std::memcpy(&h, peers[q].ipc[i], sizeof h);
+                CK(cudaIpcOpenMemHandle(&b[i], h, cudaIpcMemLazyEnablePeerAccess));
+                d.ipc_opened.push_back(b[i]);
+            } else {
+                b[i] = reinterpret_cast<void*>(peers[q].ptr[i]);
+                if (peers[q].device != d.device) {
+                    const cudaError_t e = cudaDeviceEnablePeerAccess(peers[q].device, 0);
+                    if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+                        CK(e);
+                    cudaGetLastError();
+                }
+            }
+        }
+        p.peer_succ_e[q] = static_cast<std::uint32_t*>(b[0]);
+        p.peer_succ_v[q] = static_cast<std::uint32_t*>(b[1]);
+        p.peer_succ_w[q] = b[2];
+        p.peer_changed[0][q] = static_cast<int*>(b[3]);
+        p.peer_changed[1][q] = static_cast<int*>(b[4]);
+        p.peer_xbar[q] = static_cast<unsigned*>(b[5]);
+    }
+    connected_ = true;
+}
+
+void Session::fused_launch() {
+    if (!connected_)
+        throw std::logic_error("fused sharded lane: connect the peers first");
+    CK(cudaSetDevice(d_->device));
+    if (prep_.exact)
+        launch_async<ExactTag>(kShardFused);
+    else
+        launch_async<FloatTag>(kShardFused);
+}
+
+void Session::fused_finish(ocm_solution* out, std::uint32_t* cycle_buf, std::uint32_t cap) {
+    CK(cudaSetDevice(d_->device));
+    launch_wait();
     if (prep_.exact)
         collect<ExactTag>(out, cycle_buf, cap);
     else

@@ -40,10 +40,18 @@ class Session {
     bool shard_step();
     void shard_buffers(ocm_shard_buffers* b) const;
     void shard_finish(ocm_solution* out, std::uint32_t* cycle_buf, std::uint32_t cap);
+    // Fused sharded lane: exchange buffer descriptors (device pointers + IPC
+    // handles), map the peers', then one launch per solve per rank.
+    void shard_peer_info(ocm_shard_peer* out) const;
+    void shard_connect(const ocm_shard_peer* peers, std::uint32_t world, bool ipc);
+    void fused_launch();
+    void fused_finish(ocm_solution* out, std::uint32_t* cycle_buf, std::uint32_t cap);
 
   private:
     void init(const std::function<void(DeviceState&)>& prepare);
     template <class M> float launch(int mode);
+    template <class M> void launch_async(int mode);
+    float launch_wait();
     template <class M> void collect(ocm_solution* out, std::uint32_t* cycle_buf, std::uint32_t cap);
     ocm_solve_options opt_;
     PrepInfo prep_;
@@ -55,6 +63,7 @@ class Session {
     int gi_ = 0;   // its improvement group width (index into 1, 2, 4, 8)
     std::uint32_t rank_ = 0, world_ = 1, chunk_ = 0;
     bool shard_started_ = false;
+    bool connected_ = false; // fused sharded lane: peers mapped
     double solve_ms_ = 0.0;   // event time of the current solve's launches
     std::uint64_t d2h_ = 0;   // device->host bytes of the current solve
     unsigned launches_ = 0;   // launches of the current solve

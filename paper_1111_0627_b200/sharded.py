@@ -22,10 +22,11 @@ from typing import List, Optional, Sequence, Union
 
 import numpy as np
 
-from . import (Generator, Graph, Solution, SolveOptions, _check, _lib, _ShardBuffers, _Sol,
-               _solution)
+from . import (Generator, Graph, Solution, SolveOptions, _check, _lib, _ShardBuffers, _ShardPeer,
+               _Sol, _solution)
 
-__all__ = ["ShardSession", "TorchComm", "LocalComm", "solve_sharded"]
+__all__ = ["ShardSession", "TorchComm", "LocalComm", "solve_sharded", "connect_local",
+           "connect_torch", "solve_fused"]
 
 
 class _DeviceArray:
@@ -101,6 +102,30 @@ class ShardSession:
     def values(self):
         from . import Session
         return Session.values(self)  # same native call on the session handle
+
+    # ---- fused lane (one launch per solve per rank, exchange inside the kernel)
+    def peer_info(self) -> bytes:
+        """This rank's exchange-buffer descriptor (device pointers + IPC handles)."""
+        info = _ShardPeer()
+        _check(_lib.ocm_session_shard_peer_info(self._h, C.byref(info)))
+        return bytes(info)
+
+    def connect(self, infos: Sequence[bytes], use_ipc: bool) -> None:
+        """Map every rank's buffers (rank-ordered descriptors)."""
+        arr = (_ShardPeer * len(infos))()
+        for q, raw in enumerate(infos):
+            C.memmove(C.byref(arr[q]), raw, C.sizeof(_ShardPeer))
+        _check(_lib.ocm_session_shard_connect(self._h, arr, len(infos), 1 if use_ipc else 0))
+
+    def fused_launch(self) -> None:
+        _check(_lib.ocm_session_shard_fused_launch(self._h))
+
+    def fused_finish(self) -> Solution:
+        sol = _Sol()
+        cyc = np.empty(max(self.n, 1), np.uint32)
+        _check(_lib.ocm_session_shard_fused_finish(self._h, C.byref(sol), cyc.ctypes.data_as(
+            C.POINTER(C.c_uint32)), cyc.shape[0]))
+        return _solution(sol, cyc)
 
 
 class TorchComm:
@@ -178,3 +203,29 @@ def solve_sharded(shards: Sequence[ShardSession], comm) -> List[Solution]:
             raise RuntimeError("sharded lane: ranks disagree on convergence")
         comm.exchange(shards)
     return [sh.finish() for sh in shards]
+
+
+def connect_local(shards: Sequence[ShardSession]) -> None:
+    """Connect shards held by one process (raw device pointers)."""
+    infos = [sh.peer_info() for sh in shards]
+    for sh in shards:
+        sh.connect(infos, use_ipc=False)
+
+
+def connect_torch(shard: ShardSession, group=None) -> None:
+    """Connect one shard per process: descriptors all-gathered over
+    torch.distributed, peers' buffers opened through CUDA IPC."""
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    infos = [None] * world
+    dist.all_gather_object(infos, shard.peer_info(), group=group)
+    shard.connect(infos, use_ipc=True)
+
+
+def solve_fused(shards: Sequence[ShardSession]) -> List[Solution]:
+    """One fused solve of the local (connected) shard(s): launch every local
+    rank first -- their kernels must run concurrently, they wait for each
+    other at the cross-rank barriers -- then collect."""
+    for sh in shards:
+        sh.fused_launch()
+    return [sh.fused_finish() for sh in shards]

@@ -202,3 +202,82 @@ def test_torchcomm_two_processes_one_gpu():
     for rank, res, err in got:
         assert err is None, (rank, err)
         assert all(same for _, _, same, _ in res), (rank, res)
+
+
+def _fused(source, objective, world, solves=2):
+    from paper_1111_0627_b200.sharded import ShardSession, connect_local, solve_fused
+    shards = [ShardSession(source, P.SolveOptions(objective=objective), r, world)
+              for r in range(world)]
+    connect_local(shards)
+    out = None
+    for _ in range(solves):  # re-solving exercises the persistent barrier epochs
+        out = solve_fused(shards)
+    return out, [sh.values() for sh in shards]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", sorted(SOURCES))
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("objective", ["min", "max"])
+def test_fused_shards_match_single(name, world, objective, monkeypatch):
+    """The fused lane (policy pushed into peer replicas inside the kernel,
+    cross-rank barriers on system-scope atomics): `world` ranks as concurrent
+    cooperative kernels sharing this box's GPU, each on 1/world of the SMs,
+    reproduce the unsharded solve bit for bit."""
+    src = SOURCES[name]()
+    a, va = _single(src, objective)
+    monkeypatch.setenv("OCM_GRID", str(148 * 4 // world))
+    sols, vals = _fused(src, objective, world)
+    for b, vb in zip(sols, vals):
+        _same(a, va, b, vb)
+        assert b.stats.launches == 1  # the whole sharded solve in one launch per rank
+
+
+def _fused_ipc_worker(rank, world, port, out_q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port),
+                      OCM_GRID=str(148 * 4 // world))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1111_0627_b200.sharded import ShardSession, connect_torch, solve_fused
+    try:
+        res = []
+        for spec in (P.Generator("uniform", n=40_000, deg=8, seed=23),
+                     P.Generator("powerlaw", n=30_000, deg=4, dmax=20_000, seed=24)):
+            for objective in ("min", "max"):
+                sh = ShardSession(spec, P.SolveOptions(objective=objective), rank, world)
+                connect_torch(sh)  # descriptors over torch.distributed, buffers via CUDA IPC
+                dist.barrier()
+                (sol,) = solve_fused([sh])
+                ref = P.Session.generated(spec, P.SolveOptions(objective=objective))
+                rs = ref.solve()
+                same = (sol.mu_exact == rs.mu_exact and sol.cycle_vertices == rs.cycle_vertices
+                        and sol.stats.spf_passes == rs.stats.spf_passes
+                        and np.array_equal(sh.values()["key_num"], ref.values()["key_num"]))
+                res.append((str(spec.kind), objective, same))
+                dist.barrier()  # peers unmap before the next shard frees its buffers
+                del sh
+        out_q.put((rank, res, None))
+    except Exception as e:  # reported by the parent
+        out_q.put((rank, None, repr(e)))
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_fused_two_processes_ipc():
+    """The fused lane across processes, as on a multi-GPU box: each rank maps
+    its peers' replicas through CUDA IPC handles exchanged over
+    torch.distributed, and the two kernels meet at system-scope barriers.
+    Here both processes share the box's one GPU."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_fused_ipc_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = [q.get(timeout=600) for _ in procs]
+    for p in procs:
+        p.join(timeout=120)
+    for rank, res, err in got:
+        assert err is None, (rank, err)
+        assert res and all(same for _, _, same in res), (rank, res)
