@@ -415,8 +415,11 @@ def run_sharded(a, world, rank, local):
             "policy_iterations": {o: sols[0][o].stats.spf_passes for o in ("min", "max")},
             "mu": {o: str(sols[0][o].mu_exact) for o in ("min", "max")},
             "gpu_launches": int(launches), "clocks": clocks.summary(),
-            "note": "device time = CUDA events on the session stream around each sharded solve "
-                    "(launches + NCCL exchanges), max over ranks",
+            "note": ("device time = CUDA events on the session stream around each solve (one "
+                     "persistent launch per rank, exchange inside the kernel), max over ranks"
+                     if fused else
+                     "device time = CUDA events on the session stream around each sharded solve "
+                     "(launches + NCCL exchanges), max over ranks"),
         }
         print(json.dumps(line), flush=True)
 
