@@ -1183,6 +1183,7 @@ __global__ void __launch_bounds__(kBlock, kSolveMinBlocks) k_solve(KP p, int mod
     // and waits for all ranks' bumps; a bounded wait turns a missing peer into
     // an error instead of a hang. Returns false (uniformly) on timeout.
     auto xbarrier = [&](int ph) -> bool {
+        __threadfence_system(); // this thread's peer stores, before the arrival
         sync(ph);
         if (blockIdx.x == 0 && threadIdx.x == 0) {
             __threadfence_system();
