@@ -25,6 +25,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <string>
 #include <vector>
 
 #include "../../include/ocm_b200.h"
@@ -92,7 +93,7 @@ struct PrepCounters {
     unsigned max_region;
     unsigned regions_total;
     unsigned R;
-    unsigned long long bfs_ring[2]; // cumulative frontier appends (kp_bfs_coop)
+    unsigned long long bfs_ring[4]; // cumulative frontier appends (kp_bfs2_coop: fwd, bwd)
 };
 
 __global__ void kp_row32(const std::uint64_t* r64, std::uint32_t* r32, std::size_t n1) {
@@ -146,47 +147,9 @@ __global__ void kp_bwd_fill(std::uint32_t n, const std::uint32_t* row, const std
 }
 
 // Initial trim frontier among unassigned vertices: in- or out-degree 0.
-__global__ void kp_trim_seed(std::uint32_t n, const std::uint32_t* ind, const std::uint32_t* outd,
-                             std::uint32_t* lab, std::uint32_t* q, PrepCounters* pc) {
-    for (std::size_t base = blockIdx.x * std::size_t(kBlock); base < n;
-         base += gridDim.x * std::size_t(kBlock)) {
-        const std::size_t v = base + threadIdx.x;
-        bool take = false;
-        if (v < n && lab[v] == NONE && (ind[v] == 0 || outd[v] == 0)) {
-            lab[v] = static_cast<std::uint32_t>(v);
-            take = true;
-        }
-        const unsigned slot = append_block(take, &pc->q[0]);
-        if (take)
-            q[slot] = static_cast<std::uint32_t>(v);
-    }
-}
 
 // Process one trim frontier: each trimmed vertex removes its edges from the
 // neighbours' counters; a neighbour reaching zero is trimmed next.
-__global__ void kp_trim_step(const std::uint32_t* row, const std::uint32_t* tgt,
-                             const std::uint32_t* brow, const std::uint32_t* bsrc,
-                             std::uint32_t* ind, std::uint32_t* outd, std::uint32_t* lab,
-                             const std::uint32_t* qin, unsigned nin, std::uint32_t* qout,
-                             unsigned* qout_count) {
-    for (std::size_t i = tid_(); i < nin; i += stride_()) {
-        const std::uint32_t v = qin[i];
-        for (std::uint32_t e = row[v]; e < row[v + 1]; ++e) {
-            const std::uint32_t t = tgt[e];
-            if (t == v || lab[t] != NONE)
-                continue;
-            if (atomicSub(&ind[t], 1u) == 1u && atomicCAS(&lab[t], NONE, t) == NONE)
-                qout[atomicAdd(qout_count, 1u)] = t;
-        }
-        for (std::uint32_t s = brow[v]; s < brow[v + 1]; ++s) {
-            const std::uint32_t u = bsrc[s];
-            if (lab[u] != NONE)
-                continue;
-            if (atomicSub(&outd[u], 1u) == 1u && atomicCAS(&lab[u], NONE, u) == NONE)
-                qout[atomicAdd(qout_count, 1u)] = u;
-        }
-    }
-}
 
 // Recount degrees inside the unassigned subgraph (pull, no atomics).
 __global__ void kp_recount(std::uint32_t n, const std::uint32_t* row, const std::uint32_t* tgt,
@@ -228,58 +191,129 @@ __global__ void kp_pick_pivot(std::uint32_t n, const std::uint32_t* lab, const s
     warp_atomic_max(&pc->pivot, best);
 }
 
-// A whole BFS (restricted to unassigned vertices, vis[] holding the stamp)
-// in one cooperative launch, a grid barrier per level instead of a launch and
-// a host round trip. Direction-optimising: while the frontier is a sizeable
-// share of the graph a level runs bottom-up -- every unvisited vertex scans
-// its in-edges (rrow/rcol) and stops at the first visited one -- instead of
-// pushing every frontier edge through an atomic exchange. Reachability only
-// (vis is monotone), so racing readers of vis[] stay correct; a bottom-up
-// level that adds nothing means the closure is complete.
-__global__ void __launch_bounds__(kBlock) kp_bfs_coop(const std::uint32_t* row, const std::uint32_t* col,
-                                                      const std::uint32_t* rrow, const std::uint32_t* rcol,
-                                                      std::uint32_t n, const std::uint32_t* lab,
-                                                      std::uint32_t* vis, std::uint32_t stamp,
-                                                      std::uint32_t start, std::uint32_t* q0,
-                                                      std::uint32_t* q1, unsigned long long* ring_ctr) {
+// Queue-based trimming (vertices left with no in- or out-neighbour among the
+// unassigned ones are singleton components) to its fixpoint in one
+// cooperative launch: seed pass, then one grid barrier per level.
+__global__ void __launch_bounds__(kBlock) kp_trim_coop(std::uint32_t n, const std::uint32_t* row,
+                                                       const std::uint32_t* tgt, const std::uint32_t* brow,
+                                                       const std::uint32_t* bsrc, std::uint32_t* ind,
+                                                       std::uint32_t* outd, std::uint32_t* lab,
+                                                       std::uint32_t* q0, std::uint32_t* q1,
+                                                       unsigned long long* ring_ctr) {
     cooperative_groups::grid_group grid = cooperative_groups::this_grid();
     Ring ring;
     ring.init(ring_ctr);
-    if (gtid() == 0) {
-        q0[0] = start;
-        vis[start] = stamp;
+    grid.sync(); // every CTA has read the ring bases
+    for (std::size_t base = blockIdx.x * std::size_t(kBlock); base < n;
+         base += gridDim.x * std::size_t(kBlock)) {
+        const std::size_t v = base + threadIdx.x;
+        bool take = false;
+        if (v < n && lab[v] == NONE && (ind[v] == 0 || outd[v] == 0)) {
+            lab[v] = static_cast<std::uint32_t>(v);
+            take = true;
+        }
+        const std::uint64_t slot = block_append(take, ring);
+        if (take)
+            q0[slot] = static_cast<std::uint32_t>(v);
     }
-    grid.sync(); // the seed is visible and every CTA has read the ring bases
-    std::uint64_t nin = 1;
+    grid.sync();
+    std::uint64_t nin = ring.take();
     int cur = 0;
     while (nin) {
         const std::uint32_t* qin = cur ? q1 : q0;
         std::uint32_t* qout = cur ? q0 : q1;
-        if (nin > (n >> 6)) { // bottom-up
-            for (std::uint64_t v = gtid(); v < n; v += gstride()) {
-                if (lab[v] != NONE || vis[v] == stamp)
+        for (std::uint64_t i = gtid(); i < nin; i += gstride()) {
+            const std::uint32_t v = qin[i];
+            for (std::uint32_t e = row[v]; e < row[v + 1]; ++e) {
+                const std::uint32_t t = tgt[e];
+                if (t == v || lab[t] != NONE)
                     continue;
-                for (std::uint32_t e = rrow[v]; e < rrow[v + 1]; ++e)
-                    if (ldv(vis[rcol[e]]) == stamp) {
-                        vis[v] = stamp;
-                        qout[warp_append(ring)] = static_cast<std::uint32_t>(v);
-                        break;
-                    }
+                if (atomicSub(&ind[t], 1u) == 1u && atomicCAS(&lab[t], NONE, t) == NONE)
+                    qout[warp_append(ring)] = t;
             }
-        } else { // top-down
-            for (std::uint64_t i = gtid(); i < nin; i += gstride()) {
-                const std::uint32_t u = qin[i];
-                for (std::uint32_t e = row[u]; e < row[u + 1]; ++e) {
-                    const std::uint32_t t = col[e];
-                    if (lab[t] != NONE || vis[t] == stamp)
-                        continue;
-                    if (atomicExch(&vis[t], stamp) != stamp)
-                        qout[warp_append(ring)] = t;
-                }
+            for (std::uint32_t e = brow[v]; e < brow[v + 1]; ++e) {
+                const std::uint32_t u = bsrc[e];
+                if (lab[u] != NONE)
+                    continue;
+                if (atomicSub(&outd[u], 1u) == 1u && atomicCAS(&lab[u], NONE, u) == NONE)
+                    qout[warp_append(ring)] = u;
             }
         }
         grid.sync();
         nin = ring.take();
+        cur ^= 1;
+    }
+}
+
+// One BFS level (restricted to unassigned vertices, vis[] holding the
+// stamp): top-down pushes every frontier edge through an atomic exchange;
+// bottom-up -- used while the frontier is a sizeable share of the graph --
+// lets every unvisited vertex scan its in-edges (rrow/rcol) and stop at the
+// first visited one. Reachability only (vis is monotone), so racing readers
+// of vis[] stay correct; a bottom-up level that adds nothing means the
+// closure is complete.
+__device__ __forceinline__ void bfs_level(const std::uint32_t* row, const std::uint32_t* col,
+                                          const std::uint32_t* rrow, const std::uint32_t* rcol,
+                                          std::uint32_t n, const std::uint32_t* lab, std::uint32_t* vis,
+                                          std::uint32_t stamp, const std::uint32_t* qin, std::uint64_t nin,
+                                          std::uint32_t* qout, const Ring& ring) {
+    if (nin > (n >> 6)) { // bottom-up
+        for (std::uint64_t v = gtid(); v < n; v += gstride()) {
+            if (lab[v] != NONE || vis[v] == stamp)
+                continue;
+            for (std::uint32_t e = rrow[v]; e < rrow[v + 1]; ++e)
+                if (ldv(vis[rcol[e]]) == stamp) {
+                    vis[v] = stamp;
+                    qout[warp_append(ring)] = static_cast<std::uint32_t>(v);
+                    break;
+                }
+        }
+    } else { // top-down
+        for (std::uint64_t i = gtid(); i < nin; i += gstride()) {
+            const std::uint32_t u = qin[i];
+            for (std::uint32_t e = row[u]; e < row[u + 1]; ++e) {
+                const std::uint32_t t = col[e];
+                if (lab[t] != NONE || vis[t] == stamp)
+                    continue;
+                if (atomicExch(&vis[t], stamp) != stamp)
+                    qout[warp_append(ring)] = t;
+            }
+        }
+    }
+}
+
+// The forward and the backward reachability from the pivot in one
+// cooperative launch, both searches advancing one level per grid barrier
+// (instead of a launch and a host round trip per level and search).
+__global__ void __launch_bounds__(kBlock) kp_bfs2_coop(const std::uint32_t* row, const std::uint32_t* col,
+                                                       const std::uint32_t* brow, const std::uint32_t* bcol,
+                                                       std::uint32_t n, const std::uint32_t* lab,
+                                                       std::uint32_t* visf, std::uint32_t* visb,
+                                                       std::uint32_t sf, std::uint32_t sb,
+                                                       std::uint32_t start, std::uint32_t* qf0,
+                                                       std::uint32_t* qf1, std::uint32_t* qb0,
+                                                       std::uint32_t* qb1, unsigned long long* ring_ctr) {
+    cooperative_groups::grid_group grid = cooperative_groups::this_grid();
+    Ring rf, rb;
+    rf.init(ring_ctr);
+    rb.init(ring_ctr + 2);
+    if (gtid() == 0) {
+        qf0[0] = start;
+        qb0[0] = start;
+        visf[start] = sf;
+        visb[start] = sb;
+    }
+    grid.sync(); // the seed is visible and every CTA has read the ring bases
+    std::uint64_t nf = 1, nb = 1;
+    int cur = 0;
+    while (nf || nb) {
+        if (nf)
+            bfs_level(row, col, brow, bcol, n, lab, visf, sf, cur ? qf1 : qf0, nf, cur ? qf0 : qf1, rf);
+        if (nb)
+            bfs_level(brow, bcol, row, col, n, lab, visb, sb, cur ? qb1 : qb0, nb, cur ? qb0 : qb1, rb);
+        grid.sync();
+        nf = nf ? rf.take() : 0;
+        nb = nb ? rb.take() : 0;
         cur ^= 1;
     }
 }
@@ -622,6 +656,22 @@ void device_prepare_csr(std::uint32_t n, std::uint64_t m, DBuf<std::uint32_t>& r
 
     // ---- backward CSR (no self-loops)
     const auto t_scc = std::chrono::steady_clock::now();
+    // OCM_PREP_TIMING: per-step wall times of the region split (syncs the
+    // stream at each mark; diagnostics only)
+    static const bool timing = std::getenv("OCM_PREP_TIMING") != nullptr;
+    std::string tmarks;
+    auto t_last = t_scc;
+    auto mark = [&](const char* what) {
+        if (!timing)
+            return;
+        CK(cudaStreamSynchronize(s));
+        const auto t = std::chrono::steady_clock::now();
+        char buf[96];
+        std::snprintf(buf, sizeof buf, "%s\"%s\": %.3f", tmarks.empty() ? "" : ", ", what,
+                      std::chrono::duration<double, std::milli>(t - t_last).count());
+        tmarks += buf;
+        t_last = t;
+    };
     DBuf<std::uint32_t> brow, bsrc, cursor;
     brow.alloc(std::size_t(n) + 1, s);
     CK(cudaMemsetAsync(brow.p + n, 0, 4, s));
@@ -640,6 +690,7 @@ void device_prepare_csr(std::uint32_t n, std::uint64_t m, DBuf<std::uint32_t>& r
     CK(cudaMemcpyAsync(cursor.p, brow.p, std::size_t(n) * 4, cudaMemcpyDeviceToDevice, s));
     kp_bwd_fill<<<gv, kBlock, 0, s>>>(n, row.p, tgt.p, cursor.p, bsrc.p);
     cursor.release();
+    mark("bwd_csr");
 
     // ---- SCC
     DBuf<std::uint32_t> lab, q0, q1, visf, visb, aux;
@@ -652,23 +703,21 @@ void device_prepare_csr(std::uint32_t n, std::uint64_t m, DBuf<std::uint32_t>& r
     CK(cudaMemsetAsync(visf.p, 0, std::size_t(n) * 4, s));
     CK(cudaMemsetAsync(visb.p, 0, std::size_t(n) * 4, s));
     std::uint32_t stamp = 0;
-    DBuf<std::uint32_t>* qs[2] = {&q0, &q1};
 
     auto trim = [&] {
-        CK(cudaMemsetAsync(&pcd.p->q[0], 0, 8, s));
-        kp_trim_seed<<<gv, kBlock, 0, s>>>(n, ind.p, outd.p, lab.p, q0.p, pcd.p);
-        read_pc();
-        unsigned cnt = pc.q[0];
-        int cur = 0;
-        while (cnt) {
-            CK(cudaMemsetAsync(&pcd.p->q[cur ^ 1], 0, 4, s));
-            kp_trim_step<<<grid_for(cnt, sms), kBlock, 0, s>>>(
-                row.p, tgt.p, brow.p, bsrc.p, ind.p, outd.p, lab.p, qs[cur]->p, cnt,
-                qs[cur ^ 1]->p, &pcd.p->q[cur ^ 1]);
-            read_pc();
-            cnt = pc.q[cur ^ 1];
-            cur ^= 1;
+        static int trim_per_sm = 0;
+        if (!trim_per_sm) {
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&trim_per_sm, kp_trim_coop, kBlock, 0));
+            trim_per_sm = std::max(1, std::min(trim_per_sm, 8));
         }
+        std::uint32_t nn = n;
+        const std::uint32_t *r = row.p, *t = tgt.p, *br = brow.p, *bs = bsrc.p;
+        std::uint32_t *ip = ind.p, *op = outd.p, *lp = lab.p, *a0 = q0.p, *a1 = q1.p;
+        unsigned long long* rc = pcd.p->bfs_ring;
+        void* args[] = {&nn, &r, &t, &br, &bs, &ip, &op, &lp, &a0, &a1, &rc};
+        CK(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(&kp_trim_coop),
+                                       dim3(std::min(trim_per_sm * sms, grid_for(n, sms, 8))),
+                                       dim3(kBlock), args, 0, s));
     };
     auto remaining = [&] {
         CK(cudaMemsetAsync(&pcd.p->remaining, 0, 4, s));
@@ -676,33 +725,39 @@ void device_prepare_csr(std::uint32_t n, std::uint64_t m, DBuf<std::uint32_t>& r
         read_pc();
         return pc.remaining;
     };
-    static int bfs_per_sm = 0; // cooperative occupancy of kp_bfs_coop (same on every device here)
+    static int bfs_per_sm = 0; // cooperative occupancy of kp_bfs2_coop (same on every device here)
     if (!bfs_per_sm) {
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bfs_per_sm, kp_bfs_coop, kBlock, 0));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bfs_per_sm, kp_bfs2_coop, kBlock, 0));
         bfs_per_sm = std::max(1, std::min(bfs_per_sm, 8));
     }
-    auto bfs = [&](const std::uint32_t* r, const std::uint32_t* c, const std::uint32_t* rr,
-                   const std::uint32_t* rc_, std::uint32_t* vis, std::uint32_t st, std::uint32_t start) {
-        const std::uint32_t* lp = lab.p;
-        std::uint32_t* a0 = q0.p;
-        std::uint32_t* a1 = q1.p;
+    DBuf<std::uint32_t> qb0, qb1; // backward-search frontiers
+    auto bfs_both = [&](std::uint32_t sf, std::uint32_t sb, std::uint32_t start) {
+        qb0.alloc(std::max<std::uint32_t>(n, 1), s);
+        qb1.alloc(std::max<std::uint32_t>(n, 1), s);
+        const std::uint32_t *r = row.p, *c = tgt.p, *br = brow.p, *bc = bsrc.p, *lp = lab.p;
+        std::uint32_t *vf = visf.p, *vb = visb.p, *f0 = q0.p, *f1 = q1.p, *b0 = qb0.p, *b1 = qb1.p;
         unsigned long long* rc = pcd.p->bfs_ring;
         std::uint32_t nn = n;
-        void* args[] = {&r, &c, &rr, &rc_, &nn, &lp, &vis, &st, &start, &a0, &a1, &rc};
-        CK(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(&kp_bfs_coop),
+        void* args[] = {&r, &c, &br, &bc, &nn, &lp, &vf, &vb, &sf, &sb, &start, &f0, &f1, &b0, &b1, &rc};
+        CK(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(&kp_bfs2_coop),
                                        dim3(bfs_per_sm * sms), dim3(kBlock), args, 0, s));
+        qb0.release();
+        qb1.release();
     };
 
     trim();
+    mark("trim");
     if (remaining()) {
+        mark("recount");
         // forward/backward reachability from the best-connected pivot
         CK(cudaMemsetAsync(&pcd.p->pivot, 0, 8, s));
         kp_pick_pivot<<<gv, kBlock, 0, s>>>(n, lab.p, ind.p, outd.p, pcd.p);
         read_pc();
         const std::uint32_t pivot = 0xffffffffu - static_cast<std::uint32_t>(pc.pivot & 0xffffffffull);
         const std::uint32_t sf = ++stamp, sb = ++stamp;
-        bfs(row.p, tgt.p, brow.p, bsrc.p, visf.p, sf, pivot);
-        bfs(brow.p, bsrc.p, row.p, tgt.p, visb.p, sb, pivot);
+        mark("pivot");
+        bfs_both(sf, sb, pivot);
+        mark("bfs");
         kp_assign_both<<<gv, kBlock, 0, s>>>(n, visf.p, visb.p, sf, sb, pivot, lab.p);
         // finish the rest by colouring, re-trimming between rounds
         for (;;) {
@@ -737,6 +792,7 @@ void device_prepare_csr(std::uint32_t n, std::uint64_t m, DBuf<std::uint32_t>& r
     // ---- regions: sizes, non-trivial flags, dense ids
     DBuf<std::uint32_t>& size = visf; // reuse
     CK(cudaMemsetAsync(size.p, 0, std::size_t(n) * 4, s));
+    mark("rest");
     kp_sizes<<<gv, kBlock, 0, s>>>(n, lab.p, size.p);
     DBuf<std::uint32_t> flag, rid;
     flag.alloc(std::size_t(n) + 1, s);
@@ -757,6 +813,7 @@ void device_prepare_csr(std::uint32_t n, std::uint64_t m, DBuf<std::uint32_t>& r
 
     // ---- intra-region CSR
     DBuf<std::uint32_t>& cnt = rid; // reuse (n+1)
+    mark("regions");
     kp_count_intra<<<gv, kBlock, 0, s>>>(n, R, row.p, tgt.p, d.reg.p, cnt.p);
     CK(cudaMemsetAsync(cnt.p + n, 0, 4, s));
     exclusive_scan(cnt.p, d.row.p, std::size_t(n) + 1, s);
@@ -779,8 +836,9 @@ void device_prepare_csr(std::uint32_t n, std::uint64_t m, DBuf<std::uint32_t>& r
     if (info.exact && pc.bad_weight)
         throw UnsupportedError("integer weights beyond 32 bits are not supported by the device lane");
     info.max_abs_w = static_cast<long long>(max_abs);
+    mark("pack");
     if (std::getenv("OCM_PREP_TIMING"))
-        std::fprintf(stderr, "{\"scc_ms\": %.3f, \"pack_ms\": %.3f, \"R\": %u}\n", info.scc_ms,
+        std::fprintf(stderr, "{%s}\n{\"scc_ms\": %.3f, \"pack_ms\": %.3f, \"R\": %u}\n", tmarks.c_str(), info.scc_ms,
                      std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_pack).count(),
                      R);
 }
