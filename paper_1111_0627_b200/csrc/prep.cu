@@ -60,29 +60,6 @@ __device__ __forceinline__ std::size_t tid_() {
 }
 __device__ __forceinline__ std::size_t stride_() { return std::size_t(gridDim.x) * blockDim.x; }
 
-__device__ __forceinline__ unsigned append_block(bool take, unsigned* counter) {
-    __shared__ unsigned s_cnt[kBlock / 32];
-    __shared__ unsigned s_base;
-    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const unsigned bal = __ballot_sync(FULL, take);
-    if (lane == 0)
-        s_cnt[warp] = __popc(bal);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        unsigned tot = 0;
-        for (unsigned w = 0; w < blockDim.x / 32; ++w) {
-            const unsigned c = s_cnt[w];
-            s_cnt[w] = tot;
-            tot += c;
-        }
-        s_base = tot ? atomicAdd(counter, tot) : 0u;
-    }
-    __syncthreads();
-    const unsigned slot = s_base + s_cnt[warp] + __popc(bal & ((1u << lane) - 1u));
-    __syncthreads();
-    return slot;
-}
-
 struct PrepCounters {
     unsigned q[2];       // frontier sizes
     unsigned remaining;  // unassigned vertices
@@ -93,7 +70,7 @@ struct PrepCounters {
     unsigned max_region;
     unsigned regions_total;
     unsigned R;
-    unsigned long long bfs_ring[4]; // cumulative frontier appends (kp_bfs2_coop: fwd, bwd)
+    unsigned long long bfs_ring[4]; // cumulative append counters (kp_scc_coop: fwd, bwd; kp_trim_coop)
 };
 
 __global__ void kp_row32(const std::uint64_t* r64, std::uint32_t* r32, std::size_t n1) {
@@ -177,33 +154,15 @@ __global__ void kp_recount(std::uint32_t n, const std::uint32_t* row, const std:
         atomicAdd(&pc->remaining, rem);
 }
 
-__global__ void kp_pick_pivot(std::uint32_t n, const std::uint32_t* lab, const std::uint32_t* ind,
-                              const std::uint32_t* outd, PrepCounters* pc) {
-    unsigned long long best = 0;
-    for (std::size_t vv = tid_(); vv < n; vv += stride_()) {
-        if (lab[vv] != NONE)
-            continue;
-        const unsigned long long score =
-            min(0xffffffffull, (1ull + ind[vv]) * (1ull + outd[vv]));
-        const unsigned long long key = (score << 32) | (0xffffffffull - vv);
-        best = key > best ? key : best;
-    }
-    warp_atomic_max(&pc->pivot, best);
-}
 
 // Queue-based trimming (vertices left with no in- or out-neighbour among the
 // unassigned ones are singleton components) to its fixpoint in one
 // cooperative launch: seed pass, then one grid barrier per level.
-__global__ void __launch_bounds__(kBlock) kp_trim_coop(std::uint32_t n, const std::uint32_t* row,
-                                                       const std::uint32_t* tgt, const std::uint32_t* brow,
-                                                       const std::uint32_t* bsrc, std::uint32_t* ind,
-                                                       std::uint32_t* outd, std::uint32_t* lab,
-                                                       std::uint32_t* q0, std::uint32_t* q1,
-                                                       unsigned long long* ring_ctr) {
-    cooperative_groups::grid_group grid = cooperative_groups::this_grid();
-    Ring ring;
-    ring.init(ring_ctr);
-    grid.sync(); // every CTA has read the ring bases
+__device__ __forceinline__ void trim_fixpoint(cooperative_groups::grid_group& grid, std::uint32_t n,
+                                              const std::uint32_t* row, const std::uint32_t* tgt,
+                                              const std::uint32_t* brow, const std::uint32_t* bsrc,
+                                              std::uint32_t* ind, std::uint32_t* outd, std::uint32_t* lab,
+                                              std::uint32_t* q0, std::uint32_t* q1, Ring& ring) {
     for (std::size_t base = blockIdx.x * std::size_t(kBlock); base < n;
          base += gridDim.x * std::size_t(kBlock)) {
         const std::size_t v = base + threadIdx.x;
@@ -245,86 +204,185 @@ __global__ void __launch_bounds__(kBlock) kp_trim_coop(std::uint32_t n, const st
     }
 }
 
-// One BFS level (restricted to unassigned vertices, vis[] holding the
-// stamp): top-down pushes every frontier edge through an atomic exchange;
-// bottom-up -- used while the frontier is a sizeable share of the graph --
-// lets every unvisited vertex scan its in-edges (rrow/rcol) and stop at the
-// first visited one. Reachability only (vis is monotone), so racing readers
-// of vis[] stay correct; a bottom-up level that adds nothing means the
-// closure is complete.
+__global__ void __launch_bounds__(kBlock) kp_trim_coop(std::uint32_t n, const std::uint32_t* row,
+                                                       const std::uint32_t* tgt, const std::uint32_t* brow,
+                                                       const std::uint32_t* bsrc, std::uint32_t* ind,
+                                                       std::uint32_t* outd, std::uint32_t* lab,
+                                                       std::uint32_t* q0, std::uint32_t* q1,
+                                                       unsigned long long* ring_ctr) {
+    cooperative_groups::grid_group grid = cooperative_groups::this_grid();
+    Ring ring;
+    ring.init(ring_ctr);
+    grid.sync(); // every CTA has read the ring bases
+    trim_fixpoint(grid, n, row, tgt, brow, bsrc, ind, outd, lab, q0, q1, ring);
+}
+
+// One BFS level (restricted to unassigned vertices; vis[v] = the level that
+// reached v, 0 = not reached). Top-down pushes every frontier edge through a
+// CAS and lists the newly reached vertices (warp-aggregated appends: the
+// frontier is short here). Bottom-up -- used while the frontier is a sizeable
+// share of the graph -- lets every unreached vertex scan its in-edges
+// (rrow/rcol) and stop at the first reached one; it lists nothing (one
+// contended append per hit would serialise on the counter) and only counts
+// the hits per block. Reachability only (vis is monotone), so racing readers
+// of vis[] stay correct.
 __device__ __forceinline__ void bfs_level(const std::uint32_t* row, const std::uint32_t* col,
                                           const std::uint32_t* rrow, const std::uint32_t* rcol,
                                           std::uint32_t n, const std::uint32_t* lab, std::uint32_t* vis,
-                                          std::uint32_t stamp, const std::uint32_t* qin, std::uint64_t nin,
-                                          std::uint32_t* qout, const Ring& ring) {
-    if (nin > (n >> 6)) { // bottom-up
+                                          std::uint32_t level, bool bottom_up, const std::uint32_t* qin,
+                                          std::uint64_t nin, std::uint32_t* qout, const Ring& ring) {
+    if (bottom_up) {
+        unsigned got = 0;
         for (std::uint64_t v = gtid(); v < n; v += gstride()) {
-            if (lab[v] != NONE || vis[v] == stamp)
+            if (lab[v] != NONE || vis[v] != 0)
                 continue;
-            for (std::uint32_t e = rrow[v]; e < rrow[v + 1]; ++e)
-                if (ldv(vis[rcol[e]]) == stamp) {
-                    vis[v] = stamp;
-                    qout[warp_append(ring)] = static_cast<std::uint32_t>(v);
+            const std::uint32_t b = rrow[v], e_end = rrow[v + 1];
+            // 8 in-neighbours and their marks in flight at a time
+            for (std::uint32_t e0 = b; e0 < e_end; e0 += 8) {
+                std::uint32_t src[8];
+                bool hit = false;
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    src[u] = rcol[min(e0 + u, e_end - 1)];
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    hit |= ldv(vis[src[u]]) != 0;
+                if (hit) {
+                    vis[v] = level;
+                    ++got;
                     break;
                 }
+            }
         }
-    } else { // top-down
+        block_count(got, ring);
+    } else {
         for (std::uint64_t i = gtid(); i < nin; i += gstride()) {
             const std::uint32_t u = qin[i];
             for (std::uint32_t e = row[u]; e < row[u + 1]; ++e) {
                 const std::uint32_t t = col[e];
-                if (lab[t] != NONE || vis[t] == stamp)
+                if (lab[t] != NONE || vis[t] != 0)
                     continue;
-                if (atomicExch(&vis[t], stamp) != stamp)
+                if (atomicCAS(&vis[t], 0u, level) == 0u)
                     qout[warp_append(ring)] = t;
             }
         }
     }
 }
 
-// The forward and the backward reachability from the pivot in one
-// cooperative launch, both searches advancing one level per grid barrier
-// (instead of a launch and a host round trip per level and search).
-__global__ void __launch_bounds__(kBlock) kp_bfs2_coop(const std::uint32_t* row, const std::uint32_t* col,
-                                                       const std::uint32_t* brow, const std::uint32_t* bcol,
-                                                       std::uint32_t n, const std::uint32_t* lab,
-                                                       std::uint32_t* visf, std::uint32_t* visb,
-                                                       std::uint32_t sf, std::uint32_t sb,
-                                                       std::uint32_t start, std::uint32_t* qf0,
-                                                       std::uint32_t* qf1, std::uint32_t* qb0,
-                                                       std::uint32_t* qb1, unsigned long long* ring_ctr) {
-    cooperative_groups::grid_group grid = cooperative_groups::this_grid();
-    Ring rf, rb;
-    rf.init(ring_ctr);
-    rb.init(ring_ctr + 2);
-    if (gtid() == 0) {
-        qf0[0] = start;
-        qb0[0] = start;
-        visf[start] = sf;
-        visb[start] = sb;
-    }
-    grid.sync(); // the seed is visible and every CTA has read the ring bases
-    std::uint64_t nf = 1, nb = 1;
-    int cur = 0;
-    while (nf || nb) {
-        if (nf)
-            bfs_level(row, col, brow, bcol, n, lab, visf, sf, cur ? qf1 : qf0, nf, cur ? qf0 : qf1, rf);
-        if (nb)
-            bfs_level(brow, bcol, row, col, n, lab, visb, sb, cur ? qb1 : qb0, nb, cur ? qb0 : qb1, rb);
-        grid.sync();
-        nf = nf ? rf.take() : 0;
-        nb = nb ? rb.take() : 0;
-        cur ^= 1;
+// The frontier of a top-down level that follows a bottom-up one: the
+// vertices the bottom-up level reached (block-aggregated appends).
+__device__ __forceinline__ void bfs_collect(std::uint32_t n, const std::uint32_t* vis, std::uint32_t level,
+                                            std::uint32_t* qout, const Ring& ring) {
+    for (std::size_t base = blockIdx.x * std::size_t(kBlock); base < n;
+         base += gridDim.x * std::size_t(kBlock)) {
+        const std::size_t v = base + threadIdx.x;
+        const bool take = v < n && vis[v] == level;
+        const std::uint64_t slot = block_append(take, ring);
+        if (take)
+            qout[slot] = static_cast<std::uint32_t>(v);
     }
 }
 
-__global__ void kp_assign_both(std::uint32_t n, const std::uint32_t* visf, const std::uint32_t* visb,
-                               std::uint32_t sf, std::uint32_t sb, std::uint32_t pivot,
-                               std::uint32_t* lab) {
-    for (std::size_t v = tid_(); v < n; v += stride_())
-        if (lab[v] == NONE && visf[v] == sf && visb[v] == sb)
-            lab[v] = pivot;
+
+// The whole first pass of the region split in one cooperative launch:
+// trimming to its fixpoint, the pivot (max (1+in)(1+out) among the
+// survivors, least id on ties), forward and backward reachability, the
+// pivot's component, and the count of vertices still unassigned (which
+// decides whether the colouring fallback runs). One host read follows.
+__global__ void __launch_bounds__(kBlock) kp_scc_coop(std::uint32_t n, const std::uint32_t* row,
+                                                      const std::uint32_t* col, const std::uint32_t* brow,
+                                                      const std::uint32_t* bcol, std::uint32_t* ind,
+                                                      std::uint32_t* outd, std::uint32_t* lab,
+                                                      std::uint32_t* visf, std::uint32_t* visb,
+                                                      std::uint32_t* qf0, std::uint32_t* qf1,
+                                                      std::uint32_t* qb0, std::uint32_t* qb1,
+                                                      PrepCounters* pc) {
+    cooperative_groups::grid_group grid = cooperative_groups::this_grid();
+    Ring rf, rb;
+    rf.init(pc->bfs_ring);
+    rb.init(pc->bfs_ring + 2);
+    grid.sync(); // every CTA has read the ring bases
+    trim_fixpoint(grid, n, row, col, brow, bcol, ind, outd, lab, qf0, qf1, rf);
+    // trimming kept ind/outd exact for the surviving subgraph
+    {
+        unsigned long long best = 0;
+        unsigned rem = 0;
+        for (std::size_t v = gtid(); v < n; v += gstride()) {
+            if (lab[v] != NONE)
+                continue;
+            ++rem;
+            const unsigned long long score = min(0xffffffffull, (1ull + ind[v]) * (1ull + outd[v]));
+            const unsigned long long key = (score << 32) | (0xffffffffull - v);
+            best = key > best ? key : best;
+        }
+        warp_atomic_max(&pc->pivot, best);
+        block_count(rem, rb);
+    }
+    grid.sync();
+    if (rb.take() == 0) {
+        if (gtid() == 0)
+            pc->remaining = 0;
+        return;
+    }
+    const std::uint32_t start = 0xffffffffu - static_cast<std::uint32_t>(ldr(pc->pivot) & 0xffffffffull);
+    if (gtid() == 0) {
+        qf0[0] = start;
+        qb0[0] = start;
+        visf[start] = 1;
+        visb[start] = 1;
+    }
+    grid.sync(); // the seed is visible
+    std::uint64_t nf = 1, nb = 1;
+    bool f_was_bu = false, b_was_bu = false;
+    int cf = 0, cb = 0; // which queue holds the current frontier
+    const std::uint64_t bu_from = n >> 6;
+    for (std::uint32_t level = 2; nf || nb; ++level) {
+        const bool f_bu = nf > bu_from, b_bu = nb > bu_from;
+        const bool f_cmp = nf && !f_bu && f_was_bu, b_cmp = nb && !b_bu && b_was_bu;
+        if (f_cmp || b_cmp) {
+            if (f_cmp)
+                bfs_collect(n, visf, level - 1, cf ? qf1 : qf0, rf);
+            if (b_cmp)
+                bfs_collect(n, visb, level - 1, cb ? qb1 : qb0, rb);
+            grid.sync();
+            if (f_cmp)
+                nf = rf.take();
+            if (b_cmp)
+                nb = rb.take();
+        }
+        if (nf)
+            bfs_level(row, col, brow, bcol, n, lab, visf, level, f_bu, cf ? qf1 : qf0, nf, cf ? qf0 : qf1, rf);
+        if (nb)
+            bfs_level(brow, bcol, row, col, n, lab, visb, level, b_bu, cb ? qb1 : qb0, nb, cb ? qb0 : qb1, rb);
+        grid.sync();
+        if (nf) {
+            f_was_bu = f_bu;
+            nf = rf.take();
+            cf ^= 1;
+        }
+        if (nb) {
+            b_was_bu = b_bu;
+            nb = rb.take();
+            cb ^= 1;
+        }
+    }
+    // the pivot's component; count what is left for the colouring
+    unsigned rem = 0;
+    for (std::size_t v = gtid(); v < n; v += gstride()) {
+        if (lab[v] != NONE)
+            continue;
+        if (visf[v] != 0 && visb[v] != 0)
+            lab[v] = start;
+        else
+            ++rem;
+    }
+    block_count(rem, rf);
+    grid.sync();
+    const std::uint64_t left = rf.take();
+    if (gtid() == 0)
+        pc->remaining = static_cast<unsigned>(left);
 }
+
 
 // Colouring: colour = max id among vertices reaching v (in-place, pull).
 __global__ void kp_color_init(std::uint32_t n, const std::uint32_t* lab, std::uint32_t* color) {
@@ -523,7 +581,6 @@ template <class T> void exclusive_scan(const T* in, T* out, std::size_t n, cudaS
     DBuf<unsigned char> tmp;
     tmp.alloc(std::max<std::size_t>(bytes, 1), s);
     CK(cub::DeviceScan::ExclusiveSum(tmp.p, bytes, in, out, n, s));
-    CK(cudaStreamSynchronize(s));
 }
 
 } // namespace
@@ -683,9 +740,9 @@ void device_prepare_csr(std::uint32_t n, std::uint64_t m, DBuf<std::uint32_t>& r
         CK(cudaMemcpyAsync(ind1.p, ind.p, std::size_t(n) * 4, cudaMemcpyDeviceToDevice, s));
         exclusive_scan(ind1.p, brow.p, std::size_t(n) + 1, s);
     }
-    std::uint32_t mb = 0;
-    CK(cudaMemcpy(&mb, brow.p + n, 4, cudaMemcpyDeviceToHost));
-    bsrc.alloc(std::max<std::uint32_t>(mb, 1), s);
+    // sized by m (an upper bound: self-loops are left out) instead of a
+    // host read of brow[n]
+    bsrc.alloc(std::max<std::uint64_t>(m, 1), s);
     cursor.alloc(std::max<std::uint32_t>(n, 1), s);
     CK(cudaMemcpyAsync(cursor.p, brow.p, std::size_t(n) * 4, cudaMemcpyDeviceToDevice, s));
     kp_bwd_fill<<<gv, kBlock, 0, s>>>(n, row.p, tgt.p, cursor.p, bsrc.p);
@@ -725,40 +782,35 @@ void device_prepare_csr(std::uint32_t n, std::uint64_t m, DBuf<std::uint32_t>& r
         read_pc();
         return pc.remaining;
     };
-    static int bfs_per_sm = 0; // cooperative occupancy of kp_bfs2_coop (same on every device here)
-    if (!bfs_per_sm) {
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bfs_per_sm, kp_bfs2_coop, kBlock, 0));
-        bfs_per_sm = std::max(1, std::min(bfs_per_sm, 8));
-    }
-    DBuf<std::uint32_t> qb0, qb1; // backward-search frontiers
-    auto bfs_both = [&](std::uint32_t sf, std::uint32_t sb, std::uint32_t start) {
+    // trimming, pivot, both reachability searches and the pivot's component
+    // in one cooperative launch
+    {
+        static int scc_per_sm = 0; // cooperative occupancy of kp_scc_coop
+        if (!scc_per_sm) {
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&scc_per_sm, kp_scc_coop, kBlock, 0));
+            scc_per_sm = std::max(1, std::min(scc_per_sm, 8));
+        }
+        DBuf<std::uint32_t> qb0, qb1; // backward-search frontiers
         qb0.alloc(std::max<std::uint32_t>(n, 1), s);
         qb1.alloc(std::max<std::uint32_t>(n, 1), s);
-        const std::uint32_t *r = row.p, *c = tgt.p, *br = brow.p, *bc = bsrc.p, *lp = lab.p;
-        std::uint32_t *vf = visf.p, *vb = visb.p, *f0 = q0.p, *f1 = q1.p, *b0 = qb0.p, *b1 = qb1.p;
-        unsigned long long* rc = pcd.p->bfs_ring;
+        CK(cudaMemsetAsync(&pcd.p->pivot, 0, 8, s));
         std::uint32_t nn = n;
-        void* args[] = {&r, &c, &br, &bc, &nn, &lp, &vf, &vb, &sf, &sb, &start, &f0, &f1, &b0, &b1, &rc};
-        CK(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(&kp_bfs2_coop),
-                                       dim3(bfs_per_sm * sms), dim3(kBlock), args, 0, s));
+        const std::uint32_t *r = row.p, *c = tgt.p, *br = brow.p, *bc = bsrc.p;
+        std::uint32_t *ip = ind.p, *op = outd.p, *lp = lab.p, *vf = visf.p, *vb = visb.p, *f0 = q0.p,
+                      *f1 = q1.p, *b0 = qb0.p, *b1 = qb1.p;
+        PrepCounters* pp = pcd.p;
+        void* args[] = {&nn, &r, &c, &br, &bc, &ip, &op, &lp, &vf, &vb, &f0, &f1, &b0, &b1, &pp};
+        CK(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(&kp_scc_coop),
+                                       dim3(std::min(scc_per_sm * sms, grid_for(n, sms, 8))), dim3(kBlock),
+                                       args, 0, s));
         qb0.release();
         qb1.release();
-    };
-
-    trim();
-    mark("trim");
-    if (remaining()) {
-        mark("recount");
-        // forward/backward reachability from the best-connected pivot
-        CK(cudaMemsetAsync(&pcd.p->pivot, 0, 8, s));
-        kp_pick_pivot<<<gv, kBlock, 0, s>>>(n, lab.p, ind.p, outd.p, pcd.p);
-        read_pc();
-        const std::uint32_t pivot = 0xffffffffu - static_cast<std::uint32_t>(pc.pivot & 0xffffffffull);
-        const std::uint32_t sf = ++stamp, sb = ++stamp;
-        mark("pivot");
-        bfs_both(sf, sb, pivot);
-        mark("bfs");
-        kp_assign_both<<<gv, kBlock, 0, s>>>(n, visf.p, visb.p, sf, sb, pivot, lab.p);
+    }
+    read_pc();
+    mark("trim_bfs");
+    if (pc.remaining) {
+        // visf holds BFS levels: clear it for the colouring's stamps
+        CK(cudaMemsetAsync(visf.p, 0, std::size_t(n) * 4, s));
         // finish the rest by colouring, re-trimming between rounds
         for (;;) {
             if (!remaining())
@@ -800,9 +852,9 @@ void device_prepare_csr(std::uint32_t n, std::uint64_t m, DBuf<std::uint32_t>& r
     CK(cudaMemsetAsync(flag.p + n, 0, 4, s));
     kp_nontrivial<<<gv, kBlock, 0, s>>>(n, lab.p, size.p, self.p, flag.p, pcd.p);
     exclusive_scan(flag.p, rid.p, std::size_t(n) + 1, s);
-    std::uint32_t R = 0;
-    CK(cudaMemcpy(&R, rid.p + n, 4, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpyAsync(&pcd.p->R, rid.p + n, 4, cudaMemcpyDeviceToDevice, s));
     read_pc();
+    const std::uint32_t R = pc.R;
     info.R = R;
     info.regions_total = pc.regions_total;
     info.trivial = pc.regions_total - R;
@@ -817,8 +869,9 @@ void device_prepare_csr(std::uint32_t n, std::uint64_t m, DBuf<std::uint32_t>& r
     kp_count_intra<<<gv, kBlock, 0, s>>>(n, R, row.p, tgt.p, d.reg.p, cnt.p);
     CK(cudaMemsetAsync(cnt.p + n, 0, 4, s));
     exclusive_scan(cnt.p, d.row.p, std::size_t(n) + 1, s);
-    std::uint32_t M = 0;
-    CK(cudaMemcpy(&M, d.row.p + n, 4, cudaMemcpyDeviceToHost));
+    std::uint32_t M = 0; // stream-ordered read (the session stream does not sync with stream 0)
+    CK(cudaMemcpyAsync(&M, d.row.p + n, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
     info.M = M;
     if (info.exact)
         d.ew.alloc(std::max<std::uint32_t>(M, 1), s);
