@@ -102,7 +102,9 @@ struct ChangedMarks {
     }
 };
 
-// Read-only 8/16-byte edge records through the non-coherent path.
+// Read-only 8/16-byte edge records through the non-coherent path (an
+// evict-first L2 policy on this stream measured no gain: the phases after
+// the improvement pass are bound by random-sector throughput, not capacity).
 __device__ __forceinline__ int2 ld_edge(const int2* e) { return __ldg(e); }
 __device__ __forceinline__ FEdge ld_edge(const FEdge* e) {
     const double2 raw = __ldg(reinterpret_cast<const double2*>(e));
@@ -602,13 +604,16 @@ __device__ __forceinline__ void ph_mark(const KP& p, std::uint64_t nC, int in, s
             if (v[r] == NONE)
                 continue;
             p.comp[v[r]] = mn[r];
-            p.cyc_len[v[r]] = 0;
-            if (exact)
-                p.cyc_wi[v[r]] = 0;
             // many vertices share j: read before the exchange; the first
-            // marker lists j, so M is enumerated without another full pass
-            if (p.cmark[j[r]] != stamp && atomicExch(&p.cmark[j[r]], stamp) != stamp)
+            // marker lists j, so M is enumerated without another full pass.
+            // Only M's (length, weight) records are cleared: the anchors the
+            // check phase accumulates into lie in M whenever it passes.
+            if (p.cmark[j[r]] != stamp && atomicExch(&p.cmark[j[r]], stamp) != stamp) {
                 p.wlist[warp_append(rl)] = j[r];
+                p.cyc_len[j[r]] = 0;
+                if (exact)
+                    p.cyc_wi[j[r]] = 0;
+            }
         }
     }
 }

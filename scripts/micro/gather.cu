@@ -2,6 +2,7 @@
 // (L2-resident -> HBM-resident), U independent loads in flight per thread.
 #include <cstdio>
 #include <cstdint>
+#include <cstdlib>
 
 __device__ __forceinline__ uint64_t mix(uint64_t x) {
     x ^= x >> 33; x *= 0xff51afd7ed558ccdull; x ^= x >> 33; x *= 0xc4ceb9fe1a85ec53ull; x ^= x >> 33;
@@ -22,7 +23,7 @@ __global__ void k_gather(const long long* __restrict__ a, uint64_t n, uint64_t l
     if (acc == 42) *sink = acc;
 }
 
-int main() {
+int main(int argc, char** argv) {
     int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     long long *a, *sink;
     const uint64_t maxn = (8ull << 30) / 8; // 8 GB
@@ -31,7 +32,15 @@ int main() {
     cudaMemset(a, 1, maxn * 8);
     cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
     const uint64_t loads = 1ull << 28;
-    for (uint64_t bytes : {8ull << 20, 64ull << 20, 256ull << 20, 1ull << 30, 2ull << 30, 4ull << 30, 8ull << 30}) {
+    // sizes in MB from the command line (default: L2-resident to HBM-resident)
+    uint64_t sizes[32] = {8, 64, 256, 1024, 2048, 4096, 8192};
+    int ns = 7;
+    if (argc > 1) {
+        ns = 0;
+        for (int i = 1; i < argc && ns < 32; ++i) sizes[ns++] = strtoull(argv[i], nullptr, 10);
+    }
+    for (int si = 0; si < ns; ++si) {
+        const uint64_t bytes = sizes[si] << 20;
         const uint64_t n = bytes / 8;
         for (int blocks_per_sm : {4, 8}) {
             k_gather<8><<<sms * blocks_per_sm, 256>>>(a, n, loads, sink);
