@@ -151,6 +151,47 @@ __device__ __forceinline__ void block_append2(bool ta, const Ring& ra, std::uint
     __syncthreads();
 }
 
+// Block-wide reservation of per-thread counts on two rings (every thread
+// of the block must call it): thread slots are consecutive in thread order,
+// one atomic per ring per call.
+__device__ __forceinline__ void block_reserve2(unsigned na, const Ring& ra, std::uint64_t& sa, unsigned nb,
+                                               const Ring& rb, std::uint64_t& sb) {
+    __shared__ unsigned s_a[kBlock / 32], s_b[kBlock / 32];
+    __shared__ unsigned long long s_base_a, s_base_b;
+    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // inclusive warp scans of both counts, packed 16|16 (counts <= 65535 per warp)
+    unsigned x = na | (nb << 16);
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const unsigned y = __shfl_up_sync(FULL, x, off);
+        if (static_cast<int>(lane) >= off)
+            x += y;
+    }
+    if (lane == 31) {
+        s_a[warp] = x & 0xffffu;
+        s_b[warp] = x >> 16;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned tot_a = 0, tot_b = 0;
+        for (unsigned w = 0; w < blockDim.x / 32; ++w) {
+            const unsigned ca = s_a[w], cb = s_b[w];
+            s_a[w] = tot_a;
+            s_b[w] = tot_b;
+            tot_a += ca;
+            tot_b += cb;
+        }
+        s_base_a = tot_a ? atomicAdd(ra.counter(), static_cast<unsigned long long>(tot_a)) - ra.origin()
+                         : 0ull;
+        s_base_b = tot_b ? atomicAdd(rb.counter(), static_cast<unsigned long long>(tot_b)) - rb.origin()
+                         : 0ull;
+    }
+    __syncthreads();
+    sa = s_base_a + s_a[warp] + (x & 0xffffu) - na;
+    sb = s_base_b + s_b[warp] + (x >> 16) - nb;
+    __syncthreads();
+}
+
 // Warp-aggregated append of the calling (active) lanes: one atomic per warp.
 __device__ __forceinline__ std::uint64_t warp_append(const Ring& ring) {
     const unsigned m = __activemask();

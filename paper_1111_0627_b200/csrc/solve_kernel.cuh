@@ -440,15 +440,27 @@ __global__ void k_list_heavy(std::uint32_t n, const std::uint32_t* row, std::uin
 
 // ------------------------------------------------------------ helpers
 
+// gcd(|a|, b) for b > 0 (a cycle length): one 64-bit remainder, then the
+// Euclid steps in 32 bits (64-bit division is a long software sequence, and
+// this runs on the serial tail of every iteration).
 __device__ __forceinline__ long long gcd_ll(long long a, long long b) {
     if (a < 0)
         a = -a;
-    while (b) {
-        const long long t = a % b;
-        a = b;
-        b = t;
+    if (b <= 0 || b > 0xffffffffll) {
+        while (b) {
+            const long long t = a % b;
+            a = b;
+            b = t;
+        }
+        return a;
     }
-    return a;
+    unsigned x = static_cast<unsigned>(b), y = static_cast<unsigned>(static_cast<unsigned long long>(a) % x);
+    while (y) {
+        const unsigned t = x % y;
+        x = y;
+        y = t;
+    }
+    return x;
 }
 
 __device__ __forceinline__ bool key_in_range(__int128 k) {
@@ -532,27 +544,44 @@ __device__ __forceinline__ void ph_classify(const KP& p, int par, const Ring& ra
         p.changed[par ^ 1][r] = 0;
     }
     block_count(still, ra);
-    OCM_BLOCK_LOOP(v0, 0, p.N) {
-        const std::uint64_t v = v0_b + threadIdx.x;
-        bool leaf = false, core = false;
-        if (v < p.N && changed[__ldg(&p.reg[v])]) {
-            leaf = p.indeg[v] == 0;
-            core = !leaf;
+    // four consecutive vertices per thread, one reservation per ring per
+    // 1024 vertices (a per-256 append made the two list counters the
+    // contended words of the phase); lists stay in vertex order
+    constexpr int kV = 4;
+    for (std::uint64_t base = (blockIdx.x * std::uint64_t(kBlock) + threadIdx.x) * kV; ;
+         base += gridDim.x * std::uint64_t(kBlock) * kV) {
+        const std::uint64_t blk0 = base - threadIdx.x * kV; // block-uniform loop test
+        if (blk0 >= p.N)
+            break;
+        unsigned lbits = 0, cbits = 0;
+#pragma unroll
+        for (int k = 0; k < kV; ++k) {
+            const std::uint64_t v = base + k;
+            if (v < p.N && changed[__ldg(&p.reg[v])]) {
+                if (p.indeg[v] == 0)
+                    lbits |= 1u << k;
+                else
+                    cbits |= 1u << k;
+            }
         }
         std::uint64_t ls, cs;
-        block_append2(leaf, rl, ls, core, rc, cs);
-        if (leaf)
-            p.plist[ls] = static_cast<std::uint32_t>(v);
-        if (core) {
-            // the first doubling round, straight from the policy: the
-            // successor of a core vertex is a core vertex
-            p.clist[cs] = static_cast<std::uint32_t>(v);
-            const std::uint32_t sv = p.succ_v[v];
-            PJC x;
-            x.nxt = p.succ_v[sv];
-            x.mn = min(static_cast<std::uint32_t>(v), sv);
-            x.w = EXACT ? static_cast<long long>(p.succ_wi[v]) + p.succ_wi[sv] : 0ll;
-            p.pj[1][v] = x;
+        block_reserve2(__popc(lbits), rl, ls, __popc(cbits), rc, cs);
+#pragma unroll
+        for (int k = 0; k < kV; ++k) {
+            const std::uint32_t v = static_cast<std::uint32_t>(base + k);
+            if (lbits >> k & 1u)
+                p.plist[ls++] = v;
+            if (cbits >> k & 1u) {
+                // the first doubling round, straight from the policy: the
+                // successor of a core vertex is a core vertex
+                p.clist[cs++] = v;
+                const std::uint32_t sv = p.succ_v[v];
+                PJC x;
+                x.nxt = p.succ_v[sv];
+                x.mn = min(v, sv);
+                x.w = EXACT ? static_cast<long long>(p.succ_wi[v]) + p.succ_wi[sv] : 0ll;
+                p.pj[1][v] = x;
+            }
         }
     }
 }
@@ -819,10 +848,8 @@ __device__ __forceinline__ void wincyc_shared(const KP& p, unsigned nW, int wr) 
 // are small, computes their values itself (block barriers only); otherwise
 // it raises wc_big and the grid does it after the barrier.
 template <bool EXACT>
-__device__ __forceinline__ void ph_vote(const KP& p, std::uint64_t nM, std::uint32_t stamp,
-                                        unsigned long long done_base) {
-    Ctl* c = p.c;
-    for (std::uint64_t i = gtid(); i < nM; i += gstride()) {
+__device__ __forceinline__ void vote_pass(const KP& p, std::uint64_t nM, std::uint64_t from, std::uint64_t step) {
+    for (std::uint64_t i = from; i < nM; i += step) {
         const std::uint32_t v = p.wlist[i];
         if (p.comp[v] != v)
             continue;
@@ -837,20 +864,14 @@ __device__ __forceinline__ void ph_vote(const KP& p, std::uint64_t nM, std::uint
             cur = prev;
         }
     }
-    __shared__ int s_last;
-    __shared__ unsigned s_maxlen, s_nw;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence();
-        const unsigned long long prev = atomicAdd(&c->done, 1ull);
-        s_last = prev == done_base + gridDim.x - 1;
-        s_maxlen = 0;
-        s_nw = 0;
-        __threadfence();
-    }
-    __syncthreads();
-    if (!s_last)
-        return;
+}
+
+// Adoption and the winning cycles' values by one block (s_maxlen, s_nw
+// zeroed by the caller before its last barrier).
+template <bool EXACT>
+__device__ __forceinline__ void vote_tail(const KP& p, std::uint64_t nM, std::uint32_t stamp,
+                                          unsigned& s_maxlen, unsigned& s_nw) {
+    Ctl* c = p.c;
     for (std::uint32_t r = threadIdx.x; r < p.R; r += blockDim.x)
         if (p.active[r]) {
             const unsigned len = adopt_region<EXACT>(p, r);
@@ -890,6 +911,48 @@ __device__ __forceinline__ void ph_vote(const KP& p, std::uint64_t nM, std::uint
         __syncthreads();
     }
     wc_final(p, p.rem[1], nW, wr, threadIdx.x, blockDim.x);
+}
+
+
+template <bool EXACT>
+__device__ __forceinline__ void ph_vote(const KP& p, std::uint64_t nM, std::uint32_t stamp,
+                                        unsigned long long done_base) {
+    Ctl* c = p.c;
+    vote_pass<EXACT>(p, nM, gtid(), gstride());
+    __shared__ int s_last;
+    __shared__ unsigned s_maxlen, s_nw;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const unsigned long long prev = atomicAdd(&c->done, 1ull);
+        s_last = prev == done_base + gridDim.x - 1;
+        s_maxlen = 0;
+        s_nw = 0;
+        __threadfence();
+    }
+    __syncthreads();
+    if (s_last)
+        vote_tail<EXACT>(p, nM, stamp, s_maxlen, s_nw);
+}
+
+// Few cycle vertices (the common case once the policy settles): block 0
+// votes, adopts and computes the winning cycles' values alone while the
+// grid waits at the phase barrier -- no grid-wide completion counter (two
+// gpu-scope fences and one contended atomic per block cost more than the
+// vote itself).
+constexpr std::uint64_t kVoteOneBlock = 4096;
+
+template <bool EXACT>
+__device__ __forceinline__ void ph_vote_one_block(const KP& p, std::uint64_t nM, std::uint32_t stamp) {
+    __shared__ unsigned s_maxlen, s_nw;
+    vote_pass<EXACT>(p, nM, threadIdx.x, blockDim.x);
+    __threadfence(); // the block's slot CASes, before adoption reads the slots
+    if (threadIdx.x == 0) {
+        s_maxlen = 0;
+        s_nw = 0;
+    }
+    __syncthreads();
+    vote_tail<EXACT>(p, nM, stamp, s_maxlen, s_nw);
 }
 
 // Kept component (howard_par.hpp:370/393): vertices whose policy path
@@ -1350,8 +1413,13 @@ __global__ void __launch_bounds__(kBlock, kSolveMinBlocks) k_solve(KP p, int mod
             ph_stats_float(p, nM);
             sync(PH_STATS);
         }
-        ph_vote<EXACT>(p, nM, stamp, st.done_base);
-        st.done_base += gridDim.x;
+        if (nM <= kVoteOneBlock) {
+            if (blockIdx.x == 0)
+                ph_vote_one_block<EXACT>(p, nM, stamp);
+        } else {
+            ph_vote<EXACT>(p, nM, stamp, st.done_base);
+            st.done_base += gridDim.x;
+        }
         sync(PH_VOTE);
         if (EXACT && ldr(c->wc_big[stamp & 1]) == stamp) {
             const std::uint64_t nW = static_cast<std::uint32_t>(ldr(c->wc_n[stamp & 1]));
