@@ -53,6 +53,9 @@ namespace cg = cooperative_groups;
 #define OCM_MINB 4
 #endif
 constexpr int kSolveMinBlocks = OCM_MINB; // 4: register cap 64 at 256 threads
+#ifndef OCM_ROUND_MAX
+#define OCM_ROUND_MAX 2 // doubling steps fused into one pass (1..3)
+#endif
 
 // ------------------------------------------------------------ improvement
 //
@@ -599,6 +602,26 @@ __device__ __forceinline__ void ph_round(const KP& p, std::uint64_t nC, int in) 
         z.nxt = y.nxt;
         z.mn = min(x.mn, y.mn);
         z.w = x.w + y.w;
+        o[v] = z;
+    }
+}
+
+// S doubling steps in one pass (records of 2^k steps -> 2^(k+S)): 2^S
+// chained reads of the same buffer instead of S rounds and S-1 barriers --
+// a round's cost is mostly its barrier and the latency ramp, not its loads.
+template <int S> __device__ __forceinline__ void ph_round_multi(const KP& p, std::uint64_t nC, int in) {
+    const PJC* __restrict__ a = p.pj[in];
+    PJC* __restrict__ o = p.pj[in ^ 1];
+    for (std::uint64_t i = gtid(); i < nC; i += gstride()) {
+        const std::uint32_t v = p.clist[i];
+        PJC z = a[v];
+#pragma unroll
+        for (int h = 1; h < (1 << S); ++h) {
+            const PJC y = a[z.nxt];
+            z.nxt = y.nxt;
+            z.mn = min(z.mn, y.mn);
+            z.w += y.w;
+        }
         o[v] = z;
     }
 }
@@ -1372,10 +1395,21 @@ __global__ void __launch_bounds__(kBlock, kSolveMinBlocks) k_solve(KP p, int mod
         bool first_try = true;
         std::uint64_t nM = 0;
         for (;;) {
-            for (; k < static_cast<int>(st.k_hint); ++k, in ^= 1) {
-                ph_round(p, nC, in);
-                ++st.rounds;
+            for (const int k0 = k; k < static_cast<int>(st.k_hint); in ^= 1) {
+                const int left = static_cast<int>(st.k_hint) - k;
+                if (OCM_ROUND_MAX >= 3 && left >= 3) {
+                    ph_round_multi<3>(p, nC, in);
+                    k += 3;
+                } else if (OCM_ROUND_MAX >= 2 && left >= 2) {
+                    ph_round_multi<2>(p, nC, in);
+                    k += 2;
+                } else {
+                    ph_round(p, nC, in);
+                    ++k;
+                }
                 sync(PH_ROUND);
+                if (k >= static_cast<int>(st.k_hint))
+                    st.rounds += k - k0;
             }
             const unsigned stamp = ++st.stamp;
             ++st.verifies;
