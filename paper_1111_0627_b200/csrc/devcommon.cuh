@@ -30,6 +30,7 @@ constexpr unsigned FULL = 0xffffffffu;
 #endif
 constexpr int kBlock = OCM_BLOCK;
 constexpr int kMaxShards = 8; // ranks of the fused sharded lane (one per GPU of a box)
+constexpr int kMaxPbBins = 512; // target bins of the propagation-blocked improvement pass
 
 struct __align__(16) FEdge {
     double w;
@@ -151,6 +152,16 @@ struct KP {
     unsigned* peer_xbar[kMaxShards];
     unsigned* xbar;
     int indeg_in_improve;         // 1: the improvement pass counts policy in-degrees
+    // propagation-blocked improvement pass (exact lane, HBM-resident keys)
+    int pb;
+    const int2* pb_tw;            // bin-ordered {target, weight}
+    const std::uint32_t* pb_perm; // bin position -> edge id
+    const std::uint32_t* pb_inv;  // edge id -> bin position
+    const std::uint32_t* pb_src;  // bin position -> source vertex
+    const std::uint32_t* pb_off;  // [blk * pb_nb + b]: first position of vertex block blk in bin b
+    long long* pb_cand;           // candidate per bin position
+    std::uint64_t pb_m;
+    std::uint32_t pb_nb, pb_nblk;
     // tuning (launch arguments)
     int G;                 // improvement lanes per vertex
     int U;                 // edges in flight per lane (4)
@@ -228,6 +239,9 @@ struct DeviceState {
     DBuf<long long> key_i, lam_num, lam_den, cyc_wi;
     DBuf<unsigned long long> slot;
     DBuf<Ctl> ctl;
+    DBuf<int2> pb_tw;
+    DBuf<std::uint32_t> pb_perm, pb_inv, pb_off, pb_src;
+    DBuf<long long> pb_cand;
     Ctl* h_ctl = nullptr;
     std::vector<cudaEvent_t> ev;
     cudaEvent_t ev_start = nullptr, ev_end = nullptr;
@@ -269,6 +283,12 @@ struct DeviceState {
         cyc_wi.release();
         slot.release();
         ctl.release();
+        pb_tw.release();
+        pb_perm.release();
+        pb_inv.release();
+        pb_off.release();
+        pb_src.release();
+        pb_cand.release();
         if (stream)
             cudaStreamSynchronize(stream);
         for (cudaEvent_t e : ev)

@@ -410,9 +410,165 @@ __device__ __forceinline__ void improve_heavy(const KP& p, int* changed) {
     }
 }
 
+// ---------------------------------------- propagation-blocked improvement
+//
+// Exact lane, key arrays too large for L2: a random 8-byte
+// key gather per edge from HBM runs at ~40 G/s on B200, from L2 at ~210 G/s.
+// The edges are kept a second time ordered by target bin (pb_nb bins of
+// pb_bin vertices, a bin's keys ~16 MB) and in CSR order inside a bin, so
+//   pass 1 streams the bin-ordered {target, weight} records in order -- at any
+//          moment the grid gathers keys from one bin, which L2 holds -- and
+//          streams each candidate key[t] + w*den out (the per-vertex -num
+//          is dropped, as in improve_vertex);
+//   pass 2 takes vertex blocks of pb_vb vertices: a block's candidates are
+//          one contiguous segment per bin (pb_off), reduced to the
+//          lexicographic minimum (candidate, edge id) per vertex in shared
+//          memory -- the sequential "first strictly smaller" scan -- and the
+//          incumbent's candidate is read back through pb_inv.
+// Everything after the choice (replacement test, policy, in-degree, region
+// flags) is improve_vertex's. Heavy vertices keep the block-cooperative path.
+#ifndef OCM_PB_U
+#define OCM_PB_U 4
+#endif
+__device__ __forceinline__ void pb_pass1(const KP& p) {
+    const int2* __restrict__ tw = p.pb_tw;
+    const long long* __restrict__ key = p.key_i;
+    long long* __restrict__ cand = p.pb_cand;
+    const long long den0 = p.R == 1 ? p.lam_den[0] : 1;
+    constexpr int kU = OCM_PB_U;
+    const std::uint64_t nth = gstride();
+    for (std::uint64_t i0 = gtid(); i0 < p.pb_m; i0 += kU * nth) {
+        int2 e[kU];
+        long long k[kU], d[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u)
+            e[u] = __ldcs(&tw[min(i0 + u * nth, p.pb_m - 1)]); // streamed: evict first
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            k[u] = __ldcg(&key[static_cast<std::uint32_t>(e[u].x)]);
+            d[u] = p.R == 1 ? den0 : p.lam_den[__ldg(&p.reg[static_cast<std::uint32_t>(e[u].x)])];
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u)
+            if (i0 + u * nth < p.pb_m)
+                __stcs(&cand[i0 + u * nth], k[u] + static_cast<long long>(e[u].y) * d[u]);
+    }
+}
+
+#ifndef OCM_PB_U
+#define OCM_PB_U 4
+#endif
+constexpr int kPbVB = 1024; // vertices per pass-2 block
+
+__device__ __forceinline__ void pb_pass2(const KP& p, int* changed) {
+    __shared__ std::uint32_t s_row[kPbVB + 1];
+    __shared__ long long s_best[kPbVB];
+    __shared__ std::uint32_t s_be[kPbVB];
+    __shared__ std::uint32_t s_seg[kMaxPbBins + 1]; // exclusive prefix of segment lengths
+    __shared__ std::uint32_t s_off[kMaxPbBins];     // segment starts
+    ChangedMarks marks;
+    const std::uint32_t nb = p.pb_nb;
+    constexpr int kU = 4;
+    for (std::uint32_t blk = blockIdx.x; blk < p.pb_nblk; blk += gridDim.x) {
+        const std::uint32_t v0 = blk * kPbVB;
+        const std::uint32_t nv = min(static_cast<std::uint32_t>(kPbVB), p.N - v0);
+        const std::uint32_t* off = p.pb_off + static_cast<std::size_t>(blk) * nb;
+        for (std::uint32_t j = threadIdx.x; j <= nv; j += blockDim.x)
+            s_row[j] = __ldg(&p.row[v0 + j]);
+        for (std::uint32_t j = threadIdx.x; j < nv; j += blockDim.x) {
+            s_best[j] = 0x7fffffffffffffffll;
+            s_be[j] = NONE;
+        }
+        for (std::uint32_t b = threadIdx.x; b < nb; b += blockDim.x) {
+            const std::uint32_t o = __ldg(&off[b]);
+            s_off[b] = o;
+            s_seg[b + 1] = __ldg(&off[nb + b]) - o;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            s_seg[0] = 0;
+            for (std::uint32_t b = 1; b <= nb; ++b)
+                s_seg[b] += s_seg[b - 1];
+        }
+        __syncthreads();
+        const std::uint32_t tot = s_seg[nb];
+        // two sweeps over the block's candidates (kU in flight per thread):
+        // the minimum per vertex, then the least edge id attaining it
+        for (int sweep = 0; sweep < 2; ++sweep) {
+            for (std::uint32_t f0 = threadIdx.x; f0 < tot; f0 += kU * blockDim.x) {
+                std::uint32_t pos[kU], lv[kU];
+                long long c[kU];
+#pragma unroll
+                for (int u = 0; u < kU; ++u) {
+                    const std::uint32_t f = min(f0 + u * blockDim.x, tot - 1);
+                    std::uint32_t lo = 0, hi = nb; // s_seg[lo] <= f < s_seg[lo+1]
+                    while (hi - lo > 1) {
+                        const std::uint32_t mid = (lo + hi) >> 1;
+                        if (s_seg[mid] <= f)
+                            lo = mid;
+                        else
+                            hi = mid;
+                    }
+                    pos[u] = s_off[lo] + (f - s_seg[lo]);
+                }
+#pragma unroll
+                for (int u = 0; u < kU; ++u) {
+                    lv[u] = __ldg(&p.pb_src[pos[u]]) - v0;
+                    c[u] = __ldcg(&p.pb_cand[pos[u]]);
+                }
+#pragma unroll
+                for (int u = 0; u < kU; ++u) {
+                    if (f0 + u * blockDim.x >= tot || s_row[lv[u] + 1] - s_row[lv[u]] >= p.heavy_deg)
+                        continue; // past the end, or the block-cooperative path owns it
+                    if (sweep == 0)
+                        atomicMin(&s_best[lv[u]], c[u]);
+                    else if (c[u] == s_best[lv[u]])
+                        atomicMin(&s_be[lv[u]], __ldg(&p.pb_perm[pos[u]]));
+                }
+            }
+            __syncthreads();
+        }
+        for (std::uint32_t j = threadIdx.x; j < nv; j += blockDim.x) {
+            const std::uint32_t v = v0 + j;
+            const std::uint32_t deg = s_row[j + 1] - s_row[j];
+            if (deg == 0 || deg >= p.heavy_deg)
+                continue;
+            const std::uint32_t r = p.R == 1 ? 0u : __ldg(&p.reg[v]);
+            if (!p.active[r])
+                continue;
+            const std::uint32_t be = s_be[j];
+            const std::uint32_t cur = p.succ_e[v];
+            const bool rep = cur == NONE || s_best[j] < __ldcg(&p.pb_cand[__ldg(&p.pb_inv[cur])]);
+            if (rep) {
+                const int2 ed = __ldg(&p.ew[be]);
+                const std::uint32_t t = static_cast<std::uint32_t>(ed.x);
+                p.succ_e[v] = be;
+                p.succ_wi[v] = ed.y;
+                p.succ_v[v] = t;
+                atomicAdd(&p.indeg[t], 1u);
+                marks.note(changed, r);
+            } else {
+                atomicAdd(&p.indeg[p.succ_v[v]], 1u);
+            }
+        }
+        __syncthreads(); // shared arrays reused by the next block
+    }
+    marks.flush(changed);
+}
+
 template <bool EXACT, int G, int U> __device__ __forceinline__ void improve_phase(const KP& p, int* changed) {
     if (p.nheavy)
         improve_heavy<EXACT>(p, changed);
+    if constexpr (EXACT) {
+        if (p.pb && !p.fused) {
+            if (p.R == 1 && !p.active[0])
+                return;
+            pb_pass1(p);
+            cg::this_grid().sync();
+            pb_pass2(p, changed);
+            return;
+        }
+    }
     ChangedMarks marks;
     if (p.R == 1 && !p.active[0])
         return; // the single region finished (block-uniform: no flush needed)

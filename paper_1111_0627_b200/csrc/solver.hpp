@@ -62,6 +62,7 @@ class Session {
     int grid_ = 0; // cooperative grid of the session's k_solve instantiation
     int gi_ = 0;   // its improvement group width (index into 1, 2, 4, 8)
     std::uint32_t rank_ = 0, world_ = 1, chunk_ = 0;
+    void build_blocked_edges();
     bool shard_started_ = false;
     bool connected_ = false; // fused sharded lane: peers mapped
     double solve_ms_ = 0.0;   // event time of the current solve's launches

@@ -96,6 +96,28 @@ def test_generated_graphs_vs_oracle(n, deg, seed):
         check_against(sol, sess.values(), oracle_record(n, s, d, w, objective, "tarjan"))
 
 
+@pytest.mark.parametrize("kind,n,deg,seed", [("uniform", 20000, 4, 7), ("powerlaw", 20000, 3, 8),
+                                             ("uniform", 3000, 2, 9)])
+def test_blocked_improvement_vs_oracle(kind, n, deg, seed, monkeypatch):
+    """The propagation-blocked improvement pass (OCM_PB=1, forced here with
+    tiny target bins so every vertex block spans many bins) must choose the
+    same policy as the direct pass: identical results and iteration counts."""
+    gen = P.Generator(kind, n=n, deg=deg, dmax=256 if kind == "powerlaw" else 0, wlo=1, whi=100,
+                      seed=seed)
+    g = P.generate(gen)
+    s, d, w = g.edges()
+    for objective in ("min", "max"):
+        monkeypatch.setenv("OCM_PB", "0")
+        direct = P.Session(g, P.SolveOptions(objective=objective)).solve()
+        monkeypatch.setenv("OCM_PB", "1")
+        monkeypatch.setenv("OCM_PB_BIN", "64")
+        sess = P.Session(g, P.SolveOptions(objective=objective))
+        sol = sess.solve()
+        check_against(sol, sess.values(), oracle_record(n, s, d, w, objective, "tarjan"))
+        assert sol.stats.spf_passes == direct.stats.spf_passes
+        assert sol.cycle_vertices == direct.cycle_vertices
+
+
 def test_float_weights_generated():
     g = P.generate_uniform(5000, 3, -400, 400, 9)
     s, d, w = g.edges()
