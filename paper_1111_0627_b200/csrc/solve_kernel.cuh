@@ -459,13 +459,17 @@ __device__ __forceinline__ void pb_pass1(const KP& p) {
 #define OCM_PB_U 4
 #endif
 constexpr int kPbVB = 1024; // vertices per pass-2 block
+constexpr std::size_t kPbSmem = kPbVB * 8 + (3 * kPbVB + 2 + 2 * kMaxPbBins) * 4;
 
 __device__ __forceinline__ void pb_pass2(const KP& p, int* changed) {
-    __shared__ std::uint32_t s_row[kPbVB + 1];
-    __shared__ long long s_best[kPbVB];
-    __shared__ std::uint32_t s_be[kPbVB];
-    __shared__ std::uint32_t s_seg[kMaxPbBins + 1]; // exclusive prefix of segment lengths
-    __shared__ std::uint32_t s_off[kMaxPbBins];     // segment starts
+    // dynamic shared memory (kPbSmem bytes, given only to launches with the
+    // pass enabled: a static allocation would shrink every launch's L1)
+    extern __shared__ __align__(16) unsigned char pb_smem[];
+    long long* s_best = reinterpret_cast<long long*>(pb_smem);                  // [kPbVB]
+    std::uint32_t* s_row = reinterpret_cast<std::uint32_t*>(s_best + kPbVB);   // [kPbVB + 1]
+    std::uint32_t* s_be = s_row + kPbVB + 1;                                    // [kPbVB]
+    std::uint32_t* s_seg = s_be + kPbVB;                                        // [kMaxPbBins + 1]
+    std::uint32_t* s_off = s_seg + kMaxPbBins + 1;                              // [kMaxPbBins]
     ChangedMarks marks;
     const std::uint32_t nb = p.pb_nb;
     constexpr int kU = 4;

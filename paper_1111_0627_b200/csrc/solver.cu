@@ -437,7 +437,8 @@ template <class M> void Session::launch_async(int mode) {
     CK(cudaEventRecord(d.ev_start, s));
     if (prep_.R > 0) {
         void* args[] = {&p, &mode};
-        CK(cudaLaunchCooperativeKernel(solve_fn(EXACT, gi_), dim3(grid_), dim3(kBlock), args, 0, s));
+        CK(cudaLaunchCooperativeKernel(solve_fn(EXACT, gi_), dim3(grid_), dim3(kBlock), args,
+                                       p.pb ? kPbSmem : 0, s));
         ++launches_;
     }
     CK(cudaEventRecord(d.ev_end, s));
