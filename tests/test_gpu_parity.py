@@ -118,6 +118,27 @@ def test_blocked_improvement_vs_oracle(kind, n, deg, seed, monkeypatch):
         assert sol.cycle_vertices == direct.cycle_vertices
 
 
+@pytest.mark.parametrize("n", [60, 300, 3000, 9000])
+def test_long_winning_cycle(n):
+    """Winning cycles of every size class of the vote tail: shared-memory
+    values (one block), global-memory values (one block) and the grid-wide
+    rounds (longer than small_wc)."""
+    rng = np.random.default_rng(n)
+    ring_s = np.arange(n, dtype=np.uint32)
+    ring_d = ((ring_s + 1) % n).astype(np.uint32)
+    ring_w = rng.integers(1, 4, n).astype(np.float64)  # mean < 4
+    chord_s = rng.integers(0, n, 2 * n).astype(np.uint32)
+    chord_d = rng.integers(0, n, 2 * n).astype(np.uint32)
+    chord_w = np.full(2 * n, 1e6)  # any cycle through a chord is worse
+    s = np.concatenate([ring_s, chord_s])
+    d = np.concatenate([ring_d, chord_d])
+    w = np.concatenate([ring_w, chord_w])
+    sol, vals = run(n, s, d, w, "min")
+    ref = oracle_record(n, s, d, w, "min", "tarjan")
+    check_against(sol, vals, ref)
+    assert len(sol.cycle_vertices) == n
+
+
 def test_float_weights_generated():
     g = P.generate_uniform(5000, 3, -400, 400, 9)
     s, d, w = g.edges()
