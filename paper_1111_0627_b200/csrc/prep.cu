@@ -71,6 +71,8 @@ struct PrepCounters {
     unsigned regions_total;
     unsigned R;
     unsigned long long bfs_ring[4]; // cumulative append counters (kp_scc_coop: fwd, bwd; kp_trim_coop)
+    long long clk[4];               // kp_scc_coop block-0 SM clocks: trim, pivot, reachability, assign
+    unsigned levels;                // reachability levels
 };
 
 __global__ void kp_row32(const std::uint64_t* r64, std::uint32_t* r32, std::size_t n1) {
@@ -90,37 +92,88 @@ __global__ void kp_max_abs(std::uint64_t m, const double* w, PrepCounters* pc) {
     warp_atomic_max(&pc->max_abs_bits, mx);
 }
 
+// Thread-per-vertex edge loops would leave a power-law hub's 10^4..10^5
+// edges to one thread: these kernels take 32 vertices per warp, a lane walks
+// its own vertex's edges, and the warp walks every wide vertex's (> 32
+// edges) together.
+#define OCM_WARP_VERTICES(n, BODY_NARROW, BODY_WIDE)                                             \
+    {                                                                                            \
+        const unsigned lane = threadIdx.x & 31;                                                  \
+        const std::size_t nw_ = stride_() >> 5;                                                  \
+        for (std::size_t base_ = (tid_() >> 5) * 32; base_ < (n); base_ += nw_ * 32) {           \
+            const bool on = base_ + lane < (n);                                                  \
+            const std::uint32_t v = static_cast<std::uint32_t>(base_ + lane);                    \
+            std::uint32_t b = 0, e_end = 0;                                                      \
+            if (on) {                                                                            \
+                b = row[v];                                                                      \
+                e_end = row[v + 1];                                                              \
+            }                                                                                    \
+            const bool wide = e_end - b > 32;                                                    \
+            if (on && !wide) {                                                                   \
+                BODY_NARROW                                                                      \
+            }                                                                                    \
+            for (unsigned hv_ = __ballot_sync(FULL, wide); hv_; hv_ &= hv_ - 1) {                \
+                const int j_ = __ffs(hv_) - 1;                                                   \
+                const std::uint32_t hvx = static_cast<std::uint32_t>(base_ + j_);                \
+                const std::uint32_t hb = __shfl_sync(FULL, b, j_), he = __shfl_sync(FULL, e_end, j_); \
+                BODY_WIDE                                                                        \
+            }                                                                                    \
+        }                                                                                        \
+    }
+
 __global__ void kp_degrees(std::uint32_t n, const std::uint32_t* row, const std::uint32_t* tgt,
                            std::uint32_t* outd, std::uint32_t* ind, std::uint8_t* self) {
-    for (std::size_t vv = tid_(); vv < n; vv += stride_()) {
-        const std::uint32_t v = static_cast<std::uint32_t>(vv);
+    OCM_WARP_VERTICES(n, {
         std::uint32_t o = 0;
-        std::uint8_t s = 0;
-        for (std::uint32_t e = row[v]; e < row[v + 1]; ++e) {
+        std::uint8_t sl = 0;
+        for (std::uint32_t e = b; e < e_end; ++e) {
             const std::uint32_t t = tgt[e];
             if (t == v) {
-                s = 1;
+                sl = 1;
             } else {
                 ++o;
                 atomicAdd(&ind[t], 1u);
             }
         }
         outd[v] = o;
-        self[v] = s;
-    }
+        self[v] = sl;
+    }, {
+        std::uint32_t o = 0;
+        bool sl = false;
+        for (std::uint32_t e = hb + lane; e < he; e += 32) {
+            const std::uint32_t t = tgt[e];
+            if (t == hvx) {
+                sl = true;
+            } else {
+                ++o;
+                atomicAdd(&ind[t], 1u);
+            }
+        }
+        o = __reduce_add_sync(FULL, o);
+        sl = __any_sync(FULL, sl);
+        if (lane == 0) {
+            outd[hvx] = o;
+            self[hvx] = sl ? 1 : 0;
+        }
+    })
 }
 
 // Backward CSR (no self-loops): bsrc grouped by target.
 __global__ void kp_bwd_fill(std::uint32_t n, const std::uint32_t* row, const std::uint32_t* tgt,
                             std::uint32_t* cursor, std::uint32_t* bsrc) {
-    for (std::size_t vv = tid_(); vv < n; vv += stride_()) {
-        const std::uint32_t v = static_cast<std::uint32_t>(vv);
-        for (std::uint32_t e = row[v]; e < row[v + 1]; ++e) {
+    OCM_WARP_VERTICES(n, {
+        for (std::uint32_t e = b; e < e_end; ++e) {
             const std::uint32_t t = tgt[e];
             if (t != v)
                 bsrc[atomicAdd(&cursor[t], 1u)] = v;
         }
-    }
+    }, {
+        for (std::uint32_t e = hb + lane; e < he; e += 32) {
+            const std::uint32_t t = tgt[e];
+            if (t != hvx)
+                bsrc[atomicAdd(&cursor[t], 1u)] = hvx;
+        }
+    })
 }
 
 // Initial trim frontier among unassigned vertices: in- or out-degree 0.
@@ -256,14 +309,37 @@ __device__ __forceinline__ void bfs_level(const std::uint32_t* row, const std::u
         }
         block_count(got, ring);
     } else {
-        for (std::uint64_t i = gtid(); i < nin; i += gstride()) {
-            const std::uint32_t u = qin[i];
-            for (std::uint32_t e = row[u]; e < row[u + 1]; ++e) {
-                const std::uint32_t t = col[e];
-                if (lab[t] != NONE || vis[t] != 0)
-                    continue;
-                if (atomicCAS(&vis[t], 0u, level) == 0u)
-                    qout[warp_append(ring)] = t;
+        // 32 frontier vertices per warp: a lane walks its own vertex's
+        // edges, the warp walks a high-degree vertex's together (a hub's
+        // 10^4..10^5 edges would otherwise be one thread's serial loop)
+        const unsigned lane = threadIdx.x & 31;
+        const std::uint64_t nw = gstride() >> 5;
+        for (std::uint64_t base = (gtid() >> 5) * 32; base < nin; base += nw * 32) {
+            std::uint32_t b = 0, e_end = 0;
+            if (base + lane < nin) {
+                const std::uint32_t u = qin[base + lane];
+                b = row[u];
+                e_end = row[u + 1];
+            }
+            const bool wide = e_end - b > 32;
+            if (!wide)
+                for (std::uint32_t e = b; e < e_end; ++e) {
+                    const std::uint32_t t = col[e];
+                    if (lab[t] != NONE || vis[t] != 0)
+                        continue;
+                    if (atomicCAS(&vis[t], 0u, level) == 0u)
+                        qout[warp_append(ring)] = t;
+                }
+            for (unsigned hv = __ballot_sync(FULL, wide); hv; hv &= hv - 1) {
+                const int j = __ffs(hv) - 1;
+                const std::uint32_t hb = __shfl_sync(FULL, b, j), he = __shfl_sync(FULL, e_end, j);
+                for (std::uint32_t e = hb + lane; e < he; e += 32) {
+                    const std::uint32_t t = col[e];
+                    if (lab[t] != NONE || vis[t] != 0)
+                        continue;
+                    if (atomicCAS(&vis[t], 0u, level) == 0u)
+                        qout[warp_append(ring)] = t;
+                }
             }
         }
     }
@@ -302,7 +378,17 @@ __global__ void __launch_bounds__(kBlock) kp_scc_coop(std::uint32_t n, const std
     rf.init(pc->bfs_ring);
     rb.init(pc->bfs_ring + 2);
     grid.sync(); // every CTA has read the ring bases
+    const bool clk0 = blockIdx.x == 0 && threadIdx.x == 0;
+    long long t = clk0 ? clock64() : 0;
+    auto lap = [&](int i) {
+        if (clk0) {
+            const long long u = clock64();
+            pc->clk[i] = u - t;
+            t = u;
+        }
+    };
     trim_fixpoint(grid, n, row, col, brow, bcol, ind, outd, lab, qf0, qf1, rf);
+    lap(0);
     // trimming kept ind/outd exact for the surviving subgraph
     {
         unsigned long long best = 0;
@@ -332,11 +418,13 @@ __global__ void __launch_bounds__(kBlock) kp_scc_coop(std::uint32_t n, const std
         visb[start] = 1;
     }
     grid.sync(); // the seed is visible
+    lap(1);
     std::uint64_t nf = 1, nb = 1;
     bool f_was_bu = false, b_was_bu = false;
     int cf = 0, cb = 0; // which queue holds the current frontier
     const std::uint64_t bu_from = n >> 6;
-    for (std::uint32_t level = 2; nf || nb; ++level) {
+    std::uint32_t level = 2;
+    for (; nf || nb; ++level) {
         const bool f_bu = nf > bu_from, b_bu = nb > bu_from;
         const bool f_cmp = nf && !f_bu && f_was_bu, b_cmp = nb && !b_bu && b_was_bu;
         if (f_cmp || b_cmp) {
@@ -366,6 +454,9 @@ __global__ void __launch_bounds__(kBlock) kp_scc_coop(std::uint32_t n, const std
             cb ^= 1;
         }
     }
+    if (clk0)
+        pc->levels = level - 2;
+    lap(2);
     // the pivot's component; count what is left for the colouring
     unsigned rem = 0;
     for (std::size_t v = gtid(); v < n; v += gstride()) {
@@ -379,6 +470,7 @@ __global__ void __launch_bounds__(kBlock) kp_scc_coop(std::uint32_t n, const std
     block_count(rem, rf);
     grid.sync();
     const std::uint64_t left = rf.take();
+    lap(3);
     if (gtid() == 0)
         pc->remaining = static_cast<unsigned>(left);
 }
@@ -501,14 +593,33 @@ __global__ void kp_region_ids(std::uint32_t n, const std::uint32_t* lab, const s
 __global__ void kp_count_intra(std::uint32_t n, std::uint32_t R, const std::uint32_t* row,
                                const std::uint32_t* tgt, const std::uint32_t* reg,
                                std::uint32_t* cnt) {
-    for (std::size_t vv = tid_(); vv < n; vv += stride_()) {
-        const std::uint32_t v = static_cast<std::uint32_t>(vv);
+    OCM_WARP_VERTICES(n, {
         const std::uint32_t r = reg[v];
         std::uint32_t c = 0;
         if (r != R)
-            for (std::uint32_t e = row[v]; e < row[v + 1]; ++e)
+            for (std::uint32_t e = b; e < e_end; ++e)
                 c += reg[tgt[e]] == r;
         cnt[v] = c;
+    }, {
+        const std::uint32_t r = reg[hvx];
+        std::uint32_t c = 0;
+        if (r != R)
+            for (std::uint32_t e = hb + lane; e < he; e += 32)
+                c += reg[tgt[e]] == r;
+        c = __reduce_add_sync(FULL, c);
+        if (lane == 0)
+            cnt[hvx] = c;
+    })
+}
+
+template <bool EXACT>
+__device__ __forceinline__ bool pack_one(std::uint32_t t, double x, std::uint32_t k, int2* ew, FEdge* fe) {
+    if constexpr (EXACT) {
+        ew[k] = make_int2(static_cast<int>(t), static_cast<int>(x));
+        return !(fabs(x) <= 2147483647.0);
+    } else {
+        fe[k] = FEdge{x, t, 0u};
+        return false;
     }
 }
 
@@ -518,26 +629,36 @@ __global__ void kp_pack(std::uint32_t n, std::uint32_t R, const std::uint32_t* r
                         const std::uint32_t* nrow, double sign, int2* ew, FEdge* fe,
                         PrepCounters* pc) {
     bool bad = false;
-    for (std::size_t vv = tid_(); vv < n; vv += stride_()) {
-        const std::uint32_t v = static_cast<std::uint32_t>(vv);
+    OCM_WARP_VERTICES(n, {
         const std::uint32_t r = reg[v];
-        if (r == R)
-            continue;
-        std::uint32_t k = nrow[v];
-        for (std::uint32_t e = row[v]; e < row[v + 1]; ++e) {
-            const std::uint32_t t = tgt[e];
-            if (reg[t] != r)
-                continue;
-            const double x = sign * w[e];
-            if constexpr (EXACT) {
-                bad |= !(fabs(x) <= 2147483647.0);
-                ew[k] = make_int2(static_cast<int>(t), static_cast<int>(x));
-            } else {
-                fe[k] = FEdge{x, t, 0u};
+        if (r != R) {
+            std::uint32_t k = nrow[v];
+            for (std::uint32_t e = b; e < e_end; ++e) {
+                const std::uint32_t t = tgt[e];
+                if (reg[t] == r)
+                    bad |= pack_one<EXACT>(t, sign * w[e], k++, ew, fe);
             }
-            ++k;
         }
-    }
+    }, {
+        // edge order kept: 32 edges at a time, slots from a ballot prefix
+        const std::uint32_t r = reg[hvx];
+        if (r != R) {
+            std::uint32_t k = nrow[hvx];
+            for (std::uint32_t e0 = hb; e0 < he; e0 += 32) {
+                const std::uint32_t e = e0 + lane;
+                std::uint32_t t = 0;
+                bool in = false;
+                if (e < he) {
+                    t = tgt[e];
+                    in = reg[t] == r;
+                }
+                const unsigned m = __ballot_sync(FULL, in);
+                if (in)
+                    bad |= pack_one<EXACT>(t, sign * w[e], k + __popc(m & ((1u << lane) - 1u)), ew, fe);
+                k += __popc(m);
+            }
+        }
+    })
     if (__syncthreads_or(bad) && threadIdx.x == 0)
         pc->bad_weight = 1;
 }
@@ -808,6 +929,9 @@ void device_prepare_csr(std::uint32_t n, std::uint64_t m, DBuf<std::uint32_t>& r
     }
     read_pc();
     mark("trim_bfs");
+    if (timing)
+        std::fprintf(stderr, "{\"scc_coop_Mclk\": [%.2f, %.2f, %.2f, %.2f], \"levels\": %u}\n", pc.clk[0] * 1e-6,
+                     pc.clk[1] * 1e-6, pc.clk[2] * 1e-6, pc.clk[3] * 1e-6, pc.levels);
     if (pc.remaining) {
         // visf holds BFS levels: clear it for the colouring's stamps
         CK(cudaMemsetAsync(visf.p, 0, std::size_t(n) * 4, s));
