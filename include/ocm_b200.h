@@ -159,6 +159,21 @@ int ocm_session_solve(ocm_session* s, ocm_solution* out, uint32_t* cycle_buf, ui
  * Vertices of trivial regions report 0. Any pointer may be NULL. */
 int ocm_session_values(ocm_session* s, int64_t* key_num, int64_t* lam_num, int64_t* lam_den,
                        double* fval, uint32_t* succ_vertex);
+/* Optimality certificate of the last solve, checked on the device in O(N+M)
+ * over the solved (region-compacted) graph -- the size-independent parity
+ * property at sizes the CPU oracle cannot reach (exact lane only):
+ *   every intra-region edge v->t satisfies K[v] <= K[t] + w*den - num
+ *   (K = value*den, lambda = num/den of v's region), the policy edge of every
+ *   vertex attains K[v], and every region's anchor cycle is closed, anchored
+ *   at its least vertex and of mean exactly lambda -- which together prove
+ *   lambda is the region's minimum cycle mean. Counts are of violations. */
+typedef struct ocm_certificate {
+    uint64_t vertices, edges, regions; /* checked */
+    uint64_t key_violations;           /* edges with K[v] > K[t] + w*den - num */
+    uint64_t policy_violations;        /* policy edge missing or not attaining K[v] */
+    uint64_t cycle_violations;         /* regions whose anchor cycle fails */
+} ocm_certificate;
+int ocm_session_certify(ocm_session* s, ocm_certificate* out);
 /* A session over a generated graph built in HBM (no host graph). */
 int ocm_session_create_generated(const ocm_generator* spec, const ocm_solve_options* opt,
                                  ocm_session** out);

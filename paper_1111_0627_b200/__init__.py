@@ -77,6 +77,12 @@ class _Gen(C.Structure):
                 ("wlo", C.c_int32), ("whi", C.c_int32), ("seed", C.c_uint64)]
 
 
+class _Certificate(C.Structure):
+    _fields_ = [("vertices", C.c_uint64), ("edges", C.c_uint64), ("regions", C.c_uint64),
+                ("key_violations", C.c_uint64), ("policy_violations", C.c_uint64),
+                ("cycle_violations", C.c_uint64)]
+
+
 class _ShardBuffers(C.Structure):
     _fields_ = [("rank", C.c_uint32), ("world", C.c_uint32), ("chunk", C.c_uint32),
                 ("own_lo", C.c_uint32), ("own_hi", C.c_uint32), ("n", C.c_uint32),
@@ -150,6 +156,7 @@ def _load():
         "ocm_session_solve": (C.c_int, [C.c_void_p, P(_Sol), P(C.c_uint32), C.c_uint32]),
         "ocm_session_values": (C.c_int, [C.c_void_p, P(C.c_int64), P(C.c_int64), P(C.c_int64),
                                          P(C.c_double), P(C.c_uint32)]),
+        "ocm_session_certify": (C.c_int, [C.c_void_p, P(_Certificate)]),
         "ocm_session_stream": (C.c_void_p, [C.c_void_p]),
         "ocm_session_free": (None, [C.c_void_p]),
     }
@@ -172,7 +179,7 @@ EXPORTED_SYMBOLS = (
     "ocm_session_shard_fused_launch", "ocm_session_shard_fused_finish",
     "ocm_graph_free", "ocm_graph_n", "ocm_graph_m", "ocm_graph_integer_exact", "ocm_graph_edges",
     "ocm_solve", "ocm_session_create", "ocm_session_solve", "ocm_session_values",
-    "ocm_session_stream", "ocm_session_free",
+    "ocm_session_stream", "ocm_session_free", "ocm_session_certify",
 )
 
 
@@ -481,6 +488,14 @@ class Session:
         cyc = np.empty(max(self.n, 1), np.uint32)
         _check(_lib.ocm_session_solve(self._h, C.byref(sol), _p(cyc, C.c_uint32), cyc.shape[0]))
         return _solution(sol, cyc)
+
+    def certify(self) -> dict:
+        """Device-side optimality certificate of the last solve (exact lane;
+        include/ocm_b200.h ocm_certificate): checked counts and violation
+        counts -- all violations 0 proves every region's lambda optimal."""
+        c = _Certificate()
+        _check(_lib.ocm_session_certify(self._h, C.byref(c)))
+        return {f: int(getattr(c, f)) for f, _ in _Certificate._fields_}
 
     def values(self):
         """Final value plane: dict with key_num/lam_num/lam_den (exact: value =

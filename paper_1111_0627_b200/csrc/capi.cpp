@@ -291,6 +291,14 @@ int ocm_session_values(ocm_session* s, int64_t* key_num, int64_t* lam_num, int64
     return guard([&] { s->s->values(key_num, lam_num, lam_den, fval, succ_vertex); });
 }
 
+int ocm_session_certify(ocm_session* s, ocm_certificate* out) {
+    return guard([&] {
+        if (!s || !out)
+            throw std::invalid_argument("null session or output");
+        s->s->certify(out);
+    });
+}
+
 void* ocm_session_stream(ocm_session* s) { return s ? s->s->stream() : nullptr; }
 
 void ocm_session_free(ocm_session* s) { delete s; }

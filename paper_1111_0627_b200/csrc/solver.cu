@@ -756,6 +756,98 @@ void Session::shard_buffers(ocm_shard_buffers* b) const {
     b->stream = d.stream;
 }
 
+namespace {
+__device__ __forceinline__ void cert_add(unsigned long long* dst, unsigned long long v) {
+    v = __reduce_add_sync(FULL, static_cast<unsigned>(v)); // per-thread counts stay < 2^32
+    if ((threadIdx.x & 31) == 0 && v)
+        atomicAdd(dst, v);
+}
+
+// Bellman optimality of the keys and the policy edge, one thread per vertex.
+__global__ void k_certify_vertices(KP p, unsigned long long* cnt) {
+    unsigned long long verts = 0, edges = 0, kv = 0, pv = 0;
+    for (std::size_t v = gtid(); v < p.N; v += gstride()) {
+        const std::uint32_t r = p.reg[v];
+        const std::uint32_t b = p.row[v], e_end = p.row[v + 1];
+        if (r >= p.R || b == e_end)
+            continue;
+        ++verts;
+        const long long K = p.key_i[v], num = p.lam_num[r], den = p.lam_den[r];
+        for (std::uint32_t e = b; e < e_end; ++e) {
+            const int2 ed = p.ew[e];
+            const __int128 c = static_cast<__int128>(p.key_i[static_cast<std::uint32_t>(ed.x)]) +
+                               static_cast<__int128>(ed.y) * den - num;
+            kv += c < K;
+            ++edges;
+        }
+        const std::uint32_t se = p.succ_e[v];
+        if (se < b || se >= e_end) {
+            ++pv;
+        } else {
+            const int2 ed = p.ew[se];
+            const __int128 c = static_cast<__int128>(p.key_i[static_cast<std::uint32_t>(ed.x)]) +
+                               static_cast<__int128>(ed.y) * den - num;
+            pv += c != K || p.succ_v[v] != static_cast<std::uint32_t>(ed.x) || p.succ_wi[v] != ed.y;
+        }
+    }
+    cert_add(&cnt[0], verts);
+    cert_add(&cnt[1], edges);
+    cert_add(&cnt[3], kv);
+    cert_add(&cnt[4], pv);
+}
+
+// Every region's anchor cycle, one thread per region (a dependent walk).
+__global__ void k_certify_cycles(KP p, unsigned long long* cnt) {
+    unsigned long long regs = 0, cv = 0;
+    for (std::size_t r = gtid(); r < p.R; r += gstride()) {
+        ++regs;
+        const std::uint32_t a = p.src[r];
+        if (a >= p.N) {
+            ++cv;
+            continue;
+        }
+        std::uint32_t u = a, mn = a;
+        unsigned long long len = 0;
+        long long sum = 0;
+        do {
+            sum += p.succ_wi[u];
+            u = p.succ_v[u];
+            mn = min(mn, u);
+            ++len;
+        } while (u != a && u < p.N && len <= p.N);
+        cv += u != a || mn != a ||
+              static_cast<__int128>(sum) * p.lam_den[r] != static_cast<__int128>(len) * p.lam_num[r];
+    }
+    cert_add(&cnt[2], regs);
+    cert_add(&cnt[5], cv);
+}
+} // namespace
+
+void Session::certify(ocm_certificate* out) {
+    if (!solved_)
+        throw std::logic_error("session has not been solved yet");
+    if (!prep_.exact)
+        throw UnsupportedError("the optimality certificate covers the exact (integer-weight) lane");
+    DeviceState& d = *d_;
+    std::memset(out, 0, sizeof *out);
+    if (prep_.R == 0 || prep_.n == 0)
+        return;
+    DBuf<unsigned long long> cnt;
+    cnt.alloc(6, d.stream);
+    CK(cudaMemsetAsync(cnt.p, 0, 6 * sizeof(unsigned long long), d.stream));
+    k_certify_vertices<<<grid_for(prep_.n, d.sms, 8), kBlock, 0, d.stream>>>(d.kp, cnt.p);
+    k_certify_cycles<<<grid_for(prep_.R, d.sms, 1), kBlock, 0, d.stream>>>(d.kp, cnt.p);
+    unsigned long long h[6];
+    CK(cudaMemcpyAsync(h, cnt.p, sizeof h, cudaMemcpyDeviceToHost, d.stream));
+    CK(cudaStreamSynchronize(d.stream));
+    out->vertices = h[0];
+    out->edges = h[1];
+    out->regions = h[2];
+    out->key_violations = h[3];
+    out->policy_violations = h[4];
+    out->cycle_violations = h[5];
+}
+
 void Session::values(std::int64_t* key_num, std::int64_t* lam_num, std::int64_t* lam_den,
                      double* fval, std::uint32_t* succ_vertex) {
     if (!solved_)

@@ -28,6 +28,7 @@ class Session {
             std::uint32_t world = 1);
     ~Session();
     void solve(ocm_solution* out, std::uint32_t* cycle_buf, std::uint32_t cap);
+    void certify(ocm_certificate* out);
     void values(std::int64_t* key_num, std::int64_t* lam_num, std::int64_t* lam_den, double* fval,
                 std::uint32_t* succ_vertex);
     void* stream() const;
