@@ -53,9 +53,6 @@ namespace cg = cooperative_groups;
 #define OCM_MINB 4
 #endif
 constexpr int kSolveMinBlocks = OCM_MINB; // 4: register cap 64 at 256 threads
-#ifndef OCM_ROUND_MAX
-#define OCM_ROUND_MAX 2 // doubling steps fused into one pass (1..3)
-#endif
 
 // ------------------------------------------------------------ improvement
 //
@@ -830,6 +827,45 @@ __device__ __forceinline__ void ph_mark(const KP& p, std::uint64_t nC, int in, s
     }
 }
 
+// The last doubling pass fused with the mark phase: each core vertex
+// takes S more doubling steps (2^S chained reads of the input records) and
+// then the anchor of its window, rebuilding its image j's record of the new
+// level from the same input records (another 2^S reads, least vertex only)
+// -- one phase and one barrier fewer per verification.
+template <int S>
+__device__ __forceinline__ void ph_round_mark(const KP& p, std::uint64_t nC, int in, std::uint32_t stamp,
+                                              bool exact, const Ring& rl) {
+    const PJC* __restrict__ a = p.pj[in];
+    PJC* __restrict__ o = p.pj[in ^ 1];
+    for (std::uint64_t i = gtid(); i < nC; i += gstride()) {
+        const std::uint32_t v = p.clist[i];
+        PJC z = a[v];
+#pragma unroll
+        for (int h = 1; h < (1 << S); ++h) {
+            const PJC y = a[z.nxt];
+            z.nxt = y.nxt;
+            z.mn = min(z.mn, y.mn);
+            z.w += y.w;
+        }
+        o[v] = z;
+        const std::uint32_t j = z.nxt;
+        std::uint32_t u = j, mn = NONE;
+#pragma unroll
+        for (int h = 0; h < (1 << S); ++h) {
+            const PJC y = a[u];
+            mn = min(mn, y.mn);
+            u = y.nxt;
+        }
+        p.comp[v] = mn;
+        if (p.cmark[j] != stamp && atomicExch(&p.cmark[j], stamp) != stamp) {
+            p.wlist[warp_append(rl)] = j;
+            p.cyc_len[j] = 0;
+            if (exact)
+                p.cyc_wi[j] = 0;
+        }
+    }
+}
+
 // Over the listed M only: (B) and |succ(M)|, and -- speculatively, exact
 // lane -- the per-anchor (length, weight) records (howard_par.hpp:319).
 template <bool EXACT>
@@ -1556,26 +1592,30 @@ __global__ void __launch_bounds__(kBlock, kSolveMinBlocks) k_solve(KP p, int mod
         bool first_try = true;
         std::uint64_t nM = 0;
         for (;;) {
-            for (const int k0 = k; k < static_cast<int>(st.k_hint); in ^= 1) {
-                const int left = static_cast<int>(st.k_hint) - k;
-                if (OCM_ROUND_MAX >= 3 && left >= 3) {
-                    ph_round_multi<3>(p, nC, in);
-                    k += 3;
-                } else if (OCM_ROUND_MAX >= 2 && left >= 2) {
-                    ph_round_multi<2>(p, nC, in);
-                    k += 2;
-                } else {
-                    ph_round(p, nC, in);
-                    ++k;
-                }
+            // all doubling passes but the last, two steps each
+            for (; static_cast<int>(st.k_hint) - k > 2; in ^= 1) {
+                ph_round_multi<2>(p, nC, in);
+                k += 2;
+                st.rounds += 2;
                 sync(PH_ROUND);
-                if (k >= static_cast<int>(st.k_hint))
-                    st.rounds += k - k0;
             }
             const unsigned stamp = ++st.stamp;
             ++st.verifies;
             unsigned* vflag = &c->vfail[stamp & 1];
-            ph_mark(p, nC, in, stamp, EXACT, st.rl);
+            // the last pass (one or two steps) marks as it goes
+            const int last = static_cast<int>(st.k_hint) - k;
+            if (last == 2) {
+                ph_round_mark<2>(p, nC, in, stamp, EXACT, st.rl);
+            } else if (last == 1) {
+                ph_round_mark<1>(p, nC, in, stamp, EXACT, st.rl);
+            } else {
+                ph_mark(p, nC, in, stamp, EXACT, st.rl);
+            }
+            if (last > 0) {
+                k += last;
+                st.rounds += last;
+                in ^= 1;
+            }
             sync(PH_VERIFY);
             nM = st.rl.take(); // |M|, listed in wlist
             ph_check<EXACT>(p, nM, stamp, vflag, st.rc);
