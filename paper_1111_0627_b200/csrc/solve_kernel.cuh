@@ -747,25 +747,10 @@ __device__ __forceinline__ void ph_classify(const KP& p, int par, const Ring& ra
 }
 
 // Synchronous pointer doubling of (segment end, least vertex, weight sum)
-// over the core (closed under succ: a leaf is nobody's successor).
-__device__ __forceinline__ void ph_round(const KP& p, std::uint64_t nC, int in) {
-    const PJC* __restrict__ a = p.pj[in];
-    PJC* __restrict__ o = p.pj[in ^ 1];
-    for (std::uint64_t i = gtid(); i < nC; i += gstride()) {
-        const std::uint32_t v = p.clist[i];
-        const PJC x = a[v];
-        const PJC y = a[x.nxt];
-        PJC z;
-        z.nxt = y.nxt;
-        z.mn = min(x.mn, y.mn);
-        z.w = x.w + y.w;
-        o[v] = z;
-    }
-}
-
-// S doubling steps in one pass (records of 2^k steps -> 2^(k+S)): 2^S
-// chained reads of the same buffer instead of S rounds and S-1 barriers --
-// a round's cost is mostly its barrier and the latency ramp, not its loads.
+// over the core (closed under succ: a leaf is nobody's successor), S
+// doubling steps per pass (records of 2^k steps -> 2^(k+S)): 2^S chained
+// reads of the same buffer instead of S rounds and S-1 barriers -- a
+// round's cost is mostly its barrier and the latency ramp, not its loads.
 template <int S> __device__ __forceinline__ void ph_round_multi(const KP& p, std::uint64_t nC, int in) {
     const PJC* __restrict__ a = p.pj[in];
     PJC* __restrict__ o = p.pj[in ^ 1];
