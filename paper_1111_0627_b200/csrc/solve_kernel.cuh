@@ -74,19 +74,32 @@ template <int G> __device__ __forceinline__ unsigned group_mask() {
         return ((1u << G) - 1u) << ((threadIdx.x & 31) & ~(G - 1));
 }
 
+// Raise region r's "changed" flag; in the fused sharded lane the peers'
+// replicas of the flag too (stored during the pass, ordered before the
+// cross-rank arrival by the same system fence as the policy pushes).
+__device__ __forceinline__ void raise_changed(const KP& p, int* changed, std::uint32_t r) {
+    set_once(&changed[r], 1);
+    if (p.fused) {
+        const int par = changed == p.changed[1] ? 1 : 0;
+        for (int q = 0; q < p.world; ++q)
+            if (q != p.rank)
+                p.peer_changed[par][q][r] = 1;
+    }
+}
+
 // Region "changed" bookkeeping with at most one store per block per region.
 struct ChangedMarks {
     std::uint32_t first = NONE;
     std::uint32_t last_direct = NONE;
-    __device__ __forceinline__ void note(int* changed, std::uint32_t r) {
+    __device__ __forceinline__ void note(const KP& p, int* changed, std::uint32_t r) {
         if (first == NONE)
             first = r;
         else if (r != first && r != last_direct) {
             last_direct = r;
-            set_once(&changed[r], 1);
+            raise_changed(p, changed, r);
         }
     }
-    __device__ __forceinline__ void flush(int* changed) {
+    __device__ __forceinline__ void flush(const KP& p, int* changed) {
         __shared__ std::uint32_t s_r;
         if (threadIdx.x == 0)
             s_r = NONE;
@@ -94,11 +107,11 @@ struct ChangedMarks {
         if (first != NONE) {
             const std::uint32_t prev = atomicCAS(&s_r, NONE, first);
             if (prev != NONE && prev != first)
-                set_once(&changed[first], 1);
+                raise_changed(p, changed, first);
         }
         __syncthreads();
         if (threadIdx.x == 0 && s_r != NONE)
-            set_once(&changed[s_r], 1);
+            raise_changed(p, changed, s_r);
     }
 };
 
@@ -254,7 +267,7 @@ __device__ __forceinline__ void improve_vertex(const KP& p, int* changed, Change
                 push_policy<EXACT>(p, v, be, t, ed);
             if (p.indeg_in_improve)
                 atomicAdd(&p.indeg[t], 1u);
-            marks.note(changed, r);
+            marks.note(p, changed, r);
         }
     } else if (saw_cur && p.indeg_in_improve) {
         std::uint32_t t;
@@ -397,7 +410,7 @@ __device__ __forceinline__ void improve_heavy(const KP& p, int* changed) {
                         if (p.indeg_in_improve)
                             atomicAdd(&p.indeg[ed.t], 1u);
                     }
-                    set_once(&changed[r], 1);
+                    raise_changed(p, changed, r);
                 } else if (p.indeg_in_improve) {
                     atomicAdd(&p.indeg[p.succ_v[v]], 1u);
                 }
@@ -547,14 +560,14 @@ __device__ __forceinline__ void pb_pass2(const KP& p, int* changed) {
                 p.succ_wi[v] = ed.y;
                 p.succ_v[v] = t;
                 atomicAdd(&p.indeg[t], 1u);
-                marks.note(changed, r);
+                marks.note(p, changed, r);
             } else {
                 atomicAdd(&p.indeg[p.succ_v[v]], 1u);
             }
         }
         __syncthreads(); // shared arrays reused by the next block
     }
-    marks.flush(changed);
+    marks.flush(p, changed);
 }
 
 template <bool EXACT, int G, int U> __device__ __forceinline__ void improve_phase(const KP& p, int* changed) {
@@ -576,7 +589,7 @@ template <bool EXACT, int G, int U> __device__ __forceinline__ void improve_phas
     const std::size_t gs = gstride() / G;
     for (std::size_t vv = p.own_lo + gtid() / G; vv < p.own_hi; vv += gs)
         improve_vertex<EXACT, G, U>(p, changed, marks, static_cast<std::uint32_t>(vv));
-    marks.flush(changed);
+    marks.flush(p, changed);
 }
 
 // The optimal cycle from its anchor (one thread: a dependent walk).
@@ -1451,13 +1464,14 @@ __global__ void __launch_bounds__(kBlock, kSolveMinBlocks) k_solve(KP p, int mod
             st.clk_last = t;
         }
     };
-    // cross-rank barrier of the fused sharded lane: local grid barrier, then
-    // the leader publishes (system fence) and bumps every rank's barrier word
-    // and waits for all ranks' bumps; a bounded wait turns a missing peer into
-    // an error instead of a hang. Returns false (uniformly) on timeout.
-    auto xbarrier = [&](int ph) -> bool {
-        __threadfence_system(); // this thread's peer stores, before the arrival
-        sync(ph);
+    // cross-rank barrier of the fused sharded lane, called right after a
+    // grid barrier (every CTA of this rank is through the previous phase and
+    // has fenced its peer stores at system scope before arriving there): the
+    // leader publishes (system fence) and bumps every rank's barrier word,
+    // waits for all ranks' bumps, and one more grid barrier releases the
+    // rank. A bounded wait turns a missing peer into an error instead of a
+    // hang. Returns false (uniformly) on timeout.
+    auto xsignal = [&](int ph) -> bool {
         if (blockIdx.x == 0 && threadIdx.x == 0) {
             __threadfence_system();
             const unsigned target = (++st.xepoch) * static_cast<unsigned>(p.world);
@@ -1510,8 +1524,9 @@ __global__ void __launch_bounds__(kBlock, kSolveMinBlocks) k_solve(KP p, int mod
     for (;; ++st.it) {
         if (!skip_improve) {
             // fused lane: every rank finished the previous iteration (whose
-            // replicated phases write the policy) before anyone pushes
-            if (mode == kShardFused && !xbarrier(PH_IMPROVE)) {
+            // replicated phases write the policy) before anyone pushes; the
+            // previous phase ended with a grid barrier
+            if (mode == kShardFused && !xsignal(PH_IMPROVE)) {
                 fatal = true;
                 break;
             }
@@ -1527,24 +1542,17 @@ __global__ void __launch_bounds__(kBlock, kSolveMinBlocks) k_solve(KP p, int mod
             asm volatile("" ::: "memory");
             st = s_park;
             ++st.passes;
+            if (mode == kShardFused)
+                __threadfence_system(); // this thread's policy/flag pushes, before arriving
             sync(PH_IMPROVE);
             if (mode == kShardBegin || mode == kShardResume) {
                 paused = true;
                 break;
             }
-            if (mode == kShardFused) {
-                // region flags raised here go to the peers too; then wait
-                // until every rank's policy pushes are visible
-                const int par = st.it & 1;
-                for (std::size_t r = gtid(); r < p.R; r += gstride())
-                    if (p.changed[par][r])
-                        for (int q = 0; q < p.world; ++q)
-                            if (q != p.rank)
-                                p.peer_changed[par][q][r] = 1;
-                if (!xbarrier(PH_IMPROVE)) {
-                    fatal = true;
-                    break;
-                }
+            // fused lane: wait until every rank's pushes are visible
+            if (mode == kShardFused && !xsignal(PH_IMPROVE)) {
+                fatal = true;
+                break;
             }
         }
         skip_improve = false;
