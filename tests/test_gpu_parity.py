@@ -139,12 +139,16 @@ def test_long_winning_cycle(n):
     assert len(sol.cycle_vertices) == n
 
 
-def test_float_weights_generated():
-    g = P.generate_uniform(5000, 3, -400, 400, 9)
+@pytest.mark.parametrize("n,deg,objective,scc", [(5000, 3, "min", "tarjan"), (100000, 4, "min", "tarjan"),
+                                                  (100000, 4, "max", "tarjan"), (20000, 3, "min", "off")])
+def test_float_weights_generated(n, deg, objective, scc):
+    """Float lane (non-integer weights): same summation order as the
+    reference, so means and values compare exactly, up to 10^5 vertices."""
+    g = P.generate_uniform(n, deg, -400, 400, 9)
     s, d, w = g.edges()
     w = w / 16.0 + 0.03125
-    sol, vals = run(5000, s, d, w, "min")
-    ref = oracle_record(5000, s, d, w, "min", "tarjan")
+    sol, vals = run(n, s, d, w, objective, scc)
+    ref = oracle_record(n, s, d, w, objective, scc)
     assert not sol.exact
     check_against(sol, vals, ref)
 
