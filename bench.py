@@ -280,7 +280,8 @@ def cpu_sample(a, P, steps=1):
             "sample": f"{what} (same generator), min+max, reference lane 'howard' "
                       f"(proj/src/solve.cpp run_howard_seq, single thread: the default CLI lane and "
                       f"the fastest reference lane on these workloads -- its multi-threaded "
-                      f"howard-par lane measured 3.2x slower with 16 workers at n=10^5), "
+                      f"howard-par lane measured 2.2x slower with all 16 host CPUs on this sample, "
+                      f"profiles/reference_lanes_r01.log), "
                       f"{steps} step(s), solve time only",
             "ms": tot_ms}
 
