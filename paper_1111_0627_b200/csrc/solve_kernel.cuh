@@ -437,15 +437,12 @@ __device__ __forceinline__ void improve_heavy(const KP& p, int* changed) {
 //          incumbent's candidate is read back through pb_inv.
 // Everything after the choice (replacement test, policy, in-degree, region
 // flags) is improve_vertex's. Heavy vertices keep the block-cooperative path.
-#ifndef OCM_PB_U
-#define OCM_PB_U 4
-#endif
 __device__ __forceinline__ void pb_pass1(const KP& p) {
     const int2* __restrict__ tw = p.pb_tw;
     const long long* __restrict__ key = p.key_i;
     long long* __restrict__ cand = p.pb_cand;
     const long long den0 = p.R == 1 ? p.lam_den[0] : 1;
-    constexpr int kU = OCM_PB_U;
+    constexpr int kU = 4; // 8 and 16 measured slower (register pressure)
     const std::uint64_t nth = gstride();
     for (std::uint64_t i0 = gtid(); i0 < p.pb_m; i0 += kU * nth) {
         int2 e[kU];
@@ -465,9 +462,6 @@ __device__ __forceinline__ void pb_pass1(const KP& p) {
     }
 }
 
-#ifndef OCM_PB_U
-#define OCM_PB_U 4
-#endif
 constexpr int kPbVB = 1024; // vertices per pass-2 block
 constexpr std::size_t kPbSmem = kPbVB * 8 + (3 * kPbVB + 2 + 2 * kMaxPbBins) * 4;
 
