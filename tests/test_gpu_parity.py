@@ -159,6 +159,13 @@ def test_no_cycle_and_empty():
     assert not sol.has_cycle and sol.stats.spf_passes == 0
     g = P.build_graph(0, [])
     assert not P.solve(g).has_cycle
+    # edgeless graph (scc.cpp: every vertex its own trivial region)
+    e = np.array([], np.uint32)
+    sol, _ = run(5, e, e, np.array([], np.float64))
+    assert not sol.has_cycle and sol.stats.trivial_regions == 5
+    # a lone self-loop is a non-trivial singleton region: mu = its weight
+    sol, _ = run(3, np.array([1], np.uint32), np.array([1], np.uint32), np.array([-7.0]))
+    assert sol.has_cycle and sol.mu_exact == -7 and sol.cycle_vertices == [1]
     sol, _ = run(4, np.array([0, 0, 1, 2], np.uint32), np.array([1, 2, 3, 3], np.uint32),
                  np.array([1, 2, 3, -1.0]), scc="off")
     assert not sol.has_cycle
