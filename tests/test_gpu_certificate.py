@@ -102,3 +102,18 @@ def test_certificate_detects_a_corrupted_policy():
     succ_v[v] = (int(succ_v[v]) + 1) % 5000  # the policy head no longer matches its edge
     torch.cuda.synchronize()
     assert certify()["policy_violations"] >= 1
+
+
+def test_repeated_solves_are_identical_and_certified():
+    """A hundred back-to-back solves on resident sessions (the persistent
+    kernel's counters, stamps and rings persist across launches) give the
+    same mu, cycle and iteration counts every time, and stay certified."""
+    spec = P.Generator("uniform", n=200_000, deg=8, seed=SEED)
+    for objective in ("min", "max"):
+        sess = P.Session.generated(spec, P.SolveOptions(objective=objective))
+        first = sess.solve()
+        key = (first.mu_exact, first.cycle_vertices, first.stats.spf_passes, first.stats.outer_iters)
+        for _ in range(100):
+            s = sess.solve()
+            assert (s.mu_exact, s.cycle_vertices, s.stats.spf_passes, s.stats.outer_iters) == key
+        assert clean(sess.certify())
