@@ -219,6 +219,7 @@ __device__ __forceinline__ void block_count(unsigned mine, const Ring& ring) {
     __syncthreads();
     if (threadIdx.x == 0 && s_sum)
         atomicAdd(ring.counter(), static_cast<unsigned long long>(s_sum));
+    __syncthreads(); // s_sum is reset by the block's next call (racecheck-clean)
 }
 
 } // namespace
