@@ -354,7 +354,7 @@ def run_sharded(a, world, rank, local):
     if not dist.is_initialized():
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", "29511")
-        dist.init_process_group("nccl", rank=0, world_size=1)
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=dev)
     comm = TorchComm()
     c = CONFIGS[a.config]
     if c["kind"] == "model":
@@ -430,8 +430,13 @@ def main():
     world, rank, local = dist_env()
     dist = None
     if world > 1:
+        import torch
         import torch.distributed as dist
-        dist.init_process_group("nccl" if a.impl == "b200" else "gloo")
+        if a.impl == "b200":
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
     if a.impl == "reference":
         run_reference(a, world, rank)
         if dist:
