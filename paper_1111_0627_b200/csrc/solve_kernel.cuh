@@ -1449,12 +1449,18 @@ __global__ void __launch_bounds__(kBlock, kSolveMinBlocks) k_solve(KP p, int mod
     st.clk0 = st.clk_last = 0;
     if (blockIdx.x == 0 && threadIdx.x == 0)
         st.clk_last = st.clk0 = clock64();
+    // per-phase clocks of block 0 accumulate in shared memory (a global
+    // read-modify-write right after every barrier would delay block 0, and
+    // with it the next barrier); written out once at the end of the launch
+    __shared__ long long s_clk[PH_COUNT];
+    if (threadIdx.x < PH_COUNT)
+        s_clk[threadIdx.x] = 0;
     auto sync = [&](int ph) {
         grid.sync();
         ++st.nsync;
         if (blockIdx.x == 0 && threadIdx.x == 0) {
             const long long t = clock64();
-            c->clk[ph] += t - st.clk_last;
+            s_clk[ph] += t - st.clk_last;
             st.clk_last = t;
         }
     };
@@ -1727,6 +1733,8 @@ __global__ void __launch_bounds__(kBlock, kSolveMinBlocks) k_solve(KP p, int mod
         c->layers = st.layers;
         c->syncs = st.nsync;
         c->clk_total += clock64() - st.clk0;
+        for (int ph = 0; ph < PH_COUNT; ++ph)
+            c->clk[ph] += s_clk[ph];
     }
 }
 
