@@ -10,10 +10,11 @@
 //   improve                  :146 spf_pass_iter (+ policy in-degree count)
 //   classify                 :189 finished_regions / :208 deactivate_regions,
 //                            leaf/core split + first doubling round
-//   round x k, mark, check   :249 elimination_fixpoint + :301 cycle_identification
-//                            (exact round-count verification), :319 records
-//   vote (+ last-CTA adopt,  :56 vote_min, :339 vote_and_adopt,
-//     winning-cycle values)  :494 value_propagate_fixpoint on the cycle
+//   rounds (2 steps/pass),   :249 elimination_fixpoint + :301 cycle_identification
+//   last round + mark, check (exact round-count verification), :319 records
+//   vote (block 0 when few   :56 vote_min, :339 vote_and_adopt,
+//     cycle vertices; adopt, :494 value_propagate_fixpoint on the cycle
+//     winning-cycle values)
 //   keep                     :370 set_min_cycle, :393 mark_min_component,
 //                            value propagation of kept vertices
 //   attach layers            :433 connect_gpi_fixpoint (+ values)
