@@ -1009,10 +1009,16 @@ __device__ __forceinline__ void wc_final(const KP& p, const std::uint32_t* list,
 constexpr unsigned kSmemCycle = 128; // 512 measured 2% slower: its 20 KB of static shared
                                      // memory per CTA came out of every launch's L1
 
+// One instance per CTA, shared by both winning-cycle paths.
+__shared__ std::uint32_t wc_key[2 * kSmemCycle], wc_val[2 * kSmemCycle];
+__shared__ std::uint32_t wc_nxt[2][kSmemCycle];
+__shared__ long long wc_acc[2][kSmemCycle];
+
 __device__ __forceinline__ void wincyc_shared(const KP& p, unsigned nW, int wr) {
-    __shared__ std::uint32_t s_key[2 * kSmemCycle], s_val[2 * kSmemCycle];
-    __shared__ std::uint32_t s_nxt[2][kSmemCycle];
-    __shared__ long long s_acc[2][kSmemCycle];
+    auto& s_key = wc_key;
+    auto& s_val = wc_val;
+    auto& s_nxt = wc_nxt;
+    auto& s_acc = wc_acc;
     constexpr unsigned kMask = 2 * kSmemCycle - 1;
     for (unsigned i = threadIdx.x; i < 2 * kSmemCycle; i += blockDim.x)
         s_key[i] = NONE;
@@ -1082,9 +1088,12 @@ __device__ __forceinline__ void vote_pass(const KP& p, std::uint64_t nM, std::ui
 // Adoption and the winning cycles' values by one block (s_maxlen, s_nw
 // zeroed by the caller before its last barrier).
 template <bool EXACT>
+__device__ __forceinline__ void winning_cycle_tail(const KP& p, unsigned nW, unsigned maxlen,
+                                                   std::uint32_t stamp);
+
+template <bool EXACT>
 __device__ __forceinline__ void vote_tail(const KP& p, std::uint64_t nM, std::uint32_t stamp,
                                           unsigned& s_maxlen, unsigned& s_nw) {
-    Ctl* c = p.c;
     for (std::uint32_t r = threadIdx.x; r < p.R; r += blockDim.x)
         if (p.active[r]) {
             const unsigned len = adopt_region<EXACT>(p, r);
@@ -1101,7 +1110,14 @@ __device__ __forceinline__ void vote_tail(const KP& p, std::uint64_t nM, std::ui
             p.rem[1][atomicAdd(&s_nw, 1u)] = v;
     }
     __syncthreads();
-    const unsigned nW = s_nw, maxlen = s_maxlen;
+    winning_cycle_tail<EXACT>(p, s_nw, s_maxlen, stamp);
+}
+
+// The winning cycles' values (nW vertices listed in rem[1], longest maxlen).
+template <bool EXACT>
+__device__ __forceinline__ void winning_cycle_tail(const KP& p, unsigned nW, unsigned maxlen,
+                                                   std::uint32_t stamp) {
+    Ctl* c = p.c;
     const int wr = ceil_log2_d(maxlen > 1 ? maxlen - 1 : 1); // farthest: len-1 steps
     if (nW <= kSmemCycle) {
         wincyc_shared(p, nW, wr);
@@ -1148,6 +1164,109 @@ __device__ __forceinline__ void ph_vote(const KP& p, std::uint64_t nM, std::uint
         vote_tail<EXACT>(p, nM, stamp, s_maxlen, s_nw);
 }
 
+// The common case in full (exact lane, one region, |M| <= one block, a
+// winning cycle of <= kSmemCycle vertices): thread i keeps cycle vertex
+// M[i], its anchor, successor and weight in registers from the vote to the
+// values, so adoption, the winning-cycle listing and its prefix sums add no
+// global round trips beyond the adoption's own.
+template <bool EXACT>
+__device__ __forceinline__ bool vote_small(const KP& p, unsigned nM, std::uint32_t stamp) {
+    auto& s_key = wc_key;
+    auto& s_val = wc_val;
+    auto& s_nxt = wc_nxt;
+    auto& s_acc = wc_acc;
+    __shared__ unsigned s_wcnt[kBlock / 32], s_nw;
+    __shared__ std::uint32_t s_src;
+    __shared__ unsigned s_len;
+    constexpr unsigned kMask = 2 * kSmemCycle - 1;
+    const unsigned i = threadIdx.x, lane = i & 31, warp = i >> 5;
+    std::uint32_t v = NONE, an = NONE, sv = 0;
+    int w = 0;
+    if (i < nM) {
+        v = p.wlist[i];
+        an = p.comp[v];
+        sv = p.succ_v[v];
+        w = p.succ_wi[v];
+    }
+    // vote (anchors only: usually one or two CASes on the one slot)
+    if (i < nM && an == v) {
+        unsigned long long* cell = &p.slot[0];
+        unsigned long long cur = ldv(*cell);
+        for (;;) {
+            if (cur != EMPTY && !rec_less<EXACT>(p, v, static_cast<std::uint32_t>(cur)))
+                break;
+            const unsigned long long prev = atomicCAS(cell, cur, v);
+            if (prev == cur)
+                break;
+            cur = prev;
+        }
+    }
+    for (unsigned j = i; j < 2 * kSmemCycle; j += blockDim.x)
+        s_key[j] = NONE;
+    __threadfence(); // the slot CASes, before adoption reads the slot
+    __syncthreads();
+    if (i == 0) {
+        s_len = p.active[0] ? adopt_region<EXACT>(p, 0) : 0u;
+        s_src = p.src[0];
+    }
+    __syncthreads();
+    // the winning cycle's vertices, numbered by a block-wide prefix count
+    const bool win = i < nM && an == s_src;
+    const unsigned bal = __ballot_sync(FULL, win);
+    if (lane == 0)
+        s_wcnt[warp] = __popc(bal);
+    __syncthreads();
+    if (i == 0) {
+        unsigned tot = 0;
+        for (unsigned j = 0; j < blockDim.x / 32; ++j) {
+            const unsigned c = s_wcnt[j];
+            s_wcnt[j] = tot;
+            tot += c;
+        }
+        s_nw = tot;
+    }
+    __syncthreads();
+    const unsigned nW = s_nw;
+    if (nW > kSmemCycle)
+        return false; // (block-uniform) the general path takes over
+    const unsigned idx = s_wcnt[warp] + __popc(bal & ((1u << lane) - 1u));
+    if (win) {
+        unsigned h = (v * 2654435761u) & kMask;
+        while (atomicCAS(&s_key[h], NONE, v) != NONE)
+            h = (h + 1) & kMask;
+        s_val[h] = idx;
+    }
+    __syncthreads();
+    if (win) {
+        if (v == s_src) {
+            s_acc[0][idx] = 0;
+            s_nxt[0][idx] = idx;
+        } else {
+            s_acc[0][idx] = static_cast<long long>(w) * p.lam_den[0] - p.lam_num[0];
+            unsigned h = (sv * 2654435761u) & kMask;
+            while (s_key[h] != sv)
+                h = (h + 1) & kMask;
+            s_nxt[0][idx] = s_val[h];
+        }
+    }
+    __syncthreads();
+    const unsigned maxlen = s_len;
+    const int wr = ceil_log2_d(maxlen > 1 ? maxlen - 1 : 1); // farthest: len-1 steps
+    for (int j = 0; j < wr; ++j) {
+        const int a = j & 1, o = a ^ 1;
+        if (win) {
+            const std::uint32_t x = s_nxt[a][idx];
+            s_acc[o][idx] = s_acc[a][idx] + s_acc[a][x];
+            s_nxt[o][idx] = s_nxt[a][x];
+        }
+        __syncthreads();
+    }
+    if (win)
+        p.key_i[v] = s_acc[wr & 1][idx];
+    (void)stamp;
+    return true;
+}
+
 // Few cycle vertices (the common case once the policy settles): block 0
 // votes, adopts and computes the winning cycles' values alone while the
 // grid waits at the phase barrier -- no grid-wide completion counter (two
@@ -1158,6 +1277,24 @@ constexpr std::uint64_t kVoteOneBlock = 4096;
 template <bool EXACT>
 __device__ __forceinline__ void ph_vote_one_block(const KP& p, std::uint64_t nM, std::uint32_t stamp) {
     __shared__ unsigned s_maxlen, s_nw;
+    if (EXACT && p.R == 1 && nM <= blockDim.x) {
+        if (vote_small<EXACT>(p, static_cast<unsigned>(nM), stamp))
+            return;
+        // a winning cycle too long for shared memory: list it and take the
+        // general path (adoption is already done)
+        __syncthreads();
+        if (threadIdx.x == 0)
+            s_nw = 0;
+        __syncthreads();
+        for (std::uint64_t i = threadIdx.x; i < nM; i += blockDim.x) {
+            const std::uint32_t v = p.wlist[i];
+            if (p.comp[v] == p.src[0])
+                p.rem[1][atomicAdd(&s_nw, 1u)] = v;
+        }
+        __syncthreads();
+        winning_cycle_tail<EXACT>(p, s_nw, ldv(p.cyc_len[p.src[0]]), stamp);
+        return;
+    }
     vote_pass<EXACT>(p, nM, threadIdx.x, blockDim.x);
     __threadfence(); // the block's slot CASes, before adoption reads the slots
     if (threadIdx.x == 0) {

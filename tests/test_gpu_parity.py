@@ -118,7 +118,7 @@ def test_blocked_improvement_vs_oracle(kind, n, deg, seed, monkeypatch):
         assert sol.cycle_vertices == direct.cycle_vertices
 
 
-@pytest.mark.parametrize("n", [60, 300, 3000, 9000])
+@pytest.mark.parametrize("n", [60, 200, 300, 3000, 9000])
 def test_long_winning_cycle(n):
     """Winning cycles of every size class of the vote tail: shared-memory
     values (one block), global-memory values (one block) and the grid-wide
