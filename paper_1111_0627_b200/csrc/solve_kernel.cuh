@@ -1170,7 +1170,8 @@ __device__ __forceinline__ void ph_vote(const KP& p, std::uint64_t nM, std::uint
 // values, so adoption, the winning-cycle listing and its prefix sums add no
 // global round trips beyond the adoption's own.
 template <bool EXACT>
-__device__ __forceinline__ bool vote_small(const KP& p, unsigned nM, std::uint32_t stamp) {
+__device__ __forceinline__ bool vote_small(const KP& p, unsigned nM, std::uint32_t stamp,
+                                           unsigned* vflag = nullptr) {
     auto& s_key = wc_key;
     auto& s_val = wc_val;
     auto& s_nxt = wc_nxt;
@@ -1187,6 +1188,28 @@ __device__ __forceinline__ bool vote_small(const KP& p, unsigned nM, std::uint32
         an = p.comp[v];
         sv = p.succ_v[v];
         w = p.succ_wi[v];
+    }
+    if (vflag) {
+        // the check phase's work for these few vertices (ph_check): (B)
+        // anchor constant along succ, (A) |succ(M)| = |M|, and the
+        // per-anchor (length, weight) records
+        bool fail = false;
+        int fresh = 0;
+        if (i < nM) {
+            fail = p.comp[sv] != an;
+            fresh = p.cmark2[sv] != stamp && atomicExch(&p.cmark2[sv], stamp) != stamp;
+            atomicAdd(&p.cyc_len[an], 1u);
+            atomicAdd(reinterpret_cast<unsigned long long*>(&p.cyc_wi[an]),
+                      static_cast<unsigned long long>(static_cast<long long>(w)));
+        }
+        const bool failed = __syncthreads_or(fail) || __syncthreads_count(fresh) != static_cast<int>(nM);
+        if (failed) {
+            if (i == 0)
+                *vflag = stamp; // the grid retries with one more doubling step
+            return true;
+        }
+        __threadfence(); // the records, before the vote reads them
+        __syncthreads();
     }
     // vote (anchors only: usually one or two CASes on the one slot)
     if (i < nM && an == v) {
@@ -1275,10 +1298,11 @@ __device__ __forceinline__ bool vote_small(const KP& p, unsigned nM, std::uint32
 constexpr std::uint64_t kVoteOneBlock = 4096;
 
 template <bool EXACT>
-__device__ __forceinline__ void ph_vote_one_block(const KP& p, std::uint64_t nM, std::uint32_t stamp) {
+__device__ __forceinline__ void ph_vote_one_block(const KP& p, std::uint64_t nM, std::uint32_t stamp,
+                                                  unsigned* vflag = nullptr) {
     __shared__ unsigned s_maxlen, s_nw;
     if (EXACT && p.R == 1 && nM <= blockDim.x) {
-        if (vote_small<EXACT>(p, static_cast<unsigned>(nM), stamp))
+        if (vote_small<EXACT>(p, static_cast<unsigned>(nM), stamp, vflag))
             return;
         // a winning cycle too long for shared memory: list it and take the
         // general path (adoption is already done)
@@ -1720,7 +1744,7 @@ __global__ void __launch_bounds__(kBlock, kSolveMinBlocks) k_solve(KP p, int mod
         // done by the classification)
         int in = 1, k = 1;
         ++st.rounds;
-        bool first_try = true;
+        bool first_try = true, voted = false;
         std::uint64_t nM = 0;
         for (;;) {
             // all doubling passes but the last, two steps each
@@ -1749,11 +1773,24 @@ __global__ void __launch_bounds__(kBlock, kSolveMinBlocks) k_solve(KP p, int mod
             }
             sync(PH_VERIFY);
             nM = st.rl.take(); // |M|, listed in wlist
-            ph_check<EXACT>(p, nM, stamp, vflag, st.rc);
-            sync(PH_VERIFY);
-            const std::uint64_t s_size = st.rc.take();
-            if (ldr(*vflag) != stamp && s_size == nM)
-                break;
+            if (EXACT && p.R == 1 && nM <= kBlock) {
+                // few cycle vertices, one region: block 0 checks and, if the
+                // check passes, votes, adopts and values the winning cycle
+                // in the same phase
+                if (blockIdx.x == 0)
+                    ph_vote_one_block<EXACT>(p, nM, stamp, vflag);
+                sync(PH_VERIFY);
+                if (ldr(*vflag) != stamp) {
+                    voted = true;
+                    break;
+                }
+            } else {
+                ph_check<EXACT>(p, nM, stamp, vflag, st.rc);
+                sync(PH_VERIFY);
+                const std::uint64_t s_size = st.rc.take();
+                if (ldr(*vflag) != stamp && s_size == nM)
+                    break;
+            }
             if (k >= K_max) {
                 fatal = true;
                 break;
@@ -1774,19 +1811,22 @@ __global__ void __launch_bounds__(kBlock, kSolveMinBlocks) k_solve(KP p, int mod
         }
         const unsigned stamp = st.stamp;
 
-        // ---- vote, adoption and the winning cycles' values
-        if constexpr (!EXACT) {
-            ph_stats_float(p, nM);
-            sync(PH_STATS);
+        // ---- vote, adoption and the winning cycles' values (done with the
+        // check above when the cycle vertices are few)
+        if (!voted) {
+            if constexpr (!EXACT) {
+                ph_stats_float(p, nM);
+                sync(PH_STATS);
+            }
+            if (nM <= kVoteOneBlock) {
+                if (blockIdx.x == 0)
+                    ph_vote_one_block<EXACT>(p, nM, stamp);
+            } else {
+                ph_vote<EXACT>(p, nM, stamp, st.done_base);
+                st.done_base += gridDim.x;
+            }
+            sync(PH_VOTE);
         }
-        if (nM <= kVoteOneBlock) {
-            if (blockIdx.x == 0)
-                ph_vote_one_block<EXACT>(p, nM, stamp);
-        } else {
-            ph_vote<EXACT>(p, nM, stamp, st.done_base);
-            st.done_base += gridDim.x;
-        }
-        sync(PH_VOTE);
         if (EXACT && ldr(c->wc_big[stamp & 1]) == stamp) {
             const std::uint64_t nW = static_cast<std::uint32_t>(ldr(c->wc_n[stamp & 1]));
             const unsigned maxlen = ldr(c->wc_len[stamp & 1]);
