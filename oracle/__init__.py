@@ -270,3 +270,30 @@ def ref_generate_model(kind, clients, costs=()):
           _ptr(src, C.c_uint32), _ptr(dst, C.c_uint32), _ptr(w, C.c_double)):
         raise RuntimeError("reference: " + lib.ref_last_error().decode())
     return n.value, src, dst, w
+
+
+def ref_parse_graph_text(text: str, source: str = "<text>"):
+    """The reference's ocm::parse_graph_text (src/graph_io.cpp) through
+    oracle/_ref. Returns ("ok", n, src, dst, w, integer_exact) or
+    ("parse", message, line) / ("error", message)."""
+    lib = ref_lib()
+    fn = lib.ref_parse_graph_text
+    fn.restype = C.c_int
+    fn.argtypes = [C.c_char_p, C.c_uint64, C.c_char_p, C.POINTER(C.c_uint32),
+                   C.POINTER(C.c_uint64), C.POINTER(C.c_int32), C.c_uint64,
+                   C.POINTER(C.c_uint32), C.POINTER(C.c_uint32), C.POINTER(C.c_double),
+                   C.POINTER(C.c_int32)]
+    b = text.encode() if isinstance(text, str) else bytes(text)
+    n, m, ex, line = C.c_uint32(), C.c_uint64(), C.c_int32(), C.c_int32()
+    rc = fn(b, len(b), source.encode(), C.byref(n), C.byref(m), C.byref(ex), 0, None, None, None,
+            C.byref(line))
+    if rc == 1:
+        return ("parse", lib.ref_last_error().decode(), line.value)
+    if rc:
+        return ("error", lib.ref_last_error().decode())
+    src = np.empty(m.value, np.uint32)
+    dst = np.empty(m.value, np.uint32)
+    w = np.empty(m.value, np.float64)
+    fn(b, len(b), source.encode(), C.byref(n), C.byref(m), C.byref(ex), m.value,
+       _ptr(src, C.c_uint32), _ptr(dst, C.c_uint32), _ptr(w, C.c_double), C.byref(line))
+    return ("ok", n.value, src, dst, w, bool(ex.value))

@@ -10,6 +10,7 @@
 //   ocm::HowardPar<M>::run     proj/include/ocm/howard_par.hpp:544
 //   ocm::tarjan_scc            proj/include/ocm/scc.hpp:34
 //   ocm::generate_model        proj/include/ocm/model_gen.hpp:67
+//   ocm::parse_graph_text      proj/include/ocm/graph_io.hpp:41
 //
 // Nothing here re-implements the algorithm; it only marshals arrays.
 
@@ -21,6 +22,7 @@
 #include <vector>
 
 #include "ocm/graph.hpp"
+#include "ocm/graph_io.hpp"
 #include "ocm/howard_par.hpp"
 #include "ocm/model_gen.hpp"
 #include "ocm/scc.hpp"
@@ -178,6 +180,34 @@ int ref_generate_model(int kind, const int64_t* costs, uint32_t n_costs, uint32_
     } catch (const std::exception& e) {
         g_err = e.what();
         return 1;
+    }
+}
+
+// ocm::parse_graph_text on `text`: returns 0 and n/m (+ the edges in edge-id
+// order when cap >= m), 1 with the message in ref_last_error() and the line in
+// *line_out on a ParseError, 2 on any other exception (message likewise).
+int ref_parse_graph_text(const char* text, uint64_t len, const char* source, uint32_t* n_out,
+                         uint64_t* m_out, int32_t* exact_out, uint64_t cap, uint32_t* src,
+                         uint32_t* dst, double* w, int32_t* line_out) {
+    try {
+        const ocm::Graph g = ocm::parse_graph_text(std::string_view(text, len), source);
+        *n_out = g.n;
+        *m_out = g.m;
+        *exact_out = g.integer_exact;
+        if (cap >= g.m)
+            for (uint64_t e = 0; e < g.m; ++e) {
+                src[e] = g.fwd_source[e];
+                dst[e] = g.fwd_target[e];
+                w[e] = g.fwd_weight[e];
+            }
+        return 0;
+    } catch (const ocm::ParseError& e) {
+        g_err = e.what();
+        *line_out = e.line();
+        return 1;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 2;
     }
 }
 

@@ -251,17 +251,33 @@ def _as_arrays(edges) -> Tuple[np.ndarray, np.ndarray, np.ndarray]:
         s = [e[0] for e in lst]
         d = [e[1] for e in lst]
         w = [e[2] for e in lst]
-    s = np.asarray(s)
-    d = np.asarray(d)
-    if s.size and (s.min() < 0 or d.min() < 0):
-        raise ValueError("negative vertex id")
+    s = np.asarray(s).reshape(-1)
+    d = np.asarray(d).reshape(-1)
+    w = np.asarray(w, dtype=np.float64).reshape(-1)
+    if not (s.shape[0] == d.shape[0] == w.shape[0]):
+        raise ValueError(f"edge arrays differ in length (src {s.shape[0]}, dst {d.shape[0]}, "
+                         f"weight {w.shape[0]})")
+    for name, a in (("source", s), ("target", d)):
+        if a.size == 0:
+            continue
+        if a.dtype.kind not in "iu":
+            if not np.all(np.floor(a) == a):
+                raise ValueError(f"non-integral {name} vertex id")
+        lo, hi = a.min(), a.max()
+        if lo < 0 or hi >= 2**32:
+            # the reference's Vertex is uint32 (graph.hpp:20); never wrap silently
+            raise ValueError(f"{name} vertex id {int(lo if lo < 0 else hi)} out of range")
     return (np.ascontiguousarray(s, np.uint32), np.ascontiguousarray(d, np.uint32),
-            np.ascontiguousarray(np.asarray(w, dtype=np.float64)))
+            np.ascontiguousarray(w))
 
 
 def build_graph(n: int, edges) -> Graph:
     """ocm::build_graph (graph.hpp:76). ``edges``: iterable of (u, v, w) or a
-    (src, dst, w) tuple of arrays. Raises ValueError like std::invalid_argument."""
+    (src, dst, w) tuple of arrays. Raises ValueError like std::invalid_argument:
+    on ``n`` outside [0, 2^32), arrays of unequal length, and (in the native
+    builder, with the reference's message) endpoints outside [0, n)."""
+    if int(n) != n or not 0 <= int(n) < 2**32:
+        raise ValueError(f"vertex count {n} out of range")
     s, d, w = _as_arrays(edges)
     h = C.c_void_p()
     _check(_lib.ocm_build_graph(int(n), s.shape[0], _p(s, C.c_uint32), _p(d, C.c_uint32),

@@ -6,6 +6,9 @@
 
 #include <cstring>
 #include <memory>
+#include <mutex>
+#include <utility>
+#include <vector>
 #include <string>
 
 #include "../../include/ocm_b200.h"
@@ -18,37 +21,40 @@ struct ocm_graph {
     ocmb::Graph g;
     // Host arrays are page-locked on first device use (one registration per
     // graph, released with the graph) so every later upload is a pinned copy.
-    bool pinned = false;
+    // The handle is read-only to callers and may be shared by threads: the
+    // registration runs once under a lock, and only the ranges this graph
+    // registered itself are ever unregistered.
+    std::mutex pin_mu;
+    std::vector<const void*> registered;
+    bool pin_tried = false;
     void pin() {
-        if (pinned)
+        std::lock_guard<std::mutex> lock(pin_mu);
+        if (pin_tried)
             return;
-        auto reg = [](const void* p, std::size_t bytes) {
-            return bytes == 0 || cudaHostRegister(const_cast<void*>(p), bytes,
-                                                   cudaHostRegisterPortable) == cudaSuccess;
-        };
-        const bool ok = reg(g.fwd_index.data(), g.fwd_index.size() * sizeof(std::uint64_t)) &&
-                        reg(g.fwd_target.data(), g.fwd_target.size() * sizeof(std::uint32_t)) &&
-                        reg(g.fwd_weight.data(), g.fwd_weight.size() * sizeof(double));
-        if (!ok) {
-            unpin();
-            cudaGetLastError();
-            return;
+        pin_tried = true;
+        const std::pair<const void*, std::size_t> ranges[] = {
+            {g.fwd_index.data(), g.fwd_index.size() * sizeof(std::uint64_t)},
+            {g.fwd_target.data(), g.fwd_target.size() * sizeof(std::uint32_t)},
+            {g.fwd_weight.data(), g.fwd_weight.size() * sizeof(double)}};
+        for (const auto& [p, bytes] : ranges) {
+            if (bytes == 0)
+                continue;
+            if (cudaHostRegister(const_cast<void*>(p), bytes, cudaHostRegisterPortable) !=
+                cudaSuccess) {
+                cudaGetLastError(); // pageable copies still work, only slower
+                unpin_locked();
+                return;
+            }
+            registered.push_back(p);
         }
-        pinned = true;
     }
-    void unpin() {
-        for (const void* p : {static_cast<const void*>(g.fwd_index.data()),
-                              static_cast<const void*>(g.fwd_target.data()),
-                              static_cast<const void*>(g.fwd_weight.data())})
-            if (p)
-                cudaHostUnregister(const_cast<void*>(p));
+    void unpin_locked() {
+        for (const void* p : registered)
+            cudaHostUnregister(const_cast<void*>(p));
+        registered.clear();
         cudaGetLastError();
-        pinned = false;
     }
-    ~ocm_graph() {
-        if (pinned)
-            unpin();
-    }
+    ~ocm_graph() { unpin_locked(); }
 };
 struct ocm_session {
     std::unique_ptr<ocmb::Session> s;

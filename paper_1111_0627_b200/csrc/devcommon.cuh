@@ -168,22 +168,28 @@ struct KP {
     std::uint32_t small_wc; // winning cycles up to this many vertices: one block
 };
 
+// The library's own stream-ordered memory pool for the current device
+// (created once, release threshold = keep everything cached, so re-creating
+// sessions does not pay cudaMalloc/cudaFree synchronisation). A private pool:
+// the default pool's threshold is left alone for everything else in the
+// process. Defined in solver.cu.
+cudaMemPool_t session_pool();
+
 template <class T> struct DBuf {
     T* p = nullptr;
     std::size_t n = 0;
     DBuf() = default;
     DBuf(const DBuf&) = delete;
     DBuf& operator=(const DBuf&) = delete;
-    // Stream-ordered allocation from the device's default memory pool (kept
-    // cached by the session), so re-creating sessions does not pay
-    // cudaMalloc/cudaFree synchronisation.
+    // Stream-ordered allocation from the library's private pool.
     cudaStream_t st = nullptr;
     bool plain = false; // cudaMalloc'ed (IPC-exportable), not pool memory
     void alloc(std::size_t k, cudaStream_t s = nullptr) {
         release();
         st = s;
         if (k)
-            CK(cudaMallocAsync(reinterpret_cast<void**>(&p), k * sizeof(T), st));
+            CK(cudaMallocFromPoolAsync(reinterpret_cast<void**>(&p), k * sizeof(T),
+                                       session_pool(), st));
         n = k;
     }
     // Memory other processes can map (cudaIpcGetMemHandle does not accept

@@ -76,16 +76,33 @@ const DeviceFacts& device_facts(int dev) {
                 CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, solve_fn(e == 1, gi), kBlock, 0));
                 f.per_sm[e][gi] = std::max(1, std::min(per_sm, kSolveMinBlocks));
             }
-        // keep freed blocks cached in the default pool across sessions
-        cudaMemPool_t pool;
-        CK(cudaDeviceGetDefaultMemPool(&pool, dev));
-        std::uint64_t keep = ~0ull;
-        CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
     }
     return cache.emplace(dev, f).first->second;
 }
 
 } // namespace
+
+cudaMemPool_t session_pool() {
+    static std::mutex mu;
+    static std::map<int, cudaMemPool_t> pools;
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = pools.find(dev);
+    if (it != pools.end())
+        return it->second;
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.handleTypes = cudaMemHandleTypeNone;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    cudaMemPool_t pool;
+    CK(cudaMemPoolCreate(&pool, &props));
+    std::uint64_t keep = ~0ull;
+    CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+    return pools.emplace(dev, pool).first->second;
+}
+
 
 Session::Session(const Graph& g, const ocm_solve_options& opt, std::uint32_t rank, std::uint32_t world)
     : opt_(opt), rank_(rank), world_(world) {
@@ -455,9 +472,13 @@ float Session::launch_wait() {
     CK(cudaGetLastError());
     if (prep_.R == 0)
         hc.shard_done = 1;
-    if (hc.xfail)
+    if (hc.xfail) {
+        // the cross-rank barrier words are now out of step with the peers':
+        // no later fused launch may run on this session
+        fused_broken_ = true;
         throw std::runtime_error("fused sharded lane: a peer rank never reached the cross-rank "
                                  "barrier (are all ranks launched and connected?)");
+    }
     if (hc.error)
         throw std::logic_error("howard_par: structural error (a vertex has no successor "
                                "inside its region, or a region is not strongly connected)");
@@ -720,6 +741,10 @@ void Session::shard_connect(const ocm_shard_peer* peers, std::uint32_t world, bo
 void Session::fused_launch() {
     if (!connected_)
         throw std::logic_error("fused sharded lane: connect the peers first");
+    if (fused_broken_)
+        throw std::logic_error("fused sharded lane: a previous solve timed out at a cross-rank "
+                               "barrier; the barrier epochs are out of step, recreate the "
+                               "sessions");
     CK(cudaSetDevice(d_->device));
     if (prep_.exact)
         launch_async<ExactTag>(kShardFused);

@@ -66,6 +66,7 @@ class Session {
     void build_blocked_edges();
     bool shard_started_ = false;
     bool connected_ = false; // fused sharded lane: peers mapped
+    bool fused_broken_ = false; // a cross-rank barrier timed out (epochs out of step)
     double solve_ms_ = 0.0;   // event time of the current solve's launches
     std::uint64_t d2h_ = 0;   // device->host bytes of the current solve
     unsigned launches_ = 0;   // launches of the current solve

@@ -104,3 +104,25 @@ def test_unsupported_lanes_fail_loudly():
     g = P.build_graph(2, [(0, 1, 2), (1, 0, 4)])
     with pytest.raises((P.UnsupportedError, P.DeviceError)):
         P.solve(g, P.SolveOptions(algo="lawler"))
+
+
+def test_build_graph_rejects_unequal_arrays():
+    # the native builder would read past the shorter arrays
+    with pytest.raises(ValueError, match="differ in length"):
+        P.build_graph(4, (np.arange(4), [1], [1.0]))
+    with pytest.raises(ValueError, match="differ in length"):
+        P.build_graph(4, (np.arange(2), np.arange(2), [1.0]))
+
+
+def test_build_graph_rejects_ids_that_would_wrap():
+    # ids >= 2^32 wrapped to uint32 and a negative n became 2^32-1
+    with pytest.raises(ValueError, match="out of range"):
+        P.build_graph(2, [(0, 2**32, 1.0)])
+    with pytest.raises(ValueError, match="out of range"):
+        P.build_graph(-1, [(0, 0, 1.0)])
+    with pytest.raises(ValueError, match="out of range"):
+        P.build_graph(2**32, [(0, 0, 1.0)])
+    with pytest.raises(ValueError):
+        P.build_graph(3, (np.array([0.5]), np.array([1]), np.array([1.0])))
+    g = P.build_graph(0, (np.array([], np.int64), np.array([], np.int64), np.array([])))
+    assert (g.n, g.m) == (0, 0)
