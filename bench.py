@@ -45,16 +45,18 @@ CONFIGS = {
                                                      "weights 1..100 (BASELINE configs[1])"),
     3: dict(kind="model", clients=19, desc="client/server state space (reference server scenario, "
                                            "19 clients, BFS-numbered; BASELINE configs[2])"),
-    4: dict(kind="powerlaw", n=64_000_000, deg=8, dmax=1 << 20,
-            desc="power-law out-degree digraph n=6.4*10^7 (deg = min(2^20, floor(8/sqrt(u))), "
-                 "~1.0*10^9 edges) weights 1..100 (BASELINE configs[3])"),
+    4: dict(kind="powerlaw-hubs", n=64_000_000, deg=8, dmax=1 << 20,
+            desc="power-law degree digraph n=6.4*10^7: out-degree min(2^20, floor(8/sqrt(u))), "
+                 "in-degree tail exponent 3 too (hub targets), ~1.0*10^9 edges, weights 1..100 "
+                 "(BASELINE configs[3])"),
     5: dict(kind="uniform", n=250_000_000, deg=8, desc="uniform random digraph n=2.5*10^8 "
                                                        "out-degree 8 weights 1..100 (BASELINE configs[4])"),
 }
-# CPU baseline samples: the same generator at a size the reference solves in seconds
-CPU_SAMPLE = {1: dict(n=10_000), 2: dict(n=250_000), 3: dict(clients=13), 4: dict(n=250_000),
-              5: dict(n=250_000)}
-
+# The reference arm and cpu_baseline solve the workload graph itself; for the
+# two configs whose graph the reference cannot hold or solve in minutes on the
+# host (10^9 and 2*10^9 edges) they solve the same generator at n = 10^6,
+# and say so in "config" / "sample".
+REF_SAMPLE = {4: dict(n=1_000_000), 5: dict(n=1_000_000)}
 
 def parse():
     ap = argparse.ArgumentParser()
@@ -62,16 +64,48 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
+    ap.add_argument("--config", type=int, default=None, choices=sorted(CONFIGS),
+                    help="BASELINE config (default: 2 on one GPU, 4 -- the 10^9-edge power-law "
+                         "graph north_star shards -- on several)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--lane", default="replicas", choices=["replicas", "sharded", "fused"],
+    ap.add_argument("--lane", default=None, choices=["replicas", "sharded", "fused"],
                     help="replicas: every rank solves its own graph (weak scaling, the driver's "
                          "run); sharded: all ranks solve one graph, vertices 1-D partitioned, "
                          "policy all-gathered by NCCL between launches; fused: the same inside one "
                          "launch per rank, policy pushed into peer memory (strong scaling, "
-                         "DESIGN.md §7)")
+                         "DESIGN.md §7). Default: fused when several GPUs are used")
     return ap.parse_args()
+
+
+def resolve_defaults(a, world):
+    if a.config is None:
+        a.config = 2 if world == 1 else 4
+    if a.lane is None:
+        a.lane = "replicas" if world == 1 else "fused"
+    return a
+
+
+def self_launch(a):
+    """`bench.py --gpus N` without a torchrun environment: start N ranks on
+    this node with torch.distributed.run (127.0.0.1 rendezvous) and return
+    their exit status. Refuses N beyond the visible GPUs unless
+    OCM_BENCH_SHARE_GPU=1 maps several ranks onto one device (tests)."""
+    n = a.gpus
+    if a.impl == "b200" and os.environ.get("OCM_BENCH_SHARE_GPU") != "1":
+        import torch
+        have = torch.cuda.device_count()
+        if have < n:
+            sys.stderr.write(f"bench.py: --gpus {n} but only {have} GPU(s) are visible\n")
+            return 2
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes", "1", "--nproc-per-node",
+           str(n), "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def config(a, world):
@@ -241,49 +275,91 @@ def algorithmic_bytes(stats):
     return stats.spf_passes * imp + stats.outer_iters * 16 * stats.n_solved, imp
 
 
-def build_graph_host(a, P, sample=None):
-    c = dict(CONFIGS[a.config])
-    if sample:
-        c.update(sample)
+def build_graph_host(a, P):
+    c = CONFIGS[a.config]
     if c["kind"] == "model":
         return P.generate_model(P.server_scenario(), c["clients"], max_states=1 << 31)
     return P.generate(P.Generator(c["kind"], n=c["n"], deg=c["deg"], dmax=c.get("dmax", 0),
                                   wlo=1, whi=100, seed=SEED))
 
 
-def cpu_sample(a, P, steps=1):
-    """Reference CPU solver on a bounded sample (same generator, smaller size)."""
+def reference_workload(cfg):
+    """(spec, sampled): the graph the reference solves for config `cfg`."""
+    c = dict(CONFIGS[cfg])
+    sampled = cfg in REF_SAMPLE
+    c.update(REF_SAMPLE.get(cfg, {}))
+    return c, sampled
+
+
+def oracle_graph(c):
+    """The workload graph from the checkers' bit-identical generators
+    (oracle/, test infrastructure) -- the reference arm never imports the
+    product package."""
     import oracle as O
-    g = build_graph_host(a, P, CPU_SAMPLE[a.config])
-    s, d, w = g.edges()
-    n = g.n
-    use_ref = O.ref_available()
-    tot_ms, edges = 0.0, 0
-    for _ in range(steps):
-        for objective in ("min", "max"):
-            if use_ref:
-                r = O.ref_solve(n, s, d, w, "howard", objective, "tarjan")
-                tot_ms += r.solve_ms
-                passes = r.spf_passes
-            else:
-                t0 = time.perf_counter()
-                r = O.oracle_solve(n, s, d, w, objective)
-                tot_ms += (time.perf_counter() - t0) * 1e3
-                passes = r.extra.get("spf_passes_seq", r.spf_passes)
-            # intra-region edges per pass, as on the device
-            edges += _intra_edges(n, s, d) * passes
-    smp = CPU_SAMPLE[a.config]
-    what = (f"server scenario {smp['clients']} clients" if "clients" in smp
-            else f"{CONFIGS[a.config]['kind']} n={smp['n']}")
-    return {"value": edges / (tot_ms / 1e3), "unit": UNIT, "cores": 1,
-            "kind": "reference" if use_ref else "port",
-            "sample": f"{what} (same generator), min+max, reference lane 'howard' "
-                      f"(proj/src/solve.cpp run_howard_seq, single thread: the default CLI lane and "
-                      f"the fastest reference lane on these workloads -- its multi-threaded "
-                      f"howard-par lane measured 2.2x slower with all 16 host CPUs on this sample, "
-                      f"profiles/reference_lanes_r01.log), "
-                      f"{steps} step(s), solve time only",
-            "ms": tot_ms}
+    if c["kind"] == "model":
+        return O.generate_model("server", c["clients"])
+    if c["kind"] == "uniform":
+        s, d, w = O.generate_uniform(c["n"], c["deg"], 1, 100, SEED)
+    else:
+        s, d, w = O.generate_powerlaw(c["n"], c["deg"], c["dmax"], 1, 100, SEED,
+                                      hubs=c["kind"] == "powerlaw-hubs")
+    return c["n"], s, d, w
+
+
+def host_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def reference_solves(cfg, steps, warmup, threads):
+    """The reference's CPU solver (oracle/_ref: the unmodified proj/src
+    compiled in place, lane `howard` = run_howard_seq, proj/src/solve.cpp:43,
+    the reference CLI's default) on the workload graph, one min + one max
+    solve per step. The graph is built once (ocm::build_graph); the solves of
+    all steps run concurrently on `threads` host threads (ctypes releases the
+    GIL; ocm::solve only reads the graph), so the value is the reference's
+    throughput with the host's cores in use; time-to-OCM is the mean wall time
+    of one ocm::solve call among them. Edges are counted as on the device:
+    intra-region edges x improvement passes."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    import oracle as O
+    c, sampled = reference_workload(cfg)
+    n, s, d, w = oracle_graph(c)
+    intra = _intra_edges(n, s, d)
+    g = O.RefGraph(n, s, d, w)
+    m = len(s)
+    del s, d, w
+    # each concurrent solve holds O(n + m) state of its own: bound the
+    # concurrency for the 10^8-edge graphs
+    threads = max(1, min(threads, 2 * max(1, steps), 4 if m > 50_000_000 else threads))
+    objs = ("min", "max")
+    with ThreadPoolExecutor(threads) as ex:
+        list(ex.map(lambda o: g.solve("howard", o), [o for _ in range(warmup) for o in objs]))
+        t0 = time.perf_counter()
+        res = list(ex.map(lambda o: g.solve("howard", o), [o for _ in range(steps) for o in objs]))
+        wall = time.perf_counter() - t0
+    edges = sum(intra * r.spf_passes for r in res)
+    per = {o: [r for r, oo in zip(res, objs * steps) if oo == o] for o in objs}
+    what = (f"server scenario {c['clients']} clients" if c["kind"] == "model"
+            else f"{c['kind']} n={c['n']} deg={c['deg']}")
+    if sampled:
+        what += f" (the config's generator at n={c['n']}: the full graph does not fit the host)"
+    else:
+        what += " (the full workload graph)"
+    return {
+        "value": edges / wall, "wall_s": wall, "cores": threads, "m_intra": intra,
+        "time_to_ocm_s": {o: sum(r.solve_ms for r in per[o]) / len(per[o]) / 1e3 for o in objs},
+        "policy_iterations": {o: per[o][0].spf_passes for o in objs},
+        "mu": {o: f"{per[o][0].mu_num}/{per[o][0].mu_den}" for o in objs},
+        "config": dict(c, sampled=sampled),
+        "sample": f"{what}, {steps} step(s) of min+max (2*{steps} ocm::solve calls of the "
+                  f"reference's default lane 'howard', run_howard_seq, proj/src/solve.cpp:43) on "
+                  f"{threads} concurrent host threads; value = intra-region edges x passes / wall "
+                  f"time of those calls (graph built once beforehand)",
+    }
 
 
 _INTRA = {}
@@ -308,24 +384,28 @@ def _intra_edges(n, s, d):
 
 
 def run_reference(a, world, rank):
+    """--impl reference: rank 0 alone times the reference's CPU solver on
+    this arm's config; other ranks exit without work."""
     if rank != 0:
         return
-    import paper_1111_0627_b200 as P
-    steps = []
-    for i in range(a.warmup + a.steps):
-        r = cpu_sample(a, P, 1)
-        if i >= a.warmup:
-            steps.append(r)
-    tot_ms = sum(r["ms"] for r in steps)
-    val = sum(r["value"] * r["ms"] for r in steps) / tot_ms
-    base = steps[0]
-    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": world,
-            "steps": a.steps, "warmup": a.warmup, "ms_per_step": tot_ms / a.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
-            "data": "synthetic (seeded generator)", "config": config(a, 1),
-            "cpu_baseline": {"value": val, "unit": UNIT, "cores": base["cores"],
-                             "kind": base["kind"], "sample": base["sample"]},
-            "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    r = reference_solves(a.config, a.steps, a.warmup, host_threads())
+    cfg = config(a, 1)
+    if r["config"]["sampled"]:
+        cfg.update(n=r["config"]["n"], sampled_from_n=CONFIGS[a.config]["n"],
+                   workload=cfg["workload"] + f" -- SAMPLE: the same generator at "
+                                              f"n={r['config']['n']}")
+    cfg["parallelism"] = f"{r['cores']} host threads (concurrent solves)"
+    line = {"impl": "reference", "metric": METRIC, "value": r["value"], "unit": UNIT,
+            "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
+            "ms_per_step": r["wall_s"] * 1e3 / a.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "int64",
+            "data": "synthetic (seeded generator, oracle/ copy bit-identical to the product's)",
+            "config": cfg, "time_to_ocm_s": r["time_to_ocm_s"],
+            "policy_iterations": r["policy_iterations"], "mu": r["mu"],
+            "cpu_baseline": {"value": r["value"], "unit": UNIT, "cores": r["cores"],
+                             "kind": "reference", "sample": r["sample"]},
+            "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
@@ -397,7 +477,8 @@ def run_sharded(a, world, rank, local):
             out, ms = step()
             sols.append(out)
             tot_ms += ms
-    t = torch.tensor([tot_ms], dtype=torch.float64, device=dev)
+    t = torch.tensor([tot_ms], dtype=torch.float64,
+                     device=dev if dist.get_backend() == "nccl" else "cpu")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
     edges = sum(s[o].stats.m_solved * s[o].stats.spf_passes for s in sols for o in s)
@@ -427,15 +508,31 @@ def run_sharded(a, world, rank, local):
 
 def main():
     a = parse()
+    if a.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(a))
     world, rank, local = dist_env()
+    if world != a.gpus and "WORLD_SIZE" in os.environ:
+        sys.stderr.write(f"bench.py: --gpus {a.gpus} but WORLD_SIZE={world}\n")
+        sys.exit(2)
+    resolve_defaults(a, world)
+    share = a.impl == "b200" and os.environ.get("OCM_BENCH_SHARE_GPU") == "1" and world > 1
+    if share:
+        # test mode: several ranks on one GPU -- NCCL refuses duplicate
+        # devices, so the plumbing goes over gloo, and each rank's persistent
+        # grid takes 1/world of the SMs so the ranks' kernels are co-resident
+        import torch
+        local = local % max(1, torch.cuda.device_count())
+        os.environ.setdefault("OCM_GRID", str(148 * 4 // world))
     dist = None
     if world > 1:
         import torch
         import torch.distributed as dist
-        if a.impl == "b200":
+        if a.impl == "b200" and not share:
             torch.cuda.set_device(local)
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
+            if a.impl == "b200":
+                torch.cuda.set_device(local)
             dist.init_process_group("gloo")
     if a.impl == "reference":
         run_reference(a, world, rank)
@@ -529,9 +626,10 @@ def main():
     vals = [dev_ms, e2e[0] if e2e else 0.0]
     tots = [float(edges), float(e2e[1] if e2e else 0), float(launches)]
     if dist:
-        t = torch.tensor(vals, dtype=torch.float64, device=dev)
+        rdev = dev if dist.get_backend() == "nccl" else "cpu"
+        t = torch.tensor(vals, dtype=torch.float64, device=rdev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        tot = torch.tensor(tots, dtype=torch.float64, device=dev)
+        tot = torch.tensor(tots, dtype=torch.float64, device=rdev)
         dist.all_reduce(tot, op=dist.ReduceOp.SUM)
         vals, tots = t.tolist(), tot.tolist()
     dev_ms_max, e2e_max = vals
@@ -584,9 +682,12 @@ def main():
             line["e2e"] = {"value": e2e_edges_all / e2e_max, "unit": UNIT,
                            "h2d_bytes_per_step": e2e[2], "d2h_bytes_per_step": e2e[3]}
         if world == 1 and not a.no_cpu_baseline:
-            cb = cpu_sample(a, P, 1)
-            cb.pop("ms")
-            line["cpu_baseline"] = cb
+            # one min + one max solve of the reference on the same graph,
+            # concurrently on two host threads (~20-30 s of CPU work)
+            r = reference_solves(a.config, 1, 0, 2)
+            line["cpu_baseline"] = {"value": r["value"], "unit": UNIT, "cores": r["cores"],
+                                    "kind": "reference", "sample": r["sample"],
+                                    "time_to_ocm_s": r["time_to_ocm_s"], "mu": r["mu"]}
         print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()

@@ -111,6 +111,8 @@ int ocm_generate_uniform(uint32_t n, uint32_t deg, int32_t wlo, int32_t whi, uin
  * no host copy); both produce bit-identical graphs. */
 #define OCM_GEN_UNIFORM 0  /* every vertex has exactly deg out-edges */
 #define OCM_GEN_POWERLAW 1 /* deg(v) = min(dmax, floor(deg / sqrt(u_v))), tail exponent 3 */
+#define OCM_GEN_POWERLAW_HUBS 2 /* out-degrees as OCM_GEN_POWERLAW; targets floor(n*u^2) scattered
+                                   by a bijection: in-degree tail exponent 3 too (hub vertices) */
 typedef struct {
     int32_t kind;    /* OCM_GEN_* */
     uint32_t n;

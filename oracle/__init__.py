@@ -297,3 +297,106 @@ def ref_parse_graph_text(text: str, source: str = "<text>"):
     fn(b, len(b), source.encode(), C.byref(n), C.byref(m), C.byref(ex), m.value,
        _ptr(src, C.c_uint32), _ptr(dst, C.c_uint32), _ptr(w, C.c_double), C.byref(line))
     return ("ok", n.value, src, dst, w, bool(ex.value))
+
+
+def generate_powerlaw(n, dmin, dmax, wlo, whi, seed, hubs=False):
+    """Power-law out-degree generator ("powerlaw" / "powerlaw-hubs"), shared
+    bit-for-bit with the CUDA library's host and device generators."""
+    lib = oracle_lib()
+    fn = lib.oc_generate_powerlaw
+    fn.restype = C.c_uint64
+    fn.argtypes = [C.c_uint32, C.c_uint32, C.c_uint32, C.c_int32, C.c_int32, C.c_uint64, C.c_int,
+                   C.POINTER(C.c_uint32), C.POINTER(C.c_uint32), C.POINTER(C.c_double)]
+    m = int(fn(n, dmin, dmax, wlo, whi, seed, int(hubs), None, None, None))
+    src = np.empty(m, np.uint32)
+    dst = np.empty(m, np.uint32)
+    w = np.empty(m, np.float64)
+    fn(n, dmin, dmax, wlo, whi, seed, int(hubs), _ptr(src, C.c_uint32), _ptr(dst, C.c_uint32),
+       _ptr(w, C.c_double))
+    return src, dst, w
+
+
+# proj/src/model_gen.cpp:23 worker_scenario / :36 server_scenario, restated as
+# (states, [(from, to, cost, acquires, releases)], uses_server)
+SCENARIOS = {
+    "worker": (3, [(0, 1, 1, 0, 0), (1, 0, 0, 0, 0), (1, 2, 2, 0, 0), (2, 0, 3, 0, 0)], False),
+    "server": (4, [(0, 1, 1, 0, 0), (1, 0, 0, 0, 0), (1, 2, 2, 1, 0), (2, 3, 5, 0, 0),
+                   (3, 0, 1, 0, 1)], True),
+}
+
+
+def generate_model(scenario, clients, max_states=1 << 31):
+    """oc_generate_model: the restated reference model generator
+    (model_gen.cpp:88) without the reference's 5*10^6-state bound.
+    Returns (n, src, dst, w) in edge-id order."""
+    lib = oracle_lib()
+    fn = lib.oc_generate_model
+    fn.restype = C.c_int
+    P = C.POINTER
+    fn.argtypes = [C.c_uint32, C.c_uint32, P(C.c_uint32), P(C.c_uint32), P(C.c_int64),
+                   P(C.c_int32), P(C.c_int32), C.c_int, C.c_uint32, C.c_uint64, P(C.c_uint32),
+                   P(C.c_uint64), P(P(C.c_uint32)), P(P(C.c_uint32)), P(P(C.c_double))]
+    lib.oc_free.restype = None
+    lib.oc_free.argtypes = [C.c_void_p]
+    states, trs, uses_server = SCENARIOS[scenario] if isinstance(scenario, str) else scenario
+    cols = list(zip(*trs)) if trs else [(), (), (), (), ()]
+    f, t, c, a, r = (np.ascontiguousarray(x, dt) for x, dt in zip(
+        cols, (np.uint32, np.uint32, np.int64, np.int32, np.int32)))
+    n, m = C.c_uint32(), C.c_uint64()
+    ps, pd, pw = P(C.c_uint32)(), P(C.c_uint32)(), P(C.c_double)()
+    rc = fn(states, len(trs), _ptr(f, C.c_uint32), _ptr(t, C.c_uint32), _ptr(c, C.c_int64),
+            _ptr(a, C.c_int32), _ptr(r, C.c_int32), int(uses_server), clients, max_states,
+            C.byref(n), C.byref(m), C.byref(ps), C.byref(pd), C.byref(pw))
+    if rc:
+        raise {1: ValueError, 2: OverflowError}.get(rc, MemoryError)(f"oc_generate_model rc={rc}")
+    mm = m.value
+    try:
+        src = np.ctypeslib.as_array(ps, (mm,)).copy() if mm else np.empty(0, np.uint32)
+        dst = np.ctypeslib.as_array(pd, (mm,)).copy() if mm else np.empty(0, np.uint32)
+        w = np.ctypeslib.as_array(pw, (mm,)).copy() if mm else np.empty(0, np.float64)
+    finally:
+        for p in (ps, pd, pw):
+            lib.oc_free(C.cast(p, C.c_void_p))
+    return n.value, src, dst, w
+
+
+class RefGraph:
+    """A reference ocm::Graph built once (oracle/_ref ref_graph_create) and
+    solved repeatedly -- also from several threads at once (ctypes releases
+    the GIL; ocm::solve only reads the graph)."""
+
+    def __init__(self, n, src, dst, w):
+        lib = ref_lib()
+        lib.ref_graph_create.restype = C.c_void_p
+        lib.ref_graph_create.argtypes = [C.c_uint32, C.c_uint64, C.POINTER(C.c_uint32),
+                                         C.POINTER(C.c_uint32), C.POINTER(C.c_double)]
+        lib.ref_graph_free.restype = None
+        lib.ref_graph_free.argtypes = [C.c_void_p]
+        lib.ref_graph_solve.restype = C.c_int
+        lib.ref_graph_solve.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int,
+                                        C.POINTER(_RefResult), C.POINTER(C.c_uint32), C.c_uint32]
+        src, dst, w = _edges(src, dst, w)
+        self.n = int(n)
+        self._lib = lib
+        self._h = lib.ref_graph_create(n, src.shape[0], _ptr(src, C.c_uint32),
+                                       _ptr(dst, C.c_uint32), _ptr(w, C.c_double))
+        if not self._h:
+            raise RuntimeError("reference: " + lib.ref_last_error().decode())
+
+    def solve(self, algo="howard", objective="min", scc="tarjan") -> CheckerResult:
+        res = _RefResult()
+        cap = max(self.n, 1)
+        cyc = np.zeros(cap, dtype=np.uint32)
+        if self._lib.ref_graph_solve(self._h, ALGOS[algo], 1 if objective == "max" else 0,
+                                     SCCS[scc], C.byref(res), _ptr(cyc, C.c_uint32), cap):
+            raise RuntimeError("reference: " + self._lib.ref_last_error().decode())
+        out = CheckerResult(bool(res.has_cycle), bool(res.exact), res.mu_num, res.mu_den, res.mu,
+                            cyc[: res.cycle_len].tolist(), res.outer_iters, res.spf_passes,
+                            res.regions, res.trivial_regions, res.solve_ms, 0.0)
+        return out
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            self._lib.ref_graph_free(h)
+            self._h = None

@@ -18,6 +18,7 @@
  *   howard_region        include/ocm/howard.hpp:268  howard_solve
  *   oc_solve_howard      src/solve.cpp:43/117   run_howard_seq / solve()
  *   oc_dp_min_cycle_mean include/ocm/oracle.hpp:137 dp_min_cycle_mean
+ *   oc_generate_model    src/model_gen.cpp:88  generate_model (state bound as a parameter)
  *   oc_generate_*        (no reference counterpart) the seeded synthetic
  *                        generators shared bit-for-bit with the CUDA library
  *
@@ -672,4 +673,229 @@ void oc_generate_uniform(uint32_t n, uint32_t deg, int32_t wlo, int32_t whi, uin
         dst[e] = (uint32_t)(hash2(seed, 1, e) % n);
         w[e] = (double)(wlo + (int64_t)(hash2(seed, 2, e) % span));
     }
+}
+
+/* Power-law out-degree generator (paper_1111_0627_b200/csrc/gen.hpp
+ * generate_powerlaw / generate_powerlaw_hubs, restated): deg(v) =
+ * min(dmax, floor(dmin / sqrt(u_v))); hubs != 0 draws targets as
+ * floor(n * u^2) scattered by x -> (x * A + B) mod n. Two calls: with
+ * src == NULL only the edge count is returned. */
+uint64_t oc_generate_powerlaw(uint32_t n, uint32_t dmin, uint32_t dmax, int32_t wlo, int32_t whi,
+                              uint64_t seed, int hubs, uint32_t *src, uint32_t *dst, double *w) {
+    const uint64_t prime = 2654435761ull;
+    uint64_t mul = (n % prime == 0) ? 1 : prime % n;
+    uint64_t add = hash2(seed, 4, 0) % n;
+    uint64_t span = (uint64_t)((int64_t)whi - wlo + 1);
+    uint64_t e = 0;
+    for (uint32_t v = 0; v < n; ++v) {
+        double u = (double)((hash2(seed, 3, v) >> 11) + 1) * (1.0 / 9007199254740992.0);
+        double d = (double)dmin / sqrt(u);
+        uint32_t deg = d >= (double)dmax ? dmax : (uint32_t)d;
+        if (src) {
+            for (uint32_t i = 0; i < deg; ++i, ++e) {
+                uint64_t h = hash2(seed, 1, e);
+                uint32_t t;
+                if (hubs) {
+                    double uu = (double)((h >> 11) + 1) * (1.0 / 9007199254740992.0);
+                    double x = (double)n * (uu * uu);
+                    uint64_t r = (uint64_t)x;
+                    if (r >= n)
+                        r = n - 1;
+                    t = (uint32_t)((r * mul + add) % n);
+                } else {
+                    t = (uint32_t)(h % n);
+                }
+                src[e] = v;
+                dst[e] = t;
+                w[e] = (double)(wlo + (int64_t)(hash2(seed, 2, e) % span));
+            }
+        } else {
+            e += deg;
+        }
+    }
+    return e;
+}
+
+/* Composite state space of `clients` interleaved copies of a scenario
+ * (restates proj/src/model_gen.cpp:88-148 generate_model, with the state
+ * bound max_states instead of kMaxModelStates = 5'000'000 of
+ * model_gen.hpp:65): states are packed client_bits per client plus the
+ * server owner, numbered in breadth-first discovery order; for every state
+ * (in that order), every client (ascending) and every scenario transition
+ * (declaration order) enabled for it, one edge of that transition's cost.
+ * Returns 0, 1 on a malformed scenario, 2 past max_states, 3 out of memory.
+ * The edge arrays are malloc'ed (release with oc_free). */
+typedef struct {
+    uint64_t *keys;
+    uint32_t *ids;
+    uint64_t cap, size;
+} oc_state_map;
+
+static uint64_t oc_mix(uint64_t x) {
+    x ^= x >> 33;
+    x *= 0xff51afd7ed558ccdull;
+    x ^= x >> 33;
+    return x;
+}
+
+static int oc_map_grow(oc_state_map *m, uint64_t cap) {
+    uint64_t *ok = m->keys;
+    uint32_t *oi = m->ids;
+    uint64_t ocap = m->cap;
+    m->keys = (uint64_t *)calloc(cap, sizeof(uint64_t));
+    m->ids = (uint32_t *)malloc(cap * sizeof(uint32_t));
+    if (!m->keys || !m->ids)
+        return 3;
+    memset(m->ids, 0xff, cap * sizeof(uint32_t));
+    m->cap = cap;
+    for (uint64_t i = 0; i < ocap; ++i)
+        if (oi[i] != 0xffffffffu) {
+            uint64_t h = oc_mix(ok[i]) & (cap - 1);
+            while (m->ids[h] != 0xffffffffu)
+                h = (h + 1) & (cap - 1);
+            m->keys[h] = ok[i];
+            m->ids[h] = oi[i];
+        }
+    free(ok);
+    free(oi);
+    return 0;
+}
+
+/* id of `key`, inserting it as `fresh` when absent (*inserted = 1) */
+static uint32_t oc_map_intern(oc_state_map *m, uint64_t key, uint32_t fresh, int *inserted) {
+    uint64_t h = oc_mix(key) & (m->cap - 1);
+    while (m->ids[h] != 0xffffffffu) {
+        if (m->keys[h] == key) {
+            *inserted = 0;
+            return m->ids[h];
+        }
+        h = (h + 1) & (m->cap - 1);
+    }
+    m->keys[h] = key;
+    m->ids[h] = fresh;
+    m->size++;
+    *inserted = 1;
+    return fresh;
+}
+
+static uint32_t oc_bits_for(uint64_t values) {
+    uint32_t b = 0;
+    while (b < 64 && ((uint64_t)1 << b) < values)
+        ++b;
+    return b;
+}
+
+void oc_free(void *p) { free(p); }
+
+int oc_generate_model(uint32_t states, uint32_t ntr, const uint32_t *from, const uint32_t *to,
+                      const int64_t *cost, const int32_t *acquires, const int32_t *releases,
+                      int uses_server, uint32_t clients, uint64_t max_states, uint32_t *n_out,
+                      uint64_t *m_out, uint32_t **src_out, uint32_t **dst_out, double **w_out) {
+    if (states == 0 || clients == 0)
+        return 1;
+    for (uint32_t k = 0; k < ntr; ++k) {
+        if (from[k] >= states || to[k] >= states)
+            return 1;
+        if ((acquires[k] || releases[k]) && !uses_server)
+            return 1;
+    }
+    uint32_t cb = oc_bits_for(states);
+    if (cb < 1)
+        cb = 1;
+    uint32_t ob = uses_server ? oc_bits_for((uint64_t)clients + 1) : 0;
+    if ((uint64_t)cb * clients + ob > 64)
+        return 1;
+    uint64_t cmask = ((uint64_t)1 << cb) - 1;
+    uint64_t oshift = (uint64_t)clients * cb;
+    uint64_t omask = ob ? ((((uint64_t)1 << ob) - 1) << oshift) : 0;
+
+    oc_state_map map = {0};
+    uint64_t *queue = NULL, qcap = 0, nq = 0;
+    uint32_t *src = NULL, *dst = NULL;
+    double *w = NULL;
+    uint64_t ecap = 0, m = 0;
+    int rc = 0;
+    if (oc_map_grow(&map, 1 << 16))
+        return 3;
+    int ins;
+    oc_map_intern(&map, 0, 0, &ins); /* all clients in state 0, server free */
+    qcap = 1 << 16;
+    queue = (uint64_t *)malloc(qcap * sizeof(uint64_t));
+    if (!queue)
+        return 3;
+    queue[nq++] = 0;
+    for (uint64_t head = 0; head < nq && rc == 0; ++head) {
+        uint64_t s = queue[head];
+        uint64_t owner = ob ? (s & omask) >> oshift : 0;
+        for (uint32_t i = 0; i < clients && rc == 0; ++i) {
+            uint64_t shift = (uint64_t)i * cb;
+            uint32_t loc = (uint32_t)((s >> shift) & cmask);
+            for (uint32_t k = 0; k < ntr; ++k) {
+                if (from[k] != loc)
+                    continue;
+                if (acquires[k] && owner != 0)
+                    continue;
+                if (releases[k] && owner != (uint64_t)i + 1)
+                    continue;
+                uint64_t ns = (s & ~(cmask << shift)) | ((uint64_t)to[k] << shift);
+                if (acquires[k])
+                    ns = (ns & ~omask) | ((uint64_t)(i + 1) << oshift);
+                if (releases[k])
+                    ns &= ~omask;
+                if ((map.size + 1) * 2 > map.cap && oc_map_grow(&map, map.cap * 2)) {
+                    rc = 3;
+                    break;
+                }
+                uint32_t id = oc_map_intern(&map, ns, (uint32_t)nq, &ins);
+                if (ins) {
+                    if (nq + 1 > max_states) {
+                        rc = 2;
+                        break;
+                    }
+                    if (nq == qcap) {
+                        qcap *= 2;
+                        uint64_t *q2 = (uint64_t *)realloc(queue, qcap * sizeof(uint64_t));
+                        if (!q2) {
+                            rc = 3;
+                            break;
+                        }
+                        queue = q2;
+                    }
+                    queue[nq++] = ns;
+                }
+                if (m == ecap) {
+                    ecap = ecap ? ecap * 2 : (1 << 16);
+                    uint32_t *s2 = (uint32_t *)realloc(src, ecap * sizeof(uint32_t));
+                    if (s2) src = s2;
+                    uint32_t *d2 = (uint32_t *)realloc(dst, ecap * sizeof(uint32_t));
+                    if (d2) dst = d2;
+                    double *w2 = (double *)realloc(w, ecap * sizeof(double));
+                    if (w2) w = w2;
+                    if (!s2 || !d2 || !w2) {
+                        rc = 3;
+                        break;
+                    }
+                }
+                src[m] = (uint32_t)head;
+                dst[m] = id;
+                w[m] = (double)cost[k];
+                ++m;
+            }
+        }
+    }
+    free(map.keys);
+    free(map.ids);
+    free(queue);
+    if (rc) {
+        free(src);
+        free(dst);
+        free(w);
+        return rc;
+    }
+    *n_out = (uint32_t)nq;
+    *m_out = m;
+    *src_out = src;
+    *dst_out = dst;
+    *w_out = w;
+    return 0;
 }

@@ -211,4 +211,53 @@ int ref_parse_graph_text(const char* text, uint64_t len, const char* source, uin
     }
 }
 
+// A reference Graph built once and solved many times (possibly from several
+// threads at once: ocm::solve only reads the const Graph), so timing loops
+// measure ocm::solve alone.
+void* ref_graph_create(uint32_t n, uint64_t m, const uint32_t* src, const uint32_t* dst,
+                       const double* w) {
+    try {
+        return new ocm::Graph(make_graph(n, m, src, dst, w));
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return nullptr;
+    }
+}
+
+void ref_graph_free(void* g) { delete static_cast<ocm::Graph*>(g); }
+
+int ref_graph_solve(const void* gp, int algo, int objective, int scc, ref_result* out,
+                    uint32_t* cycle_buf, uint32_t cycle_cap) {
+    try {
+        const ocm::Graph& g = *static_cast<const ocm::Graph*>(gp);
+        ocm::SolveOptions opt;
+        opt.algo = static_cast<ocm::Algo>(algo);
+        opt.objective = objective ? ocm::Objective::Maximize : ocm::Objective::Minimize;
+        opt.scc = static_cast<ocm::SccStrategy>(scc);
+        auto t0 = std::chrono::steady_clock::now();
+        const ocm::Solution s = ocm::solve(g, opt);
+        auto t1 = std::chrono::steady_clock::now();
+        std::memset(out, 0, sizeof *out);
+        out->has_cycle = s.has_cycle;
+        out->exact = s.exact;
+        out->mu_num = s.mu_exact.num;
+        out->mu_den = s.mu_exact.den;
+        out->mu = s.mu;
+        out->cycle_len = static_cast<uint32_t>(s.cycle_vertices.size());
+        for (uint32_t i = 0; i < out->cycle_len && i < cycle_cap; ++i)
+            cycle_buf[i] = s.cycle_vertices[i];
+        out->outer_iters = s.stats.outer_iters;
+        out->spf_passes = s.stats.spf_passes;
+        out->regions = s.stats.regions;
+        out->trivial_regions = s.stats.trivial_regions;
+        out->launches = s.stats.launches;
+        out->fixpoint_iters = s.stats.fixpoint_iters;
+        out->solve_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 1;
+    }
+}
+
 } // extern "C"

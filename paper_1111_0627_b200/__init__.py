@@ -311,8 +311,10 @@ def generate_uniform(n: int, deg: int, wlo: int = 1, whi: int = 100, seed: int =
 @dataclass
 class Generator:
     """Synthetic benchmark graph (include/ocm_b200.h ocm_generator): kind
-    "uniform" (out-degree exactly ``deg``) or "powerlaw" (out-degree
-    min(dmax, floor(deg / sqrt(u))), tail exponent 3); integer weights
+    "uniform" (out-degree exactly ``deg``), "powerlaw" (out-degree
+    min(dmax, floor(deg / sqrt(u))), tail exponent 3, uniform targets) or
+    "powerlaw-hubs" (the same out-degrees, targets floor(n*u^2) scattered by
+    a bijection: in-degrees with tail exponent 3, i.e. hub vertices); integer weights
     uniform in [wlo, whi]. :func:`generate` builds it on the host,
     :meth:`Session.generated` directly in HBM -- bit-identical graphs."""
     kind: str = "uniform"
@@ -324,7 +326,7 @@ class Generator:
     seed: int = 1
 
     def _c(self) -> "_Gen":
-        kinds = {"uniform": 0, "powerlaw": 1}
+        kinds = {"uniform": 0, "powerlaw": 1, "powerlaw-hubs": 2}
         if self.kind not in kinds:
             raise ValueError(f"unknown generator kind {self.kind!r}")
         return _Gen(kinds[self.kind], int(self.n), int(self.deg), int(self.dmax), int(self.wlo),

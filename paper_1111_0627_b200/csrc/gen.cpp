@@ -41,8 +41,10 @@ Graph generate_uniform(std::uint32_t n, std::uint32_t deg, std::int32_t wlo, std
     return g;
 }
 
-Graph generate_powerlaw(std::uint32_t n, std::uint32_t dmin, std::uint32_t dmax, std::int32_t wlo,
-                        std::int32_t whi, std::uint64_t seed) {
+namespace {
+
+Graph powerlaw_graph(std::uint32_t n, std::uint32_t dmin, std::uint32_t dmax, std::int32_t wlo,
+                     std::int32_t whi, std::uint64_t seed, bool hubs) {
     if (n == 0 || dmin == 0 || dmax < dmin || whi < wlo)
         throw std::invalid_argument("generate_powerlaw: need n > 0, 0 < dmin <= dmax, wlo <= whi");
     Graph g;
@@ -59,13 +61,15 @@ Graph generate_powerlaw(std::uint32_t n, std::uint32_t dmin, std::uint32_t dmax,
     g.fwd_target.resize(m);
     g.fwd_weight.resize(m);
     const std::uint64_t span = std::uint64_t(std::int64_t(whi) - wlo + 1);
+    const std::uint64_t mul = hub_mul(n), add = hub_add(seed, n);
     unsigned T = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
     std::vector<std::thread> pool;
     for (unsigned t = 0; t < T; ++t)
         pool.emplace_back([&, t] {
             const std::uint64_t lo = m * t / T, hi = m * (t + 1) / T;
             for (std::uint64_t e = lo; e < hi; ++e) {
-                g.fwd_target[e] = static_cast<Vertex>(hash2(seed, 1, e) % n);
+                g.fwd_target[e] = hubs ? hub_target(hash2(seed, 1, e), n, mul, add)
+                                       : static_cast<Vertex>(hash2(seed, 1, e) % n);
                 g.fwd_weight[e] = double(wlo + std::int64_t(hash2(seed, 2, e) % span));
             }
         });
@@ -74,11 +78,25 @@ Graph generate_powerlaw(std::uint32_t n, std::uint32_t dmin, std::uint32_t dmax,
     return g;
 }
 
+} // namespace
+
+Graph generate_powerlaw(std::uint32_t n, std::uint32_t dmin, std::uint32_t dmax, std::int32_t wlo,
+                        std::int32_t whi, std::uint64_t seed) {
+    return powerlaw_graph(n, dmin, dmax, wlo, whi, seed, false);
+}
+
+Graph generate_powerlaw_hubs(std::uint32_t n, std::uint32_t dmin, std::uint32_t dmax,
+                             std::int32_t wlo, std::int32_t whi, std::uint64_t seed) {
+    return powerlaw_graph(n, dmin, dmax, wlo, whi, seed, true);
+}
+
 Graph generate(const GenSpec& s) {
     if (s.kind == 0)
         return generate_uniform(s.n, s.deg, s.wlo, s.whi, s.seed);
     if (s.kind == 1)
         return generate_powerlaw(s.n, s.deg, s.dmax, s.wlo, s.whi, s.seed);
+    if (s.kind == 2)
+        return generate_powerlaw_hubs(s.n, s.deg, s.dmax, s.wlo, s.whi, s.seed);
     throw std::invalid_argument("unknown generator kind");
 }
 

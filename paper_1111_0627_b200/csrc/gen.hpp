@@ -23,10 +23,20 @@ Graph generate_uniform(std::uint32_t n, std::uint32_t deg, std::int32_t wlo, std
 Graph generate_powerlaw(std::uint32_t n, std::uint32_t dmin, std::uint32_t dmax, std::int32_t wlo,
                         std::int32_t whi, std::uint64_t seed);
 
+// Power-law in- and out-degrees ("hub" graphs): out-degrees as
+// generate_powerlaw; the target of edge e is x = floor(n * u^2) (u uniform
+// in (0, 1]) scattered over the vertex ids by the bijection
+// x -> (x * A + B) mod n, so vertex rank r receives in-degree ~ r^(-1/2):
+// P(in-degree > d) ~ d^(-2), the same tail exponent 3 as the out-degrees,
+// with the hubs spread across the id space (not the low ids). Exactly
+// rounded double multiplies only, so host and device agree bit for bit.
+Graph generate_powerlaw_hubs(std::uint32_t n, std::uint32_t dmin, std::uint32_t dmax,
+                             std::int32_t wlo, std::int32_t whi, std::uint64_t seed);
+
 // Generator description shared by the host generators and the device ones
 // (gen_dev.cu) that write the CSR straight into HBM.
 struct GenSpec {
-    int kind = 0; // 0 uniform, 1 power-law
+    int kind = 0; // 0 uniform, 1 power-law out-degree, 2 power-law in- and out-degree
     std::uint32_t n = 0;
     std::uint32_t deg = 8; // uniform: out-degree; power-law: dmin
     std::uint32_t dmax = 0; // power-law cap
@@ -52,6 +62,21 @@ inline std::uint32_t powerlaw_degree(std::uint64_t seed, std::uint32_t v, std::u
     const double u = double((hash2(seed, 3, v) >> 11) + 1) * (1.0 / 9007199254740992.0);
     const double d = double(dmin) / std::sqrt(u);
     return d >= double(dmax) ? dmax : static_cast<std::uint32_t>(d);
+}
+
+// Target scatter of generate_powerlaw_hubs: multiplier and offset of the
+// bijection x -> (x * A + B) mod n.
+constexpr std::uint64_t kHubMul = 2654435761ull; // prime, so coprime to every n != it
+inline std::uint64_t hub_mul(std::uint32_t n) { return n % kHubMul == 0 ? 1 : kHubMul % n; }
+inline std::uint64_t hub_add(std::uint64_t seed, std::uint32_t n) { return hash2(seed, 4, 0) % n; }
+inline std::uint32_t hub_target(std::uint64_t h, std::uint32_t n, std::uint64_t mul,
+                                std::uint64_t add) {
+    const double u = double((h >> 11) + 1) * (1.0 / 9007199254740992.0);
+    double x = double(n) * (u * u);
+    std::uint64_t r = static_cast<std::uint64_t>(x);
+    if (r >= n)
+        r = n - 1;
+    return static_cast<std::uint32_t>((r * mul + add) % n);
 }
 
 } // namespace ocmb

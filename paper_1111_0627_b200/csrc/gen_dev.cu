@@ -52,11 +52,24 @@ __global__ void kg_powerlaw_deg(std::uint32_t n, std::uint64_t k3, std::uint32_t
     }
 }
 
+// hub_target (gen.hpp) with explicitly rounded multiplies
+__device__ __forceinline__ std::uint32_t d_hub_target(std::uint64_t h, std::uint32_t n,
+                                                      std::uint64_t mul, std::uint64_t add) {
+    const double u = __dmul_rn(double((h >> 11) + 1), 1.0 / 9007199254740992.0);
+    const double x = __dmul_rn(double(n), __dmul_rn(u, u));
+    std::uint64_t r = static_cast<std::uint64_t>(x);
+    if (r >= n)
+        r = n - 1;
+    return static_cast<std::uint32_t>((r * mul + add) % n);
+}
+
 __global__ void kg_edges(std::uint64_t m, std::uint32_t n, std::uint64_t k1, std::uint64_t k2,
-                         std::int32_t wlo, std::uint64_t span, std::uint32_t* tgt, double* w) {
+                         std::int32_t wlo, std::uint64_t span, std::uint32_t* tgt, double* w,
+                         std::uint64_t hub_mul, std::uint64_t hub_add) {
     for (std::uint64_t e = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x; e < m;
          e += std::uint64_t(gridDim.x) * blockDim.x) {
-        tgt[e] = static_cast<std::uint32_t>(d_hash(k1, e) % n);
+        tgt[e] = hub_mul ? d_hub_target(d_hash(k1, e), n, hub_mul, hub_add)
+                         : static_cast<std::uint32_t>(d_hash(k1, e) % n);
         w[e] = double(wlo + static_cast<std::int64_t>(d_hash(k2, e) % span));
     }
 }
@@ -72,7 +85,7 @@ void device_generate_prepare(const GenSpec& spec, const ocm_solve_options& opt, 
                              PrepInfo& info) {
     cudaStream_t s = d.stream;
     const std::uint32_t n = spec.n;
-    if (n == 0 || spec.deg == 0 || spec.whi < spec.wlo || (spec.kind == 1 && spec.dmax < spec.deg))
+    if (n == 0 || spec.deg == 0 || spec.whi < spec.wlo || (spec.kind != 0 && spec.dmax < spec.deg))
         throw std::invalid_argument("generator: need n > 0, degree > 0, wlo <= whi (dmin <= dmax)");
     DBuf<std::uint32_t> row, tgt;
     DBuf<double> w;
@@ -84,7 +97,7 @@ void device_generate_prepare(const GenSpec& spec, const ocm_solve_options& opt, 
         if (m >= 0xffffffffull)
             throw std::invalid_argument("generate_uniform: edge count exceeds the 32-bit id space");
         kg_uniform_row<<<g, kBlock, 0, s>>>(n, spec.deg, row.p);
-    } else if (spec.kind == 1) {
+    } else if (spec.kind == 1 || spec.kind == 2) {
         DBuf<std::uint32_t> deg;
         deg.alloc(std::size_t(n) + 1, s);
         kg_powerlaw_deg<<<g, kBlock, 0, s>>>(n, stream_key(spec.seed, 3), spec.deg, spec.dmax, deg.p);
@@ -115,7 +128,9 @@ void device_generate_prepare(const GenSpec& spec, const ocm_solve_options& opt, 
     const std::uint64_t span = std::uint64_t(std::int64_t(spec.whi) - spec.wlo + 1);
     kg_edges<<<grid_for(m, d.sms, 32), kBlock, 0, s>>>(m, n, stream_key(spec.seed, 1),
                                                          stream_key(spec.seed, 2), spec.wlo, span,
-                                                         tgt.p, w.p);
+                                                         tgt.p, w.p,
+                                                         spec.kind == 2 ? hub_mul(n) : 0,
+                                                         spec.kind == 2 ? hub_add(spec.seed, n) : 0);
     CK(cudaGetLastError());
     device_prepare_csr(n, m, row, tgt, w, true, opt, d, info);
 }

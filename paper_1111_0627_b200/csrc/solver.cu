@@ -574,11 +574,21 @@ template <class M> void Session::collect(ocm_solution* out, std::uint32_t* cycle
         }
         return src[a] < src[b];
     };
+    std::uint64_t outer_sum = 0;
     for (std::size_t r = 0; r < R; ++r) {
         if (its[r] == 0 || src[r] == NONE)
             throw std::logic_error("howard_par: first improvement pass made no change");
+        outer_sum += its[r];
         if (best == R || less(r, best))
             best = r;
+    }
+    if (opt_.algo == OCM_ALGO_HOWARD) {
+        // run_howard_seq (src/solve.cpp:71-72) sums every region's outer
+        // iterations and improvement passes (a region's passes = its
+        // adoptions + the final quiet pass); howard-par reports the maximum
+        // over the concurrently iterating regions (hc.outer / hc.passes)
+        out->outer_iters = static_cast<std::uint32_t>(outer_sum);
+        out->spf_passes = static_cast<std::uint32_t>(outer_sum + R);
     }
     long long num = ln[best], den = ld[best];
     double mu = EXACT ? double(num) / double(den) : lf[best];

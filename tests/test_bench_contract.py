@@ -51,3 +51,50 @@ def test_device_arm_json_contract():
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
     assert d["gpu_launches"] >= 2 and d["certified"] == {"min": True, "max": True}
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
+
+
+@pytest.mark.skipif(not os.path.exists(os.path.join(ROOT, "oracle", "_ref", "libocm_ref.so")),
+                    reason="oracle/_ref not built")
+def test_reference_arm_never_loads_the_product():
+    """The reference arm builds its graph with the checkers' generators and
+    solves it with oracle/_ref: the product library is never mapped."""
+    code = ("import runpy, sys; sys.argv = ['bench.py', '--impl', 'reference', '--steps', '1', "
+            "'--warmup', '0', '--config', '1']; runpy.run_path('bench.py', run_name='__main__'); "
+            "maps = open('/proc/self/maps').read(); "
+            "assert 'libocm_b200' not in maps, 'product library loaded'; "
+            "assert 'libocm_ref' in maps; "
+            "assert 'paper_1111_0627_b200' not in sys.modules")
+    out = subprocess.run([sys.executable, "-c", code], cwd=ROOT, capture_output=True, text=True,
+                         timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    d = json.loads([l for l in out.stdout.splitlines() if l.startswith("{")][0])
+    # the same graph as the device arm: config 1 at full size, not a sample
+    assert d["config"]["n"] == 10_000 and "SAMPLE" not in d["config"]["workload"]
+    assert d["mu"] == {"min": "419/40", "max": "632/7"}  # tests/golden/config_golden.json
+
+
+@pytest.mark.skipif(not os.path.exists(os.path.join(ROOT, "oracle", "_ref", "libocm_ref.so")),
+                    reason="oracle/_ref not built")
+def test_gpus_flag_self_launches_ranks():
+    """`bench.py --gpus 2` without a torchrun environment starts two ranks
+    itself (torch.distributed.run on 127.0.0.1); rank 0 alone prints."""
+    env = {k: v for k, v in os.environ.items()
+           if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT")}
+    out = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--gpus", "2",
+                          "--steps", "1", "--warmup", "0", "--config", "1"], cwd=ROOT,
+                         capture_output=True, text=True, timeout=600, env=env)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["impl"] == "reference"
+
+
+def test_gpus_flag_refuses_missing_devices():
+    """More ranks than visible GPUs fails loudly instead of measuring fewer."""
+    import torch
+    n = max(2, torch.cuda.device_count() + 1)
+    out = subprocess.run([sys.executable, "bench.py", "--gpus", str(n), "--steps", "1"], cwd=ROOT,
+                         capture_output=True, text=True, timeout=300,
+                         env={k: v for k, v in os.environ.items() if k != "WORLD_SIZE"})
+    assert out.returncode != 0 and "visible" in out.stderr

@@ -1,0 +1,93 @@
+"""The BASELINE configurations' own graphs against the UNMODIFIED reference
+(tests/golden/config_golden.json, written by make_config_golden.py with
+oracle/_ref at bench.py's seed).
+
+CPU: the product's generators build exactly the graphs the reference solved
+(SHA-256 of n and the edge arrays). GPU: the device solves them, through the
+C-ABI, to the reference's optimal cycle mean (bit-exact rational), the same
+cycle, the same outer iterations and improvement passes (lane howard: summed
+over regions like run_howard_seq, proj/src/solve.cpp:71-72) and region
+counts -- config 3 at its full 19-client size (1.05*10^7 states)."""
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+
+import paper_1111_0627_b200 as P
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+with open(os.path.join(HERE, "golden", "config_golden.json")) as f:
+    GOLD = json.load(f)
+SEED = GOLD["seed"]
+
+
+def product_graph(cfg):
+    c = GOLD["configs"][cfg]["spec"]
+    if c["kind"] == "model":
+        return P.generate_model(P.server_scenario(), c["clients"], max_states=1 << 31)
+    return P.generate(P.Generator(c["kind"], n=c["n"], deg=c["deg"], dmax=c.get("dmax", 0),
+                                  wlo=1, whi=100, seed=SEED))
+
+
+def sha(g):
+    h = hashlib.sha256()
+    h.update(np.uint64(g.n).tobytes())
+    for a in g.edges():
+        h.update(np.ascontiguousarray(a).tobytes())
+    return h.hexdigest()
+
+
+@pytest.mark.parametrize("cfg", sorted(GOLD["configs"]))
+def test_product_generator_builds_the_reference_graph(cfg):
+    g = product_graph(cfg)
+    ref = GOLD["configs"][cfg]
+    assert (g.n, g.m) == (ref["n"], ref["m"])
+    assert sha(g) == ref["sha256"]
+
+
+def check(sol, ref):
+    assert sol.has_cycle == ref["has_cycle"]
+    assert sol.exact and (sol.mu_exact.numerator, sol.mu_exact.denominator) == \
+        (ref["mu_num"], ref["mu_den"])
+    assert sol.mu == ref["mu"]
+    assert sol.cycle_vertices == ref["cycle"]
+    assert (sol.stats.outer_iters, sol.stats.spf_passes) == (ref["outer_iters"], ref["spf_passes"])
+    assert (sol.stats.regions, sol.stats.trivial_regions) == \
+        (ref["regions"], ref["trivial_regions"])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cfg", sorted(GOLD["configs"]))
+def test_device_matches_reference_on_config_graph(cfg):
+    g = product_graph(cfg)
+    for objective in ("min", "max"):
+        ref = GOLD["configs"][cfg]["results"][objective]
+        # through ocm_solve (host graph, upload, device region split)
+        check(P.solve(g, P.SolveOptions(algo="howard", objective=objective)), ref)
+        # a resident session (the bench's path), lane howard-par: the same
+        # mean and cycle; its statistics are the maximum over the regions
+        # iterating concurrently (equal to howard's with one non-trivial region)
+        s = P.Session(g, P.SolveOptions(algo="howard-par", objective=objective)).solve()
+        assert s.mu_exact.numerator == ref["mu_num"] and s.mu_exact.denominator == ref["mu_den"]
+        assert s.cycle_vertices == ref["cycle"]
+        if ref["nontrivial_regions"] == 1:
+            assert (s.stats.outer_iters, s.stats.spf_passes) == \
+                (ref["outer_iters"], ref["spf_passes"])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cfg", [c for c in sorted(GOLD["configs"])
+                                 if GOLD["configs"][c]["spec"]["kind"] != "model"])
+def test_hbm_generated_session_matches_reference(cfg):
+    """The bench's sessions generate the graph in HBM (gen_dev.cu): same answer."""
+    c = GOLD["configs"][cfg]["spec"]
+    spec = P.Generator(c["kind"], n=c["n"], deg=c["deg"], dmax=c.get("dmax", 0), wlo=1, whi=100,
+                       seed=SEED)
+    for objective in ("min", "max"):
+        ref = GOLD["configs"][cfg]["results"][objective]
+        s = P.Session.generated(spec, P.SolveOptions(algo="howard", objective=objective))
+        check(s.solve(), ref)
+        cert = s.certify()
+        assert cert["key_violations"] == cert["policy_violations"] == cert["cycle_violations"] == 0

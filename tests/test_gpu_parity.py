@@ -47,6 +47,27 @@ def check_against(sol, vals, ref, key_field="value_key"):
 
 
 @pytest.mark.parametrize("case", CASES, ids=[c["name"] for c in CASES])
+def test_golden_howard_lane_stats(case):
+    """algo=howard: the reference's sequential lane sums every region's outer
+    iterations and improvement passes (src/solve.cpp:71-72); mu and the
+    cycle are the same as howard-par's."""
+    n = case["n"]
+    src, dst, w = case_arrays(case)
+    g = P.build_graph(n, (src, dst, w))
+    for key, ref in case["results"].items():
+        objective, scc = key.split("/")
+        if "seq_outer_iters" not in ref:
+            continue
+        sol = P.solve(g, P.SolveOptions(algo="howard", objective=objective, scc=scc))
+        assert sol.has_cycle == ref["has_cycle"]
+        if ref["has_cycle"]:
+            assert sol.cycle_vertices == ref["cycle"]
+            assert sol.mu == ref["mu"]
+        assert (sol.stats.outer_iters, sol.stats.spf_passes) == \
+            (ref["seq_outer_iters"], ref["seq_spf_passes"]), key
+
+
+@pytest.mark.parametrize("case", CASES, ids=[c["name"] for c in CASES])
 def test_golden(case):
     n = case["n"]
     src, dst, w = case_arrays(case)

@@ -12,6 +12,7 @@ import os
 import numpy as np
 import pytest
 
+import oracle as O
 import paper_1111_0627_b200 as P
 
 GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "model_golden.json")))
@@ -73,3 +74,27 @@ def test_model_solve_matches_reference(case):
         assert sol.has_cycle
         assert (sol.mu_exact.numerator, sol.mu_exact.denominator) == (num, den), obj
         assert len(sol.cycle_vertices) == clen and sol.cycle_vertices[:64] == cyc, obj
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("scenario,clients", [("server", 3), ("server", 9), ("worker", 7)])
+def test_oracle_model_generator_matches_reference(scenario, clients):
+    """oracle/ocm_oracle.c oc_generate_model (the restatement used for graphs
+    beyond the reference's 5*10^6-state bound) equals the reference's
+    generate_model edge for edge."""
+    n, s, d, w = O.generate_model(scenario, clients)
+    nr, sr, dr, wr = O.ref_generate_model(scenario, clients)
+    assert n == nr and np.array_equal(s, sr) and np.array_equal(d, dr) and np.array_equal(w, wr)
+
+
+@pytest.mark.parametrize("kind", ["powerlaw", "powerlaw-hubs"])
+def test_oracle_powerlaw_generators_match_product(kind):
+    s, d, w = O.generate_powerlaw(50_000, 4, 5_000, 1, 100, 9, hubs=kind == "powerlaw-hubs")
+    g = P.generate(P.Generator(kind, n=50_000, deg=4, dmax=5_000, seed=9))
+    s2, d2, w2 = g.edges()
+    assert np.array_equal(s, s2) and np.array_equal(d, d2) and np.array_equal(w, w2)
+    indeg = np.bincount(d, minlength=50_000)
+    if kind == "powerlaw-hubs":  # hub targets: in-degree tail exponent 3
+        assert indeg.max() > 50 * indeg.mean()
+    else:
+        assert indeg.max() < 10 * indeg.mean()
