@@ -150,6 +150,19 @@ int ocm_graph_edges(const ocm_graph* g, uint32_t* src, uint32_t* dst, double* w)
 int ocm_solve(const ocm_graph* g, const ocm_solve_options* opt, ocm_solution* out,
               uint32_t* cycle_buf, uint32_t cycle_cap);
 
+/* ocm::solve (solve.hpp:64) on the reference's own graph representation,
+ * without building an ocm_graph: the forward CSR of ocm::Graph exactly as it
+ * lies in the caller's memory (graph.hpp:38-41: fwd_index has n+1 EdgeId =
+ * uint32 offsets, fwd_target m vertices, fwd_weight m doubles; edge id =
+ * CSR position). The arrays are only read: pageable memory is staged through
+ * the library's pinned ring, page-locked memory is copied directly. The
+ * device checks them as build_graph would (graph.cpp:29-36: OCM_E_INVALID
+ * "edge <e> endpoint out of range" / "edge <e> has non-finite weight", and
+ * offsets that do not run from 0 to m) and derives integer_exact itself. */
+int ocm_solve_csr(uint32_t n, uint32_t m, const uint32_t* fwd_index, const uint32_t* fwd_target,
+                  const double* fwd_weight, const ocm_solve_options* opt, ocm_solution* out,
+                  uint32_t* cycle_buf, uint32_t cycle_cap);
+
 /* Resident sessions: create uploads the region-compacted CSR into HBM once;
  * each solve re-runs policy iteration from the initial policy on the device. */
 int ocm_session_create(const ocm_graph* g, const ocm_solve_options* opt, ocm_session** out);

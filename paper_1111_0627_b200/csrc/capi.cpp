@@ -324,4 +324,29 @@ int ocm_solve(const ocm_graph* g, const ocm_solve_options* opt, ocm_solution* ou
     });
 }
 
+int ocm_solve_csr(uint32_t n, uint32_t m, const uint32_t* fwd_index, const uint32_t* fwd_target,
+                  const double* fwd_weight, const ocm_solve_options* opt, ocm_solution* out,
+                  uint32_t* cycle_buf, uint32_t cycle_cap) {
+    return guard([&] {
+        if (!out || (n && !fwd_index) || (m && (!fwd_target || !fwd_weight)))
+            throw std::invalid_argument("null CSR array or output");
+        std::memset(out, 0, sizeof *out);
+        out->mu_den = 1;
+        if (n == 0) {
+            if (m)
+                throw std::invalid_argument("edge 0 endpoint out of range");
+            return; // solve.cpp:199: an empty graph has no cycle
+        }
+        ocmb::HostCsr h;
+        h.n = n;
+        h.m = m;
+        h.index32 = fwd_index;
+        h.target = fwd_target;
+        h.weight = fwd_weight;
+        h.validated = false;
+        ocmb::Session sess(h, defaults(opt));
+        sess.solve(out, cycle_buf, cycle_cap);
+    });
+}
+
 } // extern "C"

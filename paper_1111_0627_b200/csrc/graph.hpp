@@ -39,6 +39,35 @@ class ParseError : public std::runtime_error {
     int line_;
 };
 
+// A host CSR the device path uploads from: either this library's Graph
+// (64-bit offsets, registered/pinned by the C-ABI) or the reference's own
+// ocm::Graph arrays handed over as they are (32-bit EdgeId offsets,
+// graph.hpp:21/38-41; pageable memory, staged). `validated` = the arrays
+// come from build_graph (endpoints, finiteness and exactness already known);
+// otherwise the device checks them before preparing.
+struct HostCsr {
+    Vertex n = 0;
+    std::uint64_t m = 0;
+    const std::uint64_t* index64 = nullptr;
+    const std::uint32_t* index32 = nullptr;
+    const Vertex* target = nullptr;
+    const double* weight = nullptr;
+    bool integer_exact = false;
+    bool validated = false;
+};
+
+inline HostCsr csr_view(const Graph& g) {
+    HostCsr h;
+    h.n = g.n;
+    h.m = g.m;
+    h.index64 = g.fwd_index.data();
+    h.target = g.fwd_target.data();
+    h.weight = g.fwd_weight.data();
+    h.integer_exact = g.integer_exact;
+    h.validated = true;
+    return h;
+}
+
 // proj/include/ocm/graph.hpp:76 build_graph. Throws std::invalid_argument on
 // out-of-range endpoints or non-finite weights (same messages).
 Graph build_graph(Vertex n, std::uint64_t m, const Vertex* src, const Vertex* dst,

@@ -19,6 +19,10 @@
 #include <cooperative_groups.h>
 #include <cub/cub.cuh>
 
+#include <cstring>
+#include <mutex>
+#include <thread>
+
 #include <algorithm>
 #include <chrono>
 #include <cmath>
@@ -35,7 +39,7 @@
 
 namespace ocmb {
 
-void device_prepare(const Graph& g, const ocm_solve_options& opt, DeviceState& d, PrepInfo& info);
+void device_prepare(const HostCsr& g, const ocm_solve_options& opt, DeviceState& d, PrepInfo& info);
 void device_prepare_csr(std::uint32_t n, std::uint64_t m, DBuf<std::uint32_t>& row,
                         DBuf<std::uint32_t>& tgt, DBuf<double>& w, bool integer_exact,
                         const ocm_solve_options& opt, DeviceState& d, PrepInfo& info,
@@ -706,19 +710,143 @@ template <class T> void exclusive_scan(const T* in, T* out, std::size_t n, cudaS
 
 } // namespace
 
-void device_prepare(const Graph& g, const ocm_solve_options& opt, DeviceState& d, PrepInfo& info) {
+namespace {
+
+// Host->device copies from memory the library did not allocate. Page-locked
+// (or registered) sources go straight to the copy engine; pageable ones are
+// staged through a per-process ring of pinned buffers: the host copies chunk
+// i+1 into one slot (several threads) while the copy engine drains chunk i
+// from the other, so the transfer runs at PCIe speed instead of the driver's
+// pageable-copy path, and the caller's arrays are never registered or
+// modified. One ring per process, serialised by a lock.
+class StagingRing {
+  public:
+    static constexpr std::size_t kChunk = 16u << 20;
+    static constexpr int kSlots = 3;
+
+    static StagingRing& get() {
+        static StagingRing r;
+        return r;
+    }
+
+    void copy(void* dst, const void* src, std::size_t bytes, cudaStream_t s) {
+        if (bytes == 0)
+            return;
+        if (pinned(src)) {
+            CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
+            return;
+        }
+        std::lock_guard<std::mutex> lock(mu_);
+        ensure();
+        const char* from = static_cast<const char*>(src);
+        char* to = static_cast<char*>(dst);
+        for (std::size_t off = 0; off < bytes; off += kChunk) {
+            const std::size_t len = std::min(kChunk, bytes - off);
+            const int k = static_cast<int>(next_++ % kSlots);
+            CK(cudaEventSynchronize(done_[k])); // the slot's previous copy has left
+            host_copy(buf_[k], from + off, len);
+            CK(cudaMemcpyAsync(to + off, buf_[k], len, cudaMemcpyHostToDevice, s));
+            CK(cudaEventRecord(done_[k], s));
+        }
+    }
+
+  private:
+    static bool pinned(const void* p) {
+        cudaPointerAttributes a{};
+        if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+            cudaGetLastError();
+            return false;
+        }
+        return a.type == cudaMemoryTypeHost;
+    }
+    void ensure() {
+        if (buf_[0])
+            return;
+        for (int k = 0; k < kSlots; ++k) {
+            CK(cudaHostAlloc(reinterpret_cast<void**>(&buf_[k]), kChunk, cudaHostAllocPortable));
+            CK(cudaEventCreateWithFlags(&done_[k], cudaEventDisableTiming));
+            CK(cudaEventRecord(done_[k], nullptr));
+        }
+    }
+    // memcpy split over a few threads (one thread copies ~10 GB/s, below
+    // the PCIe rate)
+    static void host_copy(char* dst, const char* src, std::size_t len) {
+        constexpr int kThreads = 4;
+        if (len < (1u << 20)) {
+            std::memcpy(dst, src, len);
+            return;
+        }
+        std::thread th[kThreads - 1];
+        const std::size_t part = (len / kThreads + 63) & ~std::size_t(63);
+        for (int t = 1; t < kThreads; ++t) {
+            const std::size_t lo = std::min(len, part * t), hi = std::min(len, part * (t + 1));
+            th[t - 1] = std::thread([=] { std::memcpy(dst + lo, src + lo, hi - lo); });
+        }
+        std::memcpy(dst, src, std::min(len, part));
+        for (auto& x : th)
+            x.join();
+    }
+    std::mutex mu_;
+    char* buf_[kSlots] = {};
+    cudaEvent_t done_[kSlots] = {};
+    unsigned long long next_ = 0;
+};
+
+// Checks a caller-provided CSR on the device (the reference's build_graph
+// contract, src/graph.cpp:29-36, plus well-formed offsets): the least edge
+// id with an endpoint out of range or a non-finite weight, and whether all
+// weights are integers below 2^53 (Graph::integer_exact).
+struct CsrCheck {
+    unsigned long long bad_target;
+    unsigned long long bad_weight;
+    int non_integral;
+    int bad_offsets;
+};
+
+__global__ void kp_check_csr(std::uint32_t n, std::uint64_t m, const std::uint32_t* row,
+                             const std::uint32_t* tgt, const double* w, CsrCheck* out) {
+    const std::uint64_t tid = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x;
+    const std::uint64_t nth = std::uint64_t(gridDim.x) * blockDim.x;
+    bool bad_row = false, frac = false;
+    for (std::uint64_t v = tid; v < n; v += nth)
+        bad_row |= row[v] > row[v + 1];
+    if (tid == 0)
+        bad_row |= row[0] != 0 || row[n] != m;
+    for (std::uint64_t e = tid; e < m; e += nth) {
+        if (tgt[e] >= n)
+            atomicMin(&out->bad_target, static_cast<unsigned long long>(e));
+        const double x = w[e];
+        if (!isfinite(x))
+            atomicMin(&out->bad_weight, static_cast<unsigned long long>(e));
+        else
+            frac |= floor(x) != x || fabs(x) >= 9007199254740992.0;
+    }
+    if (__syncthreads_or(bad_row) && threadIdx.x == 0)
+        out->bad_offsets = 1;
+    if (__syncthreads_or(frac) && threadIdx.x == 0)
+        out->non_integral = 1;
+}
+
+} // namespace
+
+void device_prepare(const HostCsr& g, const ocm_solve_options& opt, DeviceState& d, PrepInfo& info) {
     cudaStream_t s = d.stream;
     const std::uint32_t n = g.n;
     const std::uint64_t m = g.m;
-    // ---- upload (the host arrays are pinned once per graph by the C-ABI)
-    DBuf<std::uint64_t> row64;
+    StagingRing& ring = StagingRing::get();
+    // ---- upload
     DBuf<std::uint32_t> row, tgt;
     DBuf<double> w;
-    row64.alloc(std::size_t(n) + 1, s);
     row.alloc(std::size_t(n) + 1, s);
     tgt.alloc(std::max<std::uint64_t>(m, 1), s);
     w.alloc(std::max<std::uint64_t>(m, 1), s);
-    CK(cudaMemcpyAsync(row64.p, g.fwd_index.data(), (std::size_t(n) + 1) * 8, cudaMemcpyHostToDevice, s));
+    DBuf<std::uint64_t> row64;
+    if (g.index64) {
+        row64.alloc(std::size_t(n) + 1, s);
+        ring.copy(row64.p, g.index64, (std::size_t(n) + 1) * 8, s);
+    } else {
+        ring.copy(row.p, g.index32, (std::size_t(n) + 1) * 4, s);
+    }
     // the weights (2/3 of the bytes) are first needed by the packing at the
     // end of the region split: they stream in on a side stream meanwhile
     cudaEvent_t w_ready = nullptr;
@@ -731,27 +859,56 @@ void device_prepare(const Graph& g, const ocm_solve_options& opt, DeviceState& d
                 cudaStreamSynchronize(d.side);
         }
     } side_guard{d};
+    bool exact = g.integer_exact;
     if (m) {
-        CK(cudaMemcpyAsync(tgt.p, g.fwd_target.data(), m * 4, cudaMemcpyHostToDevice, s));
+        ring.copy(tgt.p, g.target, m * 4, s);
         if (!d.side) {
             CK(cudaStreamCreateWithFlags(&d.side, cudaStreamNonBlocking));
             CK(cudaEventCreateWithFlags(&d.side_done, cudaEventDisableTiming));
         }
-        CK(cudaStreamWaitEvent(d.side, d.ev_alloc_done(s), 0)); // w allocated on s
-        CK(cudaMemcpyAsync(w.p, g.fwd_weight.data(), m * 8, cudaMemcpyHostToDevice, d.side));
-        CK(cudaEventRecord(d.side_done, d.side));
-        w_ready = d.side_done;
+        if (g.validated) {
+            CK(cudaStreamWaitEvent(d.side, d.ev_alloc_done(s), 0)); // w allocated on s
+            ring.copy(w.p, g.weight, m * 8, d.side);
+            CK(cudaEventRecord(d.side_done, d.side));
+            w_ready = d.side_done;
+        } else {
+            ring.copy(w.p, g.weight, m * 8, s); // checked below before anything else runs
+        }
     }
-    kp_row32<<<grid_for(n + 1, d.sms), kBlock, 0, s>>>(row64.p, row.p, std::size_t(n) + 1);
-    row64.release();
+    if (g.index64) {
+        kp_row32<<<grid_for(n + 1, d.sms), kBlock, 0, s>>>(row64.p, row.p, std::size_t(n) + 1);
+        row64.release();
+    }
+    if (!g.validated) {
+        DBuf<CsrCheck> chk;
+        chk.alloc(1, s);
+        CK(cudaMemsetAsync(chk.p, 0, sizeof(CsrCheck), s));
+        CK(cudaMemsetAsync(chk.p, 0xff, 2 * sizeof(unsigned long long), s));
+        kp_check_csr<<<grid_for(std::max<std::uint64_t>(m, n), d.sms, 16), kBlock, 0, s>>>(
+            n, m, row.p, tgt.p, w.p, chk.p);
+        CK(cudaGetLastError());
+        CsrCheck h{};
+        CK(cudaMemcpyAsync(&h, chk.p, sizeof h, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        if (h.bad_offsets)
+            throw std::invalid_argument("CSR offsets are not a non-decreasing sequence from 0 to m");
+        if (h.bad_target != ~0ull || h.bad_weight != ~0ull) {
+            if (h.bad_target <= h.bad_weight)
+                throw std::invalid_argument("edge " + std::to_string(h.bad_target) +
+                                            " endpoint out of range");
+            throw std::invalid_argument("edge " + std::to_string(h.bad_weight) +
+                                        " has non-finite weight");
+        }
+        exact = h.non_integral == 0;
+    }
     if (std::getenv("OCM_PREP_TIMING")) {
         const auto t0 = std::chrono::steady_clock::now();
         CK(cudaStreamSynchronize(s));
         std::fprintf(stderr, "{\"upload_wait_ms\": %.3f}\n",
                      std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
     }
-    device_prepare_csr(n, m, row, tgt, w, g.integer_exact, opt, d, info, w_ready);
-    info.h2d_bytes = (std::size_t(n) + 1) * 8 + m * 12;
+    device_prepare_csr(n, m, row, tgt, w, exact, opt, d, info, w_ready);
+    info.h2d_bytes = (std::size_t(n) + 1) * (g.index64 ? 8 : 4) + m * 12;
 }
 
 void device_prepare_csr(std::uint32_t n, std::uint64_t m, DBuf<std::uint32_t>& row,

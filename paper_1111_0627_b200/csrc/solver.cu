@@ -23,7 +23,7 @@
 
 namespace ocmb {
 
-void device_prepare(const Graph& g, const ocm_solve_options& opt, DeviceState& d, PrepInfo& info);
+void device_prepare(const HostCsr& g, const ocm_solve_options& opt, DeviceState& d, PrepInfo& info);
 void device_generate_prepare(const GenSpec& spec, const ocm_solve_options& opt, DeviceState& d,
                              PrepInfo& info);
 
@@ -105,6 +105,10 @@ cudaMemPool_t session_pool() {
 
 
 Session::Session(const Graph& g, const ocm_solve_options& opt, std::uint32_t rank, std::uint32_t world)
+    : Session(csr_view(g), opt, rank, world) {}
+
+Session::Session(const HostCsr& g, const ocm_solve_options& opt, std::uint32_t rank,
+                 std::uint32_t world)
     : opt_(opt), rank_(rank), world_(world) {
     init([&](DeviceState& d) { device_prepare(g, opt, d, prep_); });
 }

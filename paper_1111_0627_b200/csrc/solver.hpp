@@ -23,6 +23,9 @@ class Session {
     // improves the policy of vertices [rank*chunk, (rank+1)*chunk) only.
     Session(const Graph& g, const ocm_solve_options& opt, std::uint32_t rank = 0,
             std::uint32_t world = 1);
+    // a host CSR in the caller's memory (e.g. the reference's ocm::Graph)
+    Session(const HostCsr& g, const ocm_solve_options& opt, std::uint32_t rank = 0,
+            std::uint32_t world = 1);
     // graph generated directly in HBM (gen_dev.cu)
     Session(const GenSpec& spec, const ocm_solve_options& opt, std::uint32_t rank = 0,
             std::uint32_t world = 1);
