@@ -113,6 +113,8 @@ int ocm_generate_uniform(uint32_t n, uint32_t deg, int32_t wlo, int32_t whi, uin
 #define OCM_GEN_POWERLAW 1 /* deg(v) = min(dmax, floor(deg / sqrt(u_v))), tail exponent 3 */
 #define OCM_GEN_POWERLAW_HUBS 2 /* out-degrees as OCM_GEN_POWERLAW; targets floor(n*u^2) scattered
                                    by a bijection: in-degree tail exponent 3 too (hub vertices) */
+#define OCM_GEN_POWERLAW_WEB 3  /* as OCM_GEN_POWERLAW_HUBS with targets floor(n*u^8): in-degree
+                                   density exponent ~2.14 (web graphs) */
 typedef struct {
     int32_t kind;    /* OCM_GEN_* */
     uint32_t n;

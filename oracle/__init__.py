@@ -300,8 +300,9 @@ def ref_parse_graph_text(text: str, source: str = "<text>"):
 
 
 def generate_powerlaw(n, dmin, dmax, wlo, whi, seed, hubs=False):
-    """Power-law out-degree generator ("powerlaw" / "powerlaw-hubs"), shared
-    bit-for-bit with the CUDA library's host and device generators."""
+    """Power-law out-degree generator ("powerlaw" / "powerlaw-hubs" with
+    hubs=True or 1 / "powerlaw-web" with hubs=3), shared bit-for-bit with the
+    CUDA library's host and device generators."""
     lib = oracle_lib()
     fn = lib.oc_generate_powerlaw
     fn.restype = C.c_uint64

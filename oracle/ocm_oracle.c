@@ -677,8 +677,9 @@ void oc_generate_uniform(uint32_t n, uint32_t deg, int32_t wlo, int32_t whi, uin
 
 /* Power-law out-degree generator (paper_1111_0627_b200/csrc/gen.hpp
  * generate_powerlaw / generate_powerlaw_hubs, restated): deg(v) =
- * min(dmax, floor(dmin / sqrt(u_v))); hubs != 0 draws targets as
- * floor(n * u^2) scattered by x -> (x * A + B) mod n. Two calls: with
+ * min(dmax, floor(dmin / sqrt(u_v))); hubs = q > 0 draws targets as
+ * floor(n * u^(2^q)) scattered by x -> (x * A + B) mod n (q = 1 "powerlaw-hubs",
+ * q = 3 "powerlaw-web"). Two calls: with
  * src == NULL only the edge count is returned. */
 uint64_t oc_generate_powerlaw(uint32_t n, uint32_t dmin, uint32_t dmax, int32_t wlo, int32_t whi,
                               uint64_t seed, int hubs, uint32_t *src, uint32_t *dst, double *w) {
@@ -697,7 +698,9 @@ uint64_t oc_generate_powerlaw(uint32_t n, uint32_t dmin, uint32_t dmax, int32_t 
                 uint32_t t;
                 if (hubs) {
                     double uu = (double)((h >> 11) + 1) * (1.0 / 9007199254740992.0);
-                    double x = (double)n * (uu * uu);
+                    for (int q = 0; q < hubs; ++q) /* 1: u^2 (hubs), 3: u^8 (web) */
+                        uu = uu * uu;
+                    double x = (double)n * uu;
                     uint64_t r = (uint64_t)x;
                     if (r >= n)
                         r = n - 1;

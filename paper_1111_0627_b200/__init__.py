@@ -34,7 +34,7 @@ __all__ = [
     "Graph", "build_graph", "parse_graph_text", "read_graph_file", "generate_uniform",
     "Scenario", "Transition", "loop_scenario", "worker_scenario", "server_scenario",
     "generate_model", "K_MAX_MODEL_STATES", "Generator", "generate",
-    "SolveOptions", "SolveStats", "Solution", "solve", "Session",
+    "SolveOptions", "SolveStats", "Solution", "solve", "solve_csr", "Session",
     "ParseError", "StructuralError", "DeviceError", "UnsupportedError", "LIB_PATH",
 ]
 
@@ -152,6 +152,8 @@ def _load():
         "ocm_graph_integer_exact": (C.c_int, [C.c_void_p]),
         "ocm_graph_edges": (C.c_int, [C.c_void_p, P(C.c_uint32), P(C.c_uint32), P(C.c_double)]),
         "ocm_solve": (C.c_int, [C.c_void_p, P(_Opts), P(_Sol), P(C.c_uint32), C.c_uint32]),
+        "ocm_solve_csr": (C.c_int, [C.c_uint32, C.c_uint32, P(C.c_uint32), P(C.c_uint32),
+                                    P(C.c_double), P(_Opts), P(_Sol), P(C.c_uint32), C.c_uint32]),
         "ocm_session_create": (C.c_int, [C.c_void_p, P(_Opts), P(C.c_void_p)]),
         "ocm_session_solve": (C.c_int, [C.c_void_p, P(_Sol), P(C.c_uint32), C.c_uint32]),
         "ocm_session_values": (C.c_int, [C.c_void_p, P(C.c_int64), P(C.c_int64), P(C.c_int64),
@@ -178,7 +180,7 @@ EXPORTED_SYMBOLS = (
     "ocm_session_shard_finish", "ocm_session_shard_peer_info", "ocm_session_shard_connect",
     "ocm_session_shard_fused_launch", "ocm_session_shard_fused_finish",
     "ocm_graph_free", "ocm_graph_n", "ocm_graph_m", "ocm_graph_integer_exact", "ocm_graph_edges",
-    "ocm_solve", "ocm_session_create", "ocm_session_solve", "ocm_session_values",
+    "ocm_solve", "ocm_solve_csr", "ocm_session_create", "ocm_session_solve", "ocm_session_values",
     "ocm_session_stream", "ocm_session_free", "ocm_session_certify",
 )
 
@@ -314,7 +316,9 @@ class Generator:
     "uniform" (out-degree exactly ``deg``), "powerlaw" (out-degree
     min(dmax, floor(deg / sqrt(u))), tail exponent 3, uniform targets) or
     "powerlaw-hubs" (the same out-degrees, targets floor(n*u^2) scattered by
-    a bijection: in-degrees with tail exponent 3, i.e. hub vertices); integer weights
+    a bijection: in-degrees with tail exponent 3, i.e. hub vertices) or
+    "powerlaw-web" (targets floor(n*u^8): in-degree density exponent ~2.14,
+    the web graphs' law); integer weights
     uniform in [wlo, whi]. :func:`generate` builds it on the host,
     :meth:`Session.generated` directly in HBM -- bit-identical graphs."""
     kind: str = "uniform"
@@ -326,7 +330,7 @@ class Generator:
     seed: int = 1
 
     def _c(self) -> "_Gen":
-        kinds = {"uniform": 0, "powerlaw": 1, "powerlaw-hubs": 2}
+        kinds = {"uniform": 0, "powerlaw": 1, "powerlaw-hubs": 2, "powerlaw-web": 3}
         if self.kind not in kinds:
             raise ValueError(f"unknown generator kind {self.kind!r}")
         return _Gen(kinds[self.kind], int(self.n), int(self.deg), int(self.dmax), int(self.wlo),
@@ -465,6 +469,28 @@ def solve(g: Graph, opt: Optional[SolveOptions] = None) -> Solution:
     cyc = np.empty(max(g.n, 1), np.uint32)  # only the first cycle_len entries are read
     _check(_lib.ocm_solve(g._h, C.byref(opt._c()), C.byref(sol), _p(cyc, C.c_uint32),
                           cyc.shape[0]))
+    return _solution(sol, cyc)
+
+
+def solve_csr(n: int, fwd_index, fwd_target, fwd_weight,
+              opt: Optional[SolveOptions] = None) -> Solution:
+    """ocm::solve on the reference's own CSR arrays (ocm::Graph fwd_index /
+    fwd_target / fwd_weight, graph.hpp:38-41) through ``ocm_solve_csr``: read
+    in place (pageable memory is staged through the library's pinned ring),
+    checked on the device like build_graph (ValueError), exactness derived
+    on the device."""
+    opt = opt or SolveOptions()
+    idx = np.ascontiguousarray(fwd_index, np.uint32)
+    tgt = np.ascontiguousarray(fwd_target, np.uint32)
+    w = np.ascontiguousarray(fwd_weight, np.float64)
+    n = int(n)
+    if idx.shape[0] != n + 1 or tgt.shape[0] != w.shape[0] or tgt.shape[0] >= 2**32:
+        raise ValueError("CSR arrays: fwd_index needs n+1 entries, fwd_target and fwd_weight m each")
+    sol = _Sol()
+    cyc = np.empty(max(n, 1), np.uint32)
+    _check(_lib.ocm_solve_csr(n, tgt.shape[0], _p(idx, C.c_uint32), _p(tgt, C.c_uint32),
+                              _p(w, C.c_double), C.byref(opt._c()), C.byref(sol),
+                              _p(cyc, C.c_uint32), cyc.shape[0]))
     return _solution(sol, cyc)
 
 

@@ -140,6 +140,13 @@ struct KP {
     const std::uint32_t* heavy; // vertices of intra-region degree >= heavy_deg
     std::uint32_t nheavy;
     std::uint32_t heavy_deg;
+    // hub vertices (highest intra-region in-degree) whose keys every CTA
+    // stages in a shared-memory hash table at the start of each improvement
+    // pass (exact lane); 0 = off
+    const std::uint32_t* hot;
+    std::uint32_t nhot;
+    std::uint32_t hot_shift; // table slots = 2^(32 - hot_shift)
+    int staged;              // TMA-staged improvement pass (exact lane, HBM-resident keys)
     std::uint32_t own_lo, own_hi; // improvement range (all vertices unless sharded)
     // fused sharded lane (kShardFused): the rank's peers' policy replicas and
     // flags (peer memory: NVLink-mapped IPC pointers between GPUs, plain
@@ -235,7 +242,7 @@ struct DeviceState {
     int sms = 148;
     cudaStream_t stream = nullptr;
     DBuf<std::uint32_t> row, reg, succ_e, succ_v, comp, wlist, cyc_len, conn, rem0, rem1, src,
-        iters, indeg, plist, clist, cmark, cmark2, heavy, xbar;
+        iters, indeg, plist, clist, cmark, cmark2, heavy, xbar, hot;
     DBuf<PJV> pv0, pv1;
     DBuf<PJC> pj0, pj1;
     DBuf<int2> ew;
@@ -267,7 +274,7 @@ struct DeviceState {
         if (stream)
             cudaStreamSynchronize(stream);
         for (auto* b : {&row, &reg, &succ_e, &succ_v, &comp, &wlist, &cyc_len, &conn, &rem0, &rem1,
-                        &src, &iters, &indeg, &plist, &clist, &cmark, &cmark2, &heavy, &xbar})
+                        &src, &iters, &indeg, &plist, &clist, &cmark, &cmark2, &heavy, &xbar, &hot})
             b->release();
         pv0.release();
         pv1.release();

@@ -44,7 +44,7 @@ Graph generate_uniform(std::uint32_t n, std::uint32_t deg, std::int32_t wlo, std
 namespace {
 
 Graph powerlaw_graph(std::uint32_t n, std::uint32_t dmin, std::uint32_t dmax, std::int32_t wlo,
-                     std::int32_t whi, std::uint64_t seed, bool hubs) {
+                     std::int32_t whi, std::uint64_t seed, int hubs) {
     if (n == 0 || dmin == 0 || dmax < dmin || whi < wlo)
         throw std::invalid_argument("generate_powerlaw: need n > 0, 0 < dmin <= dmax, wlo <= whi");
     Graph g;
@@ -68,7 +68,7 @@ Graph powerlaw_graph(std::uint32_t n, std::uint32_t dmin, std::uint32_t dmax, st
         pool.emplace_back([&, t] {
             const std::uint64_t lo = m * t / T, hi = m * (t + 1) / T;
             for (std::uint64_t e = lo; e < hi; ++e) {
-                g.fwd_target[e] = hubs ? hub_target(hash2(seed, 1, e), n, mul, add)
+                g.fwd_target[e] = hubs ? hub_target(hash2(seed, 1, e), n, mul, add, hubs)
                                        : static_cast<Vertex>(hash2(seed, 1, e) % n);
                 g.fwd_weight[e] = double(wlo + std::int64_t(hash2(seed, 2, e) % span));
             }
@@ -82,12 +82,17 @@ Graph powerlaw_graph(std::uint32_t n, std::uint32_t dmin, std::uint32_t dmax, st
 
 Graph generate_powerlaw(std::uint32_t n, std::uint32_t dmin, std::uint32_t dmax, std::int32_t wlo,
                         std::int32_t whi, std::uint64_t seed) {
-    return powerlaw_graph(n, dmin, dmax, wlo, whi, seed, false);
+    return powerlaw_graph(n, dmin, dmax, wlo, whi, seed, 0);
 }
 
 Graph generate_powerlaw_hubs(std::uint32_t n, std::uint32_t dmin, std::uint32_t dmax,
                              std::int32_t wlo, std::int32_t whi, std::uint64_t seed) {
-    return powerlaw_graph(n, dmin, dmax, wlo, whi, seed, true);
+    return powerlaw_graph(n, dmin, dmax, wlo, whi, seed, 1);
+}
+
+Graph generate_powerlaw_web(std::uint32_t n, std::uint32_t dmin, std::uint32_t dmax,
+                            std::int32_t wlo, std::int32_t whi, std::uint64_t seed) {
+    return powerlaw_graph(n, dmin, dmax, wlo, whi, seed, 3);
 }
 
 Graph generate(const GenSpec& s) {
@@ -97,6 +102,8 @@ Graph generate(const GenSpec& s) {
         return generate_powerlaw(s.n, s.deg, s.dmax, s.wlo, s.whi, s.seed);
     if (s.kind == 2)
         return generate_powerlaw_hubs(s.n, s.deg, s.dmax, s.wlo, s.whi, s.seed);
+    if (s.kind == 3)
+        return generate_powerlaw_web(s.n, s.deg, s.dmax, s.wlo, s.whi, s.seed);
     throw std::invalid_argument("unknown generator kind");
 }
 

@@ -32,11 +32,16 @@ Graph generate_powerlaw(std::uint32_t n, std::uint32_t dmin, std::uint32_t dmax,
 // rounded double multiplies only, so host and device agree bit for bit.
 Graph generate_powerlaw_hubs(std::uint32_t n, std::uint32_t dmin, std::uint32_t dmax,
                              std::int32_t wlo, std::int32_t whi, std::uint64_t seed);
+// The same with targets floor(n * u^8): in-degree tail P(in > d) ~ d^(-8/7),
+// density exponent ~2.14 -- the web graphs' in-degree law; a few hundred
+// hubs receive a quarter of the edges ("powerlaw-web").
+Graph generate_powerlaw_web(std::uint32_t n, std::uint32_t dmin, std::uint32_t dmax,
+                            std::int32_t wlo, std::int32_t whi, std::uint64_t seed);
 
 // Generator description shared by the host generators and the device ones
 // (gen_dev.cu) that write the CSR straight into HBM.
 struct GenSpec {
-    int kind = 0; // 0 uniform, 1 power-law out-degree, 2 power-law in- and out-degree
+    int kind = 0; // 0 uniform, 1 power-law out-degree, 2 + hub in-degrees (u^2), 3 web-like (u^8)
     std::uint32_t n = 0;
     std::uint32_t deg = 8; // uniform: out-degree; power-law: dmin
     std::uint32_t dmax = 0; // power-law cap
@@ -70,9 +75,12 @@ constexpr std::uint64_t kHubMul = 2654435761ull; // prime, so coprime to every n
 inline std::uint64_t hub_mul(std::uint32_t n) { return n % kHubMul == 0 ? 1 : kHubMul % n; }
 inline std::uint64_t hub_add(std::uint64_t seed, std::uint32_t n) { return hash2(seed, 4, 0) % n; }
 inline std::uint32_t hub_target(std::uint64_t h, std::uint32_t n, std::uint64_t mul,
-                                std::uint64_t add) {
+                                std::uint64_t add, int squarings = 1) {
     const double u = double((h >> 11) + 1) * (1.0 / 9007199254740992.0);
-    double x = double(n) * (u * u);
+    double f = u;
+    for (int i = 0; i < squarings; ++i)
+        f = f * f;
+    double x = double(n) * f;
     std::uint64_t r = static_cast<std::uint64_t>(x);
     if (r >= n)
         r = n - 1;

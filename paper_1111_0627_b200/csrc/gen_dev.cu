@@ -54,9 +54,13 @@ __global__ void kg_powerlaw_deg(std::uint32_t n, std::uint64_t k3, std::uint32_t
 
 // hub_target (gen.hpp) with explicitly rounded multiplies
 __device__ __forceinline__ std::uint32_t d_hub_target(std::uint64_t h, std::uint32_t n,
-                                                      std::uint64_t mul, std::uint64_t add) {
+                                                      std::uint64_t mul, std::uint64_t add,
+                                                      int squarings) {
     const double u = __dmul_rn(double((h >> 11) + 1), 1.0 / 9007199254740992.0);
-    const double x = __dmul_rn(double(n), __dmul_rn(u, u));
+    double f = u;
+    for (int i = 0; i < squarings; ++i)
+        f = __dmul_rn(f, f);
+    const double x = __dmul_rn(double(n), f);
     std::uint64_t r = static_cast<std::uint64_t>(x);
     if (r >= n)
         r = n - 1;
@@ -65,10 +69,10 @@ __device__ __forceinline__ std::uint32_t d_hub_target(std::uint64_t h, std::uint
 
 __global__ void kg_edges(std::uint64_t m, std::uint32_t n, std::uint64_t k1, std::uint64_t k2,
                          std::int32_t wlo, std::uint64_t span, std::uint32_t* tgt, double* w,
-                         std::uint64_t hub_mul, std::uint64_t hub_add) {
+                         std::uint64_t hub_mul, std::uint64_t hub_add, int squarings) {
     for (std::uint64_t e = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x; e < m;
          e += std::uint64_t(gridDim.x) * blockDim.x) {
-        tgt[e] = hub_mul ? d_hub_target(d_hash(k1, e), n, hub_mul, hub_add)
+        tgt[e] = squarings ? d_hub_target(d_hash(k1, e), n, hub_mul, hub_add, squarings)
                          : static_cast<std::uint32_t>(d_hash(k1, e) % n);
         w[e] = double(wlo + static_cast<std::int64_t>(d_hash(k2, e) % span));
     }
@@ -97,7 +101,7 @@ void device_generate_prepare(const GenSpec& spec, const ocm_solve_options& opt, 
         if (m >= 0xffffffffull)
             throw std::invalid_argument("generate_uniform: edge count exceeds the 32-bit id space");
         kg_uniform_row<<<g, kBlock, 0, s>>>(n, spec.deg, row.p);
-    } else if (spec.kind == 1 || spec.kind == 2) {
+    } else if (spec.kind >= 1 && spec.kind <= 3) {
         DBuf<std::uint32_t> deg;
         deg.alloc(std::size_t(n) + 1, s);
         kg_powerlaw_deg<<<g, kBlock, 0, s>>>(n, stream_key(spec.seed, 3), spec.deg, spec.dmax, deg.p);
@@ -129,8 +133,8 @@ void device_generate_prepare(const GenSpec& spec, const ocm_solve_options& opt, 
     kg_edges<<<grid_for(m, d.sms, 32), kBlock, 0, s>>>(m, n, stream_key(spec.seed, 1),
                                                          stream_key(spec.seed, 2), spec.wlo, span,
                                                          tgt.p, w.p,
-                                                         spec.kind == 2 ? hub_mul(n) : 0,
-                                                         spec.kind == 2 ? hub_add(spec.seed, n) : 0);
+                                                         hub_mul(n), hub_add(spec.seed, n),
+                                                         spec.kind == 2 ? 1 : spec.kind == 3 ? 3 : 0);
     CK(cudaGetLastError());
     device_prepare_csr(n, m, row, tgt, w, true, opt, d, info);
 }

@@ -956,7 +956,10 @@ void device_prepare_csr(std::uint32_t n, std::uint64_t m, DBuf<std::uint32_t>& r
     };
 
     d.reg.alloc(std::max<std::uint32_t>(n, 1), s);
-    d.row.alloc(std::size_t(n) + 1 + (info.scc_off ? 0 : 0), s);
+    // +7: the staged improvement pass copies 16-byte aligned windows of the
+    // offsets and edge records (zeroed padding, never used as data)
+    d.row.alloc(std::size_t(n) + 8, s);
+    CK(cudaMemsetAsync(d.row.p + n + 1, 0, 7 * 4, s));
 
     if (info.scc_off) {
         // ---- single region: the Hamiltonian-augmented graph (solve.cpp:53)
@@ -972,10 +975,12 @@ void device_prepare_csr(std::uint32_t n, std::uint64_t m, DBuf<std::uint32_t>& r
         info.M = m + n;
         if (info.M >= 0xffffffffull)
             throw UnsupportedError("more than 2^32-1 edges after augmentation");
-        if (info.exact)
-            d.ew.alloc(info.M, s);
-        else
+        if (info.exact) {
+            d.ew.alloc(info.M + 2, s);
+            CK(cudaMemsetAsync(d.ew.p + info.M, 0, 2 * sizeof(int2), s));
+        } else {
             d.fe.alloc(info.M, s);
+        }
         if (info.exact)
             kp_pack_hamiltonian<true><<<grid_for(n + 1, sms), kBlock, 0, s>>>(
                 n, row.p, tgt.p, w.p, sign, big_w, d.ew.p, nullptr, d.row.p, d.reg.p, pcd.p);
@@ -1154,10 +1159,12 @@ void device_prepare_csr(std::uint32_t n, std::uint64_t m, DBuf<std::uint32_t>& r
     CK(cudaMemcpyAsync(&M, d.row.p + n, 4, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     info.M = M;
-    if (info.exact)
-        d.ew.alloc(std::max<std::uint32_t>(M, 1), s);
-    else
+    if (info.exact) {
+        d.ew.alloc(std::size_t(M) + 2, s);
+        CK(cudaMemsetAsync(d.ew.p + M, 0, 2 * sizeof(int2), s));
+    } else {
         d.fe.alloc(std::max<std::uint32_t>(M, 1), s);
+    }
     need_weights();
     CK(cudaMemsetAsync(&pcd.p->bad_weight, 0, 4, s));
     if (info.exact)

@@ -54,6 +54,12 @@ namespace cg = cooperative_groups;
 #define OCM_MINB 4
 #endif
 constexpr int kSolveMinBlocks = OCM_MINB; // 4: register cap 64 at 256 threads
+#ifndef OCM_KSHRINK
+#define OCM_KSHRINK 2
+#endif
+// consecutive first-try verifications before the doubling depth is tried one
+// step shallower
+constexpr unsigned kKShrink = OCM_KSHRINK;
 
 // ------------------------------------------------------------ improvement
 //
@@ -148,9 +154,49 @@ __device__ __forceinline__ void push_policy(const KP& p, std::uint32_t v, std::u
     }
 }
 
-template <bool EXACT, int G, int U>
+// Hub keys staged in shared memory (north_star item 5): every CTA copies the
+// keys of the graph's highest in-degree vertices into an open-addressed
+// table {vertex, key} at the start of the pass (the keys do not change
+// during it); an edge into a hub reads its key there instead of gathering
+// it from L2/HBM, where every SM would hit the same few sectors.
+constexpr int kHotProbe = 4;
+// table layout in dynamic shared memory: slots x i64 key, then slots x u32
+// vertex (NONE = empty); slots = 2^(32 - p.hot_shift). Addressed from the
+// kernel parameters so the pass keeps no extra live registers.
+extern __shared__ __align__(16) unsigned char dyn_smem[];
+__device__ __forceinline__ unsigned hot_hash(std::uint32_t t, unsigned shift) {
+    return (t * 2654435761u) >> shift;
+}
+__device__ __forceinline__ long long* hot_keys() { return reinterpret_cast<long long*>(dyn_smem); }
+__device__ __forceinline__ std::uint32_t* hot_verts(const KP& p) {
+    return reinterpret_cast<std::uint32_t*>(dyn_smem + (std::size_t(8) << (32 - p.hot_shift)));
+}
+__device__ __forceinline__ bool hot_find(const KP& p, std::uint32_t t, long long& key) {
+    const unsigned mask = (1u << (32 - p.hot_shift)) - 1u;
+    const std::uint32_t* hv = hot_verts(p);
+    unsigned i = hot_hash(t, p.hot_shift);
+#pragma unroll
+    for (int j = 0; j < kHotProbe; ++j) {
+        const std::uint32_t x = hv[i];
+        if (x == t) {
+            key = hot_keys()[i];
+            return true;
+        }
+        if (x == NONE)
+            return false;
+        i = (i + 1) & mask;
+    }
+    return false;
+}
+
+// STAGED: the vertex's row offsets and edges were copied into shared memory
+// by the bulk-TMA producer of improve_staged (exact lane); sedge[i] holds
+// edge ebase + i, and b / e_end are the vertex's offsets read from there.
+template <bool EXACT, int G, int U, bool HOT, bool STAGED = false>
 __device__ __forceinline__ void improve_vertex(const KP& p, int* changed, ChangedMarks& marks,
-                                               std::uint32_t v) {
+                                               std::uint32_t v, const int2* sedge = nullptr,
+                                               std::uint32_t ebase = 0, std::uint32_t sb = 0,
+                                               std::uint32_t se = 0) {
     // Register budget matters here (64 at 4 CTAs/SM): edges stay packed as
     // they were loaded, the winner's head and weight are re-read (an L1 hit)
     // only when the policy changes, and the exact candidate drops the
@@ -168,9 +214,22 @@ __device__ __forceinline__ void improve_vertex(const KP& p, int* changed, Change
     const std::uint32_t r = p.R == 1 ? 0u : __ldg(&p.reg[v]);
     if (p.R != 1 && !p.active[r])
         return;
-    const std::uint32_t b = __ldg(&p.row[v]), e_end = __ldg(&p.row[v + 1]);
+    std::uint32_t b, e_end;
+    if constexpr (STAGED) {
+        b = sb;
+        e_end = se;
+    } else {
+        b = __ldg(&p.row[v]);
+        e_end = __ldg(&p.row[v + 1]);
+    }
     if (e_end == b || e_end - b >= p.heavy_deg)
         return; // trivial, or the block-cooperative path (improve_heavy)
+    auto edge_at = [&](std::uint32_t e) -> Edge {
+        if constexpr (STAGED)
+            return reinterpret_cast<const Edge*>(sedge)[e - ebase];
+        else
+            return ld_edge(&edges[e]);
+    };
     const std::uint32_t cur = p.succ_e[v];
     long long den = 1;
     double lam = 0.0;
@@ -189,7 +248,7 @@ __device__ __forceinline__ void improve_vertex(const KP& p, int* changed, Change
         // ed[]/kk[] to local memory
 #pragma unroll
         for (int u = 0; u < U; ++u)
-            ed[u] = ld_edge(&edges[min(e0 + u * G, e_end - 1)]);
+            ed[u] = edge_at(min(e0 + u * G, e_end - 1));
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             std::uint32_t t;
@@ -197,7 +256,15 @@ __device__ __forceinline__ void improve_vertex(const KP& p, int* changed, Change
                 t = static_cast<std::uint32_t>(ed[u].x);
             else
                 t = ed[u].t;
-            kk[u] = __ldcg(&key[t]);
+            if constexpr (EXACT && HOT) {
+                long long hk;
+                if (hot_find(p, t, hk))
+                    kk[u] = hk;
+                else
+                    kk[u] = __ldcg(&key[t]);
+            } else {
+                kk[u] = __ldcg(&key[t]);
+            }
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -253,7 +320,7 @@ __device__ __forceinline__ void improve_vertex(const KP& p, int* changed, Change
     }
     if (rep) {
         if (gbe == be) { // owner lane of the winning edge
-            const Edge ed = ld_edge(&edges[be]);
+            const Edge ed = edge_at(be);
             p.succ_e[v] = be;
             std::uint32_t t;
             if constexpr (EXACT) {
@@ -273,9 +340,9 @@ __device__ __forceinline__ void improve_vertex(const KP& p, int* changed, Change
     } else if (saw_cur && p.indeg_in_improve) {
         std::uint32_t t;
         if constexpr (EXACT)
-            t = static_cast<std::uint32_t>(ld_edge(&edges[cur]).x);
+            t = static_cast<std::uint32_t>(edge_at(cur).x);
         else
-            t = ld_edge(&edges[cur]).t;
+            t = edge_at(cur).t;
         atomicAdd(&p.indeg[t], 1u);
     }
 }
@@ -469,7 +536,7 @@ constexpr std::size_t kPbSmem = kPbVB * 8 + (3 * kPbVB + 2 + 2 * kMaxPbBins) * 4
 __device__ __forceinline__ void pb_pass2(const KP& p, int* changed) {
     // dynamic shared memory (kPbSmem bytes, given only to launches with the
     // pass enabled: a static allocation would shrink every launch's L1)
-    extern __shared__ __align__(16) unsigned char pb_smem[];
+    unsigned char* pb_smem = dyn_smem;
     long long* s_best = reinterpret_cast<long long*>(pb_smem);                  // [kPbVB]
     std::uint32_t* s_row = reinterpret_cast<std::uint32_t*>(s_best + kPbVB);   // [kPbVB + 1]
     std::uint32_t* s_be = s_row + kPbVB + 1;                                    // [kPbVB]
@@ -565,6 +632,117 @@ __device__ __forceinline__ void pb_pass2(const KP& p, int* changed) {
     marks.flush(p, changed);
 }
 
+// ------------------------------------------- TMA-staged improvement pass
+//
+// For key arrays far beyond L2 (exact lane): the pass is bound by random
+// key gathers from HBM, and loading the edge stream through registers
+// limits how many of them a thread keeps in flight. Here one thread per CTA
+// copies each chunk of kBlock/G consecutive vertices -- their row offsets
+// and their edge records, contiguous in the CSR -- into shared memory with
+// 1-D bulk TMA (cp.async.bulk, completion on an mbarrier), double-buffered
+// so chunk i+1 lands while chunk i is processed; the threads then read
+// edges from shared memory and spend their registers on key gathers. A
+// chunk whose edges exceed a stage (it holds a heavy vertex, whose edges the
+// block-cooperative pass handles) is processed straight from global memory.
+constexpr int kStE = 2048 + 16; // edge records per stage
+constexpr int kStV = kBlock + 8; // row offsets per stage
+struct Staged {
+    int2 edge[2][kStE];
+    std::uint32_t row[2][kStV];
+    unsigned long long bar[2];
+    std::uint32_t ebase[2], rbase[2], v0[2], v1[2];
+    int ok[2];
+    unsigned par[2]; // mbarrier phase parity, kept across the launch's passes
+};
+constexpr std::size_t kStagedSmem = sizeof(Staged);
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void staged_init(Staged& st) {
+    if (threadIdx.x == 0) {
+        for (int k = 0; k < 2; ++k) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&st.bar[k])));
+            st.par[k] = 0;
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+}
+
+// thread 0: issue the copies of chunk [v0, v1) into stage k
+__device__ __forceinline__ void staged_produce(const KP& p, Staged& st, int k, std::uint32_t v0,
+                                               std::uint32_t v1) {
+    const std::uint32_t e0 = __ldg(&p.row[v0]), e1 = __ldg(&p.row[v1]);
+    st.v0[k] = v0;
+    st.v1[k] = v1;
+    const std::uint32_t ea = e0 & ~1u, eb = (e1 + 1) & ~1u; // 16-byte aligned window
+    if (eb - ea > static_cast<std::uint32_t>(kStE)) {
+        st.ok[k] = 0;
+        return;
+    }
+    st.ok[k] = 1;
+    const std::uint32_t rb = v0 & ~3u, rc = (v1 + 1 - rb + 3) & ~3u;
+    st.ebase[k] = ea;
+    st.rbase[k] = rb;
+    const unsigned rbytes = rc * 4, ebytes = (eb - ea) * 8;
+    const unsigned bar = smem_u32(&st.bar[k]);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                 "r"(rbytes + ebytes)
+                 : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_u32(st.row[k])), "l"(p.row + rb), "r"(rbytes), "r"(bar)
+                 : "memory");
+    if (ebytes)
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                     ::"r"(smem_u32(st.edge[k])), "l"(p.ew + ea), "r"(ebytes), "r"(bar)
+                     : "memory");
+}
+
+__device__ __forceinline__ void staged_wait(Staged& st, int k, unsigned parity) {
+    asm volatile("{\n .reg .pred p;\n WAIT_%=:\n"
+                 " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+                 " @!p bra WAIT_%=;\n}" ::"r"(smem_u32(&st.bar[k])), "r"(parity)
+                 : "memory");
+}
+
+template <int G, int U>
+__device__ __forceinline__ void improve_staged(const KP& p, int* changed, ChangedMarks& marks) {
+    Staged& st = *reinterpret_cast<Staged*>(dyn_smem);
+    constexpr std::uint32_t VC = kBlock / G; // vertices per chunk
+    const std::uint32_t lo = p.own_lo, hi = p.own_hi;
+    const std::uint32_t nch = (hi - lo + VC - 1) / VC;
+    unsigned par[2] = {st.par[0], st.par[1]};
+    std::uint32_t c = blockIdx.x;
+    int k = 0;
+    if (threadIdx.x == 0 && c < nch)
+        staged_produce(p, st, 0, lo + c * VC, min(hi, lo + (c + 1) * VC));
+    for (; c < nch; c += gridDim.x, k ^= 1) {
+        const std::uint32_t cn = c + gridDim.x;
+        if (threadIdx.x == 0 && cn < nch)
+            staged_produce(p, st, k ^ 1, lo + cn * VC, min(hi, lo + (cn + 1) * VC));
+        __syncthreads(); // stage k's bookkeeping is visible
+        const std::uint32_t v = st.v0[k] + threadIdx.x / G;
+        if (st.ok[k]) {
+            staged_wait(st, k, par[k]);
+            par[k] ^= 1;
+            if (v < st.v1[k]) {
+                const std::uint32_t r0 = v - st.rbase[k];
+                improve_vertex<true, G, U, false, true>(p, changed, marks, v, st.edge[k], st.ebase[k],
+                                                        st.row[k][r0], st.row[k][r0 + 1]);
+            }
+        } else if (v < st.v1[k]) {
+            improve_vertex<true, G, U, false>(p, changed, marks, v);
+        }
+        __syncthreads(); // stage k is consumed before it is refilled
+    }
+    if (threadIdx.x == 0) {
+        st.par[0] = par[0];
+        st.par[1] = par[1];
+    }
+}
+
 template <bool EXACT, int G, int U> __device__ __forceinline__ void improve_phase(const KP& p, int* changed) {
     if (p.nheavy)
         improve_heavy<EXACT>(p, changed);
@@ -581,9 +759,46 @@ template <bool EXACT, int G, int U> __device__ __forceinline__ void improve_phas
     ChangedMarks marks;
     if (p.R == 1 && !p.active[0])
         return; // the single region finished (block-uniform: no flush needed)
+    if constexpr (EXACT) {
+        if (p.staged) {
+            improve_staged<G, U>(p, changed, marks);
+            marks.flush(p, changed);
+            return;
+        }
+    }
+    bool hot = false;
+    if constexpr (EXACT) {
+        if (p.nhot) {
+            const unsigned slots = 1u << (32 - p.hot_shift);
+            long long* hk = hot_keys();
+            std::uint32_t* hv = hot_verts(p);
+            for (unsigned i = threadIdx.x; i < slots; i += kBlock)
+                hv[i] = NONE;
+            __syncthreads();
+            for (unsigned j = threadIdx.x; j < p.nhot; j += kBlock) {
+                const std::uint32_t x = __ldg(&p.hot[j]);
+                const long long kx = __ldcg(&p.key_i[x]);
+                unsigned i = hot_hash(x, p.hot_shift);
+                for (int q = 0; q < kHotProbe; ++q) { // a hub that finds no slot is gathered
+                    if (atomicCAS(&hv[i], NONE, x) == NONE) {
+                        hk[i] = kx;
+                        break;
+                    }
+                    i = (i + 1) & (slots - 1);
+                }
+            }
+            __syncthreads();
+            hot = true;
+        }
+    }
     const std::size_t gs = gstride() / G;
-    for (std::size_t vv = p.own_lo + gtid() / G; vv < p.own_hi; vv += gs)
-        improve_vertex<EXACT, G, U>(p, changed, marks, static_cast<std::uint32_t>(vv));
+    if (hot) {
+        for (std::size_t vv = p.own_lo + gtid() / G; vv < p.own_hi; vv += gs)
+            improve_vertex<EXACT, G, U, true>(p, changed, marks, static_cast<std::uint32_t>(vv));
+    } else {
+        for (std::size_t vv = p.own_lo + gtid() / G; vv < p.own_hi; vv += gs)
+            improve_vertex<EXACT, G, U, false>(p, changed, marks, static_cast<std::uint32_t>(vv));
+    }
     marks.flush(p, changed);
 }
 
@@ -604,6 +819,18 @@ __global__ void k_list_heavy(std::uint32_t n, const std::uint32_t* row, std::uin
     for (std::size_t v = gtid(); v < n; v += gstride())
         if (row[v + 1] - row[v] >= hdeg)
             heavy[atomicAdd(count, 1u)] = static_cast<std::uint32_t>(v);
+}
+
+// Intra-region in-degree of every vertex (the number of improvement-pass
+// gathers of its key), for the choice of hub vertices.
+__global__ void k_edge_indeg(std::uint64_t m, const int2* ew, unsigned* cnt) {
+    for (std::uint64_t e = gtid(); e < m; e += gstride())
+        atomicAdd(&cnt[static_cast<std::uint32_t>(__ldg(&ew[e]).x)], 1u);
+}
+
+__global__ void k_iota(std::uint32_t n, std::uint32_t* ids) {
+    for (std::size_t v = gtid(); v < n; v += gstride())
+        ids[v] = static_cast<std::uint32_t>(v);
 }
 
 // ------------------------------------------------------------ helpers
@@ -759,20 +986,39 @@ __device__ __forceinline__ void ph_classify(const KP& p, int par, const Ring& ra
 // doubling steps per pass (records of 2^k steps -> 2^(k+S)): 2^S chained
 // reads of the same buffer instead of S rounds and S-1 barriers -- a
 // round's cost is mostly its barrier and the latency ramp, not its loads.
+#ifndef OCM_ROUND_ILP
+#define OCM_ROUND_ILP 1
+#endif
 template <int S> __device__ __forceinline__ void ph_round_multi(const KP& p, std::uint64_t nC, int in) {
     const PJC* __restrict__ a = p.pj[in];
     PJC* __restrict__ o = p.pj[in ^ 1];
-    for (std::uint64_t i = gtid(); i < nC; i += gstride()) {
-        const std::uint32_t v = p.clist[i];
-        PJC z = a[v];
+    constexpr int kR = OCM_ROUND_ILP; // independent chains interleaved per thread
+    const std::uint64_t nth = gstride();
+    for (std::uint64_t i0 = gtid(); i0 < nC; i0 += kR * nth) {
+        std::uint32_t v[kR];
+        PJC z[kR];
+#pragma unroll
+        for (int r = 0; r < kR; ++r) {
+            v[r] = i0 + r * nth < nC ? p.clist[i0 + r * nth] : NONE;
+            if (v[r] != NONE)
+                z[r] = a[v[r]];
+        }
 #pragma unroll
         for (int h = 1; h < (1 << S); ++h) {
-            const PJC y = a[z.nxt];
-            z.nxt = y.nxt;
-            z.mn = min(z.mn, y.mn);
-            z.w += y.w;
+#pragma unroll
+            for (int r = 0; r < kR; ++r) {
+                if (v[r] == NONE)
+                    continue;
+                const PJC y = a[z[r].nxt];
+                z[r].nxt = y.nxt;
+                z[r].mn = min(z[r].mn, y.mn);
+                z[r].w += y.w;
+            }
         }
-        o[v] = z;
+#pragma unroll
+        for (int r = 0; r < kR; ++r)
+            if (v[r] != NONE)
+                o[v[r]] = z[r];
     }
 }
 
@@ -1617,6 +1863,8 @@ __global__ void __launch_bounds__(kBlock, kSolveMinBlocks) k_solve(KP p, int mod
     __shared__ long long s_clk[PH_COUNT];
     if (threadIdx.x < PH_COUNT)
         s_clk[threadIdx.x] = 0;
+    if (EXACT && p.staged)
+        staged_init(*reinterpret_cast<Staged*>(dyn_smem));
     auto sync = [&](int ph) {
         grid.sync();
         ++st.nsync;
@@ -1801,7 +2049,7 @@ __global__ void __launch_bounds__(kBlock, kSolveMinBlocks) k_solve(KP p, int mod
         if (fatal)
             break;
         // adapt the starting round count: shrink after two first-try passes
-        if (first_try && ++st.k_streak >= 2 && k > 1) {
+        if (first_try && ++st.k_streak >= kKShrink && k > 1) {
             st.k_hint = k - 1;
             st.k_streak = 0;
         } else {

@@ -33,7 +33,7 @@ namespace {
 
 int env_int(const char* name, int dflt) {
     const char* v = std::getenv(name);
-    return v ? std::atoi(v) : dflt;
+    return v && *v ? std::atoi(v) : dflt;
 }
 
 // Per-device facts looked up once per process (device properties and the
@@ -234,11 +234,25 @@ void Session::init(const std::function<void(DeviceState&)>& prepare) {
         d.kp.nheavy = nh;
         d.kp.heavy = d.heavy.p;
     }
+    choose_hubs();
 
     // one CTA per SM slot the register budget allows (<= kSolveMinBlocks);
     // small graphs take one CTA per kBlock vertices: fewer arrivals make every
     // grid barrier cheaper and there is no work for more threads anyway
     grid_ = facts.per_sm[prep_.exact ? 1 : 0][gi_] * d.sms;
+    // TMA-staged improvement for key arrays beyond the ~64 MB that random
+    // gathers keep at L2 speed (OCM_STAGED=0/1 forces it off/on)
+    {
+        const int st = env_int("OCM_STAGED", -1);
+        d.kp.staged = prep_.exact && d.kp.nhot == 0 && st != 0 &&
+                      (st == 1 || std::size_t(prep_.n) * 8 > (std::size_t(64) << 20));
+    }
+    if (dyn_smem_bytes()) { // the staged pass / hub table use dynamic shared memory
+        int per_sm = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, solve_fn(prep_.exact, gi_), kBlock,
+                                                         dyn_smem_bytes()));
+        grid_ = std::min(grid_, std::max(1, per_sm) * d.sms);
+    }
     if (const int env_grid = env_int("OCM_GRID", 0))
         grid_ = std::max(1, std::min(grid_, env_grid));
     else
@@ -370,6 +384,85 @@ __global__ void kb_offsets(std::uint32_t n, std::uint32_t nblk, std::uint32_t nb
 }
 } // namespace
 
+// Hub vertices for the staged key table (exact lane): the highest
+// intra-region in-degrees. Opt-in: measured on B200 the table is slower than
+// plain gathers even where 1024 hubs receive 25% of the edges (web-like
+// graph, 6.4*10^7 vertices: 531 vs 492 ms of improvement per min solve,
+// profiles/r02/hot_staging_r02.log) -- L2 serves the few hub sectors at full
+// rate and the per-edge probe costs more than the gathers it saves.
+// OCM_HOT=-1 chooses automatically (>= 2% of the edges into at most 1024
+// vertices of >= 64x the average in-degree), OCM_HOT=1 forces it on for any
+// graph with edges (tests), OCM_HOT_SLOTS sets the table size (power of two,
+// 2 slots per hub).
+void Session::choose_hubs() {
+    DeviceState& d = *d_;
+    KP& p = d.kp;
+    p.nhot = 0;
+    p.hot = nullptr;
+    p.hot_shift = 32;
+    hot_bytes_ = 0;
+    const int mode = env_int("OCM_HOT", 0);
+    const std::size_t N = prep_.n;
+    if (mode == 0 || !prep_.exact || prep_.M == 0 || N == 0 || d.kp.pb)
+        return;
+    unsigned slots = static_cast<unsigned>(env_int("OCM_HOT_SLOTS", 2048));
+    slots = std::max(64u, std::min(slots, 8192u));
+    while (slots & (slots - 1))
+        slots &= slots - 1;
+    const unsigned cap = slots / 2;
+    cudaStream_t s = d.stream;
+    DBuf<unsigned> cnt, ids, cnt_sorted, ids_sorted;
+    cnt.alloc(N, s);
+    ids.alloc(N, s);
+    cnt_sorted.alloc(N, s);
+    ids_sorted.alloc(N, s);
+    CK(cudaMemsetAsync(cnt.p, 0, N * 4, s));
+    k_edge_indeg<<<grid_for(prep_.M, d.sms, 16), kBlock, 0, s>>>(prep_.M, d.ew.p, cnt.p);
+    k_iota<<<grid_for(N, d.sms), kBlock, 0, s>>>(static_cast<std::uint32_t>(N), ids.p);
+    std::size_t bytes = 0;
+    CK(cub::DeviceRadixSort::SortPairsDescending(nullptr, bytes, cnt.p, cnt_sorted.p, ids.p,
+                                                 ids_sorted.p, static_cast<int>(N), 0, 32, s));
+    DBuf<unsigned char> tmp;
+    tmp.alloc(std::max<std::size_t>(bytes, 1), s);
+    CK(cub::DeviceRadixSort::SortPairsDescending(tmp.p, bytes, cnt.p, cnt_sorted.p, ids.p,
+                                                 ids_sorted.p, static_cast<int>(N), 0, 32, s));
+    const unsigned take = static_cast<unsigned>(std::min<std::size_t>(cap, N));
+    std::vector<unsigned> top(take);
+    CK(cudaMemcpyAsync(top.data(), cnt_sorted.p, take * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    const double avg = double(prep_.M) / double(std::max<std::size_t>(1, N - prep_.trivial));
+    unsigned n_hot = 0;
+    std::uint64_t covered = 0;
+    for (unsigned i = 0; i < take; ++i) {
+        if (top[i] == 0 || (mode != 1 && double(top[i]) < 64.0 * avg))
+            break;
+        ++n_hot;
+        covered += top[i];
+    }
+    hot_coverage_ = double(covered) / double(prep_.M);
+    if (n_hot == 0 || (mode != 1 && hot_coverage_ < 0.02))
+        return;
+    d.hot.alloc(n_hot, s);
+    CK(cudaMemcpyAsync(d.hot.p, ids_sorted.p, n_hot * 4ull, cudaMemcpyDeviceToDevice, s));
+    CK(cudaStreamSynchronize(s));
+    unsigned lg = 0;
+    while ((1u << lg) < slots)
+        ++lg;
+    p.hot = d.hot.p;
+    p.nhot = n_hot;
+    p.hot_shift = 32 - lg;
+    hot_bytes_ = std::size_t(slots) * 12;
+}
+
+std::size_t Session::dyn_smem_bytes() const {
+    const KP& p = d_->kp;
+    if (p.pb)
+        return kPbSmem;
+    if (p.staged)
+        return kStagedSmem;
+    return p.nhot ? hot_bytes_ : 0;
+}
+
 void Session::build_blocked_edges() {
     DeviceState& d = *d_;
     KP& p = d.kp;
@@ -423,6 +516,7 @@ void Session::build_blocked_edges() {
         CK(cudaStreamSynchronize(s));
     }
     p.pb = 1;
+    p.staged = 0; // the blocked pass replaces the staged one (and its shared memory)
     p.pb_tw = d.pb_tw.p;
     p.pb_perm = d.pb_perm.p;
     p.pb_inv = d.pb_inv.p;
@@ -459,7 +553,7 @@ template <class M> void Session::launch_async(int mode) {
     if (prep_.R > 0) {
         void* args[] = {&p, &mode};
         CK(cudaLaunchCooperativeKernel(solve_fn(EXACT, gi_), dim3(grid_), dim3(kBlock), args,
-                                       p.pb ? kPbSmem : 0, s));
+                                       dyn_smem_bytes(), s));
         ++launches_;
     }
     CK(cudaEventRecord(d.ev_end, s));
@@ -528,10 +622,10 @@ template <class M> void Session::collect(ocm_solution* out, std::uint32_t* cycle
                      "{\"device_ms\": %.3f, \"phases_ms\": {%s}, \"passes\": %u, \"outer\": %u, "
                      "\"rounds\": %u, \"verifies\": %u, \"peeled\": %llu, \"cored\": %llu, "
                      "\"layers\": %u, \"syncs\": %u, \"k_hint\": %u, \"launches\": %u, \"N\": %u, "
-                     "\"M\": %llu}\n",
+                     "\"M\": %llu, \"nhot\": %u, \"hot_coverage\": %.4f}\n",
                      ms, ph.c_str(), hc.passes, hc.outer, hc.rounds, hc.verifies,
                      (unsigned long long)hc.peeled, (unsigned long long)hc.cored, hc.layers, hc.syncs,
-                     hc.k_hint, launches_, p.N, (unsigned long long)prep_.M);
+                     hc.k_hint, launches_, p.N, (unsigned long long)prep_.M, p.nhot, hot_coverage_);
     }
 
     std::memset(out, 0, sizeof *out);

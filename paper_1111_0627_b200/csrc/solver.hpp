@@ -67,6 +67,10 @@ class Session {
     int gi_ = 0;   // its improvement group width (index into 1, 2, 4, 8)
     std::uint32_t rank_ = 0, world_ = 1, chunk_ = 0;
     void build_blocked_edges();
+    void choose_hubs();
+    std::size_t dyn_smem_bytes() const;
+    std::size_t hot_bytes_ = 0;    // dynamic shared memory of the staged hub table
+    double hot_coverage_ = 0.0;    // share of intra-region edges into the staged hubs
     bool shard_started_ = false;
     bool connected_ = false; // fused sharded lane: peers mapped
     bool fused_broken_ = false; // a cross-rank barrier timed out (epochs out of step)

@@ -14,9 +14,15 @@ ap.add_argument("--seed", type=int, default=1111_0627)
 ap.add_argument("--solves", type=int, default=1)
 ap.add_argument("--objective", default="min")
 ap.add_argument("--warmup", type=int, default=1)
+ap.add_argument("--kind", default="uniform", help="generator kind (graph built in HBM unless uniform)")
+ap.add_argument("--dmax", type=int, default=1 << 20)
 a = ap.parse_args()
-g = P.generate_uniform(a.n, a.deg, 1, 100, a.seed)
-s = P.Session(g, P.SolveOptions(objective=a.objective))
+if a.kind == "uniform":
+    g = P.generate_uniform(a.n, a.deg, 1, 100, a.seed)
+    s = P.Session(g, P.SolveOptions(objective=a.objective))
+else:
+    s = P.Session.generated(P.Generator(a.kind, n=a.n, deg=a.deg, dmax=a.dmax, seed=a.seed),
+                            P.SolveOptions(objective=a.objective))
 for _ in range(a.warmup):
     s.solve()
 for _ in range(a.solves):

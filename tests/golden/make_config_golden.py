@@ -63,7 +63,7 @@ def graph(cfg):
     if c["kind"] == "model":
         return O.generate_model(c["scenario"], c["clients"])
     s, d, w = O.generate_powerlaw(c["n"], c["deg"], c["dmax"], 1, 100, SEED,
-                                  hubs=c["kind"] == "powerlaw-hubs")
+                                  hubs={"powerlaw": 0, "powerlaw-hubs": 1, "powerlaw-web": 3}[c["kind"]])
     return c["n"], s, d, w
 
 

@@ -115,3 +115,64 @@ def test_powerlaw_certificate(objective):
     sol = sess.solve()
     assert sol.has_cycle and sol.exact
     certificate(P.generate(spec), sol, sess.values(), objective)
+
+
+@pytest.mark.parametrize("hot", ["0", "1", None])
+@pytest.mark.parametrize("slots", ["64", "2048"])
+@pytest.mark.parametrize("objective", ["min", "max"])
+def test_hub_graph_staged_keys_vs_oracle(hot, slots, objective, monkeypatch):
+    """In-degree-skewed power-law graph ("powerlaw-hubs"): the improvement
+    pass reading hub keys from the per-CTA shared-memory table (OCM_HOT=1
+    forces it on, None = the automatic choice, 0 = off; 64 slots make hubs
+    collide and fall back to gathers) equals the oracle bit for bit."""
+    if hot is not None:
+        monkeypatch.setenv("OCM_HOT", hot)
+    monkeypatch.setenv("OCM_HOT_SLOTS", slots)
+    spec = P.Generator("powerlaw-hubs", n=30_000, deg=4, dmax=20_000, seed=12)
+    g = P.generate(spec)
+    s, d, w = g.edges()
+    sess = P.Session(g, P.SolveOptions(objective=objective))
+    sol = sess.solve()
+    check_against(sol, sess.values(), oracle_record(g.n, s, d, w, objective, "tarjan"))
+
+
+@pytest.mark.parametrize("objective", ["min", "max"])
+def test_staged_keys_on_uniform_graph(objective, monkeypatch):
+    """The table forced on for a graph without hubs (every probe misses or
+    hits a vertex of ordinary degree) changes nothing."""
+    spec = P.Generator("uniform", n=100_000, deg=8, seed=3)
+    monkeypatch.setenv("OCM_HOT", "0")
+    a = P.Session.generated(spec, P.SolveOptions(objective=objective))
+    monkeypatch.setenv("OCM_HOT", "1")
+    b = P.Session.generated(spec, P.SolveOptions(objective=objective))
+    solve_both(a, b)
+
+
+@pytest.mark.parametrize("spec", [
+    P.Generator("uniform", n=100_000, deg=8, seed=3),
+    P.Generator("powerlaw", n=60_000, deg=8, dmax=1 << 20, seed=4),
+    P.Generator("powerlaw-web", n=60_000, deg=4, dmax=5000, wlo=-50, whi=50, seed=6),
+], ids=["uniform", "powerlaw", "web-signed"])
+@pytest.mark.parametrize("objective", ["min", "max"])
+def test_tma_staged_pass_matches_direct(spec, objective, monkeypatch):
+    """The improvement pass fed by bulk-TMA copies of each chunk's offsets
+    and edges into shared memory (OCM_STAGED=1; on by default only for key
+    arrays beyond 64 MB) equals the direct pass bit for bit, including chunks
+    too large for a stage (heavy vertices) that fall back to global loads."""
+    monkeypatch.setenv("OCM_STAGED", "0")
+    a = P.Session.generated(spec, P.SolveOptions(objective=objective))
+    monkeypatch.setenv("OCM_STAGED", "1")
+    b = P.Session.generated(spec, P.SolveOptions(objective=objective))
+    solve_both(a, b)
+    solve_both(a, b)  # re-solves: mbarrier phases carried across launches
+
+
+@pytest.mark.parametrize("objective", ["min", "max"])
+def test_tma_staged_pass_vs_oracle(objective, monkeypatch):
+    monkeypatch.setenv("OCM_STAGED", "1")
+    spec = P.Generator("powerlaw-hubs", n=20_000, deg=4, dmax=20_000, seed=11)
+    g = P.generate(spec)
+    s, d, w = g.edges()
+    sess = P.Session(g, P.SolveOptions(objective=objective))
+    sol = sess.solve()
+    check_against(sol, sess.values(), oracle_record(g.n, s, d, w, objective, "tarjan"))

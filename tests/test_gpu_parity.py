@@ -286,3 +286,54 @@ def test_float_session_resolve_and_sessions_interleave():
     assert (e1.mu_exact, e1.cycle_vertices) == (e2.mu_exact, e2.cycle_vertices)
     ref = oracle_record(g.n, s, d, w / 8.0 + 0.0625, "min", "tarjan")
     check_against(a, fs.values(), ref)
+
+
+def _csr(g):
+    s, d, w = g.edges()
+    idx = np.zeros(g.n + 1, np.uint32)
+    np.cumsum(np.bincount(s, minlength=g.n), out=idx[1:])
+    return idx, d, w
+
+
+@pytest.mark.parametrize("case", CASES[::3], ids=[c["name"] for c in CASES[::3]])
+def test_solve_csr_matches_solve(case):
+    """ocm_solve_csr (the reference's CSR arrays, staged from pageable
+    memory, validated and exactness-derived on the device) == ocm_solve."""
+    g = P.build_graph(case["n"], case_arrays(case))
+    idx, d, w = _csr(g)
+    for objective in ("min", "max"):
+        for scc in ("tarjan", "off"):
+            for algo in ("howard", "howard-par"):
+                o = P.SolveOptions(algo=algo, objective=objective, scc=scc)
+                a, b = P.solve(g, o), P.solve_csr(g.n, idx, d, w, o)
+                assert (a.has_cycle, a.exact, a.mu_exact, a.mu, a.cycle_vertices) == \
+                    (b.has_cycle, b.exact, b.mu_exact, b.mu, b.cycle_vertices)
+                assert (a.stats.outer_iters, a.stats.spf_passes, a.stats.regions) == \
+                    (b.stats.outer_iters, b.stats.spf_passes, b.stats.regions)
+
+
+def test_solve_csr_large_pageable_graph():
+    """A 10^6 x 8 graph (100 MB through the staging ring) equals the session."""
+    g = P.generate(P.Generator("uniform", n=1_000_000, deg=8, seed=5))
+    idx, d, w = _csr(g)
+    a = P.Session(g, P.SolveOptions()).solve()
+    b = P.solve_csr(g.n, idx, d, w)
+    assert (a.mu_exact, a.cycle_vertices, a.stats.spf_passes) == \
+        (b.mu_exact, b.cycle_vertices, b.stats.spf_passes)
+    assert b.stats.h2d_bytes == (g.n + 1) * 4 + g.m * 12
+
+
+def test_solve_csr_validates_like_build_graph():
+    idx = np.array([0, 1, 2], np.uint32)
+    with pytest.raises(ValueError, match="edge 1 endpoint out of range"):
+        P.solve_csr(2, idx, np.array([1, 2], np.uint32), np.array([1.0, 2.0]))
+    with pytest.raises(ValueError, match="edge 0 has non-finite weight"):
+        P.solve_csr(2, idx, np.array([1, 0], np.uint32), np.array([np.nan, 2.0]))
+    with pytest.raises(ValueError, match="offsets"):
+        P.solve_csr(2, np.array([0, 2, 1], np.uint32), np.array([1, 0], np.uint32),
+                    np.array([1.0, 2.0]))
+    # exactness is derived on the device: 2.5 makes the graph a float graph
+    s = P.solve_csr(2, idx, np.array([1, 0], np.uint32), np.array([2.5, 2.0]))
+    assert s.has_cycle and not s.exact and s.mu == 2.25
+    s = P.solve_csr(2, idx, np.array([1, 0], np.uint32), np.array([3.0, 2.0]))
+    assert s.exact and s.mu_exact == Fraction(5, 2)

@@ -87,14 +87,15 @@ def test_oracle_model_generator_matches_reference(scenario, clients):
     assert n == nr and np.array_equal(s, sr) and np.array_equal(d, dr) and np.array_equal(w, wr)
 
 
-@pytest.mark.parametrize("kind", ["powerlaw", "powerlaw-hubs"])
+@pytest.mark.parametrize("kind", ["powerlaw", "powerlaw-hubs", "powerlaw-web"])
 def test_oracle_powerlaw_generators_match_product(kind):
-    s, d, w = O.generate_powerlaw(50_000, 4, 5_000, 1, 100, 9, hubs=kind == "powerlaw-hubs")
+    q = {"powerlaw": 0, "powerlaw-hubs": 1, "powerlaw-web": 3}[kind]
+    s, d, w = O.generate_powerlaw(50_000, 4, 5_000, 1, 100, 9, hubs=q)
     g = P.generate(P.Generator(kind, n=50_000, deg=4, dmax=5_000, seed=9))
     s2, d2, w2 = g.edges()
     assert np.array_equal(s, s2) and np.array_equal(d, d2) and np.array_equal(w, w2)
     indeg = np.bincount(d, minlength=50_000)
-    if kind == "powerlaw-hubs":  # hub targets: in-degree tail exponent 3
-        assert indeg.max() > 50 * indeg.mean()
+    if q:  # hub targets: in-degree tail exponent 3 (hubs) / ~2.14 (web)
+        assert indeg.max() > (50 if q == 1 else 5000) * indeg.mean()
     else:
         assert indeg.max() < 10 * indeg.mean()

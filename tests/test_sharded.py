@@ -281,3 +281,16 @@ def test_fused_two_processes_ipc():
     for rank, res, err in got:
         assert err is None, (rank, err)
         assert res and all(same for _, _, same in res), (rank, res)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("objective", ["min", "max"])
+def test_fused_shards_with_tma_staged_pass(objective, monkeypatch):
+    """The fused lane's per-rank improvement range through the staged pass."""
+    src = P.Generator("uniform", n=50_000, deg=8, seed=21)
+    a, va = _single(src, objective)
+    monkeypatch.setenv("OCM_STAGED", "1")
+    monkeypatch.setenv("OCM_GRID", str(148 * 4 // 2))
+    sols, vals = _fused(src, objective, 2)
+    for b, vb in zip(sols, vals):
+        _same(a, va, b, vb)
