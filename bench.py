@@ -583,6 +583,11 @@ def main():
     launches = sum(s[o].stats.launches for s in sols for o in s)
     edges = sum(s[o].stats.m_solved * s[o].stats.spf_passes for s in sols for o in s)
     alg = sum(algorithmic_bytes(s[o].stats)[0] for s in sols for o in s)
+    # the roofline is quoted on the min-objective launches: the ncu capture
+    # (profiles/solve_traffic.json) is of a min launch, so achieved and
+    # traffic describe the same launch
+    alg_min = sum(algorithmic_bytes(s["min"].stats)[0] for s in sols)
+    ms_min = sum(s["min"].stats.device_ms for s in sols)
     imp_bytes = sum(algorithmic_bytes(s[o].stats)[1] * s[o].stats.spf_passes for s in sols for o in s)
     st0 = sols[0]["min"].stats
     for s in sols:
@@ -644,7 +649,7 @@ def main():
 
     if rank == 0:
         peak, peak_src = measured_peak()
-        achieved = alg / (dev_ms / 1e3) / 1e9
+        achieved = alg_min / (ms_min / 1e3) / 1e9
         imp_achieved = imp_bytes / (imp_ms / 1e3) / 1e9 if imp_ms else None
         line = {
             "metric": METRIC, "value": edges_all / (dev_ms_max / 1e3), "unit": UNIT,
@@ -664,7 +669,11 @@ def main():
                 "bound": "hbm", "kernel": "k_solve (persistent: one cooperative launch per solve)",
                 "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": ncu_traffic(a.config),
-                "bytes_per_launch": alg / (2 * a.steps), "avg_launch_ms": dev_ms / (2 * a.steps),
+                "bytes_per_launch": alg_min / a.steps, "avg_launch_ms": ms_min / a.steps,
+                "launches": "min-objective k_solve launches (the ncu-captured one)",
+                "all_launches": {"achieved": alg / (dev_ms / 1e3) / 1e9,
+                                 "bytes_per_launch": alg / (2 * a.steps),
+                                 "avg_launch_ms": dev_ms / (2 * a.steps)},
                 "peak_source": peak_src,
                 "improve_phase": {"achieved": imp_achieved,
                                   "frac": imp_achieved / peak if imp_achieved else None,

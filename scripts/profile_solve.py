@@ -14,10 +14,11 @@ ap.add_argument("--seed", type=int, default=1111_0627)
 ap.add_argument("--solves", type=int, default=1)
 ap.add_argument("--objective", default="min")
 ap.add_argument("--warmup", type=int, default=1)
-ap.add_argument("--kind", default="uniform", help="generator kind (graph built in HBM unless uniform)")
+ap.add_argument("--kind", default="uniform",
+                help="generator kind (graph built in HBM, except uniform graphs up to 10^7 vertices)")
 ap.add_argument("--dmax", type=int, default=1 << 20)
 a = ap.parse_args()
-if a.kind == "uniform":
+if a.kind == "uniform" and a.n <= 10_000_000:
     g = P.generate_uniform(a.n, a.deg, 1, 100, a.seed)
     s = P.Session(g, P.SolveOptions(objective=a.objective))
 else:
