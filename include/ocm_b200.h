@@ -190,6 +190,13 @@ typedef struct ocm_certificate {
     uint64_t policy_violations;        /* policy edge missing or not attaining K[v] */
     uint64_t cycle_violations;         /* regions whose anchor cycle fails */
 } ocm_certificate;
+/* Exact value keys at full width (either exact lane): key = key_hi * 2^64 +
+ * key_lo as a 128-bit two's complement, value = key / lam_den. The wide lane
+ * (128-bit keys) runs when a weight needs more than 32 bits or a key could
+ * leave +-2^62; ocm_session_values then returns OCM_E_RANGE for keys beyond
+ * 64 bits. ocm_session_is_wide reports the lane of the session's last solve. */
+int ocm_session_keys_wide(ocm_session* s, int64_t* key_hi, uint64_t* key_lo);
+int ocm_session_is_wide(const ocm_session* s);
 int ocm_session_certify(ocm_session* s, ocm_certificate* out);
 /* A session over a generated graph built in HBM (no host graph). */
 int ocm_session_create_generated(const ocm_generator* spec, const ocm_solve_options* opt,

@@ -159,6 +159,8 @@ def _load():
         "ocm_session_values": (C.c_int, [C.c_void_p, P(C.c_int64), P(C.c_int64), P(C.c_int64),
                                          P(C.c_double), P(C.c_uint32)]),
         "ocm_session_certify": (C.c_int, [C.c_void_p, P(_Certificate)]),
+        "ocm_session_keys_wide": (C.c_int, [C.c_void_p, P(C.c_int64), P(C.c_uint64)]),
+        "ocm_session_is_wide": (C.c_int, [C.c_void_p]),
         "ocm_session_stream": (C.c_void_p, [C.c_void_p]),
         "ocm_session_free": (None, [C.c_void_p]),
     }
@@ -181,7 +183,8 @@ EXPORTED_SYMBOLS = (
     "ocm_session_shard_fused_launch", "ocm_session_shard_fused_finish",
     "ocm_graph_free", "ocm_graph_n", "ocm_graph_m", "ocm_graph_integer_exact", "ocm_graph_edges",
     "ocm_solve", "ocm_solve_csr", "ocm_session_create", "ocm_session_solve", "ocm_session_values",
-    "ocm_session_stream", "ocm_session_free", "ocm_session_certify",
+    "ocm_session_stream", "ocm_session_free", "ocm_session_certify", "ocm_session_keys_wide",
+    "ocm_session_is_wide",
 )
 
 
@@ -541,16 +544,36 @@ class Session:
         _check(_lib.ocm_session_certify(self._h, C.byref(c)))
         return {f: int(getattr(c, f)) for f, _ in _Certificate._fields_}
 
+    @property
+    def wide(self) -> bool:
+        """True when the last solve ran the wide exact lane (128-bit keys)."""
+        return bool(_lib.ocm_session_is_wide(self._h))
+
+    def keys_wide(self) -> np.ndarray:
+        """Exact value keys at full width as Python ints (object array):
+        value(v) = key[v] / lam_den[v]."""
+        n = max(self.n, 1)
+        hi = np.zeros(n, np.int64)
+        lo = np.zeros(n, np.uint64)
+        _check(_lib.ocm_session_keys_wide(self._h, _p(hi, C.c_int64), _p(lo, C.c_uint64)))
+        return np.array([(int(h) << 64) | int(l) for h, l in zip(hi[: self.n], lo[: self.n])],
+                        dtype=object)
+
     def values(self):
         """Final value plane: dict with key_num/lam_num/lam_den (exact: value =
-        key_num/lam_den), fval (float graphs) and succ_vertex, in original order."""
+        key_num/lam_den), fval (float graphs) and succ_vertex, in original order.
+        After a wide-lane solve key_num holds Python ints (object array)."""
         n = max(self.n, 1)
         out = {k: np.zeros(n, t) for k, t in (("key_num", np.int64), ("lam_num", np.int64),
                                               ("lam_den", np.int64), ("fval", np.float64),
                                               ("succ_vertex", np.uint32))}
-        _check(_lib.ocm_session_values(self._h, _p(out["key_num"], C.c_int64),
+        wide = bool(_lib.ocm_session_is_wide(self._h))
+        _check(_lib.ocm_session_values(self._h, None if wide else _p(out["key_num"], C.c_int64),
                                        _p(out["lam_num"], C.c_int64),
                                        _p(out["lam_den"], C.c_int64),
                                        _p(out["fval"], C.c_double),
                                        _p(out["succ_vertex"], C.c_uint32)))
-        return {k: v[: self.n] for k, v in out.items()}
+        res = {k: v[: self.n] for k, v in out.items()}
+        if wide:
+            res["key_num"] = Session.keys_wide(self)
+        return res

@@ -305,6 +305,16 @@ int ocm_session_certify(ocm_session* s, ocm_certificate* out) {
     });
 }
 
+int ocm_session_keys_wide(ocm_session* s, int64_t* key_hi, uint64_t* key_lo) {
+    return guard([&] {
+        if (!s || !key_hi || !key_lo)
+            throw std::invalid_argument("null session or output");
+        s->s->keys_wide(key_hi, key_lo);
+    });
+}
+
+int ocm_session_is_wide(const ocm_session* s) { return s && s->s->wide() ? 1 : 0; }
+
 void* ocm_session_stream(ocm_session* s) { return s ? s->s->stream() : nullptr; }
 
 void ocm_session_free(ocm_session* s) { delete s; }

@@ -46,6 +46,14 @@ struct __align__(16) PJV {
     std::uint32_t root;
 };
 
+// The same for the wide exact lane (128-bit accumulated keys).
+struct __align__(16) PJVW {
+    __int128 acc;
+    std::uint32_t nxt;
+    std::uint32_t root;
+    std::uint64_t pad;
+};
+
 // Pointer-doubling record for cycle detection: segment end, least vertex on
 // the segment, weight sum of the segment.
 struct __align__(16) PJC {
@@ -111,6 +119,9 @@ struct KP {
     double* succ_wf;
     long long* key_i;
     double* key_f;
+    __int128* key_w;           // wide exact lane: 128-bit keys
+    const int* ew_hi;          // wide exact lane: high 32 bits of each edge weight
+    int* succ_whi;             // wide exact lane: high 32 bits of the policy weight
     long long* lam_num;
     long long* lam_den;
     double* lam_f;
@@ -134,6 +145,7 @@ struct KP {
     std::uint32_t* conn;
     std::uint32_t* rem[2];
     PJV* pv[2];
+    PJVW* pvw[2];
     Ctl* c;
     std::uint32_t max_region;
     long long max_abs_w;
@@ -244,6 +256,9 @@ struct DeviceState {
     DBuf<std::uint32_t> row, reg, succ_e, succ_v, comp, wlist, cyc_len, conn, rem0, rem1, src,
         iters, indeg, plist, clist, cmark, cmark2, heavy, xbar, hot;
     DBuf<PJV> pv0, pv1;
+    DBuf<PJVW> pvw0, pvw1;
+    DBuf<__int128> key_w;
+    DBuf<int> ew_hi, succ_whi;
     DBuf<PJC> pj0, pj1;
     DBuf<int2> ew;
     DBuf<FEdge> fe;
@@ -278,6 +293,11 @@ struct DeviceState {
             b->release();
         pv0.release();
         pv1.release();
+        pvw0.release();
+        pvw1.release();
+        key_w.release();
+        ew_hi.release();
+        succ_whi.release();
         pj0.release();
         pj1.release();
         ew.release();

@@ -616,9 +616,18 @@ __global__ void kp_count_intra(std::uint32_t n, std::uint32_t R, const std::uint
     })
 }
 
+// ew_hi != nullptr: the wide exact lane (64-bit weights, the high half in
+// ew_hi); otherwise a weight outside int32 is reported.
 template <bool EXACT>
-__device__ __forceinline__ bool pack_one(std::uint32_t t, double x, std::uint32_t k, int2* ew, FEdge* fe) {
+__device__ __forceinline__ bool pack_one(std::uint32_t t, double x, std::uint32_t k, int2* ew,
+                                         int* ew_hi, FEdge* fe) {
     if constexpr (EXACT) {
+        if (ew_hi) {
+            const long long wv = static_cast<long long>(x);
+            ew[k] = make_int2(static_cast<int>(t), static_cast<int>(static_cast<unsigned>(wv)));
+            ew_hi[k] = static_cast<int>(wv >> 32);
+            return false;
+        }
         ew[k] = make_int2(static_cast<int>(t), static_cast<int>(x));
         return !(fabs(x) <= 2147483647.0);
     } else {
@@ -630,7 +639,7 @@ __device__ __forceinline__ bool pack_one(std::uint32_t t, double x, std::uint32_
 template <bool EXACT>
 __global__ void kp_pack(std::uint32_t n, std::uint32_t R, const std::uint32_t* row,
                         const std::uint32_t* tgt, const double* w, const std::uint32_t* reg,
-                        const std::uint32_t* nrow, double sign, int2* ew, FEdge* fe,
+                        const std::uint32_t* nrow, double sign, int2* ew, int* ew_hi, FEdge* fe,
                         PrepCounters* pc) {
     bool bad = false;
     OCM_WARP_VERTICES(n, {
@@ -640,7 +649,7 @@ __global__ void kp_pack(std::uint32_t n, std::uint32_t R, const std::uint32_t* r
             for (std::uint32_t e = b; e < e_end; ++e) {
                 const std::uint32_t t = tgt[e];
                 if (reg[t] == r)
-                    bad |= pack_one<EXACT>(t, sign * w[e], k++, ew, fe);
+                    bad |= pack_one<EXACT>(t, sign * w[e], k++, ew, ew_hi, fe);
             }
         }
     }, {
@@ -658,7 +667,8 @@ __global__ void kp_pack(std::uint32_t n, std::uint32_t R, const std::uint32_t* r
                 }
                 const unsigned m = __ballot_sync(FULL, in);
                 if (in)
-                    bad |= pack_one<EXACT>(t, sign * w[e], k + __popc(m & ((1u << lane) - 1u)), ew, fe);
+                    bad |= pack_one<EXACT>(t, sign * w[e], k + __popc(m & ((1u << lane) - 1u)), ew,
+                                           ew_hi, fe);
                 k += __popc(m);
             }
         }
@@ -673,8 +683,8 @@ __global__ void kp_pack(std::uint32_t n, std::uint32_t R, const std::uint32_t* r
 template <bool EXACT>
 __global__ void kp_pack_hamiltonian(std::uint32_t n, const std::uint32_t* row,
                                     const std::uint32_t* tgt, const double* w, double sign,
-                                    double big_w, int2* ew, FEdge* fe, std::uint32_t* nrow,
-                                    std::uint32_t* reg, PrepCounters* pc) {
+                                    double big_w, int2* ew, int* ew_hi, FEdge* fe,
+                                    std::uint32_t* nrow, std::uint32_t* reg, PrepCounters* pc) {
     bool bad = false;
     for (std::size_t vv = tid_(); vv <= n; vv += stride_()) {
         const std::uint32_t v = static_cast<std::uint32_t>(vv);
@@ -687,12 +697,7 @@ __global__ void kp_pack_hamiltonian(std::uint32_t n, const std::uint32_t* row,
             const bool extra = e == row[v + 1];
             const std::uint32_t t = extra ? (v + 1) % n : tgt[e];
             const double x = extra ? big_w : sign * w[e];
-            if constexpr (EXACT) {
-                bad |= !(fabs(x) <= 2147483647.0);
-                ew[k] = make_int2(static_cast<int>(t), static_cast<int>(x));
-            } else {
-                fe[k] = FEdge{x, t, 0u};
-            }
+            bad |= pack_one<EXACT>(t, x, k, ew, ew_hi, fe);
             ++k;
         }
     }
@@ -955,6 +960,25 @@ void device_prepare_csr(std::uint32_t n, std::uint64_t m, DBuf<std::uint32_t>& r
         have_max_abs = true;
     };
 
+    // Exact lane width: 32-bit weights and 64-bit keys while every weight
+    // fits int32 (the session promotes itself to the wide lane if a key
+    // could leave +-2^62 later), else 64-bit weights and 128-bit keys -- the
+    // reference's whole ExactMode range (|w| < 2^53). Doubling sums stay
+    // 64-bit, so the wide lane needs max_region * max|w| < 2^62 (the
+    // reference's own int64 path sums overflow near there as well).
+    // OCM_WIDE=1 forces the wide lane (tests).
+    auto choose_wide = [&](double amax) {
+        const char* force = std::getenv("OCM_WIDE");
+        info.wide = amax > 2147483647.0 || (force && force[0] == '1');
+        if (!info.wide)
+            return;
+        if (static_cast<long double>(amax) * info.max_region >= 4611686018427387904.0L)
+            throw RangeError("exact weight sums would exceed 62 bits (max |w| x largest region)");
+        const std::size_t cnt = std::max<std::uint64_t>(info.M, 1) + 2;
+        d.ew_hi.alloc(cnt, s);
+        CK(cudaMemsetAsync(d.ew_hi.p, 0, cnt * 4, s));
+    };
+
     d.reg.alloc(std::max<std::uint32_t>(n, 1), s);
     // +7: the staged improvement pass copies 16-byte aligned windows of the
     // offsets and edge records (zeroed padding, never used as data)
@@ -978,19 +1002,21 @@ void device_prepare_csr(std::uint32_t n, std::uint64_t m, DBuf<std::uint32_t>& r
         if (info.exact) {
             d.ew.alloc(info.M + 2, s);
             CK(cudaMemsetAsync(d.ew.p + info.M, 0, 2 * sizeof(int2), s));
+            choose_wide(std::max(max_abs, big_w));
         } else {
             d.fe.alloc(info.M, s);
         }
         if (info.exact)
             kp_pack_hamiltonian<true><<<grid_for(n + 1, sms), kBlock, 0, s>>>(
-                n, row.p, tgt.p, w.p, sign, big_w, d.ew.p, nullptr, d.row.p, d.reg.p, pcd.p);
+                n, row.p, tgt.p, w.p, sign, big_w, d.ew.p, d.ew_hi.p, nullptr, d.row.p, d.reg.p,
+                pcd.p);
         else
             kp_pack_hamiltonian<false><<<grid_for(n + 1, sms), kBlock, 0, s>>>(
-                n, row.p, tgt.p, w.p, sign, big_w, nullptr, d.fe.p, d.row.p, d.reg.p, pcd.p);
+                n, row.p, tgt.p, w.p, sign, big_w, nullptr, nullptr, d.fe.p, d.row.p, d.reg.p, pcd.p);
         info.max_abs_w = static_cast<long long>(std::max(max_abs, big_w));
         read_pc();
         if (info.exact && pc.bad_weight)
-            throw UnsupportedError("integer weights beyond 32 bits are not supported by the device lane");
+            throw std::logic_error("weight packing: a weight outside the chosen lane's range");
         return;
     }
 
@@ -1159,23 +1185,24 @@ void device_prepare_csr(std::uint32_t n, std::uint64_t m, DBuf<std::uint32_t>& r
     CK(cudaMemcpyAsync(&M, d.row.p + n, 4, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     info.M = M;
+    need_weights();
     if (info.exact) {
         d.ew.alloc(std::size_t(M) + 2, s);
         CK(cudaMemsetAsync(d.ew.p + M, 0, 2 * sizeof(int2), s));
+        choose_wide(max_abs);
     } else {
         d.fe.alloc(std::max<std::uint32_t>(M, 1), s);
     }
-    need_weights();
     CK(cudaMemsetAsync(&pcd.p->bad_weight, 0, 4, s));
     if (info.exact)
         kp_pack<true><<<gv, kBlock, 0, s>>>(n, R, row.p, tgt.p, w.p, d.reg.p, d.row.p, sign, d.ew.p,
-                                            nullptr, pcd.p);
+                                            d.ew_hi.p, nullptr, pcd.p);
     else
         kp_pack<false><<<gv, kBlock, 0, s>>>(n, R, row.p, tgt.p, w.p, d.reg.p, d.row.p, sign,
-                                             nullptr, d.fe.p, pcd.p);
+                                             nullptr, nullptr, d.fe.p, pcd.p);
     read_pc();
     if (info.exact && pc.bad_weight)
-        throw UnsupportedError("integer weights beyond 32 bits are not supported by the device lane");
+        throw std::logic_error("weight packing: a weight outside the chosen lane's range");
     info.max_abs_w = static_cast<long long>(max_abs);
     mark("pack");
     if (std::getenv("OCM_PREP_TIMING"))

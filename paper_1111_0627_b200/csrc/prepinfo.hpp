@@ -14,6 +14,7 @@ struct PrepInfo {
     std::uint64_t M = 0;            // intra-region edges
     std::uint32_t max_region = 0;
     bool exact = false;
+    bool wide = false;              // exact lane with 128-bit keys and 64-bit weights
     bool scc_off = false;
     double no_cycle_above = 0.0;
     long long max_abs_w = 0;

@@ -61,6 +61,85 @@ constexpr int kSolveMinBlocks = OCM_MINB; // 4: register cap 64 at 256 threads
 // step shallower
 constexpr unsigned kKShrink = OCM_KSHRINK;
 
+// ------------------------------------------------------------ modes
+//
+// Arithmetic mode of a k_solve instantiation (template parameter MODE):
+//   0  FloatMode (policy.hpp) in doubles;
+//   1  ExactMode with 64-bit keys K = value*den and 32-bit edge weights --
+//      the fast lane, used while every key provably stays inside +-2^62;
+//   2  ExactMode "wide": 128-bit keys and 64-bit weights (the low half in
+//      the int2 edge record, the high half in ew_hi / succ_whi), covering
+//      the reference's whole exact range (integral |w| < 2^53, graph.cpp:15,
+//      compared as (wsum, steps) with 128-bit products, policy.hpp:71-79).
+template <int MODE> struct ModeT;
+template <> struct ModeT<0> { using Key = double; };
+template <> struct ModeT<1> { using Key = long long; };
+template <> struct ModeT<2> { using Key = __int128; };
+template <int MODE> using KeyT = typename ModeT<MODE>::Key;
+
+template <int MODE> __device__ __forceinline__ KeyT<MODE> key_ld(const KP& p, std::uint32_t v) {
+    if constexpr (MODE == 0)
+        return p.key_f[v];
+    else if constexpr (MODE == 1)
+        return p.key_i[v];
+    else
+        return p.key_w[v];
+}
+// key gather for the improvement pass (L2, bypassing L1)
+template <int MODE> __device__ __forceinline__ KeyT<MODE> key_gather(const KP& p, std::uint32_t v) {
+    if constexpr (MODE == 0)
+        return __ldcg(&p.key_f[v]);
+    else if constexpr (MODE == 1)
+        return __ldcg(&p.key_i[v]);
+    else {
+        const longlong2 x = __ldcg(reinterpret_cast<const longlong2*>(p.key_w) + v);
+        return (static_cast<__int128>(x.y) << 64) | static_cast<unsigned long long>(x.x);
+    }
+}
+template <int MODE> __device__ __forceinline__ void key_st(const KP& p, std::uint32_t v, KeyT<MODE> k) {
+    if constexpr (MODE == 0)
+        p.key_f[v] = k;
+    else if constexpr (MODE == 1)
+        p.key_i[v] = k;
+    else
+        p.key_w[v] = k;
+}
+// exact weight of edge e (its int2 record ed)
+template <int MODE> __device__ __forceinline__ long long edge_w(const KP& p, std::uint32_t e, int2 ed) {
+    if constexpr (MODE == 2)
+        return (static_cast<long long>(__ldg(&p.ew_hi[e])) << 32) | static_cast<unsigned>(ed.y);
+    else
+        return ed.y;
+}
+// exact weight of v's policy edge
+template <int MODE> __device__ __forceinline__ long long succ_w(const KP& p, std::uint32_t v) {
+    if constexpr (MODE == 2)
+        return (static_cast<long long>(p.succ_whi[v]) << 32) | static_cast<unsigned>(p.succ_wi[v]);
+    else
+        return p.succ_wi[v];
+}
+template <int MODE> __device__ __forceinline__ void succ_w_st(const KP& p, std::uint32_t v, long long w) {
+    p.succ_wi[v] = static_cast<int>(w);
+    if constexpr (MODE == 2)
+        p.succ_whi[v] = static_cast<int>(w >> 32);
+}
+// keys are proven to stay inside this bound at every adoption
+template <int MODE> __device__ __forceinline__ bool key_in_range(__int128 k) {
+    const __int128 lim = static_cast<__int128>(1) << (MODE == 2 ? 120 : 62);
+    return k < lim && k > -lim;
+}
+__device__ __forceinline__ long long shfl_key(unsigned m, long long x, int off, int w) {
+    return __shfl_xor_sync(m, x, off, w);
+}
+__device__ __forceinline__ double shfl_key(unsigned m, double x, int off, int w) {
+    return __shfl_xor_sync(m, x, off, w);
+}
+__device__ __forceinline__ __int128 shfl_key(unsigned m, __int128 x, int off, int w) {
+    const long long lo = __shfl_xor_sync(m, static_cast<long long>(static_cast<unsigned long long>(x)), off, w);
+    const long long hi = __shfl_xor_sync(m, static_cast<long long>(x >> 64), off, w);
+    return (static_cast<__int128>(hi) << 64) | static_cast<unsigned long long>(lo);
+}
+
 // ------------------------------------------------------------ improvement
 //
 // howard_par.hpp:146 spf_pass_iter / howard.hpp:63 improve_policy.
@@ -139,9 +218,10 @@ __device__ __forceinline__ FEdge ld_edge(const FEdge* e) {
 // every peer's replica (NVLink stores into peer memory; ordered before the
 // cross-rank barrier by a system-scope fence). Unchanged vertices are
 // already identical everywhere, so only changes travel.
-template <bool EXACT, class Edge>
+template <int MODE, class Edge>
 __device__ __forceinline__ void push_policy(const KP& p, std::uint32_t v, std::uint32_t e,
                                             std::uint32_t t, const Edge& ed) {
+    constexpr bool EXACT = MODE != 0;
     for (int q = 0; q < p.world; ++q) {
         if (q == p.rank)
             continue;
@@ -192,7 +272,7 @@ __device__ __forceinline__ bool hot_find(const KP& p, std::uint32_t t, long long
 // STAGED: the vertex's row offsets and edges were copied into shared memory
 // by the bulk-TMA producer of improve_staged (exact lane); sedge[i] holds
 // edge ebase + i, and b / e_end are the vertex's offsets read from there.
-template <bool EXACT, int G, int U, bool HOT, bool STAGED = false>
+template <int MODE, int G, int U, bool HOT, bool STAGED = false>
 __device__ __forceinline__ void improve_vertex(const KP& p, int* changed, ChangedMarks& marks,
                                                std::uint32_t v, const int2* sedge = nullptr,
                                                std::uint32_t ebase = 0, std::uint32_t sb = 0,
@@ -201,12 +281,11 @@ __device__ __forceinline__ void improve_vertex(const KP& p, int* changed, Change
     // they were loaded, the winner's head and weight are re-read (an L1 hit)
     // only when the policy changes, and the exact candidate drops the
     // per-vertex constant -num (compares are offset-invariant in integers).
+    constexpr bool EXACT = MODE != 0;
     const unsigned lane = threadIdx.x & (G - 1);
     const unsigned gm = group_mask<G>();
-    using Key = typename std::conditional<EXACT, long long, double>::type;
+    using Key = KeyT<MODE>;
     using Edge = typename std::conditional<EXACT, int2, FEdge>::type;
-    const Key* __restrict__ key = EXACT ? reinterpret_cast<const Key*>(p.key_i)
-                                        : reinterpret_cast<const Key*>(p.key_f);
     const Edge* __restrict__ edges = EXACT ? reinterpret_cast<const Edge*>(p.ew)
                                            : reinterpret_cast<const Edge*>(p.fe);
     // one non-trivial region (the common case): no per-vertex region
@@ -256,14 +335,14 @@ __device__ __forceinline__ void improve_vertex(const KP& p, int* changed, Change
                 t = static_cast<std::uint32_t>(ed[u].x);
             else
                 t = ed[u].t;
-            if constexpr (EXACT && HOT) {
+            if constexpr (MODE == 1 && HOT) {
                 long long hk;
                 if (hot_find(p, t, hk))
                     kk[u] = hk;
                 else
-                    kk[u] = __ldcg(&key[t]);
+                    kk[u] = key_gather<MODE>(p, t);
             } else {
-                kk[u] = __ldcg(&key[t]);
+                kk[u] = key_gather<MODE>(p, t);
             }
         }
 #pragma unroll
@@ -271,7 +350,9 @@ __device__ __forceinline__ void improve_vertex(const KP& p, int* changed, Change
             const std::uint32_t e = e0 + u * G;
             if (e < e_end) {
                 Key c;
-                if constexpr (EXACT)
+                if constexpr (MODE == 2)
+                    c = kk[u] + static_cast<Key>(edge_w<MODE>(p, e, ed[u])) * den; // + const -num
+                else if constexpr (EXACT)
                     c = kk[u] + static_cast<long long>(ed[u].y) * den; // + const -num
                 else
                     c = (kk[u] + ed[u].w) - lam; // FloatMode::extend (policy.hpp:105)
@@ -291,13 +372,13 @@ __device__ __forceinline__ void improve_vertex(const KP& p, int* changed, Change
     std::uint32_t gbe = be;
 #pragma unroll
     for (int off = G / 2; off > 0; off >>= 1) {
-        const Key ob = __shfl_xor_sync(gm, gbest, off, G);
+        const Key ob = shfl_key(gm, gbest, off, G);
         const std::uint32_t oe = __shfl_xor_sync(gm, gbe, off, G);
         if (oe != NONE && (gbe == NONE || ob < gbest || (ob == gbest && oe < gbe))) {
             gbest = ob;
             gbe = oe;
         }
-        const Key oc = __shfl_xor_sync(gm, curc, off, G);
+        const Key oc = shfl_key(gm, curc, off, G);
         const bool oh = __shfl_xor_sync(gm, have_cur ? 1 : 0, off, G) != 0;
         if (oh) {
             curc = oc;
@@ -325,14 +406,14 @@ __device__ __forceinline__ void improve_vertex(const KP& p, int* changed, Change
             std::uint32_t t;
             if constexpr (EXACT) {
                 t = static_cast<std::uint32_t>(ed.x);
-                p.succ_wi[v] = ed.y;
+                succ_w_st<MODE>(p, v, edge_w<MODE>(p, be, ed));
             } else {
                 t = ed.t;
                 p.succ_wf[v] = ed.w;
             }
             p.succ_v[v] = t;
             if (p.fused)
-                push_policy<EXACT>(p, v, be, t, ed);
+                push_policy<MODE>(p, v, be, t, ed);
             if (p.indeg_in_improve)
                 atomicAdd(&p.indeg[t], 1u);
             marks.note(p, changed, r);
@@ -351,11 +432,10 @@ __device__ __forceinline__ void improve_vertex(const KP& p, int* changed, Change
 // creation): one block per vertex, 256 threads striding its edges, then a
 // block-wide lexicographic (candidate, edge id) reduction -- the same
 // "first strictly smaller" result as the sequential scan.
-template <bool EXACT>
+template <int MODE>
 __device__ __forceinline__ void improve_heavy(const KP& p, int* changed) {
-    using Key = typename std::conditional<EXACT, long long, double>::type;
-    const Key* __restrict__ key = EXACT ? reinterpret_cast<const Key*>(p.key_i)
-                                        : reinterpret_cast<const Key*>(p.key_f);
+    constexpr bool EXACT = MODE != 0;
+    using Key = KeyT<MODE>;
     __shared__ Key s_best[kBlock / 32];
     __shared__ std::uint32_t s_be[kBlock / 32];
     __shared__ Key s_cur;
@@ -384,7 +464,7 @@ __device__ __forceinline__ void improve_heavy(const KP& p, int* changed) {
         for (std::uint32_t e0 = b + threadIdx.x; e0 < e_end; e0 += 4 * kBlock) {
             std::uint32_t tt[4];
             Key kk[4];
-            int wi[4];
+            long long wi[4];
             double wf[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
@@ -392,7 +472,7 @@ __device__ __forceinline__ void improve_heavy(const KP& p, int* changed) {
                 if constexpr (EXACT) {
                     const int2 ed = __ldg(&p.ew[e]);
                     tt[u] = static_cast<std::uint32_t>(ed.x);
-                    wi[u] = ed.y;
+                    wi[u] = edge_w<MODE>(p, e, ed);
                 } else {
                     const FEdge ed = ld_edge(&p.fe[e]);
                     tt[u] = ed.t;
@@ -401,14 +481,14 @@ __device__ __forceinline__ void improve_heavy(const KP& p, int* changed) {
             }
 #pragma unroll
             for (int u = 0; u < 4; ++u)
-                kk[u] = __ldcg(&key[tt[u]]);
+                kk[u] = key_gather<MODE>(p, tt[u]);
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 const std::uint32_t e = e0 + u * kBlock;
                 if (e < e_end) {
                     Key c;
                     if constexpr (EXACT)
-                        c = kk[u] + static_cast<long long>(wi[u]) * den - num;
+                        c = kk[u] + static_cast<Key>(wi[u]) * den - num;
                     else
                         c = (kk[u] + wf[u]) - lam;
                     if (be == NONE || c < best) { // ascending e per thread: first wins ties
@@ -424,7 +504,7 @@ __device__ __forceinline__ void improve_heavy(const KP& p, int* changed) {
         }
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) {
-            const Key ob = __shfl_xor_sync(FULL, best, off);
+            const Key ob = shfl_key(FULL, best, off, 32);
             const std::uint32_t oe = __shfl_xor_sync(FULL, be, off);
             if (oe != NONE && (be == NONE || ob < best || (ob == best && oe < be))) {
                 best = ob;
@@ -464,9 +544,9 @@ __device__ __forceinline__ void improve_heavy(const KP& p, int* changed) {
                     if constexpr (EXACT) {
                         const int2 ed = __ldg(&p.ew[ge]);
                         p.succ_v[v] = static_cast<std::uint32_t>(ed.x);
-                        p.succ_wi[v] = ed.y;
+                        succ_w_st<MODE>(p, v, edge_w<MODE>(p, ge, ed));
                         if (p.fused)
-                            push_policy<EXACT>(p, v, ge, static_cast<std::uint32_t>(ed.x), ed);
+                            push_policy<MODE>(p, v, ge, static_cast<std::uint32_t>(ed.x), ed);
                         if (p.indeg_in_improve)
                             atomicAdd(&p.indeg[ed.x], 1u);
                     } else {
@@ -474,7 +554,7 @@ __device__ __forceinline__ void improve_heavy(const KP& p, int* changed) {
                         p.succ_v[v] = ed.t;
                         p.succ_wf[v] = ed.w;
                         if (p.fused)
-                            push_policy<EXACT>(p, v, ge, ed.t, ed);
+                            push_policy<MODE>(p, v, ge, ed.t, ed);
                         if (p.indeg_in_improve)
                             atomicAdd(&p.indeg[ed.t], 1u);
                     }
@@ -729,11 +809,11 @@ __device__ __forceinline__ void improve_staged(const KP& p, int* changed, Change
             par[k] ^= 1;
             if (v < st.v1[k]) {
                 const std::uint32_t r0 = v - st.rbase[k];
-                improve_vertex<true, G, U, false, true>(p, changed, marks, v, st.edge[k], st.ebase[k],
+                improve_vertex<1, G, U, false, true>(p, changed, marks, v, st.edge[k], st.ebase[k],
                                                         st.row[k][r0], st.row[k][r0 + 1]);
             }
         } else if (v < st.v1[k]) {
-            improve_vertex<true, G, U, false>(p, changed, marks, v);
+            improve_vertex<1, G, U, false>(p, changed, marks, v);
         }
         __syncthreads(); // stage k is consumed before it is refilled
     }
@@ -743,10 +823,10 @@ __device__ __forceinline__ void improve_staged(const KP& p, int* changed, Change
     }
 }
 
-template <bool EXACT, int G, int U> __device__ __forceinline__ void improve_phase(const KP& p, int* changed) {
+template <int MODE, int G, int U> __device__ __forceinline__ void improve_phase(const KP& p, int* changed) {
     if (p.nheavy)
-        improve_heavy<EXACT>(p, changed);
-    if constexpr (EXACT) {
+        improve_heavy<MODE>(p, changed);
+    if constexpr (MODE == 1) {
         if (p.pb && !p.fused) {
             if (p.R == 1 && !p.active[0])
                 return;
@@ -759,7 +839,7 @@ template <bool EXACT, int G, int U> __device__ __forceinline__ void improve_phas
     ChangedMarks marks;
     if (p.R == 1 && !p.active[0])
         return; // the single region finished (block-uniform: no flush needed)
-    if constexpr (EXACT) {
+    if constexpr (MODE == 1) {
         if (p.staged) {
             improve_staged<G, U>(p, changed, marks);
             marks.flush(p, changed);
@@ -767,7 +847,7 @@ template <bool EXACT, int G, int U> __device__ __forceinline__ void improve_phas
         }
     }
     bool hot = false;
-    if constexpr (EXACT) {
+    if constexpr (MODE == 1) {
         if (p.nhot) {
             const unsigned slots = 1u << (32 - p.hot_shift);
             long long* hk = hot_keys();
@@ -794,10 +874,10 @@ template <bool EXACT, int G, int U> __device__ __forceinline__ void improve_phas
     const std::size_t gs = gstride() / G;
     if (hot) {
         for (std::size_t vv = p.own_lo + gtid() / G; vv < p.own_hi; vv += gs)
-            improve_vertex<EXACT, G, U, true>(p, changed, marks, static_cast<std::uint32_t>(vv));
+            improve_vertex<MODE, G, U, true>(p, changed, marks, static_cast<std::uint32_t>(vv));
     } else {
         for (std::size_t vv = p.own_lo + gtid() / G; vv < p.own_hi; vv += gs)
-            improve_vertex<EXACT, G, U, false>(p, changed, marks, static_cast<std::uint32_t>(vv));
+            improve_vertex<MODE, G, U, false>(p, changed, marks, static_cast<std::uint32_t>(vv));
     }
     marks.flush(p, changed);
 }
@@ -858,13 +938,9 @@ __device__ __forceinline__ long long gcd_ll(long long a, long long b) {
     return x;
 }
 
-__device__ __forceinline__ bool key_in_range(__int128 k) {
-    const __int128 lim = static_cast<__int128>(1) << 62;
-    return k < lim && k > -lim;
-}
-
-template <bool EXACT>
+template <int MODE>
 __device__ __forceinline__ bool rec_less(const KP& p, std::uint32_t a, std::uint32_t b) {
+    constexpr bool EXACT = MODE != 0;
     if constexpr (EXACT) {
         const __int128 l = static_cast<__int128>(ldv(p.cyc_wi[a])) * ldv(p.cyc_len[b]);
         const __int128 r = static_cast<__int128>(ldv(p.cyc_wi[b])) * ldv(p.cyc_len[a]);
@@ -894,15 +970,12 @@ __device__ __forceinline__ int ceil_log2_d(unsigned long long x) {
     for (std::uint64_t i##_b = (lo) + blockIdx.x * std::uint64_t(kBlock); i##_b < (hi);          \
          i##_b += gridDim.x * std::uint64_t(kBlock))
 
-__device__ __forceinline__ void ph_init(const KP& p, bool exact) {
+template <int MODE> __device__ __forceinline__ void ph_init(const KP& p) {
     const std::size_t tid = gtid(), nth = gstride();
     for (std::size_t v = tid; v < p.N; v += nth) {
         p.succ_e[v] = NONE;
         p.succ_v[v] = NONE;
-        if (exact)
-            p.key_i[v] = 0;
-        else
-            p.key_f[v] = 0.0;
+        key_st<MODE>(p, static_cast<std::uint32_t>(v), KeyT<MODE>(0));
         p.indeg[v] = 0;
     }
     for (std::size_t r = tid; r <= p.R; r += nth) { // slot R: trivial vertices
@@ -924,9 +997,10 @@ __device__ __forceinline__ void ph_init(const KP& p, bool exact) {
 // successor of anyone) and the core, whose first doubling round is done
 // here. A vertex still works iff its region changed in this pass (changed is
 // only ever raised for active regions).
-template <bool EXACT>
+template <int MODE>
 __device__ __forceinline__ void ph_classify(const KP& p, int par, const Ring& ra, const Ring& rl,
                                             const Ring& rc) {
+    constexpr bool EXACT = MODE != 0;
     const int* changed = p.changed[par];
     unsigned still = 0;
     for (std::size_t r = gtid(); r < p.R; r += gstride()) {
@@ -974,7 +1048,7 @@ __device__ __forceinline__ void ph_classify(const KP& p, int par, const Ring& ra
                 PJC x;
                 x.nxt = p.succ_v[sv];
                 x.mn = min(v, sv);
-                x.w = EXACT ? static_cast<long long>(p.succ_wi[v]) + p.succ_wi[sv] : 0ll;
+                x.w = EXACT ? succ_w<MODE>(p, v) + succ_w<MODE>(p, sv) : 0ll;
                 p.pj[1][v] = x;
             }
         }
@@ -1107,9 +1181,10 @@ __device__ __forceinline__ void ph_round_mark(const KP& p, std::uint64_t nC, int
 
 // Over the listed M only: (B) and |succ(M)|, and -- speculatively, exact
 // lane -- the per-anchor (length, weight) records (howard_par.hpp:319).
-template <bool EXACT>
+template <int MODE>
 __device__ __forceinline__ void ph_check(const KP& p, std::uint64_t nM, std::uint32_t stamp,
                                          unsigned* flag, const Ring& rs) {
+    constexpr bool EXACT = MODE != 0;
     bool fail = false;
     unsigned fresh = 0;
     const unsigned lane = threadIdx.x & 31;
@@ -1133,7 +1208,7 @@ __device__ __forceinline__ void ph_check(const KP& p, std::uint64_t nM, std::uin
             const int lead = __ffs(am) - 1;
             const std::uint32_t a0 = __shfl_sync(FULL, a, lead);
             const bool uni = __all_sync(FULL, !on || a == a0);
-            long long w = on ? static_cast<long long>(p.succ_wi[v]) : 0ll;
+            long long w = on ? succ_w<MODE>(p, v) : 0ll;
             if (uni) {
 #pragma unroll
                 for (int off = 16; off > 0; off >>= 1)
@@ -1175,7 +1250,8 @@ __device__ __forceinline__ void ph_stats_float(const KP& p, std::uint64_t nM) {
 }
 
 // Adoption (howard_par.hpp:349-364) of region r's winning record.
-template <bool EXACT> __device__ __forceinline__ unsigned adopt_region(const KP& p, std::uint32_t r) {
+template <int MODE> __device__ __forceinline__ unsigned adopt_region(const KP& p, std::uint32_t r) {
+    constexpr bool EXACT = MODE != 0;
     Ctl* c = p.c;
     const unsigned long long a = p.slot[r];
     p.slot[r] = EMPTY;
@@ -1197,8 +1273,12 @@ template <bool EXACT> __device__ __forceinline__ unsigned adopt_region(const KP&
             c->lambda_up = 1;
         p.lam_num[r] = num;
         p.lam_den[r] = den;
+        // every key |K| <= max_region * (max|w|*den + |num|) stays inside
+        // the lane's bound (else: the fast lane reports it, and the session
+        // re-solves in the wide lane)
         const __int128 step = static_cast<__int128>(p.max_abs_w) * den + (num < 0 ? -num : num);
-        if (static_cast<__int128>(p.max_region) * step >= (static_cast<__int128>(1) << 62))
+        if (static_cast<__int128>(p.max_region) * step >=
+            (static_cast<__int128>(1) << (MODE == 2 ? 120 : 62)))
             c->overflow = 1;
     } else {
         p.lam_f[r] = p.cyc_wf[a] / len;
@@ -1209,29 +1289,40 @@ template <bool EXACT> __device__ __forceinline__ unsigned adopt_region(const KP&
 
 // Winning-cycle values: prefix sums of w*den - num along the cycle, cut at
 // the anchor (value(anchor) = 0), by pointer jumping over those vertices.
-__device__ __forceinline__ void wc_init_one(const KP& p, std::uint32_t v, std::uint32_t r) {
-    PJV x;
+template <int MODE> struct PvOf { using T = PJV; };
+template <> struct PvOf<2> { using T = PJVW; };
+template <int MODE> __device__ __forceinline__ typename PvOf<MODE>::T* pv_buf(const KP& p, int j) {
+    if constexpr (MODE == 2)
+        return p.pvw[j];
+    else
+        return p.pv[j];
+}
+
+template <int MODE> __device__ __forceinline__ void wc_init_one(const KP& p, std::uint32_t v, std::uint32_t r) {
+    typename PvOf<MODE>::T x;
     const std::uint32_t root = p.src[r];
     if (v == root) {
         x.acc = 0;
         x.nxt = root;
     } else {
-        x.acc = static_cast<long long>(p.succ_wi[v]) * p.lam_den[r] - p.lam_num[r];
+        x.acc = static_cast<KeyT<MODE>>(succ_w<MODE>(p, v)) * p.lam_den[r] - p.lam_num[r];
         x.nxt = p.succ_v[v];
     }
     x.root = root;
-    p.pv[0][v] = x;
+    pv_buf<MODE>(p, 0)[v] = x;
 }
 
+template <int MODE>
 __device__ __forceinline__ void wc_round(const KP& p, const std::uint32_t* list, std::uint64_t nW, int j,
                                          std::uint64_t from, std::uint64_t step) {
-    const PJV* __restrict__ a = p.pv[j & 1];
-    PJV* __restrict__ o = p.pv[(j & 1) ^ 1];
+    using PV = typename PvOf<MODE>::T;
+    const PV* __restrict__ a = pv_buf<MODE>(p, j & 1);
+    PV* __restrict__ o = pv_buf<MODE>(p, (j & 1) ^ 1);
     for (std::uint64_t i = from; i < nW; i += step) {
         const std::uint32_t v = list[i];
-        const PJV x = a[v];
-        const PJV y = a[x.nxt];
-        PJV z;
+        const PV x = a[v];
+        const PV y = a[x.nxt];
+        PV z;
         z.acc = x.acc + y.acc;
         z.nxt = y.nxt;
         z.root = x.root;
@@ -1239,12 +1330,13 @@ __device__ __forceinline__ void wc_round(const KP& p, const std::uint32_t* list,
     }
 }
 
+template <int MODE>
 __device__ __forceinline__ void wc_final(const KP& p, const std::uint32_t* list, std::uint64_t nW, int wr,
                                          std::uint64_t from, std::uint64_t step) {
-    const PJV* fin = p.pv[wr & 1];
+    const typename PvOf<MODE>::T* fin = pv_buf<MODE>(p, wr & 1);
     for (std::uint64_t i = from; i < nW; i += step) {
         const std::uint32_t v = list[i];
-        p.key_i[v] = fin[v].acc;
+        key_st<MODE>(p, v, fin[v].acc);
     }
 }
 
@@ -1259,12 +1351,19 @@ constexpr unsigned kSmemCycle = 128; // 512 measured 2% slower: its 20 KB of sta
 __shared__ std::uint32_t wc_key[2 * kSmemCycle], wc_val[2 * kSmemCycle];
 __shared__ std::uint32_t wc_nxt[2][kSmemCycle];
 __shared__ long long wc_acc[2][kSmemCycle];
+__shared__ __int128 wc_acc_w[2][kSmemCycle]; // wide lane only
+template <int MODE> __device__ __forceinline__ auto& wc_acc_of() {
+    if constexpr (MODE == 2)
+        return wc_acc_w;
+    else
+        return wc_acc;
+}
 
-__device__ __forceinline__ void wincyc_shared(const KP& p, unsigned nW, int wr) {
+template <int MODE> __device__ __forceinline__ void wincyc_shared(const KP& p, unsigned nW, int wr) {
     auto& s_key = wc_key;
     auto& s_val = wc_val;
     auto& s_nxt = wc_nxt;
-    auto& s_acc = wc_acc;
+    auto& s_acc = wc_acc_of<MODE>();
     constexpr unsigned kMask = 2 * kSmemCycle - 1;
     for (unsigned i = threadIdx.x; i < 2 * kSmemCycle; i += blockDim.x)
         s_key[i] = NONE;
@@ -1284,7 +1383,7 @@ __device__ __forceinline__ void wincyc_shared(const KP& p, unsigned nW, int wr) 
             s_acc[0][i] = 0;
             s_nxt[0][i] = i;
         } else {
-            s_acc[0][i] = static_cast<long long>(p.succ_wi[v]) * p.lam_den[r] - p.lam_num[r];
+            s_acc[0][i] = static_cast<KeyT<MODE>>(succ_w<MODE>(p, v)) * p.lam_den[r] - p.lam_num[r];
             const std::uint32_t sv = p.succ_v[v];
             unsigned h = (sv * 2654435761u) & kMask;
             while (s_key[h] != sv)
@@ -1303,7 +1402,7 @@ __device__ __forceinline__ void wincyc_shared(const KP& p, unsigned nW, int wr) 
         __syncthreads();
     }
     for (unsigned i = threadIdx.x; i < nW; i += blockDim.x)
-        p.key_i[p.rem[1][i]] = s_acc[wr & 1][i];
+        key_st<MODE>(p, p.rem[1][i], s_acc[wr & 1][i]);
 }
 
 // Region-specific minimum voting (howard_par.hpp:56 vote_min; paper
@@ -1312,8 +1411,9 @@ __device__ __forceinline__ void wincyc_shared(const KP& p, unsigned nW, int wr) 
 // finish voting adopts every region's winner and, when the winning cycles
 // are small, computes their values itself (block barriers only); otherwise
 // it raises wc_big and the grid does it after the barrier.
-template <bool EXACT>
+template <int MODE>
 __device__ __forceinline__ void vote_pass(const KP& p, std::uint64_t nM, std::uint64_t from, std::uint64_t step) {
+    constexpr bool EXACT = MODE != 0;
     for (std::uint64_t i = from; i < nM; i += step) {
         const std::uint32_t v = p.wlist[i];
         if (p.comp[v] != v)
@@ -1321,7 +1421,7 @@ __device__ __forceinline__ void vote_pass(const KP& p, std::uint64_t nM, std::ui
         unsigned long long* cell = &p.slot[__ldg(&p.reg[v])];
         unsigned long long cur = ldv(*cell);
         for (;;) {
-            if (cur != EMPTY && !rec_less<EXACT>(p, v, static_cast<std::uint32_t>(cur)))
+            if (cur != EMPTY && !rec_less<MODE>(p, v, static_cast<std::uint32_t>(cur)))
                 break;
             const unsigned long long prev = atomicCAS(cell, cur, v);
             if (prev == cur)
@@ -1333,16 +1433,17 @@ __device__ __forceinline__ void vote_pass(const KP& p, std::uint64_t nM, std::ui
 
 // Adoption and the winning cycles' values by one block (s_maxlen, s_nw
 // zeroed by the caller before its last barrier).
-template <bool EXACT>
+template <int MODE>
 __device__ __forceinline__ void winning_cycle_tail(const KP& p, unsigned nW, unsigned maxlen,
                                                    std::uint32_t stamp);
 
-template <bool EXACT>
+template <int MODE>
 __device__ __forceinline__ void vote_tail(const KP& p, std::uint64_t nM, std::uint32_t stamp,
                                           unsigned& s_maxlen, unsigned& s_nw) {
+    constexpr bool EXACT = MODE != 0;
     for (std::uint32_t r = threadIdx.x; r < p.R; r += blockDim.x)
         if (p.active[r]) {
-            const unsigned len = adopt_region<EXACT>(p, r);
+            const unsigned len = adopt_region<MODE>(p, r);
             atomicMax(&s_maxlen, len);
         }
     if constexpr (!EXACT)
@@ -1356,22 +1457,23 @@ __device__ __forceinline__ void vote_tail(const KP& p, std::uint64_t nM, std::ui
             p.rem[1][atomicAdd(&s_nw, 1u)] = v;
     }
     __syncthreads();
-    winning_cycle_tail<EXACT>(p, s_nw, s_maxlen, stamp);
+    winning_cycle_tail<MODE>(p, s_nw, s_maxlen, stamp);
 }
 
 // The winning cycles' values (nW vertices listed in rem[1], longest maxlen).
-template <bool EXACT>
+template <int MODE>
 __device__ __forceinline__ void winning_cycle_tail(const KP& p, unsigned nW, unsigned maxlen,
                                                    std::uint32_t stamp) {
+    constexpr bool EXACT = MODE != 0;
     Ctl* c = p.c;
     const int wr = ceil_log2_d(maxlen > 1 ? maxlen - 1 : 1); // farthest: len-1 steps
     if (nW <= kSmemCycle) {
-        wincyc_shared(p, nW, wr);
+        wincyc_shared<MODE>(p, nW, wr);
         return;
     }
     for (std::uint64_t i = threadIdx.x; i < nW; i += blockDim.x) {
         const std::uint32_t v = p.rem[1][i];
-        wc_init_one(p, v, p.R == 1 ? 0u : __ldg(&p.reg[v]));
+        wc_init_one<MODE>(p, v, p.R == 1 ? 0u : __ldg(&p.reg[v]));
     }
     c->wc_n[stamp & 1] = (static_cast<unsigned long long>(stamp) << 32) | nW;
     c->wc_len[stamp & 1] = maxlen;
@@ -1382,18 +1484,19 @@ __device__ __forceinline__ void winning_cycle_tail(const KP& p, unsigned nW, uns
     }
     __syncthreads();
     for (int j = 0; j < wr; ++j) {
-        wc_round(p, p.rem[1], nW, j, threadIdx.x, blockDim.x);
+        wc_round<MODE>(p, p.rem[1], nW, j, threadIdx.x, blockDim.x);
         __syncthreads();
     }
-    wc_final(p, p.rem[1], nW, wr, threadIdx.x, blockDim.x);
+    wc_final<MODE>(p, p.rem[1], nW, wr, threadIdx.x, blockDim.x);
 }
 
 
-template <bool EXACT>
+template <int MODE>
 __device__ __forceinline__ void ph_vote(const KP& p, std::uint64_t nM, std::uint32_t stamp,
                                         unsigned long long done_base) {
+    constexpr bool EXACT = MODE != 0;
     Ctl* c = p.c;
-    vote_pass<EXACT>(p, nM, gtid(), gstride());
+    vote_pass<MODE>(p, nM, gtid(), gstride());
     __shared__ int s_last;
     __shared__ unsigned s_maxlen, s_nw;
     __syncthreads();
@@ -1407,7 +1510,7 @@ __device__ __forceinline__ void ph_vote(const KP& p, std::uint64_t nM, std::uint
     }
     __syncthreads();
     if (s_last)
-        vote_tail<EXACT>(p, nM, stamp, s_maxlen, s_nw);
+        vote_tail<MODE>(p, nM, stamp, s_maxlen, s_nw);
 }
 
 // The common case in full (exact lane, one region, |M| <= one block, a
@@ -1415,25 +1518,26 @@ __device__ __forceinline__ void ph_vote(const KP& p, std::uint64_t nM, std::uint
 // M[i], its anchor, successor and weight in registers from the vote to the
 // values, so adoption, the winning-cycle listing and its prefix sums add no
 // global round trips beyond the adoption's own.
-template <bool EXACT>
+template <int MODE>
 __device__ __forceinline__ bool vote_small(const KP& p, unsigned nM, std::uint32_t stamp,
                                            unsigned* vflag = nullptr) {
+    constexpr bool EXACT = MODE != 0;
     auto& s_key = wc_key;
     auto& s_val = wc_val;
     auto& s_nxt = wc_nxt;
-    auto& s_acc = wc_acc;
+    auto& s_acc = wc_acc_of<MODE>();
     __shared__ unsigned s_wcnt[kBlock / 32], s_nw;
     __shared__ std::uint32_t s_src;
     __shared__ unsigned s_len;
     constexpr unsigned kMask = 2 * kSmemCycle - 1;
     const unsigned i = threadIdx.x, lane = i & 31, warp = i >> 5;
     std::uint32_t v = NONE, an = NONE, sv = 0;
-    int w = 0;
+    long long w = 0;
     if (i < nM) {
         v = p.wlist[i];
         an = p.comp[v];
         sv = p.succ_v[v];
-        w = p.succ_wi[v];
+        w = succ_w<MODE>(p, v);
     }
     if (vflag) {
         // the check phase's work for these few vertices (ph_check): (B)
@@ -1462,7 +1566,7 @@ __device__ __forceinline__ bool vote_small(const KP& p, unsigned nM, std::uint32
         unsigned long long* cell = &p.slot[0];
         unsigned long long cur = ldv(*cell);
         for (;;) {
-            if (cur != EMPTY && !rec_less<EXACT>(p, v, static_cast<std::uint32_t>(cur)))
+            if (cur != EMPTY && !rec_less<MODE>(p, v, static_cast<std::uint32_t>(cur)))
                 break;
             const unsigned long long prev = atomicCAS(cell, cur, v);
             if (prev == cur)
@@ -1475,7 +1579,7 @@ __device__ __forceinline__ bool vote_small(const KP& p, unsigned nM, std::uint32
     __threadfence(); // the slot CASes, before adoption reads the slot
     __syncthreads();
     if (i == 0) {
-        s_len = p.active[0] ? adopt_region<EXACT>(p, 0) : 0u;
+        s_len = p.active[0] ? adopt_region<MODE>(p, 0) : 0u;
         s_src = p.src[0];
     }
     __syncthreads();
@@ -1511,7 +1615,7 @@ __device__ __forceinline__ bool vote_small(const KP& p, unsigned nM, std::uint32
             s_acc[0][idx] = 0;
             s_nxt[0][idx] = idx;
         } else {
-            s_acc[0][idx] = static_cast<long long>(w) * p.lam_den[0] - p.lam_num[0];
+            s_acc[0][idx] = static_cast<KeyT<MODE>>(w) * p.lam_den[0] - p.lam_num[0];
             unsigned h = (sv * 2654435761u) & kMask;
             while (s_key[h] != sv)
                 h = (h + 1) & kMask;
@@ -1531,7 +1635,7 @@ __device__ __forceinline__ bool vote_small(const KP& p, unsigned nM, std::uint32
         __syncthreads();
     }
     if (win)
-        p.key_i[v] = s_acc[wr & 1][idx];
+        key_st<MODE>(p, v, s_acc[wr & 1][idx]);
     (void)stamp;
     return true;
 }
@@ -1543,12 +1647,13 @@ __device__ __forceinline__ bool vote_small(const KP& p, unsigned nM, std::uint32
 // vote itself).
 constexpr std::uint64_t kVoteOneBlock = 4096;
 
-template <bool EXACT>
+template <int MODE>
 __device__ __forceinline__ void ph_vote_one_block(const KP& p, std::uint64_t nM, std::uint32_t stamp,
                                                   unsigned* vflag = nullptr) {
+    constexpr bool EXACT = MODE != 0;
     __shared__ unsigned s_maxlen, s_nw;
     if (EXACT && p.R == 1 && nM <= blockDim.x) {
-        if (vote_small<EXACT>(p, static_cast<unsigned>(nM), stamp, vflag))
+        if (vote_small<MODE>(p, static_cast<unsigned>(nM), stamp, vflag))
             return;
         // a winning cycle too long for shared memory: list it and take the
         // general path (adoption is already done)
@@ -1562,17 +1667,17 @@ __device__ __forceinline__ void ph_vote_one_block(const KP& p, std::uint64_t nM,
                 p.rem[1][atomicAdd(&s_nw, 1u)] = v;
         }
         __syncthreads();
-        winning_cycle_tail<EXACT>(p, s_nw, ldv(p.cyc_len[p.src[0]]), stamp);
+        winning_cycle_tail<MODE>(p, s_nw, ldv(p.cyc_len[p.src[0]]), stamp);
         return;
     }
-    vote_pass<EXACT>(p, nM, threadIdx.x, blockDim.x);
+    vote_pass<MODE>(p, nM, threadIdx.x, blockDim.x);
     __threadfence(); // the block's slot CASes, before adoption reads the slots
     if (threadIdx.x == 0) {
         s_maxlen = 0;
         s_nw = 0;
     }
     __syncthreads();
-    vote_tail<EXACT>(p, nM, stamp, s_maxlen, s_nw);
+    vote_tail<MODE>(p, nM, stamp, s_maxlen, s_nw);
 }
 
 // Kept component (howard_par.hpp:370/393): vertices whose policy path
@@ -1583,20 +1688,22 @@ __device__ __forceinline__ void ph_vote_one_block(const KP& p, std::uint64_t nM,
 // exactly 0, so extra turns add nothing); a leaf takes K(succ) + w*den - num,
 // recomputing its core successor's key the same way (never reading a key
 // being written in this phase). Resets the in-degree of core vertices.
-__device__ __forceinline__ long long core_key(const KP& p, const PJC* a, std::uint32_t v, std::uint32_t r,
-                                              std::uint32_t stamp, unsigned long long L, bool& ovf) {
+template <int MODE>
+__device__ __forceinline__ KeyT<MODE> core_key(const KP& p, const PJC* a, std::uint32_t v, std::uint32_t r,
+                                               std::uint32_t stamp, unsigned long long L, bool& ovf) {
     if (p.cmark[v] == stamp) // on the winning cycle: from the cycle prefix sums
-        return p.key_i[v];
+        return key_ld<MODE>(p, v);
     const PJC x = a[v];
     const __int128 kk = static_cast<__int128>(x.w) * p.lam_den[r] -
-                        static_cast<__int128>(L) * p.lam_num[r] + p.key_i[x.nxt];
-    ovf |= !key_in_range(kk);
-    return static_cast<long long>(kk);
+                        static_cast<__int128>(L) * p.lam_num[r] + key_ld<MODE>(p, x.nxt);
+    ovf |= !key_in_range<MODE>(kk);
+    return static_cast<KeyT<MODE>>(kk);
 }
 
-template <bool EXACT>
+template <int MODE>
 __device__ __forceinline__ void ph_keep(const KP& p, std::uint64_t nC, std::uint64_t nL, int in,
                                         std::uint32_t stamp, unsigned long long L, const Ring& ring) {
+    constexpr bool EXACT = MODE != 0;
     const PJC* a = p.pj[in];
     bool ovf = false;
     const std::uint64_t tot = nC + nL;
@@ -1611,8 +1718,9 @@ __device__ __forceinline__ void ph_keep(const KP& p, std::uint64_t nC, std::uint
             p.conn[v] = kept ? 0u : NONE;
             p.indeg[v] = 0;
             take = !kept;
-            if (EXACT && kept && p.cmark[v] != stamp)
-                p.key_i[v] = core_key(p, a, v, r, stamp, L, ovf);
+            if constexpr (EXACT)
+                if (kept && p.cmark[v] != stamp)
+                    key_st<MODE>(p, v, core_key<MODE>(p, a, v, r, stamp, L, ovf));
         } else if (i < tot) {
             v = p.plist[i - nC];
             const std::uint32_t s = p.succ_v[v];
@@ -1622,12 +1730,14 @@ __device__ __forceinline__ void ph_keep(const KP& p, std::uint64_t nC, std::uint
             p.comp[v] = an;
             p.conn[v] = kept ? 0u : NONE;
             take = !kept;
-            if (EXACT && kept) {
-                const __int128 kk = static_cast<__int128>(core_key(p, a, s, r, stamp, L, ovf)) +
-                                    static_cast<__int128>(p.succ_wi[v]) * p.lam_den[r] - p.lam_num[r];
-                ovf |= !key_in_range(kk);
-                p.key_i[v] = static_cast<long long>(kk);
-            }
+            if constexpr (EXACT)
+                if (kept) {
+                    const __int128 kk = static_cast<__int128>(core_key<MODE>(p, a, s, r, stamp, L, ovf)) +
+                                        static_cast<__int128>(succ_w<MODE>(p, v)) * p.lam_den[r] -
+                                        p.lam_num[r];
+                    ovf |= !key_in_range<MODE>(kk);
+                    key_st<MODE>(p, v, static_cast<KeyT<MODE>>(kk));
+                }
         }
         const std::uint64_t slot = block_append(take, ring);
         if (take)
@@ -1640,9 +1750,10 @@ __device__ __forceinline__ void ph_keep(const KP& p, std::uint64_t nC, std::uint
 // attaches through its smallest out-edge whose head was connected in an
 // earlier layer (conn < layer); the stamps make the layer discipline exact
 // under any schedule.
-template <bool EXACT>
+template <int MODE>
 __device__ __forceinline__ void ph_attach(const KP& p, int cur, std::uint64_t pending, std::uint32_t layer,
                                           const Ring& ring) {
+    constexpr bool EXACT = MODE != 0;
     const std::uint32_t* list = p.rem[cur];
     bool ovf = false;
     OCM_BLOCK_LOOP(i0, 0, pending) {
@@ -1675,13 +1786,13 @@ __device__ __forceinline__ void ph_attach(const KP& p, int cur, std::uint64_t pe
                     p.succ_e[x] = e;
                     p.succ_v[x] = t;
                     if constexpr (EXACT) {
-                        const int w = __ldg(&p.ew[e]).y;
-                        p.succ_wi[x] = w;
+                        const long long w = edge_w<MODE>(p, e, __ldg(&p.ew[e]));
+                        succ_w_st<MODE>(p, x, w);
                         const std::uint32_t r = __ldg(&p.reg[x]);
-                        const __int128 kk = static_cast<__int128>(p.key_i[t]) +
+                        const __int128 kk = static_cast<__int128>(key_ld<MODE>(p, t)) +
                                             static_cast<__int128>(w) * p.lam_den[r] - p.lam_num[r];
-                        ovf |= !key_in_range(kk);
-                        p.key_i[x] = static_cast<long long>(kk);
+                        ovf |= !key_in_range<MODE>(kk);
+                        key_st<MODE>(p, x, static_cast<KeyT<MODE>>(kk));
                     } else {
                         p.succ_wf[x] = p.fe[e].w;
                     }
@@ -1844,8 +1955,9 @@ struct LoopState {
 // carries only its own improvement variant, so ptxas allocates registers for
 // that one (a kernel holding all variants spilled inside the pass's loop).
 // G in {1, 2, 4, 8}: degrees above 128*G take the block-cooperative path.
-template <bool EXACT, int G>
+template <int MODE, int G>
 __global__ void __launch_bounds__(kBlock, kSolveMinBlocks) k_solve(KP p, int mode) {
+    constexpr bool EXACT = MODE != 0;
     cg::grid_group grid = cg::this_grid();
     Ctl* const c = p.c;
     __shared__ LoopState s_park;
@@ -1863,7 +1975,7 @@ __global__ void __launch_bounds__(kBlock, kSolveMinBlocks) k_solve(KP p, int mod
     __shared__ long long s_clk[PH_COUNT];
     if (threadIdx.x < PH_COUNT)
         s_clk[threadIdx.x] = 0;
-    if (EXACT && p.staged)
+    if (MODE == 1 && p.staged)
         staged_init(*reinterpret_cast<Staged*>(dyn_smem));
     auto sync = [&](int ph) {
         grid.sync();
@@ -1921,7 +2033,7 @@ __global__ void __launch_bounds__(kBlock, kSolveMinBlocks) k_solve(KP p, int mod
     bool paused = false; // uniform: sharded launch ends at its exchange point
 
     if (mode != kShardResume) {
-        ph_init(p, EXACT);
+        ph_init<MODE>(p);
         sync(PH_INIT);
     }
     bool skip_improve = mode == kShardResume;
@@ -1948,7 +2060,7 @@ __global__ void __launch_bounds__(kBlock, kSolveMinBlocks) k_solve(KP p, int mod
                 s_park = st;
             __syncthreads();
             asm volatile("" ::: "memory");
-            improve_phase<EXACT, G, 4>(p, p.changed[s_park.it & 1]);
+            improve_phase<MODE, G, 4>(p, p.changed[s_park.it & 1]);
             asm volatile("" ::: "memory");
             st = s_park;
             ++st.passes;
@@ -1975,7 +2087,7 @@ __global__ void __launch_bounds__(kBlock, kSolveMinBlocks) k_solve(KP p, int mod
                     atomicAdd(&p.indeg[p.succ_v[v]], 1u);
             sync(PH_CLASSIFY);
         }
-        ph_classify<EXACT>(p, par, st.ra, st.rl, st.rc);
+        ph_classify<MODE>(p, par, st.ra, st.rl, st.rc);
         sync(PH_CLASSIFY);
         const std::uint64_t n_active = st.ra.take();
         const std::uint64_t nL = st.rl.take();
@@ -2026,14 +2138,14 @@ __global__ void __launch_bounds__(kBlock, kSolveMinBlocks) k_solve(KP p, int mod
                 // check passes, votes, adopts and values the winning cycle
                 // in the same phase
                 if (blockIdx.x == 0)
-                    ph_vote_one_block<EXACT>(p, nM, stamp, vflag);
+                    ph_vote_one_block<MODE>(p, nM, stamp, vflag);
                 sync(PH_VERIFY);
                 if (ldr(*vflag) != stamp) {
                     voted = true;
                     break;
                 }
             } else {
-                ph_check<EXACT>(p, nM, stamp, vflag, st.rc);
+                ph_check<MODE>(p, nM, stamp, vflag, st.rc);
                 sync(PH_VERIFY);
                 const std::uint64_t s_size = st.rc.take();
                 if (ldr(*vflag) != stamp && s_size == nM)
@@ -2068,9 +2180,9 @@ __global__ void __launch_bounds__(kBlock, kSolveMinBlocks) k_solve(KP p, int mod
             }
             if (nM <= kVoteOneBlock) {
                 if (blockIdx.x == 0)
-                    ph_vote_one_block<EXACT>(p, nM, stamp);
+                    ph_vote_one_block<MODE>(p, nM, stamp);
             } else {
-                ph_vote<EXACT>(p, nM, stamp, st.done_base);
+                ph_vote<MODE>(p, nM, stamp, st.done_base);
                 st.done_base += gridDim.x;
             }
             sync(PH_VOTE);
@@ -2080,20 +2192,20 @@ __global__ void __launch_bounds__(kBlock, kSolveMinBlocks) k_solve(KP p, int mod
             const unsigned maxlen = ldr(c->wc_len[stamp & 1]);
             const int wr = ceil_log2_d(maxlen > 1 ? maxlen - 1 : 1);
             for (int j = 0; j < wr; ++j) {
-                wc_round(p, p.rem[1], nW, j, gtid(), gstride());
+                wc_round<MODE>(p, p.rem[1], nW, j, gtid(), gstride());
                 sync(PH_WINCYC);
             }
-            wc_final(p, p.rem[1], nW, wr, gtid(), gstride());
+            wc_final<MODE>(p, p.rem[1], nW, wr, gtid(), gstride());
             sync(PH_WINCYC);
         }
 
         // ---- kept component (core, then leaves), re-attachment
-        ph_keep<EXACT>(p, nC, nL, in, stamp, 1ull << k, st.rl);
+        ph_keep<MODE>(p, nC, nL, in, stamp, 1ull << k, st.rl);
         sync(PH_KEEP);
         std::uint64_t pending = st.rl.take();
         int cur = 0;
         for (std::uint32_t layer = 1; pending > 0; ++layer) {
-            ph_attach<EXACT>(p, cur, pending, layer, st.rl);
+            ph_attach<MODE>(p, cur, pending, layer, st.rl);
             sync(PH_ATTACH);
             const std::uint64_t next = st.rl.take();
             ++st.layers;

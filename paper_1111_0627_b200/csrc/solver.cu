@@ -40,19 +40,22 @@ int env_int(const char* name, int dflt) {
 // cooperative occupancy of k_solve cost milliseconds per query).
 constexpr int kGs[4] = {1, 2, 4, 8};
 
-// k_solve instantiation for (exact lane, group width index 0..3)
-const void* solve_fn(bool exact, int gi) {
-    static const void* fns[2][4] = {
-        {reinterpret_cast<const void*>(&k_solve<false, 1>), reinterpret_cast<const void*>(&k_solve<false, 2>),
-         reinterpret_cast<const void*>(&k_solve<false, 4>), reinterpret_cast<const void*>(&k_solve<false, 8>)},
-        {reinterpret_cast<const void*>(&k_solve<true, 1>), reinterpret_cast<const void*>(&k_solve<true, 2>),
-         reinterpret_cast<const void*>(&k_solve<true, 4>), reinterpret_cast<const void*>(&k_solve<true, 8>)}};
-    return fns[exact ? 1 : 0][gi];
+// k_solve instantiation for (mode: 0 float, 1 exact, 2 wide exact; group
+// width index 0..3)
+const void* solve_fn(int mode, int gi) {
+    static const void* fns[3][4] = {
+        {reinterpret_cast<const void*>(&k_solve<0, 1>), reinterpret_cast<const void*>(&k_solve<0, 2>),
+         reinterpret_cast<const void*>(&k_solve<0, 4>), reinterpret_cast<const void*>(&k_solve<0, 8>)},
+        {reinterpret_cast<const void*>(&k_solve<1, 1>), reinterpret_cast<const void*>(&k_solve<1, 2>),
+         reinterpret_cast<const void*>(&k_solve<1, 4>), reinterpret_cast<const void*>(&k_solve<1, 8>)},
+        {reinterpret_cast<const void*>(&k_solve<2, 1>), reinterpret_cast<const void*>(&k_solve<2, 2>),
+         reinterpret_cast<const void*>(&k_solve<2, 4>), reinterpret_cast<const void*>(&k_solve<2, 8>)}};
+    return fns[mode][gi];
 }
 
 struct DeviceFacts {
     int sms = 0, major = 0;
-    int per_sm[2][4] = {}; // cooperative CTAs per SM of k_solve<exact?, G>
+    int per_sm[3][4] = {}; // cooperative CTAs per SM of k_solve<mode, G>
     std::string name;
 };
 
@@ -70,10 +73,10 @@ const DeviceFacts& device_facts(int dev) {
     f.major = prop.major;
     f.name = prop.name;
     if (f.major >= 10) {
-        for (int e = 0; e < 2; ++e)
+        for (int e = 0; e < 3; ++e)
             for (int gi = 0; gi < 4; ++gi) {
                 int per_sm = 0;
-                CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, solve_fn(e == 1, gi), kBlock, 0));
+                CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, solve_fn(e, gi), kBlock, 0));
                 f.per_sm[e][gi] = std::max(1, std::min(per_sm, kSolveMinBlocks));
             }
     }
@@ -167,6 +170,12 @@ void Session::init(const std::function<void(DeviceState&)>& prepare) {
         d.cyc_wi.alloc(N1, d.stream);
         d.pv0.alloc(N1, d.stream);
         d.pv1.alloc(N1, d.stream);
+        if (prep_.wide) {
+            if (world_ > 1)
+                throw UnsupportedError("the sharded lanes run the 64-bit exact lane only (weights "
+                                       "below 2^31)");
+            alloc_wide();
+        }
     } else {
         xalloc(d.succ_wf, NP);
         d.key_f.alloc(N1, d.stream);
@@ -239,17 +248,18 @@ void Session::init(const std::function<void(DeviceState&)>& prepare) {
     // one CTA per SM slot the register budget allows (<= kSolveMinBlocks);
     // small graphs take one CTA per kBlock vertices: fewer arrivals make every
     // grid barrier cheaper and there is no work for more threads anyway
-    grid_ = facts.per_sm[prep_.exact ? 1 : 0][gi_] * d.sms;
+    mode_ = prep_.exact ? (prep_.wide ? 2 : 1) : 0;
+    grid_ = facts.per_sm[mode_][gi_] * d.sms;
     // TMA-staged improvement for key arrays beyond the ~64 MB that random
     // gathers keep at L2 speed (OCM_STAGED=0/1 forces it off/on)
     {
         const int st = env_int("OCM_STAGED", -1);
-        d.kp.staged = prep_.exact && d.kp.nhot == 0 && st != 0 &&
+        d.kp.staged = mode_ == 1 && d.kp.nhot == 0 && st != 0 &&
                       (st == 1 || std::size_t(prep_.n) * 8 > (std::size_t(64) << 20));
     }
     if (dyn_smem_bytes()) { // the staged pass / hub table use dynamic shared memory
         int per_sm = 0;
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, solve_fn(prep_.exact, gi_), kBlock,
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, solve_fn(mode_, gi_), kBlock,
                                                          dyn_smem_bytes()));
         grid_ = std::min(grid_, std::max(1, per_sm) * d.sms);
     }
@@ -403,7 +413,7 @@ void Session::choose_hubs() {
     hot_bytes_ = 0;
     const int mode = env_int("OCM_HOT", 0);
     const std::size_t N = prep_.n;
-    if (mode == 0 || !prep_.exact || prep_.M == 0 || N == 0 || d.kp.pb)
+    if (mode == 0 || !prep_.exact || prep_.wide || prep_.M == 0 || N == 0 || d.kp.pb)
         return;
     unsigned slots = static_cast<unsigned>(env_int("OCM_HOT_SLOTS", 2048));
     slots = std::max(64u, std::min(slots, 8192u));
@@ -454,6 +464,60 @@ void Session::choose_hubs() {
     hot_bytes_ = std::size_t(slots) * 12;
 }
 
+namespace {
+// sign extension of the 32-bit weights into the wide lane's high halves
+__global__ void k_widen(std::uint64_t m, const int2* ew, int* ew_hi, std::uint32_t n,
+                        const int* succ_wi, int* succ_whi) {
+    for (std::uint64_t e = gtid(); e < m; e += gstride())
+        ew_hi[e] = ew[e].y < 0 ? -1 : 0;
+    for (std::uint64_t v = gtid(); v < n; v += gstride())
+        succ_whi[v] = succ_wi[v] < 0 ? -1 : 0;
+}
+} // namespace
+
+// Buffers of the wide exact lane (128-bit keys, winning-cycle records, the
+// high halves of the policy weights; prep writes ew_hi for wide graphs).
+void Session::alloc_wide() {
+    DeviceState& d = *d_;
+    const std::size_t N1 = std::max<std::size_t>(prep_.n, 1);
+    d.key_w.alloc(N1, d.stream);
+    d.pvw0.alloc(N1, d.stream);
+    d.pvw1.alloc(N1, d.stream);
+    d.succ_whi.alloc(N1, d.stream);
+    d.kp.key_w = d.key_w.p;
+    d.kp.pvw[0] = d.pvw0.p;
+    d.kp.pvw[1] = d.pvw1.p;
+    d.kp.succ_whi = d.succ_whi.p;
+    d.kp.ew_hi = d.ew_hi.p;
+}
+
+// The fast lane's adoption check found that a key could leave +-2^62 (long
+// cycles with large weights): switch the session to the wide lane for good.
+// Its 32-bit weights widen by sign extension; everything else is re-run.
+void Session::promote_wide() {
+    DeviceState& d = *d_;
+    if (world_ > 1)
+        throw RangeError("exact value keys would exceed 62 bits for this graph (the sharded lanes "
+                         "run 64-bit keys only)");
+    if (!d.ew_hi.p) {
+        d.ew_hi.alloc(std::max<std::uint64_t>(prep_.M, 1) + 2, d.stream);
+        CK(cudaMemsetAsync(d.ew_hi.p, 0, (std::max<std::uint64_t>(prep_.M, 1) + 2) * 4, d.stream));
+    }
+    prep_.wide = true;
+    alloc_wide();
+    k_widen<<<grid_for(std::max<std::uint64_t>(prep_.M, prep_.n), d.sms, 8), kBlock, 0, d.stream>>>(
+        prep_.M, d.ew.p, d.ew_hi.p, prep_.n, d.succ_wi.p, d.succ_whi.p);
+    CK(cudaGetLastError());
+    d.kp.staged = 0;
+    d.kp.nhot = 0;
+    d.kp.pb = 0;
+    mode_ = 2;
+    const DeviceFacts& facts = device_facts(d.device);
+    const int before = grid_;
+    grid_ = std::min(before, facts.per_sm[2][gi_] * d.sms);
+    CK(cudaStreamSynchronize(d.stream));
+}
+
 std::size_t Session::dyn_smem_bytes() const {
     const KP& p = d_->kp;
     if (p.pb)
@@ -468,7 +532,8 @@ void Session::build_blocked_edges() {
     KP& p = d.kp;
     p.pb = 0;
     const std::uint64_t N = prep_.n, M = prep_.M;
-    if (env_int("OCM_PB", 0) != 1 || !prep_.exact || world_ != 1 || prep_.R == 0 || M == 0)
+    if (env_int("OCM_PB", 0) != 1 || !prep_.exact || prep_.wide || world_ != 1 || prep_.R == 0 ||
+        M == 0)
         return;
     // bins of ~2M vertices (16 MB of keys); OCM_PB_BIN overrides (tests)
     std::uint64_t bin = std::max<std::uint64_t>(std::uint64_t(env_int("OCM_PB_BIN", 1 << 21)),
@@ -552,7 +617,7 @@ template <class M> void Session::launch_async(int mode) {
     CK(cudaEventRecord(d.ev_start, s));
     if (prep_.R > 0) {
         void* args[] = {&p, &mode};
-        CK(cudaLaunchCooperativeKernel(solve_fn(EXACT, gi_), dim3(grid_), dim3(kBlock), args,
+        CK(cudaLaunchCooperativeKernel(solve_fn(mode_, gi_), dim3(grid_), dim3(kBlock), args,
                                        dyn_smem_bytes(), s));
         ++launches_;
     }
@@ -754,7 +819,16 @@ void Session::solve(ocm_solution* out, std::uint32_t* cycle_buf, std::uint32_t c
     if (world_ > 1)
         throw std::invalid_argument("sharded session: drive it with shard_step / shard_finish");
     if (prep_.exact) {
-        launch<ExactTag>(kSolveFull);
+        try {
+            launch<ExactTag>(kSolveFull);
+        } catch (const RangeError&) {
+            // a key could leave the fast lane's +-2^62: redo the solve with
+            // 128-bit keys (the same policy iteration, so the same result)
+            if (mode_ != 1)
+                throw;
+            promote_wide();
+            launch<ExactTag>(kSolveFull);
+        }
         collect<ExactTag>(out, cycle_buf, cap);
     } else {
         launch<FloatTag>(kSolveFull);
@@ -905,11 +979,19 @@ __global__ void k_certify_vertices(KP p, unsigned long long* cnt) {
         if (r >= p.R || b == e_end)
             continue;
         ++verts;
-        const long long K = p.key_i[v], num = p.lam_num[r], den = p.lam_den[r];
+        // keys and weights of either exact lane (wide: 128-bit keys, the
+        // weights' high halves in ew_hi / succ_whi)
+        auto key = [&](std::uint32_t x) -> __int128 { return p.key_w ? p.key_w[x] : p.key_i[x]; };
+        auto wgt = [&](std::uint32_t e, int2 ed) -> long long {
+            return p.key_w ? (static_cast<long long>(p.ew_hi[e]) << 32) | static_cast<unsigned>(ed.y)
+                           : ed.y;
+        };
+        const __int128 K = key(static_cast<std::uint32_t>(v));
+        const long long num = p.lam_num[r], den = p.lam_den[r];
         for (std::uint32_t e = b; e < e_end; ++e) {
             const int2 ed = p.ew[e];
-            const __int128 c = static_cast<__int128>(p.key_i[static_cast<std::uint32_t>(ed.x)]) +
-                               static_cast<__int128>(ed.y) * den - num;
+            const __int128 c = key(static_cast<std::uint32_t>(ed.x)) +
+                               static_cast<__int128>(wgt(e, ed)) * den - num;
             kv += c < K;
             ++edges;
         }
@@ -918,9 +1000,12 @@ __global__ void k_certify_vertices(KP p, unsigned long long* cnt) {
             ++pv;
         } else {
             const int2 ed = p.ew[se];
-            const __int128 c = static_cast<__int128>(p.key_i[static_cast<std::uint32_t>(ed.x)]) +
-                               static_cast<__int128>(ed.y) * den - num;
-            pv += c != K || p.succ_v[v] != static_cast<std::uint32_t>(ed.x) || p.succ_wi[v] != ed.y;
+            const long long we = wgt(se, ed);
+            const __int128 c = key(static_cast<std::uint32_t>(ed.x)) + static_cast<__int128>(we) * den - num;
+            const long long ws = p.key_w ? (static_cast<long long>(p.succ_whi[v]) << 32) |
+                                               static_cast<unsigned>(p.succ_wi[v])
+                                         : p.succ_wi[v];
+            pv += c != K || p.succ_v[v] != static_cast<std::uint32_t>(ed.x) || ws != we;
         }
     }
     cert_add(&cnt[0], verts);
@@ -943,7 +1028,8 @@ __global__ void k_certify_cycles(KP p, unsigned long long* cnt) {
         unsigned long long len = 0;
         long long sum = 0;
         do {
-            sum += p.succ_wi[u];
+            sum += p.key_w ? (static_cast<long long>(p.succ_whi[u]) << 32) | static_cast<unsigned>(p.succ_wi[u])
+                           : p.succ_wi[u];
             u = p.succ_v[u];
             mn = min(mn, u);
             ++len;
@@ -991,7 +1077,15 @@ void Session::values(std::int64_t* key_num, std::int64_t* lam_num, std::int64_t*
     std::vector<double> kf(n);
     std::vector<std::uint32_t> sv(n), reg(n);
     if (n) {
-        if (prep_.exact)
+        if (prep_.exact && mode_ == 2) {
+            std::vector<__int128> kw(n);
+            CK(cudaMemcpy(kw.data(), d.kp.key_w, n * sizeof(__int128), cudaMemcpyDeviceToHost));
+            for (std::size_t v = 0; v < n; ++v) {
+                if (kw[v] != static_cast<__int128>(static_cast<long long>(kw[v])) && key_num)
+                    throw RangeError("a value key exceeds 64 bits: read it with ocm_session_keys_wide");
+                key[v] = static_cast<long long>(kw[v]);
+            }
+        } else if (prep_.exact)
             CK(cudaMemcpy(key.data(), d.kp.key_i, n * sizeof(long long), cudaMemcpyDeviceToHost));
         else
             CK(cudaMemcpy(kf.data(), d.kp.key_f, n * sizeof(double), cudaMemcpyDeviceToHost));
@@ -1007,6 +1101,39 @@ void Session::values(std::int64_t* key_num, std::int64_t* lam_num, std::int64_t*
         if (lam_den) lam_den[v] = solved ? ld[reg[v]] : 1;
         if (fval) fval[v] = solved && !prep_.exact ? kf[v] : 0.0;
         if (succ_vertex) succ_vertex[v] = solved ? sv[v] : NONE;
+    }
+}
+
+} // namespace ocmb
+
+namespace ocmb {
+
+// Exact value keys at full width: hi:lo = the 128-bit key (narrow lane:
+// sign-extended 64-bit keys); vertices outside every region get 0.
+void Session::keys_wide(std::int64_t* hi, std::uint64_t* lo) {
+    if (!solved_)
+        throw std::logic_error("session has not been solved yet");
+    if (!prep_.exact)
+        throw UnsupportedError("value keys exist in the exact lane only");
+    DeviceState& d = *d_;
+    const std::size_t n = prep_.n;
+    std::vector<std::uint32_t> reg(n);
+    std::vector<__int128> k(n);
+    if (n) {
+        CK(cudaMemcpy(reg.data(), d.kp.reg, n * 4, cudaMemcpyDeviceToHost));
+        if (mode_ == 2) {
+            CK(cudaMemcpy(k.data(), d.kp.key_w, n * sizeof(__int128), cudaMemcpyDeviceToHost));
+        } else {
+            std::vector<long long> k64(n);
+            CK(cudaMemcpy(k64.data(), d.kp.key_i, n * 8, cudaMemcpyDeviceToHost));
+            for (std::size_t v = 0; v < n; ++v)
+                k[v] = k64[v];
+        }
+    }
+    for (std::size_t v = 0; v < n; ++v) {
+        const __int128 x = reg[v] != prep_.R ? k[v] : 0;
+        hi[v] = static_cast<std::int64_t>(x >> 64);
+        lo[v] = static_cast<std::uint64_t>(x);
     }
 }
 

@@ -35,6 +35,8 @@ class Session {
     void values(std::int64_t* key_num, std::int64_t* lam_num, std::int64_t* lam_den, double* fval,
                 std::uint32_t* succ_vertex);
     void* stream() const;
+    void keys_wide(std::int64_t* hi, std::uint64_t* lo);
+    bool wide() const { return mode_ == 2; }
 
     std::uint32_t n() const { return prep_.n; }
 
@@ -69,6 +71,9 @@ class Session {
     void build_blocked_edges();
     void choose_hubs();
     std::size_t dyn_smem_bytes() const;
+    void alloc_wide();
+    void promote_wide();
+    int mode_ = 1; // k_solve arithmetic: 0 float, 1 exact (64-bit keys), 2 wide exact (128-bit)
     std::size_t hot_bytes_ = 0;    // dynamic shared memory of the staged hub table
     double hot_coverage_ = 0.0;    // share of intra-region edges into the staged hubs
     bool shard_started_ = false;

@@ -91,8 +91,11 @@ def record(name, n, edges):
             if scc == "tarjan":
                 v = O.ref_values(n, src, dst, w, objective)
                 if par.exact or (len(w) and np.all(np.floor(w) == w)):
-                    key = v.wsum * v.lam_den - v.steps * v.lam_num
-                    r["value_key"] = key.tolist()
+                    # exact Python integers: with weights up to 2^52 the
+                    # products leave int64 (the wide device lane's range)
+                    key = [int(a) * int(b) - int(c) * int(d) for a, b, c, d in
+                           zip(v.wsum, v.lam_den, v.steps, v.lam_num)]
+                    r["value_key"] = key
                     r["lam_num"] = v.lam_num.tolist()
                     r["lam_den"] = v.lam_den.tolist()
                 else:
@@ -116,6 +119,14 @@ def main():
         cases.append(record(f"random_sc_{i}", n, e))
     for i, (n, e) in enumerate(random_cases(rng, 12, 60, 1, 100, 3)):
         cases.append(record(f"medium_{i}", n, e))
+    # the reference's full ExactMode range (graph.cpp:15: integral |w| < 2^53):
+    # weights of 2^40 and 2^48 -- the device's wide exact lane (2^48 keeps the
+    # Hamiltonian weight 2n(max|w|+1)+1 of --scc off below 2^53 for n <= 8)
+    wrng = np.random.default_rng(53)
+    for i, (n, e) in enumerate(random_cases(wrng, 24, 10, -(1 << 40), 1 << 40, 4)):
+        cases.append(record(f"wide40_{i}", n, e))
+    for i, (n, e) in enumerate(random_cases(wrng, 12, 8, -(1 << 48) + 1, (1 << 48) - 1, 3, sc=True)):
+        cases.append(record(f"wide48_sc_{i}", n, e))
     with open(OUT, "w") as f:
         json.dump({"generator": "tests/golden/make_golden.py",
                    "reference": "proj/src/solve.cpp via oracle/_ref/libocm_ref.so",

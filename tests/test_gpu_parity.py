@@ -260,13 +260,20 @@ def test_scc_parallel_matches_tarjan():
 
 
 def test_limits_fail_loudly():
-    # integer weights beyond 32 bits: the exact device lane refuses (documented
-    # limit) instead of silently changing arithmetic
+    # 2^40 weights run (wide lane); the remaining limit -- doubling sums of
+    # the largest region at |w| near 2^53 could leave 64 bits -- is refused
+    # loudly (OverflowError) instead of silently changing arithmetic
     src = np.array([0, 1], np.uint32)
     dst = np.array([1, 0], np.uint32)
     g = P.build_graph(2, (src, dst, np.array([2.0 ** 40, 1.0])))
-    with pytest.raises(P.UnsupportedError, match="32 bits"):
-        P.solve(g)
+    s = P.solve(g)
+    assert s.exact and s.mu_exact == Fraction(2 ** 40 + 1, 2)
+    n = 1024
+    ring = np.arange(n, dtype=np.uint32)
+    big = np.ones(n)
+    big[0] = 2.0 ** 52 + 2.0 ** 51
+    with pytest.raises(OverflowError, match="62 bits"):
+        P.solve(P.build_graph(n, (ring, (ring + 1) % n, big)))
     # a device ordinal that does not exist
     with pytest.raises(ValueError, match="device"):
         P.solve(P.build_graph(2, (src, dst, np.array([1.0, 2.0]))), P.SolveOptions(device=99))
@@ -337,3 +344,93 @@ def test_solve_csr_validates_like_build_graph():
     assert s.has_cycle and not s.exact and s.mu == 2.25
     s = P.solve_csr(2, idx, np.array([1, 0], np.uint32), np.array([3.0, 2.0]))
     assert s.exact and s.mu_exact == Fraction(5, 2)
+
+
+WIDE_CASES = [c for c in CASES if c["name"].startswith("wide")]
+
+
+@pytest.mark.parametrize("case", WIDE_CASES, ids=[c["name"] for c in WIDE_CASES])
+def test_wide_weights_run_the_wide_lane(case):
+    """Weights of 2^40-2^48 (the reference accepts integral |w| < 2^53,
+    graph.cpp:15): the device packs 64-bit weights and runs 128-bit keys --
+    same mean, cycle, policy, value keys and statistics as the reference."""
+    n = case["n"]
+    src, dst, w = case_arrays(case)
+    g = P.build_graph(n, (src, dst, w))
+    for key, ref in case["results"].items():
+        objective, scc = key.split("/")
+        s = P.Session(g, P.SolveOptions(objective=objective, scc=scc))
+        sol = s.solve()
+        check_against(sol, s.values() if scc == "tarjan" else None, ref)
+        if ref["has_cycle"]:
+            assert s.wide
+
+
+@pytest.mark.parametrize("case", CASES[::2], ids=[c["name"] for c in CASES[::2]])
+def test_forced_wide_lane_matches_reference(case, monkeypatch):
+    """OCM_WIDE=1: the 128-bit lane on ordinary graphs reproduces the
+    reference bit for bit as well (keys read at full width)."""
+    monkeypatch.setenv("OCM_WIDE", "1")
+    n = case["n"]
+    src, dst, w = case_arrays(case)
+    for key, ref in case["results"].items():
+        objective, scc = key.split("/")
+        sol, vals = run(n, src, dst, w, objective, scc)
+        check_against(sol, vals if scc == "tarjan" else None, ref)
+
+
+def test_keys_beyond_62_bits_promote_to_the_wide_lane():
+    """A 2^17-vertex ring, weights +(2^31-1) on one half and -(2^31-1) on the
+    other with a net sum of 1: mean 1/2^17 (den = 2^17) and path sums near
+    2^47, so keys K = value*den reach ~2^64. The fast lane proves at adoption
+    that a key could leave +-2^62 and the session re-solves with 128-bit keys;
+    mean, cycle and every value key (exact integers; the reference's own
+    (wsum, steps) pairs still fit int64) equal the oracle. A second graph,
+    with chords, promotes on the provable bound as well."""
+    n = 1 << 17
+    ring = np.arange(n, dtype=np.uint32)
+    w = np.where(ring < n // 2, 2.0 ** 31 - 1, -(2.0 ** 31 - 1))
+    w[-1] += 1
+    rng = np.random.default_rng(7)
+    graphs = [(ring, (ring + 1) % n, w, True)]
+    m = 1 << 16
+    r2 = np.arange(m, dtype=np.uint32)
+    graphs.append((np.concatenate([r2, rng.integers(0, m, 64).astype(np.uint32)]),
+                   np.concatenate([(r2 + 1) % m, rng.integers(0, m, 64).astype(np.uint32)]),
+                   np.concatenate([rng.integers(-(1 << 30), 1 << 30, m),
+                                   np.full(64, 1 << 30)]).astype(np.float64), False))
+    for src, dst, ww, huge in graphs:
+        nn = int(max(src.max(), dst.max())) + 1
+        g = P.build_graph(nn, (src, dst, ww))
+        for objective in ("min", "max"):
+            s = P.Session(g, P.SolveOptions(objective=objective))
+            sol = s.solve()
+            ref = oracle_record(nn, src, dst, ww, objective, "tarjan")
+            o = O.oracle_solve(nn, src, dst, ww, objective, "tarjan", values=True)
+            ref["value_key"] = [int(a) * int(b) - int(c) * int(d)
+                                for a, b, c, d in zip(o.wsum, o.lam_den, o.steps, o.lam_num)]
+            check_against(sol, s.values(), ref)
+            if huge:
+                assert s.wide and sol.mu_exact.denominator == n
+                assert max(abs(int(k)) for k in s.keys_wide()) > 1 << 62
+            elif objective == "min":  # the whole ring wins: den = 65536
+                assert s.wide
+            cert = s.certify()
+            assert cert["key_violations"] == cert["policy_violations"] == cert["cycle_violations"] == 0
+
+
+def test_wide_lane_certificate_and_generated_graph(monkeypatch):
+    monkeypatch.setenv("OCM_WIDE", "1")
+    spec = P.Generator("powerlaw", n=20_000, deg=4, dmax=2_000, wlo=-50, whi=50, seed=9)
+    a = P.Session.generated(spec, P.SolveOptions())
+    sa = a.solve()
+    assert a.wide
+    cert = a.certify()
+    assert cert["key_violations"] == cert["policy_violations"] == cert["cycle_violations"] == 0
+    monkeypatch.setenv("OCM_WIDE", "0")
+    b = P.Session.generated(spec, P.SolveOptions())
+    sb = b.solve()
+    assert not b.wide
+    assert (sa.mu_exact, sa.cycle_vertices, sa.stats.spf_passes) == \
+        (sb.mu_exact, sb.cycle_vertices, sb.stats.spf_passes)
+    assert a.keys_wide().tolist() == [int(x) for x in b.values()["key_num"]]
