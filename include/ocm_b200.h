@@ -147,6 +147,11 @@ uint32_t ocm_graph_n(const ocm_graph* g);
 uint64_t ocm_graph_m(const ocm_graph* g);
 int ocm_graph_integer_exact(const ocm_graph* g);
 int ocm_graph_edges(const ocm_graph* g, uint32_t* src, uint32_t* dst, double* w);
+/* The graph's forward CSR in place (graph.hpp:38-41: fwd_index n+1 offsets,
+ * here 64-bit; fwd_target / fwd_weight m entries): read-only pointers owned
+ * by the graph, valid until ocm_graph_free. */
+int ocm_graph_csr(const ocm_graph* g, const uint64_t** fwd_index, const uint32_t** fwd_target,
+                  const double** fwd_weight);
 
 /* One-call front door (create session, solve, free). */
 int ocm_solve(const ocm_graph* g, const ocm_solve_options* opt, ocm_solution* out,

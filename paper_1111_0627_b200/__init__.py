@@ -151,6 +151,8 @@ def _load():
         "ocm_graph_m": (C.c_uint64, [C.c_void_p]),
         "ocm_graph_integer_exact": (C.c_int, [C.c_void_p]),
         "ocm_graph_edges": (C.c_int, [C.c_void_p, P(C.c_uint32), P(C.c_uint32), P(C.c_double)]),
+        "ocm_graph_csr": (C.c_int, [C.c_void_p, P(P(C.c_uint64)), P(P(C.c_uint32)),
+                                    P(P(C.c_double))]),
         "ocm_solve": (C.c_int, [C.c_void_p, P(_Opts), P(_Sol), P(C.c_uint32), C.c_uint32]),
         "ocm_solve_csr": (C.c_int, [C.c_uint32, C.c_uint32, P(C.c_uint32), P(C.c_uint32),
                                     P(C.c_double), P(_Opts), P(_Sol), P(C.c_uint32), C.c_uint32]),
@@ -182,6 +184,7 @@ EXPORTED_SYMBOLS = (
     "ocm_session_shard_finish", "ocm_session_shard_peer_info", "ocm_session_shard_connect",
     "ocm_session_shard_fused_launch", "ocm_session_shard_fused_finish",
     "ocm_graph_free", "ocm_graph_n", "ocm_graph_m", "ocm_graph_integer_exact", "ocm_graph_edges",
+    "ocm_graph_csr",
     "ocm_solve", "ocm_solve_csr", "ocm_session_create", "ocm_session_solve", "ocm_session_values",
     "ocm_session_stream", "ocm_session_free", "ocm_session_certify", "ocm_session_keys_wide",
     "ocm_session_is_wide",
@@ -235,6 +238,25 @@ class Graph:
     @property
     def integer_exact(self) -> bool:
         return bool(_lib.ocm_graph_integer_exact(self._h))
+
+    def csr(self) -> Tuple[np.ndarray, np.ndarray, np.ndarray]:
+        """(fwd_index, fwd_target, fwd_weight) as read-only zero-copy views of
+        the graph's own CSR (graph.hpp:38-41; offsets 64-bit here). The views
+        keep the graph alive."""
+        pi, pt, pw = C.POINTER(C.c_uint64)(), C.POINTER(C.c_uint32)(), C.POINTER(C.c_double)()
+        _check(_lib.ocm_graph_csr(self._h, C.byref(pi), C.byref(pt), C.byref(pw)))
+        n, m = self.n, self.m
+        out = []
+        for ptr, cnt in ((pi, n + 1), (pt, m), (pw, m)):
+            if cnt:
+                buf = (ptr._type_ * cnt).from_address(C.addressof(ptr.contents))
+                buf._graph = self  # the array's base owns a reference to the graph
+                a = np.ctypeslib.as_array(buf)
+            else:
+                a = np.empty(0, ptr._type_)
+            a.flags.writeable = False
+            out.append(a)
+        return tuple(out)
 
     def edges(self) -> Tuple[np.ndarray, np.ndarray, np.ndarray]:
         """(source, target, weight) arrays in edge-id order (Graph::edges())."""

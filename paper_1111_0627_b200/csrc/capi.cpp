@@ -273,6 +273,17 @@ uint32_t ocm_graph_n(const ocm_graph* g) { return g ? g->g.n : 0; }
 uint64_t ocm_graph_m(const ocm_graph* g) { return g ? g->g.m : 0; }
 int ocm_graph_integer_exact(const ocm_graph* g) { return g && g->g.integer_exact ? 1 : 0; }
 
+int ocm_graph_csr(const ocm_graph* g, const uint64_t** fwd_index, const uint32_t** fwd_target,
+                  const double** fwd_weight) {
+    return guard([&] {
+        if (!g || !fwd_index || !fwd_target || !fwd_weight)
+            throw std::invalid_argument("null graph or output");
+        *fwd_index = g->g.fwd_index.data();
+        *fwd_target = g->g.fwd_target.data();
+        *fwd_weight = g->g.fwd_weight.data();
+    });
+}
+
 int ocm_graph_edges(const ocm_graph* g, uint32_t* src, uint32_t* dst, double* w) {
     return guard([&] { ocmb::graph_edges(g->g, src, dst, w); });
 }

@@ -20,6 +20,8 @@
 #include <cub/cub.cuh>
 
 #include <cstring>
+#include <condition_variable>
+#include <memory>
 #include <mutex>
 #include <thread>
 
@@ -773,24 +775,85 @@ class StagingRing {
             CK(cudaEventRecord(done_[k], nullptr));
         }
     }
-    // memcpy split over a few threads (one thread copies ~10 GB/s, below
-    // the PCIe rate)
-    static void host_copy(char* dst, const char* src, std::size_t len) {
-        constexpr int kThreads = 4;
-        if (len < (1u << 20)) {
-            std::memcpy(dst, src, len);
-            return;
+    // memcpy split over a persistent pool of host threads (one thread copies
+    // ~10 GB/s, below the PCIe rate; threads are started once per process)
+    class CopyPool {
+      public:
+        explicit CopyPool(int n) : n_(n) {
+            for (int t = 1; t < n_; ++t)
+                th_.emplace_back([this, t] { run(t); });
         }
-        std::thread th[kThreads - 1];
-        const std::size_t part = (len / kThreads + 63) & ~std::size_t(63);
-        for (int t = 1; t < kThreads; ++t) {
-            const std::size_t lo = std::min(len, part * t), hi = std::min(len, part * (t + 1));
-            th[t - 1] = std::thread([=] { std::memcpy(dst + lo, src + lo, hi - lo); });
+        ~CopyPool() {
+            {
+                std::lock_guard<std::mutex> l(m_);
+                quit_ = true;
+                ++gen_;
+            }
+            cv_.notify_all();
+            for (auto& x : th_)
+                x.join();
         }
-        std::memcpy(dst, src, std::min(len, part));
-        for (auto& x : th)
-            x.join();
+        void copy(char* dst, const char* src, std::size_t len) {
+            if (len < (1u << 20) || n_ == 1) {
+                std::memcpy(dst, src, len);
+                return;
+            }
+            {
+                std::lock_guard<std::mutex> l(m_);
+                dst_ = dst;
+                src_ = src;
+                len_ = len;
+                pending_ = n_ - 1;
+                ++gen_;
+            }
+            cv_.notify_all();
+            part(0);
+            std::unique_lock<std::mutex> l(m_);
+            done_cv_.wait(l, [this] { return pending_ == 0; });
+        }
+
+      private:
+        void part(int t) {
+            const std::size_t per = ((len_ + n_ - 1) / n_ + 63) & ~std::size_t(63);
+            const std::size_t lo = std::min(len_, per * t), hi = std::min(len_, per * (t + 1));
+            if (hi > lo)
+                std::memcpy(dst_ + lo, src_ + lo, hi - lo);
+        }
+        void run(int t) {
+            unsigned long long seen = 0;
+            for (;;) {
+                {
+                    std::unique_lock<std::mutex> l(m_);
+                    cv_.wait(l, [&] { return gen_ != seen; });
+                    seen = gen_;
+                    if (quit_)
+                        return;
+                }
+                part(t);
+                std::lock_guard<std::mutex> l(m_);
+                if (--pending_ == 0)
+                    done_cv_.notify_one();
+            }
+        }
+        int n_;
+        std::vector<std::thread> th_;
+        std::mutex m_;
+        std::condition_variable cv_, done_cv_;
+        unsigned long long gen_ = 0;
+        int pending_ = 0;
+        bool quit_ = false;
+        char* dst_ = nullptr;
+        const char* src_ = nullptr;
+        std::size_t len_ = 0;
+    };
+    void host_copy(char* dst, const char* src, std::size_t len) {
+        if (!pool_) {
+            const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+            pool_ = std::make_unique<CopyPool>(static_cast<int>(std::min(8u, std::max(1u, hw / 2))));
+        }
+        pool_->copy(dst, src, len);
     }
+    std::unique_ptr<CopyPool> pool_;
     std::mutex mu_;
     char* buf_[kSlots] = {};
     cudaEvent_t done_[kSlots] = {};
