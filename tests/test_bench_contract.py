@@ -98,3 +98,24 @@ def test_gpus_flag_refuses_missing_devices():
                          capture_output=True, text=True, timeout=300,
                          env={k: v for k, v in os.environ.items() if k != "WORLD_SIZE"})
     assert out.returncode != 0 and "visible" in out.stderr
+
+
+@pytest.mark.gpu
+def test_gpus_2_self_launch_on_one_gpu():
+    """`bench.py --gpus 2` starts two ranks itself; with both on this box's
+    one GPU (OCM_BENCH_SHARE_GPU=1: gloo plumbing, half the SMs each) the
+    fused strong-scaling lane solves config 2 across them and rank 0 prints
+    one line with n_gpus 2 and the reference's mu (config_golden.json)."""
+    env = {k: v for k, v in os.environ.items()
+           if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT")}
+    env["OCM_BENCH_SHARE_GPU"] = "1"
+    out = subprocess.run([sys.executable, "bench.py", "--gpus", "2", "--config", "2", "--steps", "1",
+                          "--warmup", "1", "--no-cpu-baseline", "--no-e2e"], cwd=ROOT,
+                         capture_output=True, text=True, timeout=900, env=env)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["scaling"] == "strong" and "fused" in d["config"]["parallelism"]
+    assert d["mu"] == {"min": "229/45", "max": "193/2"}
+    assert d["policy_iterations"] == {"min": 44, "max": 26}
