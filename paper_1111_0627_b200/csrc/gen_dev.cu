@@ -13,7 +13,7 @@
 namespace ocmb {
 
 void device_prepare_csr(std::uint32_t n, std::uint64_t m, DBuf<std::uint32_t>& row,
-                        DBuf<std::uint32_t>& tgt, DBuf<double>& w, bool integer_exact,
+                        DBuf<std::uint32_t>& tgt, DBuf<double>& w, int exactness,
                         const ocm_solve_options& opt, DeviceState& d, PrepInfo& info,
                         cudaEvent_t w_ready = nullptr);
 
@@ -136,7 +136,7 @@ void device_generate_prepare(const GenSpec& spec, const ocm_solve_options& opt, 
                                                          hub_mul(n), hub_add(spec.seed, n),
                                                          spec.kind == 2 ? 1 : spec.kind == 3 ? 3 : 0);
     CK(cudaGetLastError());
-    device_prepare_csr(n, m, row, tgt, w, true, opt, d, info);
+    device_prepare_csr(n, m, row, tgt, w, 1, opt, d, info);
 }
 
 } // namespace ocmb

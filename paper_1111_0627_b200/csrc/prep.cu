@@ -43,7 +43,7 @@ namespace ocmb {
 
 void device_prepare(const HostCsr& g, const ocm_solve_options& opt, DeviceState& d, PrepInfo& info);
 void device_prepare_csr(std::uint32_t n, std::uint64_t m, DBuf<std::uint32_t>& row,
-                        DBuf<std::uint32_t>& tgt, DBuf<double>& w, bool integer_exact,
+                        DBuf<std::uint32_t>& tgt, DBuf<double>& w, int exactness,
                         const ocm_solve_options& opt, DeviceState& d, PrepInfo& info,
                         cudaEvent_t w_ready = nullptr);
 
@@ -71,6 +71,8 @@ struct PrepCounters {
     unsigned remaining;  // unassigned vertices
     int changed;
     int bad_weight;      // exact weight outside int32
+    int non_integral;    // some weight is not an integer below 2^53 (checked graphs)
+    unsigned long long bad_weight_edge; // least edge id with a non-finite weight (checked graphs)
     unsigned long long max_abs_bits; // max |w| as double bits
     unsigned long long pivot;        // (score << 32) | ~v
     unsigned max_region;
@@ -89,13 +91,27 @@ __global__ void kp_row32(const std::uint64_t* r64, std::uint32_t* r32, std::size
 // Out-degree / in-degree without self-loops, self-loop flags, max |w|.
 // max |w| over all edges (as double bits: non-negative doubles order like
 // their bit patterns).
-__global__ void kp_max_abs(std::uint64_t m, const double* w, PrepCounters* pc) {
+// max |w|; with `check` also build_graph's weight contract for caller-provided
+// arrays (graph.cpp:33-36): the least edge with a non-finite weight, and
+// whether every weight is an integer below 2^53 (Graph::integer_exact)
+__global__ void kp_max_abs(std::uint64_t m, const double* w, PrepCounters* pc, int check) {
     unsigned long long mx = 0;
+    bool frac = false;
     for (std::uint64_t e = tid_(); e < m; e += stride_()) {
-        const unsigned long long bits = __double_as_longlong(fabs(w[e]));
+        const double x = w[e];
+        const unsigned long long bits = __double_as_longlong(fabs(x));
+        if (check) {
+            if (!isfinite(x)) {
+                atomicMin(&pc->bad_weight_edge, static_cast<unsigned long long>(e));
+                continue;
+            }
+            frac |= floor(x) != x || fabs(x) >= 9007199254740992.0;
+        }
         mx = bits > mx ? bits : mx;
     }
     warp_atomic_max(&pc->max_abs_bits, mx);
+    if (check && __syncthreads_or(frac) && threadIdx.x == 0)
+        pc->non_integral = 1;
 }
 
 // Thread-per-vertex edge loops would leave a power-law hub's 10^4..10^5
@@ -860,10 +876,11 @@ class StagingRing {
     unsigned long long next_ = 0;
 };
 
-// Checks a caller-provided CSR on the device (the reference's build_graph
-// contract, src/graph.cpp:29-36, plus well-formed offsets): the least edge
-// id with an endpoint out of range or a non-finite weight, and whether all
-// weights are integers below 2^53 (Graph::integer_exact).
+// Checks a caller-provided CSR's offsets and targets on the device (the
+// reference's build_graph contract, src/graph.cpp:29-32, plus well-formed
+// offsets) before the region split reads them; the weights stream in on
+// the side stream meanwhile and are checked where they are first read
+// (kp_max_abs with check = 1).
 struct CsrCheck {
     unsigned long long bad_target;
     unsigned long long bad_weight;
@@ -875,7 +892,7 @@ __global__ void kp_check_csr(std::uint32_t n, std::uint64_t m, const std::uint32
                              const std::uint32_t* tgt, const double* w, CsrCheck* out) {
     const std::uint64_t tid = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x;
     const std::uint64_t nth = std::uint64_t(gridDim.x) * blockDim.x;
-    bool bad_row = false, frac = false;
+    bool bad_row = false;
     for (std::uint64_t v = tid; v < n; v += nth)
         bad_row |= row[v] > row[v + 1];
     if (tid == 0)
@@ -883,16 +900,11 @@ __global__ void kp_check_csr(std::uint32_t n, std::uint64_t m, const std::uint32
     for (std::uint64_t e = tid; e < m; e += nth) {
         if (tgt[e] >= n)
             atomicMin(&out->bad_target, static_cast<unsigned long long>(e));
-        const double x = w[e];
-        if (!isfinite(x))
+        if (w && !isfinite(w[e])) // only when a bad target needs the weights' order too
             atomicMin(&out->bad_weight, static_cast<unsigned long long>(e));
-        else
-            frac |= floor(x) != x || fabs(x) >= 9007199254740992.0;
     }
     if (__syncthreads_or(bad_row) && threadIdx.x == 0)
         out->bad_offsets = 1;
-    if (__syncthreads_or(frac) && threadIdx.x == 0)
-        out->non_integral = 1;
 }
 
 } // namespace
@@ -934,40 +946,46 @@ void device_prepare(const HostCsr& g, const ocm_solve_options& opt, DeviceState&
             CK(cudaStreamCreateWithFlags(&d.side, cudaStreamNonBlocking));
             CK(cudaEventCreateWithFlags(&d.side_done, cudaEventDisableTiming));
         }
-        if (g.validated) {
-            CK(cudaStreamWaitEvent(d.side, d.ev_alloc_done(s), 0)); // w allocated on s
-            ring.copy(w.p, g.weight, m * 8, d.side);
-            CK(cudaEventRecord(d.side_done, d.side));
-            w_ready = d.side_done;
-        } else {
-            ring.copy(w.p, g.weight, m * 8, s); // checked below before anything else runs
-        }
+        CK(cudaStreamWaitEvent(d.side, d.ev_alloc_done(s), 0)); // w allocated on s
+        ring.copy(w.p, g.weight, m * 8, d.side);
+        CK(cudaEventRecord(d.side_done, d.side));
+        w_ready = d.side_done;
     }
     if (g.index64) {
         kp_row32<<<grid_for(n + 1, d.sms), kBlock, 0, s>>>(row64.p, row.p, std::size_t(n) + 1);
         row64.release();
     }
+    int exactness = exact ? 1 : 0;
     if (!g.validated) {
+        exactness = -1; // derived from the weights where they are first read
         DBuf<CsrCheck> chk;
         chk.alloc(1, s);
-        CK(cudaMemsetAsync(chk.p, 0, sizeof(CsrCheck), s));
-        CK(cudaMemsetAsync(chk.p, 0xff, 2 * sizeof(unsigned long long), s));
-        kp_check_csr<<<grid_for(std::max<std::uint64_t>(m, n), d.sms, 16), kBlock, 0, s>>>(
-            n, m, row.p, tgt.p, w.p, chk.p);
-        CK(cudaGetLastError());
-        CsrCheck h{};
-        CK(cudaMemcpyAsync(&h, chk.p, sizeof h, cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
+        auto run_check = [&](const double* wp) {
+            CK(cudaMemsetAsync(chk.p, 0, sizeof(CsrCheck), s));
+            CK(cudaMemsetAsync(chk.p, 0xff, 2 * sizeof(unsigned long long), s));
+            kp_check_csr<<<grid_for(std::max<std::uint64_t>(m, n), d.sms, 16), kBlock, 0, s>>>(
+                n, m, row.p, tgt.p, wp, chk.p);
+            CK(cudaGetLastError());
+            CsrCheck h{};
+            CK(cudaMemcpyAsync(&h, chk.p, sizeof h, cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            return h;
+        };
+        CsrCheck h = run_check(nullptr);
         if (h.bad_offsets)
             throw std::invalid_argument("CSR offsets are not a non-decreasing sequence from 0 to m");
-        if (h.bad_target != ~0ull || h.bad_weight != ~0ull) {
-            if (h.bad_target <= h.bad_weight)
-                throw std::invalid_argument("edge " + std::to_string(h.bad_target) +
-                                            " endpoint out of range");
-            throw std::invalid_argument("edge " + std::to_string(h.bad_weight) +
-                                        " has non-finite weight");
+        if (h.bad_target != ~0ull) {
+            // report the first bad edge in id order, as build_graph's loop
+            // does: a non-finite weight on an earlier edge comes first
+            if (w_ready)
+                CK(cudaStreamWaitEvent(s, w_ready, 0));
+            h = run_check(w.p);
+            if (h.bad_weight < h.bad_target)
+                throw std::invalid_argument("edge " + std::to_string(h.bad_weight) +
+                                            " has non-finite weight");
+            throw std::invalid_argument("edge " + std::to_string(h.bad_target) +
+                                        " endpoint out of range");
         }
-        exact = h.non_integral == 0;
     }
     if (std::getenv("OCM_PREP_TIMING")) {
         const auto t0 = std::chrono::steady_clock::now();
@@ -975,19 +993,22 @@ void device_prepare(const HostCsr& g, const ocm_solve_options& opt, DeviceState&
         std::fprintf(stderr, "{\"upload_wait_ms\": %.3f}\n",
                      std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
     }
-    device_prepare_csr(n, m, row, tgt, w, exact, opt, d, info, w_ready);
+    device_prepare_csr(n, m, row, tgt, w, exactness, opt, d, info, w_ready);
     info.h2d_bytes = (std::size_t(n) + 1) * (g.index64 ? 8 : 4) + m * 12;
 }
 
 void device_prepare_csr(std::uint32_t n, std::uint64_t m, DBuf<std::uint32_t>& row,
-                        DBuf<std::uint32_t>& tgt, DBuf<double>& w, bool integer_exact,
+                        DBuf<std::uint32_t>& tgt, DBuf<double>& w, int exactness,
                         const ocm_solve_options& opt, DeviceState& d, PrepInfo& info,
                         cudaEvent_t w_ready) {
     cudaStream_t s = d.stream;
     const int sms = d.sms;
     info.n = n;
     info.scc_off = opt.scc == OCM_SCC_OFF;
-    info.exact = integer_exact;
+    // exactness: 1 integer weights, 0 float, -1 unknown (caller-provided
+    // arrays: derived, with the non-finite check, where the weights are
+    // first read)
+    info.exact = exactness == 1;
     info.h2d_bytes = 0;
     const double sign = opt.objective == OCM_MAXIMIZE ? -1.0 : 1.0;
     const int gv = grid_for(n, sms);
@@ -1015,9 +1036,17 @@ void device_prepare_csr(std::uint32_t n, std::uint64_t m, DBuf<std::uint32_t>& r
             return;
         if (w_ready)
             CK(cudaStreamWaitEvent(s, w_ready, 0));
+        if (exactness < 0)
+            CK(cudaMemsetAsync(&pcd.p->bad_weight_edge, 0xff, sizeof(unsigned long long), s));
         if (m)
-            kp_max_abs<<<grid_for(m, sms, 16), kBlock, 0, s>>>(m, w.p, pcd.p);
+            kp_max_abs<<<grid_for(m, sms, 16), kBlock, 0, s>>>(m, w.p, pcd.p, exactness < 0);
         read_pc();
+        if (exactness < 0) {
+            if (pc.bad_weight_edge != ~0ull)
+                throw std::invalid_argument("edge " + std::to_string(pc.bad_weight_edge) +
+                                            " has non-finite weight");
+            info.exact = pc.non_integral == 0;
+        }
         unsigned long long bits = pc.max_abs_bits;
         std::memcpy(&max_abs, &bits, sizeof max_abs);
         have_max_abs = true;

@@ -339,6 +339,11 @@ def test_solve_csr_validates_like_build_graph():
     with pytest.raises(ValueError, match="offsets"):
         P.solve_csr(2, np.array([0, 2, 1], np.uint32), np.array([1, 0], np.uint32),
                     np.array([1.0, 2.0]))
+    # the first bad edge in id order wins, as in build_graph's loop
+    with pytest.raises(ValueError, match="edge 0 has non-finite weight"):
+        P.solve_csr(2, idx, np.array([1, 5], np.uint32), np.array([np.inf, 2.0]))
+    with pytest.raises(ValueError, match="edge 0 endpoint out of range"):
+        P.solve_csr(2, idx, np.array([7, 1], np.uint32), np.array([1.0, np.nan]))
     # exactness is derived on the device: 2.5 makes the graph a float graph
     s = P.solve_csr(2, idx, np.array([1, 0], np.uint32), np.array([2.5, 2.0]))
     assert s.has_cycle and not s.exact and s.mu == 2.25
