@@ -1109,7 +1109,7 @@ __device__ __forceinline__ void ph_mark(const KP& p, std::uint64_t nC, int in, s
     constexpr int kR = 4;
     const std::uint64_t nth = gstride();
     for (std::uint64_t i0 = gtid(); i0 < nC; i0 += kR * nth) {
-        std::uint32_t v[kR], j[kR], mn[kR];
+        std::uint32_t v[kR], j[kR];
 #pragma unroll
         for (int r = 0; r < kR; ++r)
             v[r] = i0 + r * nth < nC ? p.clist[i0 + r * nth] : NONE;
@@ -1118,14 +1118,9 @@ __device__ __forceinline__ void ph_mark(const KP& p, std::uint64_t nC, int in, s
             if (v[r] != NONE)
                 j[r] = a[v[r]].nxt;
 #pragma unroll
-        for (int r = 0; r < kR; ++r)
-            if (v[r] != NONE)
-                mn[r] = a[j[r]].mn;
-#pragma unroll
         for (int r = 0; r < kR; ++r) {
             if (v[r] == NONE)
                 continue;
-            p.comp[v[r]] = mn[r];
             // many vertices share j: read before the exchange; the first
             // marker lists j, so M is enumerated without another full pass.
             // Only M's (length, weight) records are cleared: the anchors the
@@ -1142,9 +1137,10 @@ __device__ __forceinline__ void ph_mark(const KP& p, std::uint64_t nC, int in, s
 
 // The last doubling pass fused with the mark phase: each core vertex
 // takes S more doubling steps (2^S chained reads of the input records) and
-// then the anchor of its window, rebuilding its image j's record of the new
-// level from the same input records (another 2^S reads, least vertex only)
-// -- one phase and one barrier fewer per verification.
+// marks its image j -- one phase and one barrier fewer per verification.
+// Anchors are only needed on M: the check reads them from the final
+// records (a cycle vertex's record of L steps covers its window), and every
+// other vertex finds its anchor at its image jump(v) in M.
 template <int S>
 __device__ __forceinline__ void ph_round_mark(const KP& p, std::uint64_t nC, int in, std::uint32_t stamp,
                                               bool exact, const Ring& rl) {
@@ -1162,14 +1158,6 @@ __device__ __forceinline__ void ph_round_mark(const KP& p, std::uint64_t nC, int
         }
         o[v] = z;
         const std::uint32_t j = z.nxt;
-        std::uint32_t u = j, mn = NONE;
-#pragma unroll
-        for (int h = 0; h < (1 << S); ++h) {
-            const PJC y = a[u];
-            mn = min(mn, y.mn);
-            u = y.nxt;
-        }
-        p.comp[v] = mn;
         if (p.cmark[j] != stamp && atomicExch(&p.cmark[j], stamp) != stamp) {
             p.wlist[warp_append(rl)] = j;
             p.cyc_len[j] = 0;
@@ -1183,7 +1171,7 @@ __device__ __forceinline__ void ph_round_mark(const KP& p, std::uint64_t nC, int
 // lane -- the per-anchor (length, weight) records (howard_par.hpp:319).
 template <int MODE>
 __device__ __forceinline__ void ph_check(const KP& p, std::uint64_t nM, std::uint32_t stamp,
-                                         unsigned* flag, const Ring& rs) {
+                                         unsigned* flag, const Ring& rs, const PJC* fin) {
     constexpr bool EXACT = MODE != 0;
     bool fail = false;
     unsigned fresh = 0;
@@ -1196,8 +1184,10 @@ __device__ __forceinline__ void ph_check(const KP& p, std::uint64_t nM, std::uin
         if (on) {
             v = p.wlist[i];
             const std::uint32_t s = p.succ_v[v];
-            a = p.comp[v];
-            fail |= p.comp[s] != a;
+            // v's anchor: the least vertex of the window of L steps from v
+            a = fin[v].mn;
+            fail |= fin[s].mn != a;
+            p.comp[v] = a;
             if (p.cmark2[s] != stamp && atomicExch(&p.cmark2[s], stamp) != stamp)
                 ++fresh;
         }
@@ -1520,7 +1510,7 @@ __device__ __forceinline__ void ph_vote(const KP& p, std::uint64_t nM, std::uint
 // global round trips beyond the adoption's own.
 template <int MODE>
 __device__ __forceinline__ bool vote_small(const KP& p, unsigned nM, std::uint32_t stamp,
-                                           unsigned* vflag = nullptr) {
+                                           const PJC* fin, unsigned* vflag = nullptr) {
     constexpr bool EXACT = MODE != 0;
     auto& s_key = wc_key;
     auto& s_val = wc_val;
@@ -1535,9 +1525,10 @@ __device__ __forceinline__ bool vote_small(const KP& p, unsigned nM, std::uint32
     long long w = 0;
     if (i < nM) {
         v = p.wlist[i];
-        an = p.comp[v];
+        an = fin[v].mn; // the window of L steps from v (see ph_check)
         sv = p.succ_v[v];
         w = succ_w<MODE>(p, v);
+        p.comp[v] = an;
     }
     if (vflag) {
         // the check phase's work for these few vertices (ph_check): (B)
@@ -1546,7 +1537,7 @@ __device__ __forceinline__ bool vote_small(const KP& p, unsigned nM, std::uint32
         bool fail = false;
         int fresh = 0;
         if (i < nM) {
-            fail = p.comp[sv] != an;
+            fail = fin[sv].mn != an;
             fresh = p.cmark2[sv] != stamp && atomicExch(&p.cmark2[sv], stamp) != stamp;
             atomicAdd(&p.cyc_len[an], 1u);
             atomicAdd(reinterpret_cast<unsigned long long*>(&p.cyc_wi[an]),
@@ -1649,11 +1640,11 @@ constexpr std::uint64_t kVoteOneBlock = 4096;
 
 template <int MODE>
 __device__ __forceinline__ void ph_vote_one_block(const KP& p, std::uint64_t nM, std::uint32_t stamp,
-                                                  unsigned* vflag = nullptr) {
+                                                  const PJC* fin, unsigned* vflag = nullptr) {
     constexpr bool EXACT = MODE != 0;
     __shared__ unsigned s_maxlen, s_nw;
     if (EXACT && p.R == 1 && nM <= blockDim.x) {
-        if (vote_small<MODE>(p, static_cast<unsigned>(nM), stamp, vflag))
+        if (vote_small<MODE>(p, static_cast<unsigned>(nM), stamp, fin, vflag))
             return;
         // a winning cycle too long for shared memory: list it and take the
         // general path (adoption is already done)
@@ -1714,7 +1705,8 @@ __device__ __forceinline__ void ph_keep(const KP& p, std::uint64_t nC, std::uint
         if (i < nC) {
             v = p.clist[i];
             const std::uint32_t r = p.R == 1 ? 0u : __ldg(&p.reg[v]);
-            const bool kept = p.comp[v] == p.src[r];
+            // v's anchor is its image's in M (jump(v) lies on v's cycle)
+            const bool kept = p.comp[a[v].nxt] == p.src[r];
             p.conn[v] = kept ? 0u : NONE;
             p.indeg[v] = 0;
             take = !kept;
@@ -1725,9 +1717,7 @@ __device__ __forceinline__ void ph_keep(const KP& p, std::uint64_t nC, std::uint
             v = p.plist[i - nC];
             const std::uint32_t s = p.succ_v[v];
             const std::uint32_t r = p.R == 1 ? 0u : __ldg(&p.reg[v]);
-            const std::uint32_t an = p.comp[s];
-            const bool kept = an == p.src[r];
-            p.comp[v] = an;
+            const bool kept = p.comp[a[s].nxt] == p.src[r];
             p.conn[v] = kept ? 0u : NONE;
             take = !kept;
             if constexpr (EXACT)
@@ -2138,14 +2128,14 @@ __global__ void __launch_bounds__(kBlock, kSolveMinBlocks) k_solve(KP p, int mod
                 // check passes, votes, adopts and values the winning cycle
                 // in the same phase
                 if (blockIdx.x == 0)
-                    ph_vote_one_block<MODE>(p, nM, stamp, vflag);
+                    ph_vote_one_block<MODE>(p, nM, stamp, p.pj[in], vflag);
                 sync(PH_VERIFY);
                 if (ldr(*vflag) != stamp) {
                     voted = true;
                     break;
                 }
             } else {
-                ph_check<MODE>(p, nM, stamp, vflag, st.rc);
+                ph_check<MODE>(p, nM, stamp, vflag, st.rc, p.pj[in]);
                 sync(PH_VERIFY);
                 const std::uint64_t s_size = st.rc.take();
                 if (ldr(*vflag) != stamp && s_size == nM)
@@ -2180,7 +2170,7 @@ __global__ void __launch_bounds__(kBlock, kSolveMinBlocks) k_solve(KP p, int mod
             }
             if (nM <= kVoteOneBlock) {
                 if (blockIdx.x == 0)
-                    ph_vote_one_block<MODE>(p, nM, stamp);
+                    ph_vote_one_block<MODE>(p, nM, stamp, p.pj[in]);
             } else {
                 ph_vote<MODE>(p, nM, stamp, st.done_base);
                 st.done_base += gridDim.x;
