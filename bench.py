@@ -631,6 +631,9 @@ def main():
                 e2e_edges += s.stats.m_solved * s.stats.spf_passes
                 h2d += s.stats.h2d_bytes
                 d2h += s.stats.d2h_bytes
+                if os.environ.get("OCM_BENCH_E2E_TRACE"):
+                    sys.stderr.write(f"e2e {o}: {1e3 * (time.perf_counter() - t0):.3f} ms "
+                                     f"device {s.stats.device_ms:.3f} prep {s.stats.host_prep_ms:.3f}\n")
             e2e_s += time.perf_counter() - t0
         e2e = (e2e_s, e2e_edges, h2d // e2e_steps, d2h // e2e_steps)
         del hidx, hd, hw, idx64, g

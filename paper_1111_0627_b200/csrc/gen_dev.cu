@@ -4,6 +4,7 @@
 
 #include <cub/cub.cuh>
 
+#include <functional>
 #include <stdexcept>
 
 #include "../../include/ocm_b200.h"
@@ -15,7 +16,8 @@ namespace ocmb {
 void device_prepare_csr(std::uint32_t n, std::uint64_t m, DBuf<std::uint32_t>& row,
                         DBuf<std::uint32_t>& tgt, DBuf<double>& w, int exactness,
                         const ocm_solve_options& opt, DeviceState& d, PrepInfo& info,
-                        cudaEvent_t w_ready = nullptr);
+                        cudaEvent_t w_ready = nullptr,
+                        const std::function<void()>& w_host_done = nullptr);
 
 namespace {
 

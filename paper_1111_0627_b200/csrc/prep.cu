@@ -21,6 +21,8 @@
 
 #include <cstring>
 #include <condition_variable>
+#include <exception>
+#include <functional>
 #include <memory>
 #include <mutex>
 #include <thread>
@@ -45,7 +47,8 @@ void device_prepare(const HostCsr& g, const ocm_solve_options& opt, DeviceState&
 void device_prepare_csr(std::uint32_t n, std::uint64_t m, DBuf<std::uint32_t>& row,
                         DBuf<std::uint32_t>& tgt, DBuf<double>& w, int exactness,
                         const ocm_solve_options& opt, DeviceState& d, PrepInfo& info,
-                        cudaEvent_t w_ready = nullptr);
+                        cudaEvent_t w_ready = nullptr,
+                        const std::function<void()>& w_host_done = nullptr);
 
 namespace {
 
@@ -940,6 +943,27 @@ void device_prepare(const HostCsr& g, const ocm_solve_options& opt, DeviceState&
         }
     } side_guard{d};
     bool exact = g.integer_exact;
+    // the weights (2/3 of the bytes) are staged by a host thread of their own
+    // while this one goes on to launch the region split; whoever first needs
+    // them joins it (the event is recorded by then). Declared after w and
+    // the side-stream guard: on any exit the thread is joined first.
+    struct WeightStager {
+        std::thread th;
+        std::exception_ptr err;
+        void join() {
+            if (th.joinable())
+                th.join();
+            if (err) {
+                auto e = err;
+                err = nullptr;
+                std::rethrow_exception(e);
+            }
+        }
+        ~WeightStager() {
+            if (th.joinable())
+                th.join();
+        }
+    } wstage;
     if (m) {
         ring.copy(tgt.p, g.target, m * 4, s);
         if (!d.side) {
@@ -947,8 +971,18 @@ void device_prepare(const HostCsr& g, const ocm_solve_options& opt, DeviceState&
             CK(cudaEventCreateWithFlags(&d.side_done, cudaEventDisableTiming));
         }
         CK(cudaStreamWaitEvent(d.side, d.ev_alloc_done(s), 0)); // w allocated on s
-        ring.copy(w.p, g.weight, m * 8, d.side);
-        CK(cudaEventRecord(d.side_done, d.side));
+        const int dev = d.device;
+        cudaStream_t side = d.side;
+        cudaEvent_t done = d.side_done;
+        wstage.th = std::thread([&ring, &wstage, &w, &g, m, dev, side, done] {
+            try {
+                CK(cudaSetDevice(dev));
+                ring.copy(w.p, g.weight, m * 8, side);
+                CK(cudaEventRecord(done, side));
+            } catch (...) {
+                wstage.err = std::current_exception();
+            }
+        });
         w_ready = d.side_done;
     }
     if (g.index64) {
@@ -977,6 +1011,7 @@ void device_prepare(const HostCsr& g, const ocm_solve_options& opt, DeviceState&
         if (h.bad_target != ~0ull) {
             // report the first bad edge in id order, as build_graph's loop
             // does: a non-finite weight on an earlier edge comes first
+            wstage.join();
             if (w_ready)
                 CK(cudaStreamWaitEvent(s, w_ready, 0));
             h = run_check(w.p);
@@ -993,14 +1028,16 @@ void device_prepare(const HostCsr& g, const ocm_solve_options& opt, DeviceState&
         std::fprintf(stderr, "{\"upload_wait_ms\": %.3f}\n",
                      std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
     }
-    device_prepare_csr(n, m, row, tgt, w, exactness, opt, d, info, w_ready);
+    device_prepare_csr(n, m, row, tgt, w, exactness, opt, d, info, w_ready,
+                       [&wstage] { wstage.join(); });
+    wstage.join();
     info.h2d_bytes = (std::size_t(n) + 1) * (g.index64 ? 8 : 4) + m * 12;
 }
 
 void device_prepare_csr(std::uint32_t n, std::uint64_t m, DBuf<std::uint32_t>& row,
                         DBuf<std::uint32_t>& tgt, DBuf<double>& w, int exactness,
                         const ocm_solve_options& opt, DeviceState& d, PrepInfo& info,
-                        cudaEvent_t w_ready) {
+                        cudaEvent_t w_ready, const std::function<void()>& w_host_done) {
     cudaStream_t s = d.stream;
     const int sms = d.sms;
     info.n = n;
@@ -1034,6 +1071,8 @@ void device_prepare_csr(std::uint32_t n, std::uint64_t m, DBuf<std::uint32_t>& r
     auto need_weights = [&] {
         if (have_max_abs)
             return;
+        if (w_host_done)
+            w_host_done(); // the host thread staging the weights has enqueued them
         if (w_ready)
             CK(cudaStreamWaitEvent(s, w_ready, 0));
         if (exactness < 0)

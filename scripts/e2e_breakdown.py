@@ -21,6 +21,9 @@ else:
     g = P.generate_uniform(n, 8, 1, 100, 1111_0627)
 idx64, tgt, w = g.csr()
 idx = idx64.astype(np.uint32)
+# ocm_solve pins the graph's own arrays (cudaHostRegister); the CSR leg gets
+# private pageable copies, as a reference ocm::Graph would be
+tgt, w = tgt.copy(), w.copy()
 # host memcpy rate of this box (pageable -> pageable), for reference
 buf = np.empty_like(w)
 t0 = time.perf_counter()
@@ -36,3 +39,11 @@ for name, call in (("ocm_solve", lambda: P.solve(g, P.SolveOptions(objective="mi
         t1 = time.perf_counter()
         print(f"{name}: e2e_ms={1e3 * (t1 - t0):.3f} device_ms={s.stats.device_ms:.3f} "
               f"prep_ms={s.stats.host_prep_ms:.3f} h2d={s.stats.h2d_bytes}", file=sys.stderr)
+# the bench's e2e loop: min then max per step, timed per call
+for step in range(4):
+    for o in ("min", "max"):
+        t0 = time.perf_counter()
+        s = P.solve_csr(g.n, idx, tgt, w, P.SolveOptions(objective=o))
+        t1 = time.perf_counter()
+        print(f"step {step} {o}: e2e_ms={1e3 * (t1 - t0):.3f} device_ms={s.stats.device_ms:.3f} "
+              f"prep_ms={s.stats.host_prep_ms:.3f}", file=sys.stderr)
