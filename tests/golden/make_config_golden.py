@@ -52,6 +52,11 @@ CONFIGS = {
     "2": dict(kind="uniform", n=1_000_000, deg=8),
     "3": dict(kind="model", scenario="server", clients=19),
     "4s": dict(kind="powerlaw-hubs", n=1_000_000, deg=8, dmax=1 << 20),
+    # the same config-2 graph through the reference's other options: float
+    # weights (w/8 + 1/8: FloatMode, exact dyadic inputs) and --scc off
+    # (the Hamiltonian-augmented single region, solve.cpp:48)
+    "2f": dict(kind="uniform", n=1_000_000, deg=8, weights="float"),
+    "2off": dict(kind="uniform", n=1_000_000, deg=8, scc="off"),
 }
 
 
@@ -59,6 +64,8 @@ def graph(cfg):
     c = CONFIGS[cfg]
     if c["kind"] == "uniform":
         s, d, w = O.generate_uniform(c["n"], c["deg"], 1, 100, SEED)
+        if c.get("weights") == "float":
+            w = w / 8 + 0.125
         return c["n"], s, d, w
     if c["kind"] == "model":
         return O.generate_model(c["scenario"], c["clients"])
@@ -79,7 +86,7 @@ def solve(job):
     cfg, objective = job
     n, s, d, w = graph(cfg)
     t0 = time.time()
-    r = O.ref_solve(n, s, d, w, "howard", objective, "tarjan")
+    r = O.ref_solve(n, s, d, w, "howard", objective, CONFIGS[cfg].get("scc", "tarjan"))
     wall = time.time() - t0
     return cfg, objective, {
         "has_cycle": r.has_cycle, "exact": r.exact, "mu_num": r.mu_num, "mu_den": r.mu_den,
