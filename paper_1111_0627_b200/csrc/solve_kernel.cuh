@@ -54,6 +54,9 @@ namespace cg = cooperative_groups;
 #define OCM_MINB 4
 #endif
 constexpr int kSolveMinBlocks = OCM_MINB; // 4: register cap 64 at 256 threads
+#ifndef OCM_HOIST_DEN
+#define OCM_HOIST_DEN 1
+#endif
 #ifndef OCM_KSHRINK
 #define OCM_KSHRINK 2
 #endif
@@ -274,7 +277,8 @@ __device__ __forceinline__ bool hot_find(const KP& p, std::uint32_t t, long long
 // edge ebase + i, and b / e_end are the vertex's offsets read from there.
 template <int MODE, int G, int U, bool HOT, bool STAGED = false>
 __device__ __forceinline__ void improve_vertex(const KP& p, int* changed, ChangedMarks& marks,
-                                               std::uint32_t v, const int2* sedge = nullptr,
+                                               std::uint32_t v, long long den1,
+                                               const int2* sedge = nullptr,
                                                std::uint32_t ebase = 0, std::uint32_t sb = 0,
                                                std::uint32_t se = 0) {
     // Register budget matters here (64 at 4 CTAs/SM): edges stay packed as
@@ -313,7 +317,7 @@ __device__ __forceinline__ void improve_vertex(const KP& p, int* changed, Change
     long long den = 1;
     double lam = 0.0;
     if constexpr (EXACT)
-        den = p.lam_den[r];
+        den = OCM_HOIST_DEN && p.R == 1 ? den1 : p.lam_den[r]; // den1: region 0's, read once
     else
         lam = p.lam_f[r];
     Key best = 0, curc = 0;
@@ -794,6 +798,7 @@ __device__ __forceinline__ void improve_staged(const KP& p, int* changed, Change
     const std::uint32_t lo = p.own_lo, hi = p.own_hi;
     const std::uint32_t nch = (hi - lo + VC - 1) / VC;
     unsigned par[2] = {st.par[0], st.par[1]};
+    const long long den1 = p.lam_den[0];
     std::uint32_t c = blockIdx.x;
     int k = 0;
     if (threadIdx.x == 0 && c < nch)
@@ -809,11 +814,11 @@ __device__ __forceinline__ void improve_staged(const KP& p, int* changed, Change
             par[k] ^= 1;
             if (v < st.v1[k]) {
                 const std::uint32_t r0 = v - st.rbase[k];
-                improve_vertex<1, G, U, false, true>(p, changed, marks, v, st.edge[k], st.ebase[k],
+                improve_vertex<1, G, U, false, true>(p, changed, marks, v, den1, st.edge[k], st.ebase[k],
                                                         st.row[k][r0], st.row[k][r0 + 1]);
             }
         } else if (v < st.v1[k]) {
-            improve_vertex<1, G, U, false>(p, changed, marks, v);
+            improve_vertex<1, G, U, false>(p, changed, marks, v, den1);
         }
         __syncthreads(); // stage k is consumed before it is refilled
     }
@@ -872,12 +877,13 @@ template <int MODE, int G, int U> __device__ __forceinline__ void improve_phase(
         }
     }
     const std::size_t gs = gstride() / G;
+    const long long den1 = MODE != 0 ? p.lam_den[0] : 1;
     if (hot) {
         for (std::size_t vv = p.own_lo + gtid() / G; vv < p.own_hi; vv += gs)
-            improve_vertex<MODE, G, U, true>(p, changed, marks, static_cast<std::uint32_t>(vv));
+            improve_vertex<MODE, G, U, true>(p, changed, marks, static_cast<std::uint32_t>(vv), den1);
     } else {
         for (std::size_t vv = p.own_lo + gtid() / G; vv < p.own_hi; vv += gs)
-            improve_vertex<MODE, G, U, false>(p, changed, marks, static_cast<std::uint32_t>(vv));
+            improve_vertex<MODE, G, U, false>(p, changed, marks, static_cast<std::uint32_t>(vv), den1);
     }
     marks.flush(p, changed);
 }
@@ -1698,8 +1704,9 @@ __device__ __forceinline__ void ph_keep(const KP& p, std::uint64_t nC, std::uint
     const PJC* a = p.pj[in];
     bool ovf = false;
     const std::uint64_t tot = nC + nL;
-    OCM_BLOCK_LOOP(i0, 0, tot) {
-        const std::uint64_t i = i0_b + threadIdx.x;
+    // re-attachment candidates are appended per warp (no block barrier per
+    // 256 items: list order does not matter to the layer discipline)
+    for (std::uint64_t i = gtid(); i < tot; i += gstride()) {
         bool take = false;
         std::uint32_t v = 0;
         if (i < nC) {
@@ -1713,7 +1720,7 @@ __device__ __forceinline__ void ph_keep(const KP& p, std::uint64_t nC, std::uint
             if constexpr (EXACT)
                 if (kept && p.cmark[v] != stamp)
                     key_st<MODE>(p, v, core_key<MODE>(p, a, v, r, stamp, L, ovf));
-        } else if (i < tot) {
+        } else {
             v = p.plist[i - nC];
             const std::uint32_t s = p.succ_v[v];
             const std::uint32_t r = p.R == 1 ? 0u : __ldg(&p.reg[v]);
@@ -1729,9 +1736,8 @@ __device__ __forceinline__ void ph_keep(const KP& p, std::uint64_t nC, std::uint
                     key_st<MODE>(p, v, static_cast<KeyT<MODE>>(kk));
                 }
         }
-        const std::uint64_t slot = block_append(take, ring);
         if (take)
-            p.rem[0][slot] = v;
+            p.rem[0][warp_append(ring)] = v;
     }
     block_flag(ovf, &p.c->overflow, 1);
 }
@@ -1746,6 +1752,9 @@ __device__ __forceinline__ void ph_attach(const KP& p, int cur, std::uint64_t pe
     constexpr bool EXACT = MODE != 0;
     const std::uint32_t* list = p.rem[cur];
     bool ovf = false;
+    // block-ordered appends: the next layer's list keeps the vertex order of
+    // this one (warp-order appends measured 12% slower at config 5, where
+    // layers are long and the row/edge reads profit from the order)
     OCM_BLOCK_LOOP(i0, 0, pending) {
         const std::uint64_t i = i0_b + threadIdx.x;
         bool pend = false;
