@@ -169,6 +169,12 @@ int ocm_solve(const ocm_graph* g, const ocm_solve_options* opt, ocm_solution* ou
 int ocm_solve_csr(uint32_t n, uint32_t m, const uint32_t* fwd_index, const uint32_t* fwd_target,
                   const double* fwd_weight, const ocm_solve_options* opt, ocm_solution* out,
                   uint32_t* cycle_buf, uint32_t cycle_cap);
+/* A resident session on the reference's CSR arrays (as ocm_solve_csr; the
+ * arrays are only read during the call): repeated solves reuse the prepared
+ * graph in HBM (ocm_session_solve / _values / _certify / _free). */
+int ocm_session_create_csr(uint32_t n, uint32_t m, const uint32_t* fwd_index,
+                           const uint32_t* fwd_target, const double* fwd_weight,
+                           const ocm_solve_options* opt, ocm_session** out);
 
 /* Resident sessions: create uploads the region-compacted CSR into HBM once;
  * each solve re-runs policy iteration from the initial policy on the device. */

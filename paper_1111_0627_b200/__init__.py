@@ -156,6 +156,8 @@ def _load():
         "ocm_solve": (C.c_int, [C.c_void_p, P(_Opts), P(_Sol), P(C.c_uint32), C.c_uint32]),
         "ocm_solve_csr": (C.c_int, [C.c_uint32, C.c_uint32, P(C.c_uint32), P(C.c_uint32),
                                     P(C.c_double), P(_Opts), P(_Sol), P(C.c_uint32), C.c_uint32]),
+        "ocm_session_create_csr": (C.c_int, [C.c_uint32, C.c_uint32, P(C.c_uint32), P(C.c_uint32),
+                                             P(C.c_double), P(_Opts), P(C.c_void_p)]),
         "ocm_session_create": (C.c_int, [C.c_void_p, P(_Opts), P(C.c_void_p)]),
         "ocm_session_solve": (C.c_int, [C.c_void_p, P(_Sol), P(C.c_uint32), C.c_uint32]),
         "ocm_session_values": (C.c_int, [C.c_void_p, P(C.c_int64), P(C.c_int64), P(C.c_int64),
@@ -185,7 +187,7 @@ EXPORTED_SYMBOLS = (
     "ocm_session_shard_fused_launch", "ocm_session_shard_fused_finish",
     "ocm_graph_free", "ocm_graph_n", "ocm_graph_m", "ocm_graph_integer_exact", "ocm_graph_edges",
     "ocm_graph_csr",
-    "ocm_solve", "ocm_solve_csr", "ocm_session_create", "ocm_session_solve", "ocm_session_values",
+    "ocm_solve", "ocm_solve_csr", "ocm_session_create_csr", "ocm_session_create", "ocm_session_solve", "ocm_session_values",
     "ocm_session_stream", "ocm_session_free", "ocm_session_certify", "ocm_session_keys_wide",
     "ocm_session_is_wide",
 )
@@ -529,6 +531,26 @@ class Session:
         h = C.c_void_p()
         _check(_lib.ocm_session_create(g._h, C.byref(self.opt._c()), C.byref(h)))
         self._h = h
+
+    @classmethod
+    def from_csr(cls, n: int, fwd_index, fwd_target, fwd_weight,
+                 opt: Optional[SolveOptions] = None) -> "Session":
+        """Session on the reference's CSR arrays (ocm::Graph fwd_index /
+        fwd_target / fwd_weight), checked on the device like build_graph."""
+        self = cls.__new__(cls)
+        self.opt = opt or SolveOptions()
+        idx = np.ascontiguousarray(fwd_index, np.uint32)
+        tgt = np.ascontiguousarray(fwd_target, np.uint32)
+        w = np.ascontiguousarray(fwd_weight, np.float64)
+        if idx.shape[0] != int(n) + 1 or tgt.shape[0] != w.shape[0]:
+            raise ValueError("CSR arrays: fwd_index needs n+1 entries, fwd_target and fwd_weight m each")
+        h = C.c_void_p()
+        _check(_lib.ocm_session_create_csr(int(n), tgt.shape[0], _p(idx, C.c_uint32),
+                                           _p(tgt, C.c_uint32), _p(w, C.c_double),
+                                           C.byref(self.opt._c()), C.byref(h)))
+        self._h = h
+        self.n = int(n)
+        return self
 
     @classmethod
     def generated(cls, spec: Generator, opt: Optional[SolveOptions] = None) -> "Session":

@@ -370,4 +370,23 @@ int ocm_solve_csr(uint32_t n, uint32_t m, const uint32_t* fwd_index, const uint3
     });
 }
 
+int ocm_session_create_csr(uint32_t n, uint32_t m, const uint32_t* fwd_index,
+                           const uint32_t* fwd_target, const double* fwd_weight,
+                           const ocm_solve_options* opt, ocm_session** out) {
+    return guard([&] {
+        if (!out || !fwd_index || (m && (!fwd_target || !fwd_weight)))
+            throw std::invalid_argument("null CSR array or output");
+        ocmb::HostCsr h;
+        h.n = n;
+        h.m = m;
+        h.index32 = fwd_index;
+        h.target = fwd_target;
+        h.weight = fwd_weight;
+        h.validated = false;
+        auto s = std::make_unique<ocm_session>();
+        s->s = std::make_unique<ocmb::Session>(h, defaults(opt));
+        *out = s.release();
+    });
+}
+
 } // extern "C"

@@ -439,3 +439,23 @@ def test_wide_lane_certificate_and_generated_graph(monkeypatch):
     assert (sa.mu_exact, sa.cycle_vertices, sa.stats.spf_passes) == \
         (sb.mu_exact, sb.cycle_vertices, sb.stats.spf_passes)
     assert a.keys_wide().tolist() == [int(x) for x in b.values()["key_num"]]
+
+
+def test_session_from_reference_csr():
+    """ocm_session_create_csr: a resident session on the reference's CSR
+    arrays solves, re-solves and certifies like a session on the graph."""
+    g = P.generate(P.Generator("powerlaw", n=40_000, deg=4, dmax=4_000, seed=13))
+    idx, d, w = _csr(g)
+    for objective in ("min", "max"):
+        a = P.Session(g, P.SolveOptions(objective=objective))
+        b = P.Session.from_csr(g.n, idx, d, w, P.SolveOptions(objective=objective))
+        for _ in range(2):
+            sa, sb = a.solve(), b.solve()
+            assert (sa.mu_exact, sa.cycle_vertices, sa.stats.spf_passes) == \
+                (sb.mu_exact, sb.cycle_vertices, sb.stats.spf_passes)
+        assert np.array_equal(a.values()["key_num"], b.values()["key_num"])
+        c = b.certify()
+        assert c["key_violations"] == c["policy_violations"] == c["cycle_violations"] == 0
+    with pytest.raises(ValueError, match="endpoint out of range"):
+        P.Session.from_csr(2, np.array([0, 1, 2], np.uint32), np.array([1, 9], np.uint32),
+                           np.array([1.0, 1.0]))
