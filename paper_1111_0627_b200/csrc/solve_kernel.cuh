@@ -64,6 +64,34 @@ constexpr int kSolveMinBlocks = OCM_MINB; // 4: register cap 64 at 256 threads
 // step shallower
 constexpr unsigned kKShrink = OCM_KSHRINK;
 
+// Policy in-degree is only ever tested for zero (leaf split): with
+// OCM_PRED_FLAG a vertex with a predecessor gets a byte flag (plain store,
+// one byte per vertex in the indeg buffer) instead of an atomic counter.
+#ifndef OCM_PRED_FLAG
+#define OCM_PRED_FLAG 1
+#endif
+__device__ __forceinline__ void mark_pred(const KP& p, std::uint32_t t) {
+#if OCM_PRED_FLAG
+    reinterpret_cast<unsigned char*>(p.indeg)[t] = 1;
+#else
+    atomicAdd(&p.indeg[t], 1u);
+#endif
+}
+__device__ __forceinline__ bool has_pred(const KP& p, std::uint32_t v) {
+#if OCM_PRED_FLAG
+    return reinterpret_cast<const unsigned char*>(p.indeg)[v] != 0;
+#else
+    return p.indeg[v] != 0;
+#endif
+}
+__device__ __forceinline__ void clear_pred(const KP& p, std::uint32_t v) {
+#if OCM_PRED_FLAG
+    reinterpret_cast<unsigned char*>(p.indeg)[v] = 0;
+#else
+    p.indeg[v] = 0;
+#endif
+}
+
 // ------------------------------------------------------------ modes
 //
 // Arithmetic mode of a k_solve instantiation (template parameter MODE):
@@ -419,7 +447,7 @@ __device__ __forceinline__ void improve_vertex(const KP& p, int* changed, Change
             if (p.fused)
                 push_policy<MODE>(p, v, be, t, ed);
             if (p.indeg_in_improve)
-                atomicAdd(&p.indeg[t], 1u);
+                mark_pred(p, t);
             marks.note(p, changed, r);
         }
     } else if (saw_cur && p.indeg_in_improve) {
@@ -428,7 +456,7 @@ __device__ __forceinline__ void improve_vertex(const KP& p, int* changed, Change
             t = static_cast<std::uint32_t>(edge_at(cur).x);
         else
             t = edge_at(cur).t;
-        atomicAdd(&p.indeg[t], 1u);
+        mark_pred(p, t);
     }
 }
 
@@ -552,7 +580,7 @@ __device__ __forceinline__ void improve_heavy(const KP& p, int* changed) {
                         if (p.fused)
                             push_policy<MODE>(p, v, ge, static_cast<std::uint32_t>(ed.x), ed);
                         if (p.indeg_in_improve)
-                            atomicAdd(&p.indeg[ed.x], 1u);
+                            mark_pred(p, ed.x);
                     } else {
                         const FEdge ed = ld_edge(&p.fe[ge]);
                         p.succ_v[v] = ed.t;
@@ -560,11 +588,11 @@ __device__ __forceinline__ void improve_heavy(const KP& p, int* changed) {
                         if (p.fused)
                             push_policy<MODE>(p, v, ge, ed.t, ed);
                         if (p.indeg_in_improve)
-                            atomicAdd(&p.indeg[ed.t], 1u);
+                            mark_pred(p, ed.t);
                     }
                     raise_changed(p, changed, r);
                 } else if (p.indeg_in_improve) {
-                    atomicAdd(&p.indeg[p.succ_v[v]], 1u);
+                    mark_pred(p, p.succ_v[v]);
                 }
             }
         }
@@ -705,10 +733,10 @@ __device__ __forceinline__ void pb_pass2(const KP& p, int* changed) {
                 p.succ_e[v] = be;
                 p.succ_wi[v] = ed.y;
                 p.succ_v[v] = t;
-                atomicAdd(&p.indeg[t], 1u);
+                mark_pred(p, t);
                 marks.note(p, changed, r);
             } else {
-                atomicAdd(&p.indeg[p.succ_v[v]], 1u);
+                mark_pred(p, p.succ_v[v]);
             }
         }
         __syncthreads(); // shared arrays reused by the next block
@@ -1033,7 +1061,7 @@ __device__ __forceinline__ void ph_classify(const KP& p, int par, const Ring& ra
         for (int k = 0; k < kV; ++k) {
             const std::uint64_t v = base + k;
             if (v < p.N && changed[__ldg(&p.reg[v])]) {
-                if (p.indeg[v] == 0)
+                if (!has_pred(p, static_cast<std::uint32_t>(v)))
                     lbits |= 1u << k;
                 else
                     cbits |= 1u << k;
@@ -1715,7 +1743,7 @@ __device__ __forceinline__ void ph_keep(const KP& p, std::uint64_t nC, std::uint
             // v's anchor is its image's in M (jump(v) lies on v's cycle)
             const bool kept = p.comp[a[v].nxt] == p.src[r];
             p.conn[v] = kept ? 0u : NONE;
-            p.indeg[v] = 0;
+            clear_pred(p, v);
             take = !kept;
             if constexpr (EXACT)
                 if (kept && p.cmark[v] != stamp)
@@ -2083,7 +2111,7 @@ __global__ void __launch_bounds__(kBlock, kSolveMinBlocks) k_solve(KP p, int mod
             // in-degrees over the full policy (replicated on every rank)
             for (std::size_t v = gtid(); v < p.N; v += gstride())
                 if (p.changed[par][__ldg(&p.reg[v])])
-                    atomicAdd(&p.indeg[p.succ_v[v]], 1u);
+                    mark_pred(p, p.succ_v[v]);
             sync(PH_CLASSIFY);
         }
         ph_classify<MODE>(p, par, st.ra, st.rl, st.rc);
