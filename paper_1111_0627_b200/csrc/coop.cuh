@@ -42,6 +42,15 @@ __device__ __forceinline__ int ldr(const int& x) {
     asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(&x) : "memory");
     return v;
 }
+// Four consecutive 16-byte aligned control ints in one relaxed load.
+__device__ __forceinline__ int4 ldr4(const int* x) {
+    int4 v;
+    asm volatile("ld.relaxed.gpu.global.v4.s32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(x)
+                 : "memory");
+    return v;
+}
 // Data another thread may write in the same phase.
 template <class T> __device__ __forceinline__ T ldv(const T& x) {
     return *reinterpret_cast<const volatile T*>(&x);

@@ -105,6 +105,11 @@ struct Ctl {
     long long clk[PH_COUNT];       // ... per phase (time up to the phase's barrier)
 };
 constexpr std::size_t kCtlSolveOffset = offsetof(Ctl, error);
+// error, overflow, lambda_up, nonconv are read together after every
+// classification barrier (one 16-byte load)
+static_assert(offsetof(Ctl, error) % 16 == 0 && offsetof(Ctl, overflow) == offsetof(Ctl, error) + 4 &&
+                  offsetof(Ctl, lambda_up) == offsetof(Ctl, error) + 8,
+              "Ctl failure flags must form one aligned 16-byte group");
 
 // Everything a kernel may touch, passed by value.
 struct KP {

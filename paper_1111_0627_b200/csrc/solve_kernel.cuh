@@ -2121,7 +2121,8 @@ __global__ void __launch_bounds__(kBlock, kSolveMinBlocks) k_solve(KP p, int mod
         const std::uint64_t nC = st.rc.take();
         // written only by improve/adopt/keep/attach, never by the rounds
         // that follow: every block reads the same values here
-        if (n_active == 0 || ldr(c->error) || ldr(c->overflow) || ldr(c->lambda_up))
+        const int4 fl = ldr4(&c->error); // error, overflow, lambda_up, nonconv
+        if (n_active == 0 || fl.x || fl.y || fl.z)
             break; // quiet pass (or a failure the host reports)
         ++st.outer;
         st.peeled += nL;
