@@ -104,3 +104,15 @@ def test_hbm_generated_session_matches_reference(cfg):
         check(s.solve(), ref)
         cert = s.certify()
         assert cert["key_violations"] == cert["policy_violations"] == cert["cycle_violations"] == 0
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cfg", ["1", "2"])
+def test_scc_parallel_option_gives_the_reference_result(cfg):
+    """--scc parallel (the reference's trim + pivot decomposition on its
+    engine, scc.cpp:105) partitions into the same regions as Tarjan, so
+    ocm::solve returns the same answer; so does the device."""
+    g = product_graph(cfg)
+    for objective in ("min", "max"):
+        ref = GOLD["configs"][cfg]["results"][objective]
+        check(P.solve(g, P.SolveOptions(algo="howard", objective=objective, scc="parallel")), ref)
