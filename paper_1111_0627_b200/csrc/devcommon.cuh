@@ -127,6 +127,7 @@ struct KP {
     __int128* key_w;           // wide exact lane: 128-bit keys
     const int* ew_hi;          // wide exact lane: high 32 bits of each edge weight
     int* succ_whi;             // wide exact lane: high 32 bits of the policy weight
+    int2* succ_vw;             // fast exact lane, one rank: packed {head, weight} shadow of the policy
     long long* lam_num;
     long long* lam_den;
     double* lam_f;
@@ -264,6 +265,7 @@ struct DeviceState {
     DBuf<PJVW> pvw0, pvw1;
     DBuf<__int128> key_w;
     DBuf<int> ew_hi, succ_whi;
+    DBuf<int2> succ_vw;
     DBuf<PJC> pj0, pj1;
     DBuf<int2> ew;
     DBuf<FEdge> fe;
@@ -303,6 +305,7 @@ struct DeviceState {
         key_w.release();
         ew_hi.release();
         succ_whi.release();
+        succ_vw.release();
         pj0.release();
         pj1.release();
         ew.release();

@@ -149,10 +149,17 @@ template <int MODE> __device__ __forceinline__ long long succ_w(const KP& p, std
     else
         return p.succ_wi[v];
 }
-template <int MODE> __device__ __forceinline__ void succ_w_st(const KP& p, std::uint32_t v, long long w) {
+// policy weight of v whose new head is t; the fast exact lane also keeps the
+// packed {head, weight} shadow the leaf split reads at random (one sector
+// instead of two)
+template <int MODE>
+__device__ __forceinline__ void succ_w_st(const KP& p, std::uint32_t v, std::uint32_t t, long long w) {
     p.succ_wi[v] = static_cast<int>(w);
     if constexpr (MODE == 2)
         p.succ_whi[v] = static_cast<int>(w >> 32);
+    if constexpr (MODE == 1)
+        if (p.succ_vw)
+            p.succ_vw[v] = make_int2(static_cast<int>(t), static_cast<int>(w));
 }
 // keys are proven to stay inside this bound at every adoption
 template <int MODE> __device__ __forceinline__ bool key_in_range(__int128 k) {
@@ -438,7 +445,7 @@ __device__ __forceinline__ void improve_vertex(const KP& p, int* changed, Change
             std::uint32_t t;
             if constexpr (EXACT) {
                 t = static_cast<std::uint32_t>(ed.x);
-                succ_w_st<MODE>(p, v, edge_w<MODE>(p, be, ed));
+                succ_w_st<MODE>(p, v, t, edge_w<MODE>(p, be, ed));
             } else {
                 t = ed.t;
                 p.succ_wf[v] = ed.w;
@@ -576,7 +583,7 @@ __device__ __forceinline__ void improve_heavy(const KP& p, int* changed) {
                     if constexpr (EXACT) {
                         const int2 ed = __ldg(&p.ew[ge]);
                         p.succ_v[v] = static_cast<std::uint32_t>(ed.x);
-                        succ_w_st<MODE>(p, v, edge_w<MODE>(p, ge, ed));
+                        succ_w_st<MODE>(p, v, static_cast<std::uint32_t>(ed.x), edge_w<MODE>(p, ge, ed));
                         if (p.fused)
                             push_policy<MODE>(p, v, ge, static_cast<std::uint32_t>(ed.x), ed);
                         if (p.indeg_in_improve)
@@ -731,7 +738,7 @@ __device__ __forceinline__ void pb_pass2(const KP& p, int* changed) {
                 const int2 ed = __ldg(&p.ew[be]);
                 const std::uint32_t t = static_cast<std::uint32_t>(ed.x);
                 p.succ_e[v] = be;
-                p.succ_wi[v] = ed.y;
+                succ_w_st<1>(p, v, t, ed.y);
                 p.succ_v[v] = t;
                 mark_pred(p, t);
                 marks.note(p, changed, r);
@@ -1009,6 +1016,8 @@ template <int MODE> __device__ __forceinline__ void ph_init(const KP& p) {
     for (std::size_t v = tid; v < p.N; v += nth) {
         p.succ_e[v] = NONE;
         p.succ_v[v] = NONE;
+        if (MODE == 1 && p.succ_vw)
+            p.succ_vw[v] = make_int2(static_cast<int>(NONE), 0);
         key_st<MODE>(p, static_cast<std::uint32_t>(v), KeyT<MODE>(0));
         p.indeg[v] = 0;
     }
@@ -1078,11 +1087,19 @@ __device__ __forceinline__ void ph_classify(const KP& p, int par, const Ring& ra
                 // the first doubling round, straight from the policy: the
                 // successor of a core vertex is a core vertex
                 p.clist[cs++] = v;
-                const std::uint32_t sv = p.succ_v[v];
                 PJC x;
-                x.nxt = p.succ_v[sv];
-                x.mn = min(v, sv);
-                x.w = EXACT ? succ_w<MODE>(p, v) + succ_w<MODE>(p, sv) : 0ll;
+                if (MODE == 1 && p.succ_vw) {
+                    const int2 a1 = p.succ_vw[v];
+                    const int2 a2 = p.succ_vw[a1.x];
+                    x.nxt = static_cast<std::uint32_t>(a2.x);
+                    x.mn = min(v, static_cast<std::uint32_t>(a1.x));
+                    x.w = static_cast<long long>(a1.y) + a2.y;
+                } else {
+                    const std::uint32_t sv = p.succ_v[v];
+                    x.nxt = p.succ_v[sv];
+                    x.mn = min(v, sv);
+                    x.w = EXACT ? succ_w<MODE>(p, v) + succ_w<MODE>(p, sv) : 0ll;
+                }
                 p.pj[1][v] = x;
             }
         }
@@ -1814,7 +1831,7 @@ __device__ __forceinline__ void ph_attach(const KP& p, int cur, std::uint64_t pe
                     p.succ_v[x] = t;
                     if constexpr (EXACT) {
                         const long long w = edge_w<MODE>(p, e, __ldg(&p.ew[e]));
-                        succ_w_st<MODE>(p, x, w);
+                        succ_w_st<MODE>(p, x, t, w);
                         const std::uint32_t r = __ldg(&p.reg[x]);
                         const __int128 kk = static_cast<__int128>(key_ld<MODE>(p, t)) +
                                             static_cast<__int128>(w) * p.lam_den[r] - p.lam_num[r];

@@ -170,6 +170,12 @@ void Session::init(const std::function<void(DeviceState&)>& prepare) {
         d.cyc_wi.alloc(N1, d.stream);
         d.pv0.alloc(N1, d.stream);
         d.pv1.alloc(N1, d.stream);
+        if (!prep_.wide && world_ == 1) {
+            // packed {head, weight} shadow of the policy for the leaf split's
+            // random reads (kept in step by every policy write of the fast
+            // exact lane; the sharded lanes exchange the plain arrays)
+            d.succ_vw.alloc(N1, d.stream);
+        }
         if (prep_.wide) {
             if (world_ > 1)
                 throw UnsupportedError("the sharded lanes run the 64-bit exact lane only (weights "
@@ -280,6 +286,7 @@ void Session::init(const std::function<void(DeviceState&)>& prepare) {
     p.succ_v = d.succ_v.p;
     p.succ_wi = d.succ_wi.p;
     p.succ_wf = d.succ_wf.p;
+    p.succ_vw = d.succ_vw.p;
     p.key_i = d.key_i.p;
     p.key_f = d.key_f.p;
     p.lam_num = d.lam_num.p;
