@@ -64,31 +64,58 @@ constexpr int kSolveMinBlocks = OCM_MINB; // 4: register cap 64 at 256 threads
 // step shallower
 constexpr unsigned kKShrink = OCM_KSHRINK;
 
-// Policy in-degree is only ever tested for zero (leaf split): with
-// OCM_PRED_FLAG a vertex with a predecessor gets a byte flag (plain store,
-// one byte per vertex in the indeg buffer) instead of an atomic counter.
+// Policy in-degree is only ever tested for zero (leaf split). OCM_PRED_FLAG
+// selects how a vertex records that it has a predecessor:
+//   0  atomic u32 counter (round 1), reset per core vertex in keep;
+//   1  byte flag, plain store, reset per core vertex in keep;
+//   2  bit in a packed bitmap (N/8 bytes: L2-resident even at 2.5*10^8
+//      vertices), atomicOr, whole bitmap cleared by keep;
+//   3  as 2, but the bit is read first and the atomic skipped when set
+//      (hub targets).
 #ifndef OCM_PRED_FLAG
-#define OCM_PRED_FLAG 1
+#define OCM_PRED_FLAG 2
 #endif
 __device__ __forceinline__ void mark_pred(const KP& p, std::uint32_t t) {
-#if OCM_PRED_FLAG
+#if OCM_PRED_FLAG == 0
+    atomicAdd(&p.indeg[t], 1u);
+#elif OCM_PRED_FLAG == 1
     reinterpret_cast<unsigned char*>(p.indeg)[t] = 1;
 #else
-    atomicAdd(&p.indeg[t], 1u);
+    const unsigned bit = 1u << (t & 31);
+#if OCM_PRED_FLAG == 3
+    if (ldv(p.indeg[t >> 5]) & bit)
+        return;
+#endif
+    atomicOr(&p.indeg[t >> 5], bit);
 #endif
 }
 __device__ __forceinline__ bool has_pred(const KP& p, std::uint32_t v) {
-#if OCM_PRED_FLAG
+#if OCM_PRED_FLAG == 0
+    return p.indeg[v] != 0;
+#elif OCM_PRED_FLAG == 1
     return reinterpret_cast<const unsigned char*>(p.indeg)[v] != 0;
 #else
-    return p.indeg[v] != 0;
+    return (p.indeg[v >> 5] >> (v & 31)) & 1u;
 #endif
 }
+// per core vertex in keep (modes 0, 1)
 __device__ __forceinline__ void clear_pred(const KP& p, std::uint32_t v) {
-#if OCM_PRED_FLAG
+#if OCM_PRED_FLAG == 0
+    p.indeg[v] = 0;
+#elif OCM_PRED_FLAG == 1
     reinterpret_cast<unsigned char*>(p.indeg)[v] = 0;
 #else
-    p.indeg[v] = 0;
+    (void)p;
+    (void)v;
+#endif
+}
+// whole-array clear in keep (modes 2, 3)
+__device__ __forceinline__ void clear_pred_all(const KP& p) {
+#if OCM_PRED_FLAG >= 2
+    for (std::size_t w = gtid(); w < (std::size_t(p.N) + 31) / 32; w += gstride())
+        p.indeg[w] = 0;
+#else
+    (void)p;
 #endif
 }
 
@@ -1784,6 +1811,7 @@ __device__ __forceinline__ void ph_keep(const KP& p, std::uint64_t nC, std::uint
         if (take)
             p.rem[0][warp_append(ring)] = v;
     }
+    clear_pred_all(p);
     block_flag(ovf, &p.c->overflow, 1);
 }
 
