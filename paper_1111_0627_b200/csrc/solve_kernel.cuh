@@ -1948,26 +1948,39 @@ __device__ __forceinline__ void st_release(std::uint32_t* a, unsigned v) {
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a), "r"(v) : "memory");
 }
 
-constexpr int kAsyncPerThread = 32;
+#ifndef OCM_ASYNC_PER_THREAD
+#define OCM_ASYNC_PER_THREAD 16
+#endif
+constexpr int kAsyncPerThread = OCM_ASYNC_PER_THREAD;
 
 __device__ __forceinline__ void ph_fprop_async(const KP& p, int cur, std::uint64_t pending,
                                                std::uint32_t level) {
     const std::uint64_t tid = gtid(), nth = gstride();
     const std::uint32_t* list = p.rem[cur];
+    // the thread's vertices and their successors stay in registers (constant
+    // indices after unrolling), so a poll is one acquire load per vertex
+    std::uint32_t vv[kAsyncPerThread], ss[kAsyncPerThread];
     unsigned todo = 0;
-    for (int j = 0; j < kAsyncPerThread; ++j)
-        if (tid + j * nth < pending)
+#pragma unroll
+    for (int j = 0; j < kAsyncPerThread; ++j) {
+        vv[j] = ss[j] = 0;
+        if (tid + j * nth < pending) {
+            vv[j] = list[tid + j * nth];
+            ss[j] = p.succ_v[vv[j]];
             todo |= 1u << j;
+        }
+    }
     long long idle = 0;
     while (todo) {
         bool progress = false;
-        for (unsigned m = todo; m; m &= m - 1) {
-            const int j = __ffs(m) - 1;
-            const std::uint32_t v = list[tid + j * nth];
-            const std::uint32_t s = p.succ_v[v];
-            if (ld_acquire(&p.conn[s]) == NONE)
+#pragma unroll
+        for (int j = 0; j < kAsyncPerThread; ++j) {
+            if (!(todo >> j & 1u))
                 continue;
-            const double ks = __ldcg(&p.key_f[s]);
+            if (ld_acquire(&p.conn[ss[j]]) == NONE)
+                continue;
+            const std::uint32_t v = vv[j];
+            const double ks = __ldcg(&p.key_f[ss[j]]);
             p.key_f[v] = (ks + p.succ_wf[v]) - p.lam_f[p.R == 1 ? 0u : __ldg(&p.reg[v])];
             st_release(&p.conn[v], level);
             todo &= ~(1u << j);
