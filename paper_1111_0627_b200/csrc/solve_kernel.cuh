@@ -2225,7 +2225,7 @@ __global__ void __launch_bounds__(kBlock, kSolveMinBlocks) k_solve(KP p, int mod
                 // in the same phase
                 if (blockIdx.x == 0)
                     ph_vote_one_block<MODE>(p, nM, stamp, p.pj[in], vflag);
-                sync(PH_VERIFY);
+                sync(PH_VOTE); // (phase clock: the one-block check+vote)
                 if (ldr(*vflag) != stamp) {
                     voted = true;
                     break;
