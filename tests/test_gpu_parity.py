@@ -459,3 +459,21 @@ def test_session_from_reference_csr():
     with pytest.raises(ValueError, match="endpoint out of range"):
         P.Session.from_csr(2, np.array([0, 1, 2], np.uint32), np.array([1, 9], np.uint32),
                            np.array([1.0, 1.0]))
+
+
+def test_scc_off_hamiltonian_overflow_matches_reference():
+    """--scc off with weights near 2^52: the Hamiltonian weight 2n(max|w|+1)+1
+    leaves the exact doubles; the reference throws std::overflow_error
+    (graph.cpp:116), the device reports the same (OverflowError)."""
+    src = np.array([0, 1, 2], np.uint32)
+    dst = np.array([1, 2, 0], np.uint32)
+    w = np.array([2.0 ** 52 - 1, -(2.0 ** 52 - 1), 3.0])
+    if O.ref_available():
+        with pytest.raises(RuntimeError, match="hamiltonian weight too large to stay exact"):
+            O.ref_solve(3, src, dst, w, "howard", "min", "off")
+    g = P.build_graph(3, (src, dst, w))
+    with pytest.raises(OverflowError, match="hamiltonian weight too large to stay exact"):
+        P.solve(g, P.SolveOptions(scc="off"))
+    # with tarjan regions the same graph solves (wide lane): mean 1
+    s = P.solve(g)
+    assert s.exact and s.mu_exact == Fraction(1, 1)
