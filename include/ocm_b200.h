@@ -206,6 +206,12 @@ typedef struct ocm_certificate {
  * (128-bit keys) runs when a weight needs more than 32 bits or a key could
  * leave +-2^62; ocm_session_values then returns OCM_E_RANGE for keys beyond
  * 64 bits. ocm_session_is_wide reports the lane of the session's last solve. */
+/* Lambda of the (single) non-trivial region after each policy iteration of
+ * the last solve -- the reference's HowardTrace (howard_par.hpp:588, which
+ * records it when there is one region): exact lanes fill num/den, the float
+ * lane f; *len = the number of iterations (at most 4096 entries kept). */
+int ocm_session_lambda_trace(ocm_session* s, int64_t* num, int64_t* den, double* f, uint32_t cap,
+                             uint32_t* len);
 int ocm_session_keys_wide(ocm_session* s, int64_t* key_hi, uint64_t* key_lo);
 int ocm_session_is_wide(const ocm_session* s);
 int ocm_session_certify(ocm_session* s, ocm_certificate* out);

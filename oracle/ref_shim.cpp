@@ -260,4 +260,44 @@ int ref_graph_solve(const void* gp, int algo, int objective, int scc, ref_result
     }
 }
 
+// The reference's per-iteration lambda trace (HowardPar::run(trace),
+// howard_par.hpp:588, recorded when the graph is a single region): exact
+// graphs fill num/den, float graphs f; returns the iteration count in *len
+// (at most cap entries written). Returns 1 on an exception, 2 when the graph
+// is not one region.
+int ref_lambda_trace(uint32_t n, uint64_t m, const uint32_t* src, const uint32_t* dst,
+                     const double* w, int objective, int64_t* num, int64_t* den, double* f,
+                     uint32_t cap, uint32_t* len) {
+    try {
+        ocm::Graph g = make_graph(n, m, src, dst, w);
+        if (objective)
+            g = ocm::negate_weights(g);
+        const ocm::RegionMap rm = ocm::tarjan_scc(g);
+        if (rm.count != 1)
+            return 2;
+        ocm::Engine eng({ocm::Schedule::Seq, 1, 1});
+        if (g.integer_exact) {
+            ocm::HowardPar<ocm::ExactMode> hp(eng, g, rm);
+            ocm::HowardTrace<ocm::ExactMode> tr;
+            hp.run(&tr);
+            *len = static_cast<uint32_t>(tr.size());
+            for (uint32_t i = 0; i < tr.size() && i < cap; ++i) {
+                num[i] = tr[i].lambda.num;
+                den[i] = tr[i].lambda.den;
+            }
+        } else {
+            ocm::HowardPar<ocm::FloatMode> hp(eng, g, rm);
+            ocm::HowardTrace<ocm::FloatMode> tr;
+            hp.run(&tr);
+            *len = static_cast<uint32_t>(tr.size());
+            for (uint32_t i = 0; i < tr.size() && i < cap; ++i)
+                f[i] = tr[i].lambda;
+        }
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 1;
+    }
+}
+
 } // extern "C"

@@ -165,6 +165,8 @@ def _load():
         "ocm_session_certify": (C.c_int, [C.c_void_p, P(_Certificate)]),
         "ocm_session_keys_wide": (C.c_int, [C.c_void_p, P(C.c_int64), P(C.c_uint64)]),
         "ocm_session_is_wide": (C.c_int, [C.c_void_p]),
+        "ocm_session_lambda_trace": (C.c_int, [C.c_void_p, P(C.c_int64), P(C.c_int64), P(C.c_double),
+                                               C.c_uint32, P(C.c_uint32)]),
         "ocm_session_stream": (C.c_void_p, [C.c_void_p]),
         "ocm_session_free": (None, [C.c_void_p]),
     }
@@ -189,7 +191,7 @@ EXPORTED_SYMBOLS = (
     "ocm_graph_csr",
     "ocm_solve", "ocm_solve_csr", "ocm_session_create_csr", "ocm_session_create", "ocm_session_solve", "ocm_session_values",
     "ocm_session_stream", "ocm_session_free", "ocm_session_certify", "ocm_session_keys_wide",
-    "ocm_session_is_wide",
+    "ocm_session_is_wide", "ocm_session_lambda_trace",
 )
 
 
@@ -592,6 +594,22 @@ class Session:
     def wide(self) -> bool:
         """True when the last solve ran the wide exact lane (128-bit keys)."""
         return bool(_lib.ocm_session_is_wide(self._h))
+
+    def lambda_trace(self) -> list:
+        """Lambda of the non-trivial region after each policy iteration of the
+        last solve (Fractions in the exact lanes, floats in the float lane):
+        the reference's HowardTrace (howard_par.hpp:588)."""
+        cap = 4096
+        num = np.zeros(cap, np.int64)
+        den = np.zeros(cap, np.int64)
+        f = np.zeros(cap, np.float64)
+        ln = C.c_uint32()
+        _check(_lib.ocm_session_lambda_trace(self._h, _p(num, C.c_int64), _p(den, C.c_int64),
+                                             _p(f, C.c_double), cap, C.byref(ln)))
+        k = min(int(ln.value), cap)
+        if den[:k].any():
+            return [Fraction(int(a), int(b)) for a, b in zip(num[:k], den[:k])]
+        return f[:k].tolist()
 
     def keys_wide(self) -> np.ndarray:
         """Exact value keys at full width as Python ints (object array):

@@ -324,6 +324,15 @@ int ocm_session_keys_wide(ocm_session* s, int64_t* key_hi, uint64_t* key_lo) {
     });
 }
 
+int ocm_session_lambda_trace(ocm_session* s, int64_t* num, int64_t* den, double* f, uint32_t cap,
+                             uint32_t* len) {
+    return guard([&] {
+        if (!s || !len)
+            throw std::invalid_argument("null session or output");
+        s->s->lambda_trace(num, den, f, cap, len);
+    });
+}
+
 int ocm_session_is_wide(const ocm_session* s) { return s && s->s->wide() ? 1 : 0; }
 
 void* ocm_session_stream(ocm_session* s) { return s ? s->s->stream() : nullptr; }

@@ -128,6 +128,12 @@ struct KP {
     const int* ew_hi;          // wide exact lane: high 32 bits of each edge weight
     int* succ_whi;             // wide exact lane: high 32 bits of the policy weight
     int2* succ_vw;             // fast exact lane, one rank: packed {head, weight} shadow of the policy
+    // lambda of region 0 after each adoption (the reference's HowardTrace,
+    // howard_par.hpp:588), up to tr_cap iterations
+    long long* tr_num;
+    long long* tr_den;
+    double* tr_f;
+    unsigned tr_cap;
     long long* lam_num;
     long long* lam_den;
     double* lam_f;
@@ -266,6 +272,8 @@ struct DeviceState {
     DBuf<__int128> key_w;
     DBuf<int> ew_hi, succ_whi;
     DBuf<int2> succ_vw;
+    DBuf<long long> tr_num, tr_den;
+    DBuf<double> tr_f;
     DBuf<PJC> pj0, pj1;
     DBuf<int2> ew;
     DBuf<FEdge> fe;
@@ -306,6 +314,9 @@ struct DeviceState {
         ew_hi.release();
         succ_whi.release();
         succ_vw.release();
+        tr_num.release();
+        tr_den.release();
+        tr_f.release();
         pj0.release();
         pj1.release();
         ew.release();

@@ -1341,6 +1341,10 @@ template <int MODE> __device__ __forceinline__ unsigned adopt_region(const KP& p
             c->lambda_up = 1;
         p.lam_num[r] = num;
         p.lam_den[r] = den;
+        if (r == 0 && p.iters[0] < p.tr_cap) { // lambda trace of region 0
+            p.tr_num[p.iters[0]] = num;
+            p.tr_den[p.iters[0]] = den;
+        }
         // every key |K| <= max_region * (max|w|*den + |num|) stays inside
         // the lane's bound (else: the fast lane reports it, and the session
         // re-solves in the wide lane)
@@ -1350,6 +1354,8 @@ template <int MODE> __device__ __forceinline__ unsigned adopt_region(const KP& p
             c->overflow = 1;
     } else {
         p.lam_f[r] = p.cyc_wf[a] / len;
+        if (r == 0 && p.iters[0] < p.tr_cap)
+            p.tr_f[p.iters[0]] = p.lam_f[r];
     }
     p.iters[r] += 1;
     return len;

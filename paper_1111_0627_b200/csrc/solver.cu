@@ -287,6 +287,13 @@ void Session::init(const std::function<void(DeviceState&)>& prepare) {
     p.succ_wi = d.succ_wi.p;
     p.succ_wf = d.succ_wf.p;
     p.succ_vw = d.succ_vw.p;
+    d.tr_num.alloc(kTraceCap, d.stream);
+    d.tr_den.alloc(kTraceCap, d.stream);
+    d.tr_f.alloc(kTraceCap, d.stream);
+    p.tr_num = d.tr_num.p;
+    p.tr_den = d.tr_den.p;
+    p.tr_f = d.tr_f.p;
+    p.tr_cap = kTraceCap;
     p.key_i = d.key_i.p;
     p.key_f = d.key_f.p;
     p.lam_num = d.lam_num.p;
@@ -1141,6 +1148,33 @@ void Session::keys_wide(std::int64_t* hi, std::uint64_t* lo) {
         const __int128 x = reg[v] != prep_.R ? k[v] : 0;
         hi[v] = static_cast<std::int64_t>(x >> 64);
         lo[v] = static_cast<std::uint64_t>(x);
+    }
+}
+
+} // namespace ocmb
+
+namespace ocmb {
+
+// lambda of region 0 after each adoption of the last solve
+void Session::lambda_trace(std::int64_t* num, std::int64_t* den, double* f, std::uint32_t cap,
+                           std::uint32_t* len) {
+    if (!solved_)
+        throw std::logic_error("session has not been solved yet");
+    DeviceState& d = *d_;
+    std::uint32_t it = 0;
+    if (prep_.R > 0)
+        CK(cudaMemcpy(&it, d.kp.iters, 4, cudaMemcpyDeviceToHost));
+    const std::uint32_t k = std::min({it, cap, kTraceCap});
+    *len = it;
+    if (k == 0)
+        return;
+    if (prep_.exact) {
+        if (num)
+            CK(cudaMemcpy(num, d.kp.tr_num, k * 8ull, cudaMemcpyDeviceToHost));
+        if (den)
+            CK(cudaMemcpy(den, d.kp.tr_den, k * 8ull, cudaMemcpyDeviceToHost));
+    } else if (f) {
+        CK(cudaMemcpy(f, d.kp.tr_f, k * 8ull, cudaMemcpyDeviceToHost));
     }
 }
 

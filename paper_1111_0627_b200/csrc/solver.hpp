@@ -17,6 +17,8 @@ namespace ocmb {
 
 struct DeviceState; // devcommon.cuh
 
+constexpr std::uint32_t kTraceCap = 4096; // lambda trace entries kept per solve
+
 class Session {
   public:
     // rank/world > 1: a shard of the sharded lane; the rank
@@ -36,6 +38,8 @@ class Session {
                 std::uint32_t* succ_vertex);
     void* stream() const;
     void keys_wide(std::int64_t* hi, std::uint64_t* lo);
+    void lambda_trace(std::int64_t* num, std::int64_t* den, double* f, std::uint32_t cap,
+                      std::uint32_t* len);
     bool wide() const { return mode_ == 2; }
 
     std::uint32_t n() const { return prep_.n; }

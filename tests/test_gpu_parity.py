@@ -477,3 +477,31 @@ def test_scc_off_hamiltonian_overflow_matches_reference():
     # with tarjan regions the same graph solves (wide lane): mean 1
     s = P.solve(g)
     assert s.exact and s.mu_exact == Fraction(1, 1)
+
+
+def _sc_graph(rng, n, extra, float_w=False):
+    perm = rng.permutation(n)
+    s = np.concatenate([perm, rng.integers(0, n, extra * n)]).astype(np.uint32)
+    d = np.concatenate([np.roll(perm, -1), rng.integers(0, n, extra * n)]).astype(np.uint32)
+    w = rng.integers(-50, 51, len(s)).astype(np.float64)
+    return n, s, d, (w / 8 + 0.1 if float_w else w)
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("seed,n,extra,float_w", [(1, 50, 2, False), (2, 2000, 4, False),
+                                                  (3, 20000, 7, False), (4, 2000, 4, True),
+                                                  (5, 20000, 3, True)])
+@pytest.mark.parametrize("objective", ["min", "max"])
+def test_lambda_trace_lockstep_with_reference(seed, n, extra, float_w, objective):
+    """Lockstep with the reference iteration by iteration (its acceptance
+    criterion 6 compares the parallel and sequential lanes the same way,
+    acceptance_main.cpp:260): on strongly connected graphs the device's
+    lambda after every policy iteration equals the reference HowardPar's
+    trace (howard_par.hpp:588) -- exact rationals, or the same doubles in the
+    float lane."""
+    n, s, d, w = _sc_graph(np.random.default_rng(seed), n, extra, float_w)
+    ref = O.ref_lambda_trace(n, s, d, w, objective)
+    assert ref is not None and len(ref) > 0
+    sess = P.Session(P.build_graph(n, (s, d, w)), P.SolveOptions(objective=objective))
+    sess.solve()
+    assert sess.lambda_trace() == ref
