@@ -212,6 +212,12 @@ typedef struct ocm_certificate {
  * lane f; *len = the number of iterations (at most 4096 entries kept). */
 int ocm_session_lambda_trace(ocm_session* s, int64_t* num, int64_t* den, double* f, uint32_t cap,
                              uint32_t* len);
+/* Debug trace of a session created with the environment variable
+ * OCM_TRACE_ITERS=k (one rank): the policy edge ids and value keys (exact,
+ * low 64 bits; float values in fval) after iteration `iter` < k of the last
+ * solve -- what HowardTrace records per iteration (howard_par.hpp:588). */
+int ocm_session_iter_trace(ocm_session* s, uint32_t iter, uint32_t* succ_edge, int64_t* key,
+                           double* fval);
 int ocm_session_keys_wide(ocm_session* s, int64_t* key_hi, uint64_t* key_lo);
 int ocm_session_is_wide(const ocm_session* s);
 int ocm_session_certify(ocm_session* s, ocm_certificate* out);

@@ -431,3 +431,35 @@ def ref_lambda_trace(n, src, dst, w, objective="min"):
     if den[:k].any():
         return [Fraction(int(a), int(b)) for a, b in zip(num[:k], den[:k])]
     return f[:k].tolist()
+
+
+def ref_iter_trace(n, src, dst, w, objective="min", cap_iters=64):
+    """The reference HowardPar trace of a single-region graph, per iteration:
+    list of dicts {succ_edge, wsum, steps} (exact) or {succ_edge, fval}."""
+    lib = ref_lib()
+    fn = lib.ref_iter_trace
+    fn.restype = C.c_int
+    P = C.POINTER
+    fn.argtypes = [C.c_uint32, C.c_uint64, P(C.c_uint32), P(C.c_uint32), P(C.c_double), C.c_int,
+                   C.c_uint32, P(C.c_uint32), P(C.c_int64), P(C.c_int64), P(C.c_double),
+                   P(C.c_uint32)]
+    src, dst, w = _edges(src, dst, w)
+    cells = cap_iters * int(n)
+    se = np.zeros(cells, np.uint32)
+    ws = np.zeros(cells, np.int64)
+    st = np.zeros(cells, np.int64)
+    fv = np.zeros(cells, np.float64)
+    ln = C.c_uint32()
+    rc = fn(n, src.shape[0], _ptr(src, C.c_uint32), _ptr(dst, C.c_uint32), _ptr(w, C.c_double),
+            1 if objective == "max" else 0, cap_iters, _ptr(se, C.c_uint32), _ptr(ws, C.c_int64),
+            _ptr(st, C.c_int64), _ptr(fv, C.c_double), C.byref(ln))
+    if rc == 2:
+        return None
+    if rc:
+        raise RuntimeError("reference: " + lib.ref_last_error().decode())
+    out = []
+    for i in range(min(int(ln.value), cap_iters)):
+        sl = slice(i * n, (i + 1) * n)
+        out.append({"succ_edge": se[sl].copy(), "wsum": ws[sl].copy(), "steps": st[sl].copy(),
+                    "fval": fv[sl].copy()})
+    return out

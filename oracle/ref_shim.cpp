@@ -300,4 +300,47 @@ int ref_lambda_trace(uint32_t n, uint64_t m, const uint32_t* src, const uint32_t
     }
 }
 
+// The reference's full per-iteration trace on a single-region graph: for
+// iteration i < cap_iters, succ_edge[i*n + v], and the value plane (exact:
+// wsum/steps, float: fval). *len = iterations. Returns 2 when not one region.
+int ref_iter_trace(uint32_t n, uint64_t m, const uint32_t* src, const uint32_t* dst,
+                   const double* w, int objective, uint32_t cap_iters, uint32_t* succ_edge,
+                   int64_t* wsum, int64_t* steps, double* fval, uint32_t* len) {
+    try {
+        ocm::Graph g = make_graph(n, m, src, dst, w);
+        if (objective)
+            g = ocm::negate_weights(g);
+        const ocm::RegionMap rm = ocm::tarjan_scc(g);
+        if (rm.count != 1)
+            return 2;
+        ocm::Engine eng({ocm::Schedule::Seq, 1, 1});
+        auto dump = [&](const auto& tr, auto&& put) {
+            *len = static_cast<uint32_t>(tr.size());
+            for (uint32_t i = 0; i < tr.size() && i < cap_iters; ++i)
+                for (uint32_t v = 0; v < n; ++v) {
+                    succ_edge[std::size_t(i) * n + v] = tr[i].succ_edge[v];
+                    put(std::size_t(i) * n + v, tr[i].values[v]);
+                }
+        };
+        if (g.integer_exact) {
+            ocm::HowardPar<ocm::ExactMode> hp(eng, g, rm);
+            ocm::HowardTrace<ocm::ExactMode> tr;
+            hp.run(&tr);
+            dump(tr, [&](std::size_t k, const auto& val) {
+                wsum[k] = val.wsum;
+                steps[k] = val.steps;
+            });
+        } else {
+            ocm::HowardPar<ocm::FloatMode> hp(eng, g, rm);
+            ocm::HowardTrace<ocm::FloatMode> tr;
+            hp.run(&tr);
+            dump(tr, [&](std::size_t k, const auto& val) { fval[k] = val; });
+        }
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 1;
+    }
+}
+
 } // extern "C"

@@ -167,6 +167,8 @@ def _load():
         "ocm_session_is_wide": (C.c_int, [C.c_void_p]),
         "ocm_session_lambda_trace": (C.c_int, [C.c_void_p, P(C.c_int64), P(C.c_int64), P(C.c_double),
                                                C.c_uint32, P(C.c_uint32)]),
+        "ocm_session_iter_trace": (C.c_int, [C.c_void_p, C.c_uint32, P(C.c_uint32), P(C.c_int64),
+                                             P(C.c_double)]),
         "ocm_session_stream": (C.c_void_p, [C.c_void_p]),
         "ocm_session_free": (None, [C.c_void_p]),
     }
@@ -191,7 +193,7 @@ EXPORTED_SYMBOLS = (
     "ocm_graph_csr",
     "ocm_solve", "ocm_solve_csr", "ocm_session_create_csr", "ocm_session_create", "ocm_session_solve", "ocm_session_values",
     "ocm_session_stream", "ocm_session_free", "ocm_session_certify", "ocm_session_keys_wide",
-    "ocm_session_is_wide", "ocm_session_lambda_trace",
+    "ocm_session_is_wide", "ocm_session_lambda_trace", "ocm_session_iter_trace",
 )
 
 
@@ -610,6 +612,17 @@ class Session:
         if den[:k].any():
             return [Fraction(int(a), int(b)) for a, b in zip(num[:k], den[:k])]
         return f[:k].tolist()
+
+    def iteration_trace(self, it: int) -> dict:
+        """Debug (session created with OCM_TRACE_ITERS=k in the environment):
+        policy edge ids, value keys (exact) / values (float) after iteration
+        `it` of the last solve."""
+        n = max(self.n, 1)
+        out = {"succ_edge": np.zeros(n, np.uint32), "key_num": np.zeros(n, np.int64),
+               "fval": np.zeros(n, np.float64)}
+        _check(_lib.ocm_session_iter_trace(self._h, int(it), _p(out["succ_edge"], C.c_uint32),
+                                           _p(out["key_num"], C.c_int64), _p(out["fval"], C.c_double)))
+        return {k: v[: self.n] for k, v in out.items()}
 
     def keys_wide(self) -> np.ndarray:
         """Exact value keys at full width as Python ints (object array):

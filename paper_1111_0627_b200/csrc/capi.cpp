@@ -333,6 +333,15 @@ int ocm_session_lambda_trace(ocm_session* s, int64_t* num, int64_t* den, double*
     });
 }
 
+int ocm_session_iter_trace(ocm_session* s, uint32_t iter, uint32_t* succ_edge, int64_t* key,
+                           double* fval) {
+    return guard([&] {
+        if (!s)
+            throw std::invalid_argument("null session");
+        s->s->iter_trace(iter, succ_edge, key, fval);
+    });
+}
+
 int ocm_session_is_wide(const ocm_session* s) { return s && s->s->wide() ? 1 : 0; }
 
 void* ocm_session_stream(ocm_session* s) { return s ? s->s->stream() : nullptr; }

@@ -134,6 +134,10 @@ struct KP {
     long long* tr_den;
     double* tr_f;
     unsigned tr_cap;
+    std::uint32_t* tr_pol; // debug: policy per iteration (tr_iters x N), or null
+    long long* tr_key;     // debug: value keys per iteration (exact lanes, low 64 bits)
+    double* tr_keyf;       // debug: values per iteration (float lane)
+    unsigned tr_iters;
     long long* lam_num;
     long long* lam_den;
     double* lam_f;
@@ -274,6 +278,9 @@ struct DeviceState {
     DBuf<int2> succ_vw;
     DBuf<long long> tr_num, tr_den;
     DBuf<double> tr_f;
+    DBuf<std::uint32_t> tr_pol;
+    DBuf<long long> tr_key;
+    DBuf<double> tr_keyf;
     DBuf<PJC> pj0, pj1;
     DBuf<int2> ew;
     DBuf<FEdge> fe;
@@ -317,6 +324,9 @@ struct DeviceState {
         tr_num.release();
         tr_den.release();
         tr_f.release();
+        tr_pol.release();
+        tr_key.release();
+        tr_keyf.release();
         pj0.release();
         pj1.release();
         ew.release();

@@ -2343,6 +2343,20 @@ __global__ void __launch_bounds__(kBlock, kSolveMinBlocks) k_solve(KP p, int mod
             if (fatal)
                 break;
         }
+        // debug trace (sessions created with OCM_TRACE_ITERS): the policy and
+        // the value plane after this iteration, as HowardTrace records them
+        // (howard_par.hpp:588)
+        if (p.tr_pol && st.outer - 1 < p.tr_iters) {
+            const std::size_t base = std::size_t(st.outer - 1) * p.N;
+            for (std::size_t v = gtid(); v < p.N; v += gstride()) {
+                p.tr_pol[base + v] = p.succ_e[v];
+                if constexpr (EXACT)
+                    p.tr_key[base + v] = static_cast<long long>(key_ld<MODE>(p, static_cast<std::uint32_t>(v)));
+                else
+                    p.tr_keyf[base + v] = p.key_f[v];
+            }
+            sync(PH_FLOAT); // before the next pass rewrites the policy
+        }
     }
 
     if (blockIdx.x == 0 && threadIdx.x == 0) {

@@ -294,6 +294,19 @@ void Session::init(const std::function<void(DeviceState&)>& prepare) {
     p.tr_den = d.tr_den.p;
     p.tr_f = d.tr_f.p;
     p.tr_cap = kTraceCap;
+    if (const int ti = env_int("OCM_TRACE_ITERS", 0); ti > 0 && world_ == 1) {
+        // debug: keep the policy and values of the first ti iterations
+        const std::size_t cells = std::size_t(ti) * std::max<std::size_t>(N, 1);
+        d.tr_pol.alloc(cells, d.stream);
+        if (prep_.exact)
+            d.tr_key.alloc(cells, d.stream);
+        else
+            d.tr_keyf.alloc(cells, d.stream);
+        p.tr_pol = d.tr_pol.p;
+        p.tr_key = d.tr_key.p;
+        p.tr_keyf = d.tr_keyf.p;
+        p.tr_iters = static_cast<unsigned>(ti);
+    }
     p.key_i = d.key_i.p;
     p.key_f = d.key_f.p;
     p.lam_num = d.lam_num.p;
@@ -1176,6 +1189,27 @@ void Session::lambda_trace(std::int64_t* num, std::int64_t* den, double* f, std:
     } else if (f) {
         CK(cudaMemcpy(f, d.kp.tr_f, k * 8ull, cudaMemcpyDeviceToHost));
     }
+}
+
+} // namespace ocmb
+
+namespace ocmb {
+
+// debug trace (OCM_TRACE_ITERS sessions): policy edge ids and value keys
+// (exact, low 64 bits) or values (float) after iteration `it` of the last solve
+void Session::iter_trace(std::uint32_t it, std::uint32_t* succ_e, std::int64_t* key, double* fval) {
+    DeviceState& d = *d_;
+    if (!d.kp.tr_pol)
+        throw std::logic_error("session created without OCM_TRACE_ITERS");
+    if (it >= d.kp.tr_iters)
+        throw std::invalid_argument("iteration beyond the traced ones");
+    const std::size_t n = prep_.n, base = std::size_t(it) * n;
+    if (succ_e)
+        CK(cudaMemcpy(succ_e, d.kp.tr_pol + base, n * 4, cudaMemcpyDeviceToHost));
+    if (key && d.kp.tr_key)
+        CK(cudaMemcpy(key, d.kp.tr_key + base, n * 8, cudaMemcpyDeviceToHost));
+    if (fval && d.kp.tr_keyf)
+        CK(cudaMemcpy(fval, d.kp.tr_keyf + base, n * 8, cudaMemcpyDeviceToHost));
 }
 
 } // namespace ocmb

@@ -40,6 +40,7 @@ class Session {
     void keys_wide(std::int64_t* hi, std::uint64_t* lo);
     void lambda_trace(std::int64_t* num, std::int64_t* den, double* f, std::uint32_t cap,
                       std::uint32_t* len);
+    void iter_trace(std::uint32_t it, std::uint32_t* succ_e, std::int64_t* key, double* fval);
     bool wide() const { return mode_ == 2; }
 
     std::uint32_t n() const { return prep_.n; }

@@ -505,3 +505,30 @@ def test_lambda_trace_lockstep_with_reference(seed, n, extra, float_w, objective
     sess = P.Session(P.build_graph(n, (s, d, w)), P.SolveOptions(objective=objective))
     sess.solve()
     assert sess.lambda_trace() == ref
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("seed,n,extra,float_w", [(11, 40, 2, False), (12, 1500, 4, False),
+                                                  (13, 1500, 3, True), (14, 300, 6, True)])
+@pytest.mark.parametrize("objective", ["min", "max"])
+def test_policy_and_values_lockstep_with_reference(seed, n, extra, float_w, objective, monkeypatch):
+    """Move for move: after EVERY policy iteration the device's policy (edge
+    ids) and value plane equal the reference HowardPar's trace entry
+    (howard_par.hpp:588: lambda, succ_edge, the plane just written) -- exact
+    keys K = wsum*den - steps*num, or the same doubles in the float lane."""
+    monkeypatch.setenv("OCM_TRACE_ITERS", "64")
+    n, s, d, w = _sc_graph(np.random.default_rng(seed), n, extra, float_w)
+    ref = O.ref_iter_trace(n, s, d, w, objective, cap_iters=64)
+    lam = O.ref_lambda_trace(n, s, d, w, objective)
+    assert ref and len(ref) == len(lam)
+    sess = P.Session(P.build_graph(n, (s, d, w)), P.SolveOptions(objective=objective))
+    sess.solve()
+    assert sess.lambda_trace() == lam
+    for i, (r, l) in enumerate(zip(ref, lam)):
+        got = sess.iteration_trace(i)
+        assert np.array_equal(got["succ_edge"], r["succ_edge"]), i
+        if float_w:
+            assert np.array_equal(got["fval"], r["fval"]), i
+        else:
+            key = [int(a) * l.denominator - int(b) * l.numerator for a, b in zip(r["wsum"], r["steps"])]
+            assert got["key_num"].tolist() == key, i
