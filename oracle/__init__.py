@@ -403,16 +403,17 @@ class RefGraph:
             self._h = None
 
 
-def ref_lambda_trace(n, src, dst, w, objective="min"):
+def ref_lambda_trace(n, src, dst, w, objective="min", scc="tarjan"):
     """The reference's lambda after each policy iteration (HowardPar::run
-    trace, howard_par.hpp:588) of a single-region graph: Fractions (exact)
-    or floats; None when the graph is not strongly connected."""
+    trace, howard_par.hpp:588) of a single-region graph (or, scc="off", of
+    the Hamiltonian-augmented graph): Fractions (exact) or floats; None when
+    the graph is not strongly connected."""
     lib = ref_lib()
-    fn = lib.ref_lambda_trace
+    fn = lib.ref_lambda_trace2
     fn.restype = C.c_int
     fn.argtypes = [C.c_uint32, C.c_uint64, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32),
-                   C.POINTER(C.c_double), C.c_int, C.POINTER(C.c_int64), C.POINTER(C.c_int64),
-                   C.POINTER(C.c_double), C.c_uint32, C.POINTER(C.c_uint32)]
+                   C.POINTER(C.c_double), C.c_int, C.c_int, C.POINTER(C.c_int64),
+                   C.POINTER(C.c_int64), C.POINTER(C.c_double), C.c_uint32, C.POINTER(C.c_uint32)]
     src, dst, w = _edges(src, dst, w)
     cap = 1 << 16
     num = np.zeros(cap, np.int64)
@@ -420,8 +421,8 @@ def ref_lambda_trace(n, src, dst, w, objective="min"):
     f = np.zeros(cap, np.float64)
     ln = C.c_uint32()
     rc = fn(n, src.shape[0], _ptr(src, C.c_uint32), _ptr(dst, C.c_uint32), _ptr(w, C.c_double),
-            1 if objective == "max" else 0, _ptr(num, C.c_int64), _ptr(den, C.c_int64),
-            _ptr(f, C.c_double), cap, C.byref(ln))
+            1 if objective == "max" else 0, 1 if scc == "off" else 0, _ptr(num, C.c_int64),
+            _ptr(den, C.c_int64), _ptr(f, C.c_double), cap, C.byref(ln))
     if rc == 2:
         return None
     if rc:

@@ -260,6 +260,10 @@ int ref_graph_solve(const void* gp, int algo, int objective, int scc, ref_result
     }
 }
 
+int ref_lambda_trace2(uint32_t n, uint64_t m, const uint32_t* src, const uint32_t* dst,
+                      const double* w, int objective, int scc_off, int64_t* num, int64_t* den,
+                      double* f, uint32_t cap, uint32_t* len);
+
 // The reference's per-iteration lambda trace (HowardPar::run(trace),
 // howard_par.hpp:588, recorded when the graph is a single region): exact
 // graphs fill num/den, float graphs f; returns the iteration count in *len
@@ -268,10 +272,20 @@ int ref_graph_solve(const void* gp, int algo, int objective, int scc, ref_result
 int ref_lambda_trace(uint32_t n, uint64_t m, const uint32_t* src, const uint32_t* dst,
                      const double* w, int objective, int64_t* num, int64_t* den, double* f,
                      uint32_t cap, uint32_t* len) {
+    return ref_lambda_trace2(n, m, src, dst, w, objective, 0, num, den, f, cap, len);
+}
+
+// scc_off: the trace of the Hamiltonian-augmented graph solve() runs for
+// --scc off (solve.cpp:48, graph.cpp:105) -- one region by construction
+int ref_lambda_trace2(uint32_t n, uint64_t m, const uint32_t* src, const uint32_t* dst,
+                      const double* w, int objective, int scc_off, int64_t* num, int64_t* den,
+                      double* f, uint32_t cap, uint32_t* len) {
     try {
         ocm::Graph g = make_graph(n, m, src, dst, w);
         if (objective)
             g = ocm::negate_weights(g);
+        if (scc_off)
+            g = ocm::augment_hamiltonian(g).graph;
         const ocm::RegionMap rm = ocm::tarjan_scc(g);
         if (rm.count != 1)
             return 2;

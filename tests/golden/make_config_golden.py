@@ -88,11 +88,18 @@ def solve(job):
     t0 = time.time()
     r = O.ref_solve(n, s, d, w, "howard", objective, CONFIGS[cfg].get("scc", "tarjan"))
     wall = time.time() - t0
+    trace = None
+    if CONFIGS[cfg].get("scc") == "off":
+        # one region by construction: the reference's lambda after every
+        # policy iteration (HowardPar::run(trace), howard_par.hpp:588)
+        tr = O.ref_lambda_trace(n, s, d, w, objective, "off")
+        trace = [[x.numerator, x.denominator] if hasattr(x, "numerator") else x for x in tr]
     return cfg, objective, {
         "has_cycle": r.has_cycle, "exact": r.exact, "mu_num": r.mu_num, "mu_den": r.mu_den,
         "mu": r.mu, "cycle": [int(x) for x in r.cycle], "outer_iters": r.outer_iters,
         "spf_passes": r.spf_passes, "regions": r.regions, "trivial_regions": r.trivial_regions,
-        "ref_solve_ms": r.solve_ms, "ref_wall_s": wall}
+        "ref_solve_ms": r.solve_ms, "ref_wall_s": wall,
+        **({"lambda_trace": trace} if trace is not None else {})}
 
 
 def main():

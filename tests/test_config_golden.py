@@ -116,3 +116,19 @@ def test_scc_parallel_option_gives_the_reference_result(cfg):
     for objective in ("min", "max"):
         ref = GOLD["configs"][cfg]["results"][objective]
         check(P.solve(g, P.SolveOptions(algo="howard", objective=objective, scc="parallel")), ref)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cfg", [c for c in sorted(GOLD["configs"])
+                                 if "lambda_trace" in GOLD["configs"][c]["results"].get("min", {})])
+def test_lambda_trace_lockstep_at_full_size(cfg):
+    """Config 2's graph with --scc off (one region, 10^6 vertices, 9*10^6
+    edges): the device's lambda after every one of its policy iterations
+    equals the reference HowardPar trace recorded at full size."""
+    from fractions import Fraction
+    g = product_graph(cfg)
+    for objective in ("min", "max"):
+        ref = GOLD["configs"][cfg]["results"][objective]["lambda_trace"]
+        sess = P.Session(g, opts(cfg, objective=objective))
+        sess.solve()
+        assert sess.lambda_trace() == [Fraction(a, b) for a, b in ref]
