@@ -5,7 +5,7 @@
 // howard_b200_lane.hpp, linked to the product library libocm_b200.so.
 // For every graph file on the command line it reads the graph with the
 // reference's read_graph_file (graph_io.hpp:45), then for each objective and
-// SCC strategy solves it twice:
+// SCC strategy (tarjan, parallel, off) solves it twice:
 //   * the reference's ocm::solve (solve.cpp:198) with lane howard and with
 //     lane howard-par;
 //   * the same solve() front end (negation for Maximize, solve.cpp:203-215)
@@ -81,14 +81,17 @@ int main(int argc, char** argv) {
             continue;
         }
         for (const auto obj : {ocm::Objective::Minimize, ocm::Objective::Maximize})
-            for (const auto scc : {ocm::SccStrategy::Tarjan, ocm::SccStrategy::Off})
+            for (const auto scc : {ocm::SccStrategy::Tarjan, ocm::SccStrategy::Parallel,
+                                   ocm::SccStrategy::Off})
                 for (const auto lane : {ocm::Algo::HowardSeq, ocm::Algo::HowardPar}) {
                     ocm::SolveOptions opt;
                     opt.algo = lane;
                     opt.objective = obj;
                     opt.scc = scc;
                     const char* on = obj == ocm::Objective::Minimize ? "min" : "max";
-                    const char* sn = scc == ocm::SccStrategy::Off ? "off" : "tarjan";
+                    const char* sn = scc == ocm::SccStrategy::Off        ? "off"
+                                     : scc == ocm::SccStrategy::Parallel ? "parallel"
+                                                                         : "tarjan";
                     const char* ln = lane == ocm::Algo::HowardSeq ? "howard" : "howard-par";
                     try {
                         const ocm::Solution ref = ocm::solve(g, opt);

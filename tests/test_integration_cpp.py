@@ -49,7 +49,7 @@ def test_golden_cases_through_the_cpp_lane(tmp_path):
         files.append(str(p))
     out = subprocess.run([BIN] + files, capture_output=True, text=True, timeout=1200)
     lines = out.stdout.splitlines()
-    assert len(lines) == 8 * len(files)
+    assert len(lines) == 12 * len(files)
     bad = [l for l in lines if not l.startswith("OK")]
     assert out.returncode == 0 and not bad, bad[:10]
 
