@@ -69,6 +69,8 @@ def parse():
                          "graph north_star shards -- on several)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-single-baseline", action="store_true",
+                    help="N > 1: skip rank 0's single-GPU run of the same graph after the timed region")
     ap.add_argument("--lane", default=None, choices=["replicas", "sharded", "fused"],
                     help="replicas: every rank solves its own graph (weak scaling, the driver's "
                          "run); sharded: all ranks solve one graph, vertices 1-D partitioned, "
@@ -420,6 +422,32 @@ def make_sessions(a, P, rank, local):
     return spec, {o: P.Session.generated(spec, opts[o]) for o in opts}
 
 
+def single_gpu_same_config(a, P, local, flush, steps=2):
+    """Rank 0 alone: the single-GPU session lane on the sharded run's graph,
+    one warm-up and `steps` timed min+max steps (CUDA events, L2 flushed)."""
+    import torch
+    c = CONFIGS[a.config]
+    if c["kind"] == "model":
+        g = build_graph_host(a, P)
+        sess = {o: P.Session(g, P.SolveOptions(objective=o, device=local)) for o in ("min", "max")}
+    else:
+        spec = P.Generator(c["kind"], n=c["n"], deg=c["deg"], dmax=c.get("dmax", 0), wlo=1,
+                           whi=100, seed=SEED)
+        sess = {o: P.Session.generated(spec, P.SolveOptions(objective=o, device=local))
+                for o in ("min", "max")}
+    ms, edges = 0.0, 0
+    for i in range(steps + 1):
+        for o in ("min", "max"):
+            flush.fill_(1)
+            torch.cuda.synchronize()
+            sol = sess[o].solve()
+            if i:
+                ms += sol.stats.device_ms
+                edges += sol.stats.m_solved * sol.stats.spf_passes
+    return {"value": edges / (ms / 1e3), "unit": UNIT, "ms_per_step": ms / steps, "steps": steps,
+            "note": "rank 0's GPU alone, single-GPU session lane, same graph, device time per solve"}
+
+
 def run_sharded(a, world, rank, local):
     """Strong scaling: one graph, every rank improves its vertex slice, the
     policy slices are all-gathered over NCCL each iteration."""
@@ -453,7 +481,7 @@ def run_sharded(a, world, rank, local):
                for o in shards}
 
     def step():
-        out, ms = {}, 0.0
+        out, ms = {}, {}
         for o in ("min", "max"):
             flush.fill_(1)
             torch.cuda.synchronize()
@@ -466,21 +494,30 @@ def run_sharded(a, world, rank, local):
                 (out[o],) = solve_sharded([shards[o]], comm)
             e1.record(streams[o])
             e1.synchronize()
-            ms += e0.elapsed_time(e1)
+            ms[o] = e0.elapsed_time(e1)
         return out, ms
 
     for _ in range(a.warmup):
         step()
-    sols, tot_ms = [], 0.0
+    sols, tot = [], {"min": 0.0, "max": 0.0}
     with ClockSampler(local) as clocks:
         for _ in range(a.steps):
             out, ms = step()
             sols.append(out)
-            tot_ms += ms
-    t = torch.tensor([tot_ms], dtype=torch.float64,
+            for o in ms:
+                tot[o] += ms[o]
+    # per objective, max over ranks (a step's time is the sum of the two maxima)
+    t = torch.tensor([tot["min"], tot["max"]], dtype=torch.float64,
                      device=dev if dist.get_backend() == "nccl" else "cpu")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
+    ms_obj = {"min": float(t[0].item()), "max": float(t[1].item())}
+    ms_max = ms_obj["min"] + ms_obj["max"]
+    # (the shard sessions stay alive: their memory is mapped by the peers)
+    dist.barrier()
+    single = None
+    if rank == 0 and not a.no_single_baseline:
+        single = single_gpu_same_config(a, P, local, flush)
+    dist.barrier()
     edges = sum(s[o].stats.m_solved * s[o].stats.spf_passes for s in sols for o in s)
     launches = sum(s[o].stats.launches for s in sols for o in s)
     if rank == 0:
@@ -493,10 +530,17 @@ def run_sharded(a, world, rank, local):
                 f"fused x{world} (1-D vertex partition, policy pushed into peer memory inside one "
                 f"launch per rank)" if fused else
                 f"sharded x{world} (1-D vertex partition, policy all-gather per iteration)")),
-            "time_to_ocm_s": {o: None for o in ("min", "max")},
+            "time_to_ocm_s": {o: ms_obj[o] / a.steps / 1e3 for o in ("min", "max")},
             "policy_iterations": {o: sols[0][o].stats.spf_passes for o in ("min", "max")},
             "mu": {o: str(sols[0][o].mu_exact) for o in ("min", "max")},
             "gpu_launches": int(launches), "clocks": clocks.summary(),
+            # the same graph on rank 0's GPU alone (the single-GPU lane,
+            # after the timed region): the strong-scaling reference point --
+            # the N=1 bench line measures config 2, not this config
+            "single_gpu_same_config": single,
+            # the graph is generated in HBM on every rank (10^9 edges): no
+            # host-to-device leg to time at N > 1
+            "e2e": None,
             "note": ("device time = CUDA events on the session stream around each solve (one "
                      "persistent launch per rank, exchange inside the kernel), max over ranks"
                      if fused else

@@ -119,3 +119,9 @@ def test_gpus_2_self_launch_on_one_gpu():
     assert d["n_gpus"] == 2 and d["scaling"] == "strong" and "fused" in d["config"]["parallelism"]
     assert d["mu"] == {"min": "229/45", "max": "193/2"}
     assert d["policy_iterations"] == {"min": 44, "max": 26}
+    assert all(d["time_to_ocm_s"][o] > 0 for o in ("min", "max"))
+    assert abs(sum(d["time_to_ocm_s"].values()) * 1e3 - d["ms_per_step"]) < 1e-6 * d["ms_per_step"]
+    # the strong-scaling reference point: the same graph on one GPU alone
+    single = d["single_gpu_same_config"]
+    assert single["value"] > 0 and single["unit"] == d["unit"] and single["steps"] == 2
+    assert d["e2e"] is None

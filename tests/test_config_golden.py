@@ -23,6 +23,12 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 with open(os.path.join(HERE, "golden", "config_golden.json")) as f:
     GOLD = json.load(f)
 SEED = GOLD["seed"]
+# configs 4 and 5 at their full sizes (10^9 and 2*10^9 edges, solved by the
+# reference on the GPU box: make_config_golden_full.py) are checked through
+# the bench's own path only -- sessions generated in HBM; building them on
+# the host would take tens of GB and minutes per test
+FULL = {c for c, v in GOLD["configs"].items() if v["m"] > 500_000_000}
+HOSTED = sorted(set(GOLD["configs"]) - FULL)
 
 
 def product_graph(cfg):
@@ -49,7 +55,7 @@ def sha(g):
     return h.hexdigest()
 
 
-@pytest.mark.parametrize("cfg", sorted(GOLD["configs"]))
+@pytest.mark.parametrize("cfg", HOSTED)
 def test_product_generator_builds_the_reference_graph(cfg):
     g = product_graph(cfg)
     ref = GOLD["configs"][cfg]
@@ -70,7 +76,7 @@ def check(sol, ref):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("cfg", sorted(GOLD["configs"]))
+@pytest.mark.parametrize("cfg", HOSTED)
 def test_device_matches_reference_on_config_graph(cfg):
     g = product_graph(cfg)
     for objective in ("min", "max"):
@@ -94,7 +100,8 @@ def test_device_matches_reference_on_config_graph(cfg):
                                  if GOLD["configs"][c]["spec"]["kind"] != "model"
                                  and "weights" not in GOLD["configs"][c]["spec"]])
 def test_hbm_generated_session_matches_reference(cfg):
-    """The bench's sessions generate the graph in HBM (gen_dev.cu): same answer."""
+    """The bench's sessions generate the graph in HBM (gen_dev.cu): same
+    answer -- for configs 4 and 5 at their full BASELINE sizes too."""
     c = GOLD["configs"][cfg]["spec"]
     spec = P.Generator(c["kind"], n=c["n"], deg=c["deg"], dmax=c.get("dmax", 0), wlo=1, whi=100,
                        seed=SEED)
