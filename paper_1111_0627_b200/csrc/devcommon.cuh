@@ -103,6 +103,7 @@ struct Ctl {
     unsigned syncs;                // grid barriers
     long long clk_total;           // block-0 SM clock over the launch
     long long clk[PH_COUNT];       // ... per phase (time up to the phase's barrier)
+    unsigned gbar;                 // grid-barrier arrivals (OCM_GBAR)
 };
 constexpr std::size_t kCtlSolveOffset = offsetof(Ctl, error);
 // error, overflow, lambda_up, nonconv are read together after every

@@ -2046,10 +2046,19 @@ struct LoopState {
 // carries only its own improvement variant, so ptxas allocates registers for
 // that one (a kernel holding all variants spilled inside the pass's loop).
 // G in {1, 2, 4, 8}: degrees above 128*G take the block-cooperative path.
+// OCM_GBAR=1 (default): the kernel's own release/acquire grid barrier;
+// 0: cooperative_groups grid.sync() (2-4% slower per solve,
+// profiles/r02/ab_gbar_r02.log)
+#ifndef OCM_GBAR
+#define OCM_GBAR 1
+#endif
+
 template <int MODE, int G>
 __global__ void __launch_bounds__(kBlock, kSolveMinBlocks) k_solve(KP p, int mode) {
     constexpr bool EXACT = MODE != 0;
+#if !OCM_GBAR
     cg::grid_group grid = cg::this_grid();
+#endif
     Ctl* const c = p.c;
     __shared__ LoopState s_park;
     LoopState st;
@@ -2069,7 +2078,24 @@ __global__ void __launch_bounds__(kBlock, kSolveMinBlocks) k_solve(KP p, int mod
     if (MODE == 1 && p.staged)
         staged_init(*reinterpret_cast<Staged*>(dyn_smem));
     auto sync = [&](int ph) {
+#if OCM_GBAR
+        // arrive (release) / wait (acquire) on a per-launch counter (zeroed
+        // with the per-solve Ctl fields): the k-th barrier completes when
+        // the counter reaches k * gridDim.x; the CTA barriers on both sides
+        // extend each side to the whole block
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const unsigned target = (st.nsync + 1) * gridDim.x;
+            asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(&c->gbar) : "memory");
+            unsigned v;
+            do {
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(&c->gbar) : "memory");
+            } while (static_cast<int>(v - target) < 0);
+        }
+        __syncthreads();
+#else
         grid.sync();
+#endif
         ++st.nsync;
         if (blockIdx.x == 0 && threadIdx.x == 0) {
             const long long t = clock64();

@@ -640,6 +640,10 @@ template <class M> void Session::launch_async(int mode) {
         d2h_ = 0;
         solve_ms_ = 0.0;
         launches_ = 0;
+    } else {
+        // a resumed launch keeps the solve's counters but counts its grid
+        // barriers from zero
+        CK(cudaMemsetAsync(&p.c->gbar, 0, sizeof(unsigned), s));
     }
     CK(cudaEventRecord(d.ev_start, s));
     if (prep_.R > 0) {
