@@ -19,7 +19,11 @@
 #include <cooperative_groups.h>
 #include <cub/cub.cuh>
 
+#include <atomic>
 #include <cstring>
+#if defined(__SSE2__)
+#include <emmintrin.h>
+#endif
 #include <condition_variable>
 #include <exception>
 #include <functional>
@@ -745,6 +749,33 @@ namespace {
 // from the other, so the transfer runs at PCIe speed instead of the driver's
 // pageable-copy path, and the caller's arrays are never registered or
 // modified. One ring per process, serialised by a lock.
+// out[i] = (int)in[i]; true if any in[i] is not an integer in int32 range
+// (or not finite). SSE2 truncation returns INT_MIN for out-of-range and NaN
+// inputs, so "converts back to itself" is the whole test (-0.0 passes as 0).
+bool narrow_i32(int* out, const double* in, std::size_t n) {
+    std::size_t i = 0;
+    bool bad = false;
+#if defined(__SSE2__)
+    __m128d acc = _mm_setzero_pd();
+    for (; i + 4 <= n; i += 4) {
+        const __m128d a = _mm_loadu_pd(in + i), b = _mm_loadu_pd(in + i + 2);
+        const __m128i ia = _mm_cvttpd_epi32(a), ib = _mm_cvttpd_epi32(b);
+        acc = _mm_or_pd(acc, _mm_cmpneq_pd(_mm_cvtepi32_pd(ia), a));
+        acc = _mm_or_pd(acc, _mm_cmpneq_pd(_mm_cvtepi32_pd(ib), b));
+        _mm_storeu_si128(reinterpret_cast<__m128i*>(out + i), _mm_unpacklo_epi64(ia, ib));
+    }
+    bad = _mm_movemask_pd(acc) != 0;
+#endif
+    for (; i < n; ++i) {
+        const double x = in[i];
+        const bool inr = x >= -2147483648.0 && x <= 2147483647.0; // false for NaN
+        const int v = inr ? static_cast<int>(x) : 0;
+        bad |= !inr || static_cast<double>(v) != x;
+        out[i] = v;
+    }
+    return bad;
+}
+
 class StagingRing {
   public:
     static constexpr std::size_t kChunk = 16u << 20;
@@ -774,6 +805,37 @@ class StagingRing {
             CK(cudaMemcpyAsync(to + off, buf_[k], len, cudaMemcpyHostToDevice, s));
             CK(cudaEventRecord(done_[k], s));
         }
+    }
+
+    // Weights that are all integers in int32 range cross PCIe as int32 --
+    // half the bytes -- into `tmp`, converted (and checked) by the host
+    // threads filling the staging slots. Returns false at the first chunk
+    // holding any other value (non-integral, too large, non-finite): the
+    // caller then copies the doubles. Pinned sources return false at once
+    // (the copy engine reads them directly, faster than a host pass).
+    bool copy_narrow(int* tmp, const double* src, std::size_t count, cudaStream_t s) {
+        if (count == 0 || pinned(src))
+            return false;
+        std::lock_guard<std::mutex> lock(mu_);
+        ensure();
+        constexpr std::size_t kPer = kChunk / sizeof(int);
+        for (std::size_t off = 0; off < count; off += kPer) {
+            const std::size_t len = std::min(kPer, count - off);
+            const int k = static_cast<int>(next_++ % kSlots);
+            CK(cudaEventSynchronize(done_[k]));
+            int* out = reinterpret_cast<int*>(buf_[k]);
+            const double* in = src + off;
+            std::atomic<bool> bad{false};
+            host_parts(len, [out, in, &bad](std::size_t lo, std::size_t hi) {
+                if (narrow_i32(out + lo, in + lo, hi - lo))
+                    bad.store(true, std::memory_order_relaxed);
+            });
+            if (bad.load())
+                return false;
+            CK(cudaMemcpyAsync(tmp + off, out, len * sizeof(int), cudaMemcpyHostToDevice, s));
+            CK(cudaEventRecord(done_[k], s));
+        }
+        return true;
     }
 
   private:
@@ -813,14 +875,19 @@ class StagingRing {
                 x.join();
         }
         void copy(char* dst, const char* src, std::size_t len) {
+            run_parts(len, [dst, src](std::size_t lo, std::size_t hi) {
+                std::memcpy(dst + lo, src + lo, hi - lo);
+            });
+        }
+        // fn(lo, hi) over [0, len) in n_ parts of multiples of 64
+        void run_parts(std::size_t len, const std::function<void(std::size_t, std::size_t)>& fn) {
             if (len < (1u << 20) || n_ == 1) {
-                std::memcpy(dst, src, len);
+                fn(0, len);
                 return;
             }
             {
                 std::lock_guard<std::mutex> l(m_);
-                dst_ = dst;
-                src_ = src;
+                fn_ = &fn;
                 len_ = len;
                 pending_ = n_ - 1;
                 ++gen_;
@@ -836,7 +903,7 @@ class StagingRing {
             const std::size_t per = ((len_ + n_ - 1) / n_ + 63) & ~std::size_t(63);
             const std::size_t lo = std::min(len_, per * t), hi = std::min(len_, per * (t + 1));
             if (hi > lo)
-                std::memcpy(dst_ + lo, src_ + lo, hi - lo);
+                (*fn_)(lo, hi);
         }
         void run(int t) {
             unsigned long long seen = 0;
@@ -861,8 +928,7 @@ class StagingRing {
         unsigned long long gen_ = 0;
         int pending_ = 0;
         bool quit_ = false;
-        char* dst_ = nullptr;
-        const char* src_ = nullptr;
+        const std::function<void(std::size_t, std::size_t)>* fn_ = nullptr;
         std::size_t len_ = 0;
     };
     void host_copy(char* dst, const char* src, std::size_t len) {
@@ -871,6 +937,11 @@ class StagingRing {
             pool_ = std::make_unique<CopyPool>(static_cast<int>(std::min(8u, std::max(1u, hw / 2))));
         }
         pool_->copy(dst, src, len);
+    }
+    void host_parts(std::size_t len, const std::function<void(std::size_t, std::size_t)>& fn) {
+        if (!pool_)
+            host_copy(nullptr, nullptr, 0); // starts the pool
+        pool_->run_parts(len, fn);
     }
     std::unique_ptr<CopyPool> pool_;
     std::mutex mu_;
@@ -884,6 +955,12 @@ class StagingRing {
 // offsets) before the region split reads them; the weights stream in on
 // the side stream meanwhile and are checked where they are first read
 // (kp_max_abs with check = 1).
+__global__ void kp_widen_w(std::uint64_t m, const int* wi, double* w) {
+    for (std::uint64_t e = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x; e < m;
+         e += std::uint64_t(gridDim.x) * blockDim.x)
+        w[e] = static_cast<double>(wi[e]);
+}
+
 struct CsrCheck {
     unsigned long long bad_target;
     unsigned long long bad_weight;
@@ -950,6 +1027,7 @@ void device_prepare(const HostCsr& g, const ocm_solve_options& opt, DeviceState&
     struct WeightStager {
         std::thread th;
         std::exception_ptr err;
+        bool narrow = false; // the weights crossed PCIe as int32
         void join() {
             if (th.joinable())
                 th.join();
@@ -974,10 +1052,19 @@ void device_prepare(const HostCsr& g, const ocm_solve_options& opt, DeviceState&
         const int dev = d.device;
         cudaStream_t side = d.side;
         cudaEvent_t done = d.side_done;
-        wstage.th = std::thread([&ring, &wstage, &w, &g, m, dev, side, done] {
+        const int sms = d.sms;
+        wstage.th = std::thread([&ring, &wstage, &w, &g, m, dev, sms, side, done] {
             try {
                 CK(cudaSetDevice(dev));
-                ring.copy(w.p, g.weight, m * 8, side);
+                DBuf<int> wi; // freed in order on the side stream
+                wi.alloc(m, side);
+                if (!std::getenv("OCM_NO_NARROW") && ring.copy_narrow(wi.p, g.weight, m, side)) {
+                    kp_widen_w<<<grid_for(m, sms, 8), kBlock, 0, side>>>(m, wi.p, w.p);
+                    CK(cudaGetLastError());
+                    wstage.narrow = true;
+                } else {
+                    ring.copy(w.p, g.weight, m * 8, side);
+                }
                 CK(cudaEventRecord(done, side));
             } catch (...) {
                 wstage.err = std::current_exception();
@@ -1031,7 +1118,7 @@ void device_prepare(const HostCsr& g, const ocm_solve_options& opt, DeviceState&
     device_prepare_csr(n, m, row, tgt, w, exactness, opt, d, info, w_ready,
                        [&wstage] { wstage.join(); });
     wstage.join();
-    info.h2d_bytes = (std::size_t(n) + 1) * (g.index64 ? 8 : 4) + m * 12;
+    info.h2d_bytes = (std::size_t(n) + 1) * (g.index64 ? 8 : 4) + m * (wstage.narrow ? 8 : 12);
 }
 
 void device_prepare_csr(std::uint32_t n, std::uint64_t m, DBuf<std::uint32_t>& row,

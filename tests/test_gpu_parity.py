@@ -327,7 +327,32 @@ def test_solve_csr_large_pageable_graph():
     b = P.solve_csr(g.n, idx, d, w)
     assert (a.mu_exact, a.cycle_vertices, a.stats.spf_passes) == \
         (b.mu_exact, b.cycle_vertices, b.stats.spf_passes)
-    assert b.stats.h2d_bytes == (g.n + 1) * 4 + g.m * 12
+    # integral weights in int32 range cross PCIe as int32 (widened on the device)
+    assert b.stats.h2d_bytes == (g.n + 1) * 4 + g.m * 8
+
+
+@pytest.mark.parametrize("last", [2.5, 2.0**31, -2.0**31 - 1, -0.0, np.nan])
+def test_solve_csr_weight_narrowing_falls_back(last):
+    """The int32 upload of pageable weights gives up at the first chunk
+    holding any other value -- here the very last edge of a 10^6 x 8 graph,
+    after ~3 chunks went up as int32 -- and copies the doubles instead: the
+    result equals the pinned ocm_solve path (float lane, wide lane, the
+    non-finite error of build_graph)."""
+    g = P.generate(P.Generator("uniform", n=1_000_000, deg=8, seed=6))
+    idx, d, w = _csr(g)
+    w = w.copy()
+    w[-1] = last
+    if np.isnan(last):
+        with pytest.raises(ValueError, match=f"edge {g.m - 1} has non-finite weight"):
+            P.solve_csr(g.n, idx, d, w)
+        return
+    src = np.repeat(np.arange(g.n, dtype=np.uint32), np.diff(idx).astype(np.int64))
+    a = P.solve(P.build_graph(g.n, (src, d, w)))
+    b = P.solve_csr(g.n, idx, d, w)
+    assert (a.exact, a.mu_exact, a.mu, a.cycle_vertices, a.stats.spf_passes) == \
+        (b.exact, b.mu_exact, b.mu, b.cycle_vertices, b.stats.spf_passes)
+    narrow = last == 0.0  # -0.0 is the integer 0
+    assert b.stats.h2d_bytes == (g.n + 1) * 4 + g.m * (8 if narrow else 12)
 
 
 def test_solve_csr_validates_like_build_graph():
