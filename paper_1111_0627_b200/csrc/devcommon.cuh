@@ -160,6 +160,7 @@ struct KP {
     long long* cyc_wi;
     double* cyc_wf;
     std::uint32_t* conn;
+    std::uint32_t* cbits; // connected-vertex bitmap (attach's head test), N/8 bytes
     std::uint32_t* rem[2];
     PJV* pv[2];
     PJVW* pvw[2];
@@ -271,7 +272,7 @@ struct DeviceState {
     int sms = 148;
     cudaStream_t stream = nullptr;
     DBuf<std::uint32_t> row, reg, succ_e, succ_v, comp, wlist, cyc_len, conn, rem0, rem1, src,
-        iters, indeg, plist, clist, cmark, cmark2, heavy, xbar, hot;
+        iters, indeg, plist, clist, cmark, cmark2, heavy, xbar, hot, cbits;
     DBuf<PJV> pv0, pv1;
     DBuf<PJVW> pvw0, pvw1;
     DBuf<__int128> key_w;
@@ -312,7 +313,8 @@ struct DeviceState {
         if (stream)
             cudaStreamSynchronize(stream);
         for (auto* b : {&row, &reg, &succ_e, &succ_v, &comp, &wlist, &cyc_len, &conn, &rem0, &rem1,
-                        &src, &iters, &indeg, &plist, &clist, &cmark, &cmark2, &heavy, &xbar, &hot})
+                        &src, &iters, &indeg, &plist, &clist, &cmark, &cmark2, &heavy, &xbar, &hot,
+                        &cbits})
             b->release();
         pv0.release();
         pv1.release();

@@ -119,6 +119,31 @@ __device__ __forceinline__ void clear_pred_all(const KP& p) {
 #endif
 }
 
+// Connected-vertex bitmap (OCM_CBITS=1, default): bit v is set once v is
+// connected to its region's winning cycle (kept, or attached in a layer).
+// Attach tests an edge's head with one bit of this N/8-byte array -- L2-
+// resident even at 2.5*10^8 vertices -- instead of a 4-byte gather of conn[]
+// from HBM, and confirms only set bits against conn[] (a head attached in
+// the current layer has its bit set but conn == layer). Cleared by classify.
+// Used when conn[] outgrows L2 (p.cbits != null: N >= 2^24 by default,
+// OCM_CBITS_MIN_N): -10% per solve at configs 4 and 5, +4% at config 2,
+// where conn[] is L2-resident and keep's extra atomics cost more than
+// attach saves (profiles/r02/ab_cbits_r02.log).
+#ifndef OCM_CBITS
+#define OCM_CBITS 1
+#endif
+__device__ __forceinline__ void cbit_set(const KP& p, std::uint32_t v, bool on) {
+    // one atomicOr per bitmap word per warp
+    const unsigned act = __activemask();
+    const unsigned want = __ballot_sync(act, on);
+    if (!on)
+        return;
+    const unsigned peers = __match_any_sync(want, v >> 5);
+    const unsigned bits = __reduce_or_sync(peers, 1u << (v & 31));
+    if (static_cast<unsigned>(__ffs(peers) - 1) == (threadIdx.x & 31))
+        atomicOr(&p.cbits[v >> 5], bits);
+}
+
 // ------------------------------------------------------------ modes
 //
 // Arithmetic mode of a k_solve instantiation (template parameter MODE):
@@ -1083,6 +1108,11 @@ __device__ __forceinline__ void ph_classify(const KP& p, int par, const Ring& ra
         p.changed[par ^ 1][r] = 0;
     }
     block_count(still, ra);
+#if OCM_CBITS
+    if (p.cbits)
+        for (std::size_t w = gtid(); w < (std::size_t(p.N) + 31) / 32; w += gstride())
+            p.cbits[w] = 0; // set again by keep and attach
+#endif
     // four consecutive vertices per thread, one reservation per ring per
     // 1024 vertices (a per-256 append made the two list counters the
     // contended words of the phase); lists stay in vertex order
@@ -1814,6 +1844,10 @@ __device__ __forceinline__ void ph_keep(const KP& p, std::uint64_t nC, std::uint
                     key_st<MODE>(p, v, static_cast<KeyT<MODE>>(kk));
                 }
         }
+#if OCM_CBITS
+        if (p.cbits)
+            cbit_set(p, v, !take);
+#endif
         if (take)
             p.rem[0][warp_append(ring)] = v;
     }
@@ -1851,14 +1885,33 @@ __device__ __forceinline__ void ph_attach(const KP& p, int cur, std::uint64_t pe
                     const std::uint32_t e = min(e0 + u, e_end - 1); // tail masked below
                     tt[u] = EXACT ? static_cast<std::uint32_t>(__ldg(&p.ew[e]).x) : p.fe[e].t;
                 }
+                int hit = -1;
+#if OCM_CBITS
+                if (p.cbits) {
+                unsigned set = 0;
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    if (e0 + u < e_end && (ldv(p.cbits[tt[u] >> 5]) >> (tt[u] & 31) & 1u))
+                        set |= 1u << u;
+                (void)cc;
+                for (; set; set &= set - 1) {
+                    const int u = __ffs(set) - 1;
+                    if (ldv(p.conn[tt[u]]) < layer) {
+                        hit = u;
+                        break;
+                    }
+                }
+                } else
+#endif
+                {
 #pragma unroll
                 for (int u = 0; u < 8; ++u)
                     cc[u] = e0 + u < e_end ? ldv(p.conn[tt[u]]) : NONE;
-                int hit = -1;
 #pragma unroll
                 for (int u = 7; u >= 0; --u)
                     if (cc[u] < layer)
                         hit = u;
+                }
                 if (hit >= 0) {
                     const std::uint32_t e = e0 + hit, t = tt[hit];
                     p.succ_e[x] = e;
@@ -1876,6 +1929,10 @@ __device__ __forceinline__ void ph_attach(const KP& p, int cur, std::uint64_t pe
                     }
                     p.conn[x] = layer;
                     pend = false;
+#if OCM_CBITS
+                    if (p.cbits)
+                        atomicOr(&p.cbits[x >> 5], 1u << (x & 31));
+#endif
                 }
             }
         }

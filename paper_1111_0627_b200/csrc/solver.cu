@@ -193,6 +193,7 @@ void Session::init(const std::function<void(DeviceState&)>& prepare) {
     for (auto* b : {&d.comp, &d.wlist, &d.cyc_len, &d.conn, &d.rem0, &d.rem1,
                     &d.indeg, &d.plist, &d.clist, &d.cmark, &d.cmark2})
         b->alloc(N1, d.stream);
+    d.cbits.alloc((N1 + 31) / 32, d.stream);
     d.pj0.alloc(N1, d.stream);
     d.pj1.alloc(N1, d.stream);
     d.src.alloc(R1, d.stream);
@@ -331,6 +332,7 @@ void Session::init(const std::function<void(DeviceState&)>& prepare) {
     p.cyc_wi = d.cyc_wi.p;
     p.cyc_wf = d.cyc_wf.p;
     p.conn = d.conn.p;
+    p.cbits = N >= static_cast<std::size_t>(env_int("OCM_CBITS_MIN_N", 1 << 24)) ? d.cbits.p : nullptr;
     p.rem[0] = d.rem0.p;
     p.rem[1] = d.rem1.p;
     p.pv[0] = d.pv0.p;

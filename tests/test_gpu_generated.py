@@ -176,3 +176,35 @@ def test_tma_staged_pass_vs_oracle(objective, monkeypatch):
     sess = P.Session(g, P.SolveOptions(objective=objective))
     sol = sess.solve()
     check_against(sol, sess.values(), oracle_record(g.n, s, d, w, objective, "tarjan"))
+
+
+@pytest.mark.parametrize("spec", [
+    P.Generator("uniform", n=100_000, deg=8, seed=3),
+    P.Generator("powerlaw-hubs", n=100_000, deg=8, dmax=1 << 20, seed=4),
+    P.Generator("powerlaw", n=50_000, deg=2, dmax=5000, wlo=-50, whi=50, seed=6),
+], ids=["uniform", "powerlaw-hubs", "powerlaw-signed"])
+@pytest.mark.parametrize("objective", ["min", "max"])
+def test_connected_bitmap_attach_matches_gathers(spec, objective, monkeypatch):
+    """Attach testing heads with the connected-vertex bitmap (on by default
+    from 2^24 vertices; OCM_CBITS_MIN_N=0 forces it) equals the conn[]
+    gathers bit for bit: same policy, values, statistics."""
+    monkeypatch.setenv("OCM_CBITS_MIN_N", "2147483647")
+    a = P.Session.generated(spec, P.SolveOptions(objective=objective))
+    monkeypatch.setenv("OCM_CBITS_MIN_N", "0")
+    b = P.Session.generated(spec, P.SolveOptions(objective=objective))
+    solve_both(a, b)
+    solve_both(a, b)
+
+
+@pytest.mark.parametrize("objective", ["min", "max"])
+def test_connected_bitmap_attach_vs_oracle(objective, monkeypatch):
+    """Forced bitmap on a multi-region graph, exact and float lanes, against
+    the pinned oracle."""
+    monkeypatch.setenv("OCM_CBITS_MIN_N", "0")
+    g = P.generate(P.Generator("powerlaw", n=20_000, deg=2, dmax=2000, seed=12))
+    s, d, w = g.edges()
+    for ww in (w, w / 8 + 0.125):
+        gg = P.build_graph(g.n, (s, d, ww))
+        sess = P.Session(gg, P.SolveOptions(objective=objective))
+        sol = sess.solve()
+        check_against(sol, sess.values(), oracle_record(g.n, s, d, ww, objective, "tarjan"))
