@@ -1793,11 +1793,14 @@ __device__ __forceinline__ void ph_vote_one_block(const KP& p, std::uint64_t nM,
 // exactly 0, so extra turns add nothing); a leaf takes K(succ) + w*den - num,
 // recomputing its core successor's key the same way (never reading a key
 // being written in this phase). Resets the in-degree of core vertices.
+// The formula also holds ON the winning cycle (its reduced weight is 0, so
+// K(u) = w(u)*den - num + K(succ u) at every cycle vertex, the anchor
+// included): a leaf's successor needs no cycle-membership test (a random
+// 4-byte gather at HBM-resident sizes); core vertices skip their cycle
+// vertices (keys already written by the vote) with a coalesced test.
 template <int MODE>
 __device__ __forceinline__ KeyT<MODE> core_key(const KP& p, const PJC* a, std::uint32_t v, std::uint32_t r,
-                                               std::uint32_t stamp, unsigned long long L, bool& ovf) {
-    if (p.cmark[v] == stamp) // on the winning cycle: from the cycle prefix sums
-        return key_ld<MODE>(p, v);
+                                               unsigned long long L, bool& ovf) {
     const PJC x = a[v];
     const __int128 kk = static_cast<__int128>(x.w) * p.lam_den[r] -
                         static_cast<__int128>(L) * p.lam_num[r] + key_ld<MODE>(p, x.nxt);
@@ -1827,7 +1830,7 @@ __device__ __forceinline__ void ph_keep(const KP& p, std::uint64_t nC, std::uint
             take = !kept;
             if constexpr (EXACT)
                 if (kept && p.cmark[v] != stamp)
-                    key_st<MODE>(p, v, core_key<MODE>(p, a, v, r, stamp, L, ovf));
+                    key_st<MODE>(p, v, core_key<MODE>(p, a, v, r, L, ovf));
         } else {
             v = p.plist[i - nC];
             const std::uint32_t s = p.succ_v[v];
@@ -1837,7 +1840,7 @@ __device__ __forceinline__ void ph_keep(const KP& p, std::uint64_t nC, std::uint
             take = !kept;
             if constexpr (EXACT)
                 if (kept) {
-                    const __int128 kk = static_cast<__int128>(core_key<MODE>(p, a, s, r, stamp, L, ovf)) +
+                    const __int128 kk = static_cast<__int128>(core_key<MODE>(p, a, s, r, L, ovf)) +
                                         static_cast<__int128>(succ_w<MODE>(p, v)) * p.lam_den[r] -
                                         p.lam_num[r];
                     ovf |= !key_in_range<MODE>(kk);
