@@ -198,13 +198,15 @@ def test_connected_bitmap_attach_matches_gathers(spec, objective, monkeypatch):
 
 @pytest.mark.parametrize("objective", ["min", "max"])
 def test_connected_bitmap_attach_vs_oracle(objective, monkeypatch):
-    """Forced bitmap on a multi-region graph, exact and float lanes, against
-    the pinned oracle."""
+    """Forced bitmap on a multi-region graph, exact (64- and 128-bit keys)
+    and float lanes, against the pinned oracle."""
     monkeypatch.setenv("OCM_CBITS_MIN_N", "0")
     g = P.generate(P.Generator("powerlaw", n=20_000, deg=2, dmax=2000, seed=12))
     s, d, w = g.edges()
-    for ww in (w, w / 8 + 0.125):
+    for ww, wide in ((w, "0"), (w / 8 + 0.125, "0"), (w * 2.0**33, "1")):
+        monkeypatch.setenv("OCM_WIDE", wide)
         gg = P.build_graph(g.n, (s, d, ww))
         sess = P.Session(gg, P.SolveOptions(objective=objective))
         sol = sess.solve()
+        assert sess.wide == (wide == "1")
         check_against(sol, sess.values(), oracle_record(g.n, s, d, ww, objective, "tarjan"))

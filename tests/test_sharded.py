@@ -299,3 +299,20 @@ def test_fused_shards_with_tma_staged_pass(objective, monkeypatch):
     sols, vals = _fused(src, objective, 2)
     for b, vb in zip(sols, vals):
         _same(a, va, b, vb)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("objective", ["min", "max"])
+def test_fused_and_sharded_with_connected_bitmap(objective, monkeypatch):
+    """The replicated keep/attach phases of both sharded lanes with the
+    connected-vertex bitmap forced on (by default only from 2^24 vertices)."""
+    src = P.Generator("powerlaw", n=50_000, deg=2, dmax=5000, wlo=-50, whi=50, seed=22)
+    a, va = _single(src, objective)
+    monkeypatch.setenv("OCM_CBITS_MIN_N", "0")
+    monkeypatch.setenv("OCM_GRID", str(148 * 4 // 2))
+    sols, vals = _fused(src, objective, 2)
+    for b, vb in zip(sols, vals):
+        _same(a, va, b, vb)
+    sols, vals = _sharded(src, objective, 3)
+    for b, vb in zip(sols, vals):
+        _same(a, va, b, vb)
