@@ -1861,13 +1861,57 @@ __device__ __forceinline__ void ph_keep(const KP& p, std::uint64_t nC, std::uint
 // One breadth layer of howard_par.hpp:433 connectGpi: a pending vertex
 // attaches through its smallest out-edge whose head was connected in an
 // earlier layer (conn < layer); the stamps make the layer discipline exact
-// under any schedule.
+// under any schedule. Pending vertices of degree >= kAttachHeavy are scanned
+// by their whole block, 2048 edges per step with a block-wide minimum of the
+// hit edge ids (one thread walking a 10^5..10^6-edge hub row 8 edges at a
+// time held every other block at the layer's barrier).
+#ifndef OCM_ATTACH_HEAVY
+#define OCM_ATTACH_HEAVY 256
+#endif
+constexpr std::uint32_t kAttachHeavy = OCM_ATTACH_HEAVY;
+
+// Is edge e's head connected in an earlier layer? (bitmap first when on)
+template <int MODE>
+__device__ __forceinline__ bool head_connected(const KP& p, std::uint32_t t, std::uint32_t layer) {
+#if OCM_CBITS
+    if (p.cbits && !(ldv(p.cbits[t >> 5]) >> (t & 31) & 1u))
+        return false;
+#endif
+    return ldv(p.conn[t]) < layer;
+}
+
+template <int MODE>
+__device__ __forceinline__ void attach_via(const KP& p, std::uint32_t x, std::uint32_t e, std::uint32_t t,
+                                           std::uint32_t layer, bool& ovf) {
+    constexpr bool EXACT = MODE != 0;
+    p.succ_e[x] = e;
+    p.succ_v[x] = t;
+    if constexpr (EXACT) {
+        const long long w = edge_w<MODE>(p, e, __ldg(&p.ew[e]));
+        succ_w_st<MODE>(p, x, t, w);
+        const std::uint32_t r = __ldg(&p.reg[x]);
+        const __int128 kk = static_cast<__int128>(key_ld<MODE>(p, t)) +
+                            static_cast<__int128>(w) * p.lam_den[r] - p.lam_num[r];
+        ovf |= !key_in_range<MODE>(kk);
+        key_st<MODE>(p, x, static_cast<KeyT<MODE>>(kk));
+    } else {
+        p.succ_wf[x] = p.fe[e].w;
+    }
+    p.conn[x] = layer;
+#if OCM_CBITS
+    if (p.cbits)
+        atomicOr(&p.cbits[x >> 5], 1u << (x & 31));
+#endif
+}
+
 template <int MODE>
 __device__ __forceinline__ void ph_attach(const KP& p, int cur, std::uint64_t pending, std::uint32_t layer,
                                           const Ring& ring) {
     constexpr bool EXACT = MODE != 0;
     const std::uint32_t* list = p.rem[cur];
     bool ovf = false;
+    __shared__ std::uint32_t s_hx[kBlock], s_hown[kBlock];
+    __shared__ unsigned s_nh, s_min;
     // block-ordered appends: the next layer's list keeps the vertex order of
     // this one (warp-order appends measured 12% slower at config 5, where
     // layers are long and the row/edge reads profit from the order)
@@ -1875,10 +1919,18 @@ __device__ __forceinline__ void ph_attach(const KP& p, int cur, std::uint64_t pe
         const std::uint64_t i = i0_b + threadIdx.x;
         bool pend = false;
         std::uint32_t x = 0;
+        if (threadIdx.x == 0)
+            s_nh = 0;
+        __syncthreads();
         if (i < pending) {
             x = list[i];
             pend = true;
             const std::uint32_t b = __ldg(&p.row[x]), e_end = __ldg(&p.row[x + 1]);
+            if (e_end - b >= kAttachHeavy) {
+                const unsigned h = atomicAdd(&s_nh, 1u);
+                s_hx[h] = x;
+                s_hown[h] = threadIdx.x;
+            } else {
             // the first out-edge (CSR order) into a vertex connected earlier;
             // 8 edges and their heads' stamps in flight at a time
             for (std::uint32_t e0 = b; pend && e0 < e_end; e0 += 8) {
@@ -1916,27 +1968,44 @@ __device__ __forceinline__ void ph_attach(const KP& p, int cur, std::uint64_t pe
                         hit = u;
                 }
                 if (hit >= 0) {
-                    const std::uint32_t e = e0 + hit, t = tt[hit];
-                    p.succ_e[x] = e;
-                    p.succ_v[x] = t;
-                    if constexpr (EXACT) {
-                        const long long w = edge_w<MODE>(p, e, __ldg(&p.ew[e]));
-                        succ_w_st<MODE>(p, x, t, w);
-                        const std::uint32_t r = __ldg(&p.reg[x]);
-                        const __int128 kk = static_cast<__int128>(key_ld<MODE>(p, t)) +
-                                            static_cast<__int128>(w) * p.lam_den[r] - p.lam_num[r];
-                        ovf |= !key_in_range<MODE>(kk);
-                        key_st<MODE>(p, x, static_cast<KeyT<MODE>>(kk));
-                    } else {
-                        p.succ_wf[x] = p.fe[e].w;
-                    }
-                    p.conn[x] = layer;
+                    attach_via<MODE>(p, x, e0 + hit, tt[hit], layer, ovf);
                     pend = false;
-#if OCM_CBITS
-                    if (p.cbits)
-                        atomicOr(&p.cbits[x >> 5], 1u << (x & 31));
-#endif
                 }
+            }
+            }
+        }
+        __syncthreads();
+        // the block's high-degree pending vertices, one at a time, by all
+        // its threads: 8 consecutive edges per thread per step, the least
+        // hit edge id wins (= the first in CSR order)
+        const unsigned nh = s_nh;
+        for (unsigned h = 0; h < nh; ++h) {
+            const std::uint32_t hx = s_hx[h];
+            const std::uint32_t b = __ldg(&p.row[hx]), e_end = __ldg(&p.row[hx + 1]);
+            std::uint32_t found = NONE;
+            for (std::uint32_t w0 = b; w0 < e_end; w0 += kBlock * 8) {
+                if (threadIdx.x == 0)
+                    s_min = NONE;
+                __syncthreads();
+                const std::uint32_t e0 = w0 + threadIdx.x * 8;
+                for (std::uint32_t e = e0; e < min(e0 + 8, e_end); ++e) {
+                    const std::uint32_t t = EXACT ? static_cast<std::uint32_t>(__ldg(&p.ew[e]).x) : p.fe[e].t;
+                    if (head_connected<MODE>(p, t, layer)) {
+                        atomicMin(&s_min, e);
+                        break;
+                    }
+                }
+                __syncthreads();
+                found = s_min;
+                __syncthreads(); // everyone read s_min before the next reset
+                if (found != NONE)
+                    break;
+            }
+            if (found != NONE && threadIdx.x == s_hown[h]) {
+                const std::uint32_t t = EXACT ? static_cast<std::uint32_t>(__ldg(&p.ew[found]).x)
+                                              : p.fe[found].t;
+                attach_via<MODE>(p, hx, found, t, layer, ovf);
+                pend = false;
             }
         }
         const std::uint64_t slot = block_append(pend, ring);

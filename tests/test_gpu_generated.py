@@ -210,3 +210,22 @@ def test_connected_bitmap_attach_vs_oracle(objective, monkeypatch):
         sol = sess.solve()
         assert sess.wide == (wide == "1")
         check_against(sol, sess.values(), oracle_record(g.n, s, d, ww, objective, "tarjan"))
+
+
+@pytest.mark.parametrize("objective", ["min", "max"])
+@pytest.mark.parametrize("cbits", ["0", "2147483647"])
+def test_block_cooperative_attach_vs_oracle(objective, cbits, monkeypatch):
+    """Pending vertices of out-degree >= 256 attach by a block-wide scan of
+    their row (first hit in CSR order = least hit edge id): a dense
+    power-law graph where ~6% of the vertices are that heavy, exact and
+    float lanes, with and without the connected bitmap, against the oracle."""
+    monkeypatch.setenv("OCM_CBITS_MIN_N", cbits)
+    g = P.generate(P.Generator("powerlaw", n=4000, deg=64, dmax=4000, seed=23))
+    s, d, w = g.edges()
+    assert (np.bincount(s, minlength=g.n) >= 256).mean() > 0.03
+    for ww in (w, w / 8 + 0.125):
+        gg = P.build_graph(g.n, (s, d, ww))
+        sess = P.Session(gg, P.SolveOptions(objective=objective))
+        sol = sess.solve()
+        assert sol.stats.fixpoint_iters > 0
+        check_against(sol, sess.values(), oracle_record(g.n, s, d, ww, objective, "tarjan"))
