@@ -778,7 +778,9 @@ bool narrow_i32(int* out, const double* in, std::size_t n) {
 
 class StagingRing {
   public:
-    static constexpr std::size_t kChunk = 16u << 20;
+    // chunk size (OCM_STAGE_MB) and host copy threads (OCM_COPY_THREADS) are
+    // read once per process
+    std::size_t kChunk = 8u << 20; // 8 MB: +2.7% e2e over 16 MB (profiles/r02/e2e_staging_r02.log)
     static constexpr int kSlots = 3;
 
     static StagingRing& get() {
@@ -818,7 +820,7 @@ class StagingRing {
             return false;
         std::lock_guard<std::mutex> lock(mu_);
         ensure();
-        constexpr std::size_t kPer = kChunk / sizeof(int);
+        const std::size_t kPer = kChunk / sizeof(int);
         for (std::size_t off = 0; off < count; off += kPer) {
             const std::size_t len = std::min(kPer, count - off);
             const int k = static_cast<int>(next_++ % kSlots);
@@ -850,6 +852,9 @@ class StagingRing {
     void ensure() {
         if (buf_[0])
             return;
+        if (const char* mb = std::getenv("OCM_STAGE_MB"))
+            if (std::atoi(mb) > 0)
+                kChunk = std::size_t(std::atoi(mb)) << 20;
         for (int k = 0; k < kSlots; ++k) {
             CK(cudaHostAlloc(reinterpret_cast<void**>(&buf_[k]), kChunk, cudaHostAllocPortable));
             CK(cudaEventCreateWithFlags(&done_[k], cudaEventDisableTiming));
@@ -934,7 +939,11 @@ class StagingRing {
     void host_copy(char* dst, const char* src, std::size_t len) {
         if (!pool_) {
             const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-            pool_ = std::make_unique<CopyPool>(static_cast<int>(std::min(8u, std::max(1u, hw / 2))));
+            int nt = static_cast<int>(std::min(8u, std::max(1u, hw / 2)));
+            if (const char* e = std::getenv("OCM_COPY_THREADS"))
+                if (std::atoi(e) > 0)
+                    nt = std::atoi(e);
+            pool_ = std::make_unique<CopyPool>(nt);
         }
         pool_->copy(dst, src, len);
     }
