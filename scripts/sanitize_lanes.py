@@ -7,7 +7,8 @@ Lanes: exact (uniform + power-law with the heavy path), float, sccoff,
 staged (TMA-staged improvement pass forced on), wide (128-bit keys forced
 on; and a weight of 2^40), hot (shared-memory hub table forced on), csr
 (ocm_solve_csr from pageable arrays: the staging ring), certify, sharded,
-fused. Each checks its answer against the oracle or the plain exact lane."""
+fused, cbits (connected-vertex bitmap forced on), heavyattach (block-
+cooperative attach of high-degree pending vertices). Each checks its answer against the oracle or the plain exact lane."""
 import os
 import sys
 
@@ -18,7 +19,7 @@ import oracle as O  # noqa: E402
 import paper_1111_0627_b200 as P  # noqa: E402
 
 LANES = sys.argv[1:] or ["exact", "float", "sccoff", "staged", "wide", "hot", "csr", "certify",
-                         "sharded", "fused"]
+                         "sharded", "fused", "cbits", "heavyattach"]
 
 
 def check(g, opt, env=None):
@@ -67,6 +68,20 @@ for lane in LANES:
             idx, t, w = uni.csr()
             sol = P.solve_csr(uni.n, idx.astype(np.uint32), t, w, o)
             assert sol.mu_exact == P.solve(uni, o).mu_exact
+            # int32 narrowing of pageable weights, and its fallback
+            wf = w.copy()
+            wf[-1] = 2.5
+            sol = P.solve_csr(uni.n, idx.astype(np.uint32), t, wf, o)
+            assert not sol.exact
+        elif lane == "cbits":
+            check(uni, o, {"OCM_CBITS_MIN_N": "0"})
+            check(plaw, o, {"OCM_CBITS_MIN_N": "0"})
+            s, d, w = plaw.edges()
+            check(P.build_graph(plaw.n, (s, d, w / 8 + 0.125)), o, {"OCM_CBITS_MIN_N": "0"})
+        elif lane == "heavyattach":
+            dense = P.generate(P.Generator("powerlaw", n=1500, deg=64, dmax=1500, seed=3))
+            check(dense, o)
+            check(dense, o, {"OCM_CBITS_MIN_N": "0"})
         elif lane == "certify":
             s = check(uni, o)
             c = s.certify()
