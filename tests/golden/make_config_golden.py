@@ -23,10 +23,10 @@ Configs (BASELINE.json "configs"; bench.py CONFIGS):
       to the reference's solve directly)
   4s  power-law in+out-degree ("powerlaw-hubs") at n = 10^6 -- config 4's
       generator at a size the reference solves in about a minute. Config 4
-      itself (6.4*10^7 vertices, ~10^9 edges) and config 5 (2*10^9 edges) do
-      not fit: the reference's Graph plus the EdgeInput copy its build_graph
-      needs is ~40 B/edge (40-80 GB, this container has 62 GB) and its
-      ~1.6*10^7 edge-passes/s would take 2-4 h per objective.
+      itself (6.4*10^7 vertices, ~10^9 edges) is written by
+      make_config_golden_full.py (memory-mapped inputs, ~1.5-3 h per
+      objective); config 5 (2*10^9 edges, ~80 GB in the reference's
+      representation) fits neither this container nor the time budget.
 """
 from __future__ import annotations
 
