@@ -11,7 +11,7 @@ counts -- config 3 at its full 19-client size (1.05*10^7 states); config 2's
 graph also with float weights (FloatMode: the same double mu) and with
 --scc off (the Hamiltonian-augmented graph); config 4 at its full size
 (6.4*10^7 vertices, 9.9*10^8 edges: make_config_golden_full.py, the
-reference ran ~1.5 h per objective), through the bench's HBM-generated
+reference ran 1.5 h (min) and 2.8 h (max)), through the bench's HBM-generated
 sessions. That the product's generator builds the graph the reference
 solved at that size is recorded once: profiles/r02/full_config_product_r02.log
 (SHA-256 equal to the fixture's)."""
