@@ -161,6 +161,7 @@ struct KP {
     double* cyc_wf;
     std::uint32_t* conn;
     std::uint32_t* cbits; // connected-vertex bitmap (attach's head test), N/8 bytes
+    int round_s;          // doubling steps per pass (2 or 3; selects the k_solve instantiation)
     std::uint32_t* rem[2];
     PJV* pv[2];
     PJVW* pvw[2];

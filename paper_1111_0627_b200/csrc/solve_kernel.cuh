@@ -1171,6 +1171,18 @@ __device__ __forceinline__ void ph_classify(const KP& p, int par, const Ring& ra
 #ifndef OCM_ROUND_ILP
 #define OCM_ROUND_ILP 1
 #endif
+// Doubling steps per pass S: 2^S - 1 chained gathers take records of 2^k
+// steps to 2^(k+S). Fewer passes (barriers) against more gathers per step:
+// S = 3 while the records are L2-resident (config 2: -2%), S = 2 beyond
+// (configs 4/5: S = 3 +3-5%, S = 1 +1-3%; profiles/r02/ab_rounds_r02.log).
+// A kernel per S (template SR: the exact lane has an S = 3 instantiation; a
+// runtime switch inside one kernel cost configs 4/5 1-2%, the code of both
+// passes living in one register allocation), chosen per session
+// (OCM_ROUND_S env); -DOCM_ROUND_S=<S> fixes it at compile time.
+#ifndef OCM_ROUND_S
+#define OCM_ROUND_S 0
+#endif
+constexpr int kRoundS = OCM_ROUND_S;
 template <int S> __device__ __forceinline__ void ph_round_multi(const KP& p, std::uint64_t nC, int in) {
     const PJC* __restrict__ a = p.pj[in];
     PJC* __restrict__ o = p.pj[in ^ 1];
@@ -2182,7 +2194,7 @@ struct LoopState {
 #define OCM_GBAR 1
 #endif
 
-template <int MODE, int G>
+template <int MODE, int G, int SR = 2>
 __global__ void __launch_bounds__(kBlock, kSolveMinBlocks) k_solve(KP p, int mode) {
     constexpr bool EXACT = MODE != 0;
 #if !OCM_GBAR
@@ -2354,11 +2366,12 @@ __global__ void __launch_bounds__(kBlock, kSolveMinBlocks) k_solve(KP p, int mod
         bool first_try = true, voted = false;
         std::uint64_t nM = 0;
         for (;;) {
-            // all doubling passes but the last, two steps each
-            for (; static_cast<int>(st.k_hint) - k > 2; in ^= 1) {
-                ph_round_multi<2>(p, nC, in);
-                k += 2;
-                st.rounds += 2;
+            // all doubling passes but the last, S steps each
+            constexpr int S = kRoundS ? kRoundS : SR;
+            for (; static_cast<int>(st.k_hint) - k > S; in ^= 1) {
+                ph_round_multi<S>(p, nC, in);
+                k += S;
+                st.rounds += S;
                 sync(PH_ROUND);
             }
             const unsigned stamp = ++st.stamp;
@@ -2366,7 +2379,9 @@ __global__ void __launch_bounds__(kBlock, kSolveMinBlocks) k_solve(KP p, int mod
             unsigned* vflag = &c->vfail[stamp & 1];
             // the last pass (one or two steps) marks as it goes
             const int last = static_cast<int>(st.k_hint) - k;
-            if (last == 2) {
+            if (S >= 3 && last == 3) {
+                ph_round_mark<(S >= 3 ? 3 : 2)>(p, nC, in, stamp, EXACT, st.rl);
+            } else if (last == 2) {
                 ph_round_mark<2>(p, nC, in, stamp, EXACT, st.rl);
             } else if (last == 1) {
                 ph_round_mark<1>(p, nC, in, stamp, EXACT, st.rl);

@@ -42,20 +42,23 @@ constexpr int kGs[4] = {1, 2, 4, 8};
 
 // k_solve instantiation for (mode: 0 float, 1 exact, 2 wide exact; group
 // width index 0..3)
+// row 3: the exact lane with three doubling steps per pass (small graphs)
 const void* solve_fn(int mode, int gi) {
-    static const void* fns[3][4] = {
+    static const void* fns[4][4] = {
         {reinterpret_cast<const void*>(&k_solve<0, 1>), reinterpret_cast<const void*>(&k_solve<0, 2>),
          reinterpret_cast<const void*>(&k_solve<0, 4>), reinterpret_cast<const void*>(&k_solve<0, 8>)},
         {reinterpret_cast<const void*>(&k_solve<1, 1>), reinterpret_cast<const void*>(&k_solve<1, 2>),
          reinterpret_cast<const void*>(&k_solve<1, 4>), reinterpret_cast<const void*>(&k_solve<1, 8>)},
         {reinterpret_cast<const void*>(&k_solve<2, 1>), reinterpret_cast<const void*>(&k_solve<2, 2>),
-         reinterpret_cast<const void*>(&k_solve<2, 4>), reinterpret_cast<const void*>(&k_solve<2, 8>)}};
+         reinterpret_cast<const void*>(&k_solve<2, 4>), reinterpret_cast<const void*>(&k_solve<2, 8>)},
+        {reinterpret_cast<const void*>(&k_solve<1, 1, 3>), reinterpret_cast<const void*>(&k_solve<1, 2, 3>),
+         reinterpret_cast<const void*>(&k_solve<1, 4, 3>), reinterpret_cast<const void*>(&k_solve<1, 8, 3>)}};
     return fns[mode][gi];
 }
 
 struct DeviceFacts {
     int sms = 0, major = 0;
-    int per_sm[3][4] = {}; // cooperative CTAs per SM of k_solve<mode, G>
+    int per_sm[4][4] = {}; // cooperative CTAs per SM of solve_fn(row, G)
     std::string name;
 };
 
@@ -73,7 +76,7 @@ const DeviceFacts& device_facts(int dev) {
     f.major = prop.major;
     f.name = prop.name;
     if (f.major >= 10) {
-        for (int e = 0; e < 3; ++e)
+        for (int e = 0; e < 4; ++e)
             for (int gi = 0; gi < 4; ++gi) {
                 int per_sm = 0;
                 CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, solve_fn(e, gi), kBlock, 0));
@@ -256,7 +259,10 @@ void Session::init(const std::function<void(DeviceState&)>& prepare) {
     // small graphs take one CTA per kBlock vertices: fewer arrivals make every
     // grid barrier cheaper and there is no work for more threads anyway
     mode_ = prep_.exact ? (prep_.wide ? 2 : 1) : 0;
-    grid_ = facts.per_sm[mode_][gi_] * d.sms;
+    // two 16-byte doubling records per vertex: 3 steps per pass while they
+    // stay within ~64 MB of L2, 2 beyond (exact lane)
+    d.kp.round_s = std::max(2, std::min(3, env_int("OCM_ROUND_S", N <= (std::size_t(1) << 21) ? 3 : 2)));
+    grid_ = facts.per_sm[krow()][gi_] * d.sms;
     // TMA-staged improvement for key arrays beyond the ~64 MB that random
     // gathers keep at L2 speed (OCM_STAGED=0/1 forces it off/on)
     {
@@ -266,7 +272,7 @@ void Session::init(const std::function<void(DeviceState&)>& prepare) {
     }
     if (dyn_smem_bytes()) { // the staged pass / hub table use dynamic shared memory
         int per_sm = 0;
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, solve_fn(mode_, gi_), kBlock,
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, solve_fn(krow(), gi_), kBlock,
                                                          dyn_smem_bytes()));
         grid_ = std::min(grid_, std::max(1, per_sm) * d.sms);
     }
@@ -547,6 +553,8 @@ void Session::promote_wide() {
     CK(cudaStreamSynchronize(d.stream));
 }
 
+int Session::krow() const { return mode_ == 1 && d_->kp.round_s == 3 ? 3 : mode_; }
+
 std::size_t Session::dyn_smem_bytes() const {
     const KP& p = d_->kp;
     if (p.pb)
@@ -650,7 +658,7 @@ template <class M> void Session::launch_async(int mode) {
     CK(cudaEventRecord(d.ev_start, s));
     if (prep_.R > 0) {
         void* args[] = {&p, &mode};
-        CK(cudaLaunchCooperativeKernel(solve_fn(mode_, gi_), dim3(grid_), dim3(kBlock), args,
+        CK(cudaLaunchCooperativeKernel(solve_fn(krow(), gi_), dim3(grid_), dim3(kBlock), args,
                                        dyn_smem_bytes(), s));
         ++launches_;
     }

@@ -79,6 +79,7 @@ class Session {
     void alloc_wide();
     void promote_wide();
     int mode_ = 1; // k_solve arithmetic: 0 float, 1 exact (64-bit keys), 2 wide exact (128-bit)
+    int krow() const; // solve_fn row: mode_, or 3 for the exact lane with 3 doubling steps per pass
     std::size_t hot_bytes_ = 0;    // dynamic shared memory of the staged hub table
     double hot_coverage_ = 0.0;    // share of intra-region edges into the staged hubs
     bool shard_started_ = false;
