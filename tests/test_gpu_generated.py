@@ -229,3 +229,20 @@ def test_block_cooperative_attach_vs_oracle(objective, cbits, monkeypatch):
         sol = sess.solve()
         assert sol.stats.fixpoint_iters > 0
         check_against(sol, sess.values(), oracle_record(g.n, s, d, ww, objective, "tarjan"))
+
+
+@pytest.mark.parametrize("spec", [
+    P.Generator("uniform", n=100_000, deg=8, seed=3),
+    P.Generator("powerlaw", n=50_000, deg=2, dmax=5000, wlo=-50, whi=50, seed=6),
+], ids=["uniform", "powerlaw-signed"])
+@pytest.mark.parametrize("objective", ["min", "max"])
+def test_doubling_steps_per_pass_agree(spec, objective, monkeypatch):
+    """Two doubling steps per pass (the k_solve instantiation graphs beyond
+    2^21 vertices use) and three (the default below) give bit-identical
+    solves: same policy, values and statistics."""
+    monkeypatch.setenv("OCM_ROUND_S", "2")
+    a = P.Session.generated(spec, P.SolveOptions(objective=objective))
+    monkeypatch.setenv("OCM_ROUND_S", "3")
+    b = P.Session.generated(spec, P.SolveOptions(objective=objective))
+    solve_both(a, b)
+    solve_both(a, b)
